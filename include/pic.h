@@ -1,0 +1,187 @@
+/*
+ * pic.h — C ABI of the B200-native particle hot path of the implicit-moment
+ * PIC cycle (arXiv 2507.20719, iPIC3D): the implicit predictor-corrector
+ * mover (Eq. 2) and the moment gatherer (Eq. 3), with slab decomposition and
+ * NCCL exchange of ghost-node moments and migrating particles.
+ *
+ *   PAPER.md:141-145  Eq. 1  equations of motion; q_s, m_s, x_p, v_p, E_p, B_p
+ *   PAPER.md:149-165  Eq. 2  predictor-corrector mover, fixed-point on v-bar
+ *   PAPER.md:184-187  Eq. 3  {rho, J, Pi}_g = sum_p q {1, v, vv} W(x - x_p)
+ *   PAPER.md:235-236  §III-B open boundaries (outflow particles are removed)
+ *   PAPER.md:256-261, 291-334  Alg. 1: mover -> interpolation -> MPI exchange
+ * Readings of the paper (R1..R23) are listed in DESIGN.md §3.
+ *
+ * Conventions (all calls):
+ *  - Every entry point returns pic_status; none throws, exits or prints.
+ *    The text of the last error is pic_last_error(ctx).
+ *  - Units are the caller's code units (the generators use c = 1, lengths in
+ *    d_i, time in 1/omega_pi).  Positions are absolute, origin 0, global.
+ *  - Pointers documented "host or device" may be either (the library copies
+ *    with cudaMemcpyDefault on the context stream).  Host pointers should be
+ *    pinned for asynchronous copies.  Device pointers must be on the device
+ *    that was current at pic_init.
+ *  - All GPU work is enqueued on the context stream (pic_set_stream) and is
+ *    asynchronous unless stated; device-side errors (non-finite values,
+ *    particles beyond ghost reach, capacity overflow) are latched in device
+ *    flags and surfaced by the next pic_sync / pic_exchange.
+ *  - Per cycle the call order is pic_mover -> pic_moments -> pic_exchange
+ *    (for each species, mover before moments); other orders return
+ *    PIC_ESTATE.  pic_exchange is COLLECTIVE over the nranks of the config.
+ */
+#ifndef PIC_H
+#define PIC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PIC_ABI_VERSION 1
+#define PIC_MAX_SPECIES 8
+#define PIC_NCCL_ID_BYTES 128
+#define PIC_N_MOMENTS 10  /* rho, Jx, Jy, Jz, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz (R16) */
+
+typedef struct pic_ctx pic_ctx;
+
+typedef enum {
+  PIC_OK = 0,
+  PIC_EINVAL = 1,       /* bad argument / config                                  */
+  PIC_ECUDA = 2,        /* CUDA runtime error                                     */
+  PIC_ENCCL = 3,        /* NCCL error                                             */
+  PIC_ENOMEM = 4,       /* workspace too small                                    */
+  PIC_ESTATE = 5,       /* call order violated (e.g. moments before mover)        */
+  PIC_ERANGE = 6,       /* particle beyond ghost reach / > 1 periodic wrap /
+                           particle capacity exceeded                            */
+  PIC_ENONFINITE = 7    /* NaN/Inf seen in a field sample or particle update      */
+} pic_status;
+
+typedef enum { PIC_BC_PERIODIC = 0, PIC_BC_OPEN = 1 } pic_bc;
+
+/* Kernel family selection (pic_config.kernel).                               */
+typedef enum {
+  PIC_KERNEL_AUTO = 0,     /* best available (tiled where the config allows)  */
+  PIC_KERNEL_BASIC = 1,    /* one thread per particle, global field reads,
+                              global fp64 atomics for the deposit              */
+  PIC_KERNEL_TILED = 2     /* cell-sorted, tile-staged fused mover + deposit   */
+} pic_kernel;
+
+typedef struct {
+  /* Global grid: cells [0, ncell) per axis, origin 0, Delta_d = len_d/ncell_d. */
+  int64_t ncell[3];
+  double  len[3];
+  int32_t bc[3];                 /* pic_bc per axis                              */
+  double  dt;                    /* time step Delta t                            */
+  double  c;                     /* speed of light (Omega = q B /(m c), Eq. 2)   */
+  int32_t n_species;             /* 1 .. PIC_MAX_SPECIES                          */
+  double  qom[PIC_MAX_SPECIES];  /* q_s / m_s, signed (R8)                        */
+  int32_t n_iter[PIC_MAX_SPECIES];   /* fixed PC iterations, >= 1 (R2; default 3) */
+  int64_t capacity[PIC_MAX_SPECIES]; /* particle slots per species on this rank,
+                                        including migration headroom             */
+  double  planet_center[3];      /* absorbing sphere (R21); radius 0 = none       */
+  double  planet_radius;
+  int32_t rank, nranks;          /* slab decomposition along x                    */
+  int64_t slab_lo, slab_hi;      /* this rank owns x-cells [slab_lo, slab_hi)     */
+  int32_t ghost;                 /* G >= 1: field-window ghost nodes per side and
+                                    moment ghost node planes per x-side (R22)     */
+  int32_t sort_every;            /* cycles between cell sorts (0 = never)         */
+  int32_t kernel;                /* pic_kernel                                    */
+} pic_config;
+
+/* ABI version (PIC_ABI_VERSION).                                             */
+int32_t pic_abi_version(void);
+
+/* Fill out[PIC_NCCL_ID_BYTES] with a fresh ncclUniqueId (call on rank 0 and
+ * broadcast the bytes to the other ranks, e.g. with torch.distributed).      */
+pic_status pic_nccl_id(void *out);
+
+/* Bytes of device workspace pic_init needs for this config (particle store
+ * x2 for sorting, keys, field window, moments with ghost planes, exchange
+ * buffers, sort scratch).  Needs the CUDA device that pic_init will use.     */
+pic_status pic_workspace_bytes(const pic_config *cfg, int64_t *bytes);
+
+/* Create a context.  workspace: device pointer to >= bytes bytes (e.g. one
+ * torch.empty(bytes, dtype=uint8, device='cuda')), 256-byte aligned, owned by
+ * the caller and kept alive until pic_destroy; libpic never cudaMallocs.
+ * nccl_id: PIC_NCCL_ID_BYTES bytes from pic_nccl_id on rank 0 (ignored and
+ * may be NULL when nranks == 1).  The config is copied.                      */
+pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
+                    int64_t bytes, pic_ctx **out);
+
+/* Stream for all subsequent work (a cudaStream_t, e.g. torch's current
+ * stream).  NULL = the legacy default stream.                                */
+pic_status pic_set_stream(pic_ctx *ctx, void *stream);
+
+/* Load n particles of species s, replacing the previous ones.  xyzuvwq[7]:
+ * host or device fp64 arrays x, y, z, u, v, w (velocity) and q (per-particle
+ * charge q_s w_p, R14); id: host or device int64 ids (may be NULL: ids
+ * become 0..n-1).  Particles must lie in this rank's slab [slab_lo, slab_hi)
+ * x [0, ncell_y) x [0, ncell_z) (in cells).  Returns PIC_ERANGE if
+ * n > capacity[s].  Copied; the caller's buffers may be reused on return of
+ * the next pic_sync.                                                         */
+pic_status pic_set_particles(pic_ctx *ctx, int32_t s, int64_t n,
+                             const double *const xyzuvwq[7], const int64_t *id);
+
+/* Number of live particles of species s on this rank (synchronises the
+ * stream).                                                                   */
+pic_status pic_count(pic_ctx *ctx, int32_t s, int64_t *n);
+
+/* Copy the live particles of species s out (in store order — the order is
+ * unspecified; compare by id, R20).  xyzuvwq[7]/id: host or device buffers of
+ * >= pic_count elements (any entry may be NULL to skip it).  Synchronises.   */
+pic_status pic_get_particles(pic_ctx *ctx, int32_t s, double *const xyzuvwq[7],
+                             int64_t *id);
+
+/* Set E and B for the next mover call.  EB: host or device fp64 window
+ * EB[kz][ky][kx][6] (Ex Ey Ez Bx By Bz) over global node indices
+ *   x: [slab_lo - G, slab_hi + G],  y: [-G, ncell_y + G],  z: [-G, ncell_z + G]
+ * i.e. (slab_hi - slab_lo + 1 + 2G) x (ncell_y + 1 + 2G) x (ncell_z + 1 + 2G)
+ * nodes, periodic images replicated by the caller (R10, R11).  Copied into
+ * the context (the caller's buffer may be reused after the next pic_sync).   */
+pic_status pic_set_fields(pic_ctx *ctx, const double *EB);
+
+/* Advance species s (-1 = all) one cycle with Eq. 2 (R1-R3, R7-R9), then
+ * apply the boundary conditions (R10, R11, R21).  The library may fuse the
+ * moment deposit of the new state into this pass.                            */
+pic_status pic_mover(pic_ctx *ctx, int32_t s);
+
+/* Gather rho_s, J_s, Pi_s (Eq. 3, R12-R18) of the current state of species s
+ * (-1 = all) into the context's ghosted node arrays (owned values become
+ * final after pic_exchange).                                                 */
+pic_status pic_moments(pic_ctx *ctx, int32_t s);
+
+/* COLLECTIVE.  Sum ghost-node moment planes into their owners (periodic fold
+ * when nranks == 1) and migrate particles that left the slab to their new
+ * owner rank (R21).  Surfaces latched device errors.                         */
+pic_status pic_exchange(pic_ctx *ctx);
+
+/* Shorthand for one full cycle: pic_mover(-1), pic_moments(-1),
+ * pic_exchange.                                                              */
+pic_status pic_cycle(pic_ctx *ctx);
+
+/* Node counts of the moment output of this rank: out[0] = owned x-planes
+ * (slab_hi - slab_lo, +1 on the last rank when x is open), out[1], out[2] =
+ * y, z unique nodes (ncell for periodic axes, ncell + 1 for open, R18).      */
+pic_status pic_moment_shape(const pic_ctx *ctx, int64_t out[3]);
+
+/* Copy the owned moments of species s to out[10][nz][ny][nx] (shape from
+ * pic_moment_shape; host or device).  Valid after pic_exchange.             */
+pic_status pic_get_moments(pic_ctx *ctx, int32_t s, double *out);
+
+/* Wait for the stream and return counters accumulated since pic_init:
+ * stats[0] removed (open faces / planet), [1] sent, [2] received,
+ * [3] far-flyers (deposit fallback), [4] field samples clamped to the window,
+ * [5] non-finite, [6] capacity overflow, [7] multi-wrap.  stats may be NULL.
+ * Returns the first latched device error as a status.                        */
+pic_status pic_sync(pic_ctx *ctx, int64_t stats[8]);
+
+/* Human-readable text of the last error on this context (never NULL).       */
+const char *pic_last_error(const pic_ctx *ctx);
+
+/* Free the context (not the workspace).                                      */
+pic_status pic_destroy(pic_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIC_H */

@@ -1,0 +1,141 @@
+"""CPU oracle of the particle half of the implicit-moment PIC cycle.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product path (``libpic`` and ``paper_2507_20719_b200``) never
+imports it, and it imports nothing from the product path.
+
+The arithmetic lives in ``oracle/oracle.c`` (plain C, fp64, ``-O2
+-ffp-contract=off``); this module only builds it with gcc and marshals numpy
+arrays.  Passages followed: Eq. 2 for the mover, Eq. 3
+ for the moments; readings R1..R23 in DESIGN.md §3.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+PERIODIC, OPEN = 0, 1
+ALIVE, REMOVED, BAD = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into liboracle.so with gcc (no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class Grid(C.Structure):
+    _fields_ = [("ncell", C.c_int64 * 3), ("len", C.c_double * 3), ("bc", C.c_int32 * 3),
+                ("dt", C.c_double), ("c", C.c_double),
+                ("planet_center", C.c_double * 3), ("planet_radius", C.c_double)]
+
+
+class Field(C.Structure):
+    _fields_ = [("lo", C.c_int64 * 3), ("n", C.c_int64 * 3), ("EB", C.POINTER(C.c_double))]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = C.CDLL(build())
+        P = C.POINTER
+        d = P(C.c_double)
+        lib.oracle_sample.argtypes = [P(Grid), P(Field), d, d]
+        lib.oracle_sample.restype = C.c_int
+        lib.oracle_mover.argtypes = [P(Grid), P(Field), C.c_double, C.c_int, C.c_int64,
+                                     d, d, d, d, d, d, P(C.c_int8)]
+        lib.oracle_mover.restype = C.c_int64
+        lib.oracle_moments.argtypes = [P(Grid), C.c_int64, d, d, d, d, d, d, d, P(C.c_int8), d, d]
+        lib.oracle_moments.restype = C.c_int64
+        lib.oracle_node_counts.argtypes = [P(Grid), P(C.c_int64)]
+        _lib = lib
+    return _lib
+
+
+def _dptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def make_grid(ncell, length, bc=(PERIODIC,) * 3, dt=0.5, c=1.0,
+              planet_center=(0.0, 0.0, 0.0), planet_radius=0.0) -> Grid:
+    g = Grid()
+    for d in range(3):
+        g.ncell[d] = int(ncell[d])
+        g.len[d] = float(length[d])
+        g.bc[d] = int(bc[d])
+        g.planet_center[d] = float(planet_center[d])
+    g.dt, g.c, g.planet_radius = float(dt), float(c), float(planet_radius)
+    return g
+
+
+class FieldWindow:
+    """E,B node window: global node indices [lo, lo+n) per axis, EB[k][j][i][6]."""
+
+    def __init__(self, lo, EB: np.ndarray):
+        EB = np.ascontiguousarray(EB, dtype=np.float64)
+        assert EB.ndim == 4 and EB.shape[3] == 6
+        self.EB = EB
+        self.lo = tuple(int(v) for v in lo)
+        self.n = (EB.shape[2], EB.shape[1], EB.shape[0])
+        f = Field()
+        for d in range(3):
+            f.lo[d] = self.lo[d]
+            f.n[d] = self.n[d]
+        f.EB = _dptr(self.EB)
+        self.c = f
+
+
+def node_counts(g: Grid):
+    out = (C.c_int64 * 3)()
+    _load().oracle_node_counts(C.byref(g), out)
+    return tuple(out)
+
+
+def sample(g: Grid, F: FieldWindow, pos) -> np.ndarray:
+    p = np.ascontiguousarray(pos, dtype=np.float64)
+    out = np.zeros(6)
+    _load().oracle_sample(C.byref(g), C.byref(F.c), _dptr(p), _dptr(out))
+    return out
+
+
+def mover(g: Grid, F: FieldWindow, qom: float, n_iter: int, parts: dict, status=None):
+    """Push one species in place.  parts: dict of float64 arrays x y z u v w."""
+    n = len(parts["x"])
+    if status is None:
+        status = np.zeros(n, dtype=np.int8)
+    for k in "xyzuvw":
+        assert parts[k].dtype == np.float64 and parts[k].flags.c_contiguous
+    bad = _load().oracle_mover(C.byref(g), C.byref(F.c), float(qom), int(n_iter), n,
+                               *[_dptr(parts[k]) for k in "xyzuvw"],
+                               status.ctypes.data_as(C.POINTER(C.c_int8)))
+    return status, int(bad)
+
+
+def moments(g: Grid, parts: dict, status=None, with_abs: bool = True):
+    """Moments of one species: (mom[10][nz][ny][nx], absmom or None)."""
+    nx, ny, nz = node_counts(g)
+    mom = np.zeros((10, nz, ny, nx))
+    am = np.zeros((10, nz, ny, nx)) if with_abs else None
+    n = len(parts["x"])
+    st = status.ctypes.data_as(C.POINTER(C.c_int8)) if status is not None else None
+    out = _load().oracle_moments(C.byref(g), n, *[_dptr(parts[k]) for k in "xyzuvwq"], st,
+                                 _dptr(mom), _dptr(am) if am is not None else None)
+    if out:
+        raise ValueError(f"{out} particles outside the grid in oracle.moments")
+    return mom, am

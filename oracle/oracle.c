@@ -1,0 +1,264 @@
+/*
+ * oracle.c — plain, slow, obviously-correct CPU oracle of the particle half of
+ * the implicit-moment PIC cycle (arXiv 2507.20719, iPIC3D).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (libpic, paper_2507_20719_b200/) never links, imports or
+ * calls it, and this file includes no header of the product path.
+ *
+ * fp64 throughout, compiled with -O2 -ffp-contract=off (no FMA contraction, no
+ * fast-math) so every operation below is one IEEE-754 rounding in the order
+ * written.  One particle at a time, in input order; no blocking, no fusion,
+ * no reordering beyond what the equations state.
+ *
+ * Passages followed (PAPER.md line numbers, /root/reference/PAPER.md):
+ *   Eq. 1   PAPER.md:141-145  equations of motion (hot path: gamma == 1)
+ *   Eq. 2   PAPER.md:149-165  predictor-corrector mover, fixed-point on v-bar
+ *   Eq. 3   PAPER.md:184-187  moments {rho, J, Pi}_g = sum_p q {1, v, vv} W
+ *   Alg. 1  PAPER.md:291-334  phase order: mover, then interpolation
+ *   §III-B  PAPER.md:235-236  open boundaries: particles leaving are removed
+ * Readings where the paper is silent or garbled are R1..R23 in DESIGN.md §3
+ * (taken from SURVEY.md §8(c)); each use below names its reading.
+ *
+ * Pins (tests/test_oracle_pins.py) tie every function here to closed forms:
+ * free streaming, gyration angle/radius, ExB drift, uniform-E kick, the
+ * linear-field worked example, node/cell-centre stencils, global sums,
+ * gather/scatter adjointness, lattice loading and exact-rational brute force.
+ * oracle_mover with open boundaries near the ghost clamp (R11) is
+ * "parity unpinned" for the clamp branch itself.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- types -- */
+
+/* Global grid: cells [0, ncell) per axis, origin 0, Delta = len / ncell.   */
+typedef struct {
+  int64_t ncell[3];
+  double  len[3];
+  int32_t bc[3];            /* 0 = periodic, 1 = open                       */
+  double  dt, c;
+  double  planet_center[3];
+  double  planet_radius;    /* 0 = no absorbing body                        */
+} oracle_grid;
+
+/* Field window: node-interleaved E,B on global node indices
+ * [lo_d, lo_d + n_d) per axis, layout EB[k][j][i][6] = Ex Ey Ez Bx By Bz.
+ * Periodic images are replicated by the caller (the window is plain data). */
+typedef struct {
+  int64_t lo[3];
+  int64_t n[3];
+  const double *EB;
+} oracle_field;
+
+enum { ORACLE_ALIVE = 0, ORACLE_REMOVED = 1, ORACLE_BAD = 2 };
+
+/* ------------------------------------------------------- field sampling -- */
+
+/* Trilinear interpolation W of E and B at position p (R12):
+ * xi = (p - lo*Delta)/Delta, i = floor(xi), f = xi - i, weights (1-f, f) per
+ * axis, product over axes.  Outside the window xi is clamped to the window
+ * (constant extension, R11).  Returns 1 if a clamp happened.                */
+int oracle_sample(const oracle_grid *g, const oracle_field *F,
+                  const double p[3], double out[6]) {
+  int64_t idx[3];
+  double f[3];
+  int clamped = 0;
+  for (int d = 0; d < 3; ++d) {
+    double delta = g->len[d] / (double)g->ncell[d];
+    double xi = p[d] / delta - (double)F->lo[d];
+    double top = (double)(F->n[d] - 1);
+    if (!(xi >= 0.0)) { xi = 0.0; clamped = 1; }     /* also catches NaN */
+    if (xi > top) { xi = top; clamped = 1; }
+    double fl = floor(xi);
+    if (fl > top - 1.0) fl = top - 1.0;
+    idx[d] = (int64_t)fl;
+    f[d] = xi - fl;
+  }
+  for (int m = 0; m < 6; ++m) out[m] = 0.0;
+  for (int c = 0; c < 8; ++c) {
+    int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
+    double wx = bx ? f[0] : 1.0 - f[0];
+    double wy = by ? f[1] : 1.0 - f[1];
+    double wz = bz ? f[2] : 1.0 - f[2];
+    double S = wx * wy * wz;
+    int64_t i = idx[0] + bx, j = idx[1] + by, k = idx[2] + bz;
+    const double *node = F->EB + 6 * ((k * F->n[1] + j) * F->n[0] + i);
+    for (int m = 0; m < 6; ++m) out[m] += S * node[m];
+  }
+  return clamped;
+}
+
+/* ------------------------------------------------------------- the mover -- */
+
+/* Boundary treatment after the push (R10, R11, R21).
+ * Periodic: one wrap, x >= L -> x - L; x < 0 -> x + L (and L -> 0).
+ * Open: outside [0, L) on any open axis, or inside the planet -> removed.   */
+static int apply_bc(const oracle_grid *g, double x[3]) {
+  int status = ORACLE_ALIVE;
+  for (int d = 0; d < 3; ++d) {
+    double L = g->len[d];
+    if (g->bc[d] == 0) {
+      if (x[d] >= L) {
+        x[d] = x[d] - L;
+      } else if (x[d] < 0.0) {
+        x[d] = x[d] + L;
+        if (x[d] == L) x[d] = 0.0;
+      }
+      if (!(x[d] >= 0.0 && x[d] < L)) status = ORACLE_BAD;   /* > one wrap */
+    } else {
+      if (!(x[d] >= 0.0 && x[d] < L)) {
+        if (status == ORACLE_ALIVE) status = ORACLE_REMOVED;
+        if (x[d] != x[d]) status = ORACLE_BAD;
+      }
+    }
+  }
+  if (status == ORACLE_ALIVE && g->planet_radius > 0.0) {
+    double r2 = 0.0;
+    for (int d = 0; d < 3; ++d) {
+      double dx = x[d] - g->planet_center[d];
+      r2 += dx * dx;
+    }
+    if (r2 < g->planet_radius * g->planet_radius) status = ORACLE_REMOVED;
+  }
+  return status;
+}
+
+/* Eq. 2 in the gamma == 1 limit (R3), one particle:
+ *   xb <- xn                                   (R1: first sample at x^n)
+ *   repeat n_iter times, no early exit         (R2)
+ *     (E,B) <- W(xb)                           (R12)
+ *     vt    <- vn + (q/m)(dt/2) E              (Eq. 2 line 3, R7)
+ *     a     <- (q/m)(dt/2) B / c   = Omega dt/2 (R8: q signed)
+ *     vb    <- (vt + vt x a + (vt.a) a) / (1 + a.a)   (Eq. 2 line 4, D)
+ *     xb    <- xn + vb dt/2
+ *   x^{n+1} <- xn + vb dt ;  v^{n+1} <- 2 vb - vn     (Eq. 2 lines 1-2)
+ *   boundary conditions                                                    */
+static int push_one(const oracle_grid *g, const oracle_field *F, double qom,
+                    int n_iter, double xn[3], double vn[3]) {
+  double ks = qom * (g->dt / 2.0);
+  double xb[3] = {xn[0], xn[1], xn[2]};
+  double vb[3] = {vn[0], vn[1], vn[2]};
+  for (int it = 0; it < n_iter; ++it) {
+    double EB[6];
+    oracle_sample(g, F, xb, EB);
+    double vt[3], a[3];
+    for (int d = 0; d < 3; ++d) vt[d] = vn[d] + ks * EB[d];
+    for (int d = 0; d < 3; ++d) a[d] = (ks / g->c) * EB[3 + d];
+    double cross[3];
+    cross[0] = vt[1] * a[2] - vt[2] * a[1];
+    cross[1] = vt[2] * a[0] - vt[0] * a[2];
+    cross[2] = vt[0] * a[1] - vt[1] * a[0];
+    double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
+    double D = 1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    for (int d = 0; d < 3; ++d) vb[d] = (vt[d] + cross[d] + dot * a[d]) / D;
+    for (int d = 0; d < 3; ++d) xb[d] = xn[d] + vb[d] * (g->dt / 2.0);
+  }
+  for (int d = 0; d < 3; ++d) {
+    double v_new = 2.0 * vb[d] - vn[d];
+    xn[d] = xn[d] + vb[d] * g->dt;
+    vn[d] = v_new;
+  }
+  int status = apply_bc(g, xn);
+  for (int d = 0; d < 3; ++d)
+    if (!(vn[d] == vn[d]) || isinf(vn[d])) status = ORACLE_BAD;
+  return status;
+}
+
+/* Mover over np particles of one species (SoA, updated in place).  status[p]
+ * on entry: ORACLE_ALIVE particles are pushed, others are skipped.  Returns
+ * the number of particles whose status became ORACLE_BAD.                   */
+int64_t oracle_mover(const oracle_grid *g, const oracle_field *F, double qom,
+                     int n_iter, int64_t np, double *x, double *y, double *z,
+                     double *u, double *v, double *w, int8_t *status) {
+  int64_t bad = 0;
+  for (int64_t p = 0; p < np; ++p) {
+    if (status[p] != ORACLE_ALIVE) continue;
+    double xn[3] = {x[p], y[p], z[p]};
+    double vn[3] = {u[p], v[p], w[p]};
+    int s = push_one(g, F, qom, n_iter, xn, vn);
+    x[p] = xn[0]; y[p] = xn[1]; z[p] = xn[2];
+    u[p] = vn[0]; v[p] = vn[1]; w[p] = vn[2];
+    status[p] = (int8_t)s;
+    if (s == ORACLE_BAD) ++bad;
+  }
+  return bad;
+}
+
+/* ----------------------------------------------------------- the moments -- */
+
+/* Number of unique nodes per axis (R18): periodic N (node N == node 0),
+ * open N + 1.                                                               */
+static int64_t nodes_axis(const oracle_grid *g, int d) {
+  return g->bc[d] == 0 ? g->ncell[d] : g->ncell[d] + 1;
+}
+
+/* Eq. 3 for one species, over alive particles in input
+ * order (R15), into mom[10][nz][ny][nx] on the unique node set (R18):
+ *   rho += q S / V ; J += q v S / V ; Pi_ab += q v_a v_b S / V
+ * with S the trilinear weight of the corner (R12), V = dx dy dz (R13), q the
+ * per-particle charge q_s w_p (R14), Pi in order xx xy xz yy yz zz (R16).
+ * absmom (may be NULL) accumulates |each contribution| for the R19 bound.
+ * mom/absmom are accumulated into (caller zeroes them).  Returns the number
+ * of particles whose stencil left the grid (only possible for bad input).  */
+int64_t oracle_moments(const oracle_grid *g, int64_t np, const double *x,
+                       const double *y, const double *z, const double *u,
+                       const double *v, const double *w, const double *q,
+                       const int8_t *status, double *mom, double *absmom) {
+  int64_t nn[3] = {nodes_axis(g, 0), nodes_axis(g, 1), nodes_axis(g, 2)};
+  int64_t plane = nn[0] * nn[1] * nn[2];
+  double delta[3], V = 1.0;
+  for (int d = 0; d < 3; ++d) {
+    delta[d] = g->len[d] / (double)g->ncell[d];
+  }
+  V = delta[0] * delta[1] * delta[2];
+  int64_t outside = 0;
+  for (int64_t p = 0; p < np; ++p) {
+    if (status && status[p] != ORACLE_ALIVE) continue;
+    double pos[3] = {x[p], y[p], z[p]};
+    double vel[3] = {u[p], v[p], w[p]};
+    int64_t idx[3];
+    double f[3];
+    int ok = 1;
+    for (int d = 0; d < 3; ++d) {
+      double xi = pos[d] / delta[d];
+      double fl = floor(xi);
+      idx[d] = (int64_t)fl;
+      f[d] = xi - fl;
+      if (idx[d] < 0 || idx[d] >= g->ncell[d]) ok = 0;
+    }
+    if (!ok) { ++outside; continue; }
+    double val[10];
+    val[0] = 1.0;
+    val[1] = vel[0]; val[2] = vel[1]; val[3] = vel[2];
+    val[4] = vel[0] * vel[0]; val[5] = vel[0] * vel[1]; val[6] = vel[0] * vel[2];
+    val[7] = vel[1] * vel[1]; val[8] = vel[1] * vel[2]; val[9] = vel[2] * vel[2];
+    for (int c = 0; c < 8; ++c) {
+      int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
+      double wx = bx ? f[0] : 1.0 - f[0];
+      double wy = by ? f[1] : 1.0 - f[1];
+      double wz = bz ? f[2] : 1.0 - f[2];
+      double S = wx * wy * wz;
+      int64_t i = idx[0] + bx, j = idx[1] + by, k = idx[2] + bz;
+      if (g->bc[0] == 0 && i == nn[0]) i = 0;     /* R18 periodic fold */
+      if (g->bc[1] == 0 && j == nn[1]) j = 0;
+      if (g->bc[2] == 0 && k == nn[2]) k = 0;
+      int64_t node = (k * nn[1] + j) * nn[0] + i;
+      double qs = q[p] * S / V;
+      for (int m = 0; m < 10; ++m) {
+        double contrib = qs * val[m];
+        mom[m * plane + node] += contrib;
+        if (absmom) absmom[m * plane + node] += fabs(contrib);
+      }
+    }
+  }
+  return outside;
+}
+
+/* Convenience for tests: unique node counts per axis.                      */
+void oracle_node_counts(const oracle_grid *g, int64_t out[3]) {
+  for (int d = 0; d < 3; ++d) out[d] = nodes_axis(g, d);
+}
