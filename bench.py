@@ -1,0 +1,360 @@
+#!/usr/bin/env python3
+"""Bench: particle updates/s (mover + moments) of the implicit-moment PIC particle
+path on 1..8 B200, and its fraction of the HBM roofline (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+A step is one full particle cycle through the C ABI (pic_cycle = pic_mover,
+pic_moments, pic_exchange) for every species of the workload.  The default
+workload is C2 (GEM Harris sheet, 128 x 64 x 32 cells, 2 species, 125 ppc,
+65.5 M particles, 3.67 GB) per GPU; with N GPUs it is weak-scaled along x
+(128 N x 64 x 32 cells, one x-slab of C2's size per rank).  Inputs live in HBM
+and are larger than L2 (no flush needed).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_ALG_PARTICLE = 104.0       # read x,v,q (56 B) + write x,v (48 B) per update
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
+    ap.add_argument("--sort-every", type=int, default=1)
+    ap.add_argument("--ghost", type=int, default=2)
+    ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args, nranks, rank):
+    from paper_2507_20719_b200 import inputs as I
+    if args.config == "c2":
+        w = I.c2(scale_x=nranks, ppc=args.ppc or 125)
+        per = 128
+        desc = "C2 GEM double Harris sheet, 128x64x32 cells per GPU (x-slab weak scaling), 2 species, 125 ppc, mass ratio 256, 3 PC iterations"
+    elif args.config == "c3":
+        w = I.c3(nranks=nranks, ppc=args.ppc or 64)
+        per = 192
+        desc = "C3 weak-scaling cube 192^3 cells per GPU, 2 species, 64 ppc, 3 PC iterations"
+    else:
+        w = I.c1()
+        per = 16 // nranks
+        desc = "C1 16^3 periodic uniform Maxwellian, 2 species, 27 ppc (L2-resident; not a roofline config)"
+    return w.with_slab(rank * per, (rank + 1) * per), desc
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------- oracle (CPU) --
+def oracle_rate(w, parts_cpu, target_s, n_iter=3):
+    """Time the CPU oracle (mover + moments, one cycle) on a bounded sample of the
+    workload's particles; returns (updates/s, sample description, cores)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle as O
+    from paper_2507_20719_b200 import inputs as I
+    g = O.make_grid(w.ncell, w.length, w.bc, w.dt, w.c, w.planet_center, w.planet_radius)
+    lo, EB = I.field_window(w.with_slab(0, w.ncell[0]) if w.slab_or_all() == (0, w.ncell[0]) else w, 2)
+    F = O.FieldWindow(lo, EB.numpy())
+    # the oracle deposits on the global grid; restrict the sample to this rank's
+    # slab (rank 0) -- a global grid of the same shape is used for the timing
+    def run(n_per_species):
+        tot = 0
+        t0 = time.perf_counter()
+        for s, sp in enumerate(w.species):
+            P = {k: parts_cpu[s][k][:n_per_species].numpy().copy() for k in "xyzuvwq"}
+            st = np.zeros(len(P["x"]), dtype=np.int8)
+            O.mover(g, F, sp.qom, n_iter, P, st)
+            O.moments(g, P, st, with_abs=False)
+            tot += len(P["x"])
+        return tot, time.perf_counter() - t0
+    n0 = min(20000, min(p["x"].numel() for p in parts_cpu))
+    tot, dt = run(n0)
+    rate = tot / dt
+    n1 = int(min(min(p["x"].numel() for p in parts_cpu), max(n0, rate * target_s / len(w.species))))
+    tot, dt = run(n1)
+    return tot / dt, f"{n1} particles per species (first {n1} in id order of rank 0's slab), 1 cycle, mover+moments, single thread", 1
+
+
+def oracle_sample_parts(w, device="cpu"):
+    from paper_2507_20719_b200 import inputs as I
+    return I.make_species(w, device=device)
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle as it stands, timed on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    torch.set_num_threads(1)
+    w, desc = workload(args, args.gpus, 0)
+    # generate a bounded sub-slab of the workload on the CPU (same recipe)
+    from paper_2507_20719_b200 import inputs as I
+    sub = w.with_slab(0, max(1, min(w.slab_or_all()[1], 4)))
+    parts = I.make_species(sub, device="cpu")
+    vals = []
+    for _ in range(args.warmup):
+        oracle_rate(w, parts, min(2.0, args.cpu_seconds / 4))
+    for _ in range(args.steps):
+        r, sample, cores = oracle_rate(w, parts, args.cpu_seconds / max(1, args.steps))
+        vals.append(r)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": "particle updates/s (mover+moments)", "value": v,
+            "unit": "particle updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "particle updates/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "particle updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm ----
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2507_20719_b200 import decomp, inputs as I, pic
+
+    w, desc = workload(args, world, rank)
+    parts = I.make_species(w, device="cuda")
+    n_local = [p["x"].numel() for p in parts]
+    cap = [int(n * 1.08) + 65536 for n in n_local]
+    nccl_id = decomp.broadcast_nccl_id(pic.pic_nccl_id) if world > 1 else None
+    cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
+                          sort_every=args.sort_every, kernel=args.kernel)
+    stream = torch.cuda.current_stream()
+    ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, p)
+    lo, EB = I.field_window(w, args.ghost, device="cuda")
+    ctx.set_fields(EB)
+    parts_cpu_sample = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded oracle sample: first particles of the store in id order (x-planes 0..)
+        parts_cpu_sample = [{k: v[: min(v.numel(), 2_000_000)].cpu() for k, v in p.items()} for p in parts]
+    del parts
+    torch.cuda.empty_cache()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ctx.cycle()
+    ctx.sync()
+    n_alive = sum(ctx.count(s) for s in range(len(w.species)))
+
+    # ---- timed region (device time, CUDA events on the context stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    updates = 0
+    barrier()
+    with ClockSampler(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k in range(args.steps):
+            e0, e1, e2 = ev[k]
+            e0.record(stream)
+            ctx.mover(-1)
+            e1.record(stream)
+            ctx.moments(-1)
+            ctx.exchange()
+            e2.record(stream)
+        end.record(stream)
+        barrier()
+    launches = ctx.launch_count() - launches0
+    stats = ctx.sync()
+    t_ms = start.elapsed_time(end)
+    mover_ms = [a.elapsed_time(b) for a, b, c in ev]
+    rest_ms = [b.elapsed_time(c) for a, b, c in ev]
+    tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([float(n_alive)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    t_ms = float(tt.item())
+    total_updates = float(tot.item()) * args.steps
+    value = total_updates / (t_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the mover launch, fused with the
+    # deposit in the tiled family): algorithmic bytes / its event-timed duration
+    peak, peak_kind = measured_peaks()
+    fused = args.kernel in (0, 2)
+    n_sp = len(w.species)
+    ppc = w.species[0].ppc
+    grid_share = (48.0 + 80.0 * n_sp) / (ppc * n_sp)
+    b_mover = (B_ALG_PARTICLE + grid_share) if fused else (96.0 + 48.0 / (ppc * n_sp))
+    mover_avg = sum(mover_ms) / len(mover_ms)
+    achieved = n_alive * b_mover / (mover_avg / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "tiled fused mover+deposit" if fused else "mover_basic",
+            "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "bytes_per_update": b_mover, "launch_ms": mover_avg,
+            "step_frac": (value / world) * (B_ALG_PARTICLE + grid_share) / (peak * 1e9)}
+
+    # ---- e2e through the public API with host buffers (paper's discrete-GPU
+    # cycle: fields host->device, moments device->host)
+    e2e = None
+    if not args.no_e2e:
+        EB_h = EB.cpu().pin_memory()
+        shape = ctx.moment_shape()
+        mom_h = [torch.empty((10, shape[2], shape[1], shape[0]), dtype=torch.float64).pin_memory()
+                 for _ in range(n_sp)]
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            ctx.set_fields(EB_h)
+            ctx.cycle()
+            for s in range(n_sp):
+                ctx.get_moments(s, out=mom_h[s])
+        b.record(stream)
+        barrier()
+        te = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        n_alive2 = sum(ctx.count(s) for s in range(n_sp))
+        tot2 = torch.tensor([float(n_alive2)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tot2, op=dist.ReduceOp.SUM)
+        e2e = {"value": float(tot2.item()) * args.steps / (float(te.item()) / 1e3), "unit": "particle updates/s",
+               "h2d_bytes_per_step": EB_h.numel() * 8,
+               "d2h_bytes_per_step": sum(m.numel() * 8 for m in mom_h)}
+        ctx.sync()
+
+    cpu = None
+    if parts_cpu_sample is not None:
+        threads = torch.get_num_threads()
+        torch.set_num_threads(1)
+        r, sample, cores = oracle_rate(w, parts_cpu_sample, args.cpu_seconds)
+        torch.set_num_threads(threads)
+        cpu = {"value": r, "unit": "particle updates/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "particle updates/s (mover+moments)", "value": value, "unit": "particle updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": desc, "particles_per_gpu": n_alive, "cells_per_gpu": list(w.ncell[1:]),
+                       "kernel": ["auto", "basic", "tiled"][args.kernel], "sort_every": args.sort_every,
+                       "l2": "inputs (%.2f GB per GPU) exceed the 126 MB L2; no flush" % (n_alive * 64 / 1e9),
+                       "parallelism": f"x-slabs{world}"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "phase_ms": {"mover": mover_avg, "moments+exchange": sum(rest_ms) / len(rest_ms)},
+            "stats": stats,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

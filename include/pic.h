@@ -33,6 +33,12 @@
 
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define PIC_API __attribute__((visibility("default")))
+#else
+#define PIC_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -89,28 +95,28 @@ typedef struct {
 } pic_config;
 
 /* ABI version (PIC_ABI_VERSION).                                             */
-int32_t pic_abi_version(void);
+PIC_API int32_t pic_abi_version(void);
 
 /* Fill out[PIC_NCCL_ID_BYTES] with a fresh ncclUniqueId (call on rank 0 and
  * broadcast the bytes to the other ranks, e.g. with torch.distributed).      */
-pic_status pic_nccl_id(void *out);
+PIC_API pic_status pic_nccl_id(void *out);
 
 /* Bytes of device workspace pic_init needs for this config (particle store
  * x2 for sorting, keys, field window, moments with ghost planes, exchange
  * buffers, sort scratch).  Needs the CUDA device that pic_init will use.     */
-pic_status pic_workspace_bytes(const pic_config *cfg, int64_t *bytes);
+PIC_API pic_status pic_workspace_bytes(const pic_config *cfg, int64_t *bytes);
 
 /* Create a context.  workspace: device pointer to >= bytes bytes (e.g. one
  * torch.empty(bytes, dtype=uint8, device='cuda')), 256-byte aligned, owned by
  * the caller and kept alive until pic_destroy; libpic never cudaMallocs.
  * nccl_id: PIC_NCCL_ID_BYTES bytes from pic_nccl_id on rank 0 (ignored and
  * may be NULL when nranks == 1).  The config is copied.                      */
-pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
+PIC_API pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
                     int64_t bytes, pic_ctx **out);
 
 /* Stream for all subsequent work (a cudaStream_t, e.g. torch's current
  * stream).  NULL = the legacy default stream.                                */
-pic_status pic_set_stream(pic_ctx *ctx, void *stream);
+PIC_API pic_status pic_set_stream(pic_ctx *ctx, void *stream);
 
 /* Load n particles of species s, replacing the previous ones.  xyzuvwq[7]:
  * host or device fp64 arrays x, y, z, u, v, w (velocity) and q (per-particle
@@ -119,17 +125,17 @@ pic_status pic_set_stream(pic_ctx *ctx, void *stream);
  * x [0, ncell_y) x [0, ncell_z) (in cells).  Returns PIC_ERANGE if
  * n > capacity[s].  Copied; the caller's buffers may be reused on return of
  * the next pic_sync.                                                         */
-pic_status pic_set_particles(pic_ctx *ctx, int32_t s, int64_t n,
+PIC_API pic_status pic_set_particles(pic_ctx *ctx, int32_t s, int64_t n,
                              const double *const xyzuvwq[7], const int64_t *id);
 
 /* Number of live particles of species s on this rank (synchronises the
  * stream).                                                                   */
-pic_status pic_count(pic_ctx *ctx, int32_t s, int64_t *n);
+PIC_API pic_status pic_count(pic_ctx *ctx, int32_t s, int64_t *n);
 
 /* Copy the live particles of species s out (in store order — the order is
  * unspecified; compare by id, R20).  xyzuvwq[7]/id: host or device buffers of
  * >= pic_count elements (any entry may be NULL to skip it).  Synchronises.   */
-pic_status pic_get_particles(pic_ctx *ctx, int32_t s, double *const xyzuvwq[7],
+PIC_API pic_status pic_get_particles(pic_ctx *ctx, int32_t s, double *const xyzuvwq[7],
                              int64_t *id);
 
 /* Set E and B for the next mover call.  EB: host or device fp64 window
@@ -138,48 +144,52 @@ pic_status pic_get_particles(pic_ctx *ctx, int32_t s, double *const xyzuvwq[7],
  * i.e. (slab_hi - slab_lo + 1 + 2G) x (ncell_y + 1 + 2G) x (ncell_z + 1 + 2G)
  * nodes, periodic images replicated by the caller (R10, R11).  Copied into
  * the context (the caller's buffer may be reused after the next pic_sync).   */
-pic_status pic_set_fields(pic_ctx *ctx, const double *EB);
+PIC_API pic_status pic_set_fields(pic_ctx *ctx, const double *EB);
 
 /* Advance species s (-1 = all) one cycle with Eq. 2 (R1-R3, R7-R9), then
  * apply the boundary conditions (R10, R11, R21).  The library may fuse the
  * moment deposit of the new state into this pass.                            */
-pic_status pic_mover(pic_ctx *ctx, int32_t s);
+PIC_API pic_status pic_mover(pic_ctx *ctx, int32_t s);
 
 /* Gather rho_s, J_s, Pi_s (Eq. 3, R12-R18) of the current state of species s
  * (-1 = all) into the context's ghosted node arrays (owned values become
  * final after pic_exchange).                                                 */
-pic_status pic_moments(pic_ctx *ctx, int32_t s);
+PIC_API pic_status pic_moments(pic_ctx *ctx, int32_t s);
 
 /* COLLECTIVE.  Sum ghost-node moment planes into their owners (periodic fold
  * when nranks == 1) and migrate particles that left the slab to their new
  * owner rank (R21).  Surfaces latched device errors.                         */
-pic_status pic_exchange(pic_ctx *ctx);
+PIC_API pic_status pic_exchange(pic_ctx *ctx);
 
 /* Shorthand for one full cycle: pic_mover(-1), pic_moments(-1),
  * pic_exchange.                                                              */
-pic_status pic_cycle(pic_ctx *ctx);
+PIC_API pic_status pic_cycle(pic_ctx *ctx);
 
 /* Node counts of the moment output of this rank: out[0] = owned x-planes
  * (slab_hi - slab_lo, +1 on the last rank when x is open), out[1], out[2] =
  * y, z unique nodes (ncell for periodic axes, ncell + 1 for open, R18).      */
-pic_status pic_moment_shape(const pic_ctx *ctx, int64_t out[3]);
+PIC_API pic_status pic_moment_shape(const pic_ctx *ctx, int64_t out[3]);
 
 /* Copy the owned moments of species s to out[10][nz][ny][nx] (shape from
  * pic_moment_shape; host or device).  Valid after pic_exchange.             */
-pic_status pic_get_moments(pic_ctx *ctx, int32_t s, double *out);
+PIC_API pic_status pic_get_moments(pic_ctx *ctx, int32_t s, double *out);
 
 /* Wait for the stream and return counters accumulated since pic_init:
  * stats[0] removed (open faces / planet), [1] sent, [2] received,
  * [3] far-flyers (deposit fallback), [4] field samples clamped to the window,
  * [5] non-finite, [6] capacity overflow, [7] multi-wrap.  stats may be NULL.
  * Returns the first latched device error as a status.                        */
-pic_status pic_sync(pic_ctx *ctx, int64_t stats[8]);
+PIC_API pic_status pic_sync(pic_ctx *ctx, int64_t stats[8]);
+
+/* Number of libpic kernel launches enqueued on this context since pic_init
+ * (the bench's gpu_launches evidence).                                       */
+PIC_API pic_status pic_launch_count(const pic_ctx *ctx, int64_t *n);
 
 /* Human-readable text of the last error on this context (never NULL).       */
-const char *pic_last_error(const pic_ctx *ctx);
+PIC_API const char *pic_last_error(const pic_ctx *ctx);
 
 /* Free the context (not the workspace).                                      */
-pic_status pic_destroy(pic_ctx *ctx);
+PIC_API pic_status pic_destroy(pic_ctx *ctx);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,422 @@
+// api.cu — the C ABI of include/pic.h: validation, workspace layout, call-order
+// state machine, stream handling and dispatch to the kernel families.
+#include <nccl.h>
+
+#include <algorithm>
+#include <new>
+
+#include "pic_internal.cuh"
+
+using namespace pic;
+
+namespace {
+
+constexpr int64_t ALIGN = 256;
+
+inline int64_t align_up(int64_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
+
+struct Layout {
+  int64_t total = 0;
+  int64_t take(int64_t bytes) {
+    int64_t off = total;
+    total += align_up(bytes);
+    return off;
+  }
+};
+
+pic_status validate(const pic_config *c, std::string *why) {
+  if (!c) { *why = "null config"; return PIC_EINVAL; }
+  for (int d = 0; d < 3; ++d) {
+    if (c->ncell[d] < 2) { *why = "ncell must be >= 2 per axis"; return PIC_EINVAL; }
+    if (!(c->len[d] > 0)) { *why = "len must be > 0"; return PIC_EINVAL; }
+    if (c->bc[d] != PIC_BC_PERIODIC && c->bc[d] != PIC_BC_OPEN) { *why = "bad bc"; return PIC_EINVAL; }
+  }
+  if (!(c->dt > 0) || !(c->c > 0)) { *why = "dt and c must be > 0"; return PIC_EINVAL; }
+  if (c->n_species < 1 || c->n_species > PIC_MAX_SPECIES) { *why = "n_species out of range"; return PIC_EINVAL; }
+  for (int s = 0; s < c->n_species; ++s) {
+    if (c->n_iter[s] < 1 || c->n_iter[s] > 64) { *why = "n_iter must be in [1, 64]"; return PIC_EINVAL; }
+    if (c->capacity[s] < 0 || c->capacity[s] > (int64_t(1) << 30)) {
+      *why = "capacity must be in [0, 2^30] per species per rank"; return PIC_EINVAL;
+    }
+  }
+  if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) { *why = "bad rank/nranks"; return PIC_EINVAL; }
+  if (c->slab_lo < 0 || c->slab_hi > c->ncell[0] || c->slab_hi - c->slab_lo < 1) {
+    *why = "bad slab"; return PIC_EINVAL;
+  }
+  if (c->nranks == 1 && (c->slab_lo != 0 || c->slab_hi != c->ncell[0])) {
+    *why = "single rank must own all x cells"; return PIC_EINVAL;
+  }
+  if (c->ghost < 1 || c->ghost > 8) { *why = "ghost must be in [1, 8]"; return PIC_EINVAL; }
+  if (c->nranks > 1 && c->slab_hi - c->slab_lo < c->ghost + 1) {
+    *why = "slab narrower than ghost + 1 cells"; return PIC_EINVAL;
+  }
+  const int64_t cells = (c->slab_hi - c->slab_lo) * c->ncell[1] * c->ncell[2];
+  if (cells >= (int64_t)KEY_FIRST_RESERVED) { *why = "too many local cells for 32-bit keys"; return PIC_EINVAL; }
+  if (c->planet_radius < 0) { *why = "planet_radius < 0"; return PIC_EINVAL; }
+  if (c->sort_every < 0) { *why = "sort_every < 0"; return PIC_EINVAL; }
+  if (c->kernel < 0 || c->kernel > 2) { *why = "bad kernel"; return PIC_EINVAL; }
+  return PIC_OK;
+}
+
+void make_geom(const pic_config *c, Geom *g) {
+  memset(g, 0, sizeof(*g));
+  for (int d = 0; d < 3; ++d) {
+    g->ncell[d] = c->ncell[d];
+    g->periodic[d] = c->bc[d] == PIC_BC_PERIODIC;
+    g->delta[d] = c->len[d] / (double)c->ncell[d];
+    g->inv_delta[d] = 1.0 / g->delta[d];
+    g->planet_c[d] = c->planet_center[d] / g->delta[d];
+  }
+  g->dt = c->dt;
+  g->c = c->c;
+  g->planet_r2 = c->planet_radius * c->planet_radius;
+  g->has_planet = c->planet_radius > 0;
+  g->slab_lo = c->slab_lo;
+  g->slab_hi = c->slab_hi;
+  g->G = c->ghost;
+  g->multi_rank = c->nranks > 1;
+  const int64_t G = c->ghost;
+  g->f_lo[0] = c->slab_lo - G; g->f_lo[1] = -G; g->f_lo[2] = -G;
+  g->f_n[0] = c->slab_hi - c->slab_lo + 1 + 2 * G;
+  g->f_n[1] = c->ncell[1] + 1 + 2 * G;
+  g->f_n[2] = c->ncell[2] + 1 + 2 * G;
+  g->m_lo[0] = c->slab_lo - G; g->m_lo[1] = 0; g->m_lo[2] = 0;
+  g->m_n[0] = c->slab_hi - c->slab_lo + 1 + 2 * G;
+  g->m_n[1] = c->ncell[1] + 1;
+  g->m_n[2] = c->ncell[2] + 1;
+  g->m_plane = g->m_n[0] * g->m_n[1] * g->m_n[2];
+  g->k_n[0] = c->slab_hi - c->slab_lo;
+  g->k_n[1] = c->ncell[1];
+  g->k_n[2] = c->ncell[2];
+}
+
+// Workspace plan; if base != nullptr, assigns pointers into ctx.
+int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cub_bytes) {
+  Layout L;
+  int64_t cap_max = 0;
+  for (int s = 0; s < c->n_species; ++s) cap_max = std::max<int64_t>(cap_max, c->capacity[s]);
+  cap_max = std::max<int64_t>(cap_max, 1);
+  const int64_t mig_cap = std::max<int64_t>(cap_max / 4, 4096);
+  for (int s = 0; s < c->n_species; ++s) {
+    // every per-particle array has cap_max slots: the sort and the compaction
+    // rotate arrays through the shared scratch array (R20: order is free)
+    const int64_t cap = cap_max;
+    int64_t o[7];
+    for (int k = 0; k < 7; ++k) o[k] = L.take(8 * cap);
+    int64_t oid = L.take(8 * cap);
+    int64_t okey = L.take(4 * cap), okey2 = L.take(4 * cap), oidx = L.take(4 * cap), oidx2 = L.take(4 * cap);
+    int64_t omom = L.take(8 * 10 * g.m_plane);
+    if (base) {
+      SpeciesStore &sp = ctx->sp[s];
+      for (int k = 0; k < 7; ++k) sp.a[k] = (double *)(base + o[k]);
+      sp.id = (int64_t *)(base + oid);
+      sp.key = (uint32_t *)(base + okey);
+      sp.key_alt = (uint32_t *)(base + okey2);
+      sp.idx = (uint32_t *)(base + oidx);
+      sp.idx_alt = (uint32_t *)(base + oidx2);
+      sp.mom = (double *)(base + omom);
+      sp.cap = c->capacity[s];
+      sp.qom = c->qom[s];
+      sp.n_iter = c->n_iter[s];
+    }
+  }
+  int64_t oscr = L.take(8 * cap_max);
+  int64_t field_elems = g.f_n[0] * g.f_n[1] * g.f_n[2] * 6;
+  int64_t ofield = L.take(8 * field_elems);
+  int64_t ostats = L.take(8 * ST_N);
+  int64_t ocounts = L.take(8 * 64);
+  const int64_t face = g.m_n[1] * g.m_n[2] * 10;
+  const int64_t ghost_elems = (int64_t)(c->ghost + 1) * face;
+  int64_t og[4];
+  const bool multi = c->nranks > 1;
+  for (int k = 0; k < 4; ++k) og[k] = L.take(multi ? 8 * ghost_elems : 8);
+  int64_t om[4];
+  for (int k = 0; k < 4; ++k) om[k] = L.take(multi || k < 2 ? 8 * 8 * mig_cap : 8);
+  const int64_t pack_elems = (g.k_n[0] + 1) * g.m_n[1] * g.m_n[2] * 10;
+  int64_t opack = L.take(8 * pack_elems);
+  int64_t ocub = L.take((int64_t)cub_bytes);
+  if (base) {
+    ctx->scratch = (double *)(base + oscr);
+    ctx->field = (double *)(base + ofield);
+    ctx->field_elems = field_elems;
+    ctx->stats = (unsigned long long *)(base + ostats);
+    ctx->dev_counts = (int64_t *)(base + ocounts);
+    ctx->ghost_send[0] = (double *)(base + og[0]);
+    ctx->ghost_send[1] = (double *)(base + og[1]);
+    ctx->ghost_recv[0] = (double *)(base + og[2]);
+    ctx->ghost_recv[1] = (double *)(base + og[3]);
+    ctx->ghost_elems = ghost_elems;
+    ctx->mig_send[0] = (double *)(base + om[0]);
+    ctx->mig_send[1] = (double *)(base + om[1]);
+    ctx->mig_recv[0] = (double *)(base + om[2]);
+    ctx->mig_recv[1] = (double *)(base + om[3]);
+    ctx->mig_cap = mig_cap;
+    ctx->pack = (double *)(base + opack);
+    ctx->cub_temp = base + ocub;
+    ctx->cub_bytes = cub_bytes;
+    ctx->cap_max = cap_max;
+  }
+  return L.total + ALIGN;
+}
+
+inline Ctx *C(pic_ctx *p) { return reinterpret_cast<Ctx *>(p); }
+inline const Ctx *C(const pic_ctx *p) { return reinterpret_cast<const Ctx *>(p); }
+
+pic_status check_species(Ctx *ctx, int32_t s, bool allow_all) {
+  if (allow_all && s == -1) return PIC_OK;
+  if (s < 0 || s >= ctx->cfg.n_species) return fail(ctx, PIC_EINVAL, "species index out of range");
+  return PIC_OK;
+}
+
+bool use_tiled(const Ctx *ctx) {
+  return ctx->cfg.kernel == PIC_KERNEL_TILED || ctx->cfg.kernel == PIC_KERNEL_AUTO;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pic_abi_version(void) { return PIC_ABI_VERSION; }
+
+pic_status pic_nccl_id(void *out) {
+  if (!out) return PIC_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PIC_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == PIC_NCCL_ID_BYTES, "nccl id size");
+  memcpy(out, &id, sizeof(id));
+  return PIC_OK;
+}
+
+pic_status pic_workspace_bytes(const pic_config *cfg, int64_t *bytes) {
+  std::string why;
+  pic_status st = validate(cfg, &why);
+  if (st != PIC_OK) return st;
+  if (!bytes) return PIC_EINVAL;
+  Geom g;
+  make_geom(cfg, &g);
+  int64_t cap_max = 1;
+  for (int s = 0; s < cfg->n_species; ++s) cap_max = std::max<int64_t>(cap_max, cfg->capacity[s]);
+  *bytes = plan(cfg, g, nullptr, nullptr, sort_temp_bytes(cap_max));
+  return PIC_OK;
+}
+
+pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace, int64_t bytes,
+                    pic_ctx **out) {
+  if (!out) return PIC_EINVAL;
+  *out = nullptr;
+  std::string why;
+  pic_status st = validate(cfg, &why);
+  if (st != PIC_OK) return st;
+  if (!workspace || ((uintptr_t)workspace % ALIGN) != 0) return PIC_EINVAL;
+  Ctx *ctx = new (std::nothrow) Ctx();
+  if (!ctx) return PIC_ENOMEM;
+  ctx->cfg = *cfg;
+  make_geom(cfg, &ctx->geom);
+  int64_t cap_max = 1;
+  for (int s = 0; s < cfg->n_species; ++s) cap_max = std::max<int64_t>(cap_max, cfg->capacity[s]);
+  const size_t cub_bytes = sort_temp_bytes(cap_max);
+  const int64_t need = plan(cfg, ctx->geom, nullptr, nullptr, cub_bytes);
+  if (bytes < need) {
+    delete ctx;
+    return PIC_ENOMEM;
+  }
+  plan(cfg, ctx->geom, ctx, (char *)workspace, cub_bytes);
+  ctx->host_counts = new int64_t[16]();
+  cudaError_t e = cudaMemset(ctx->stats, 0, 8 * ST_N);
+  if (e != cudaSuccess) { delete[] ctx->host_counts; delete ctx; return PIC_ECUDA; }
+  e = cudaMemset(ctx->field, 0, 8 * ctx->field_elems);
+  if (e != cudaSuccess) { delete[] ctx->host_counts; delete ctx; return PIC_ECUDA; }
+  if (cfg->nranks > 1) {
+    if (!nccl_id) { delete[] ctx->host_counts; delete ctx; return PIC_EINVAL; }
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    ncclComm_t comm;
+    if (ncclCommInitRank(&comm, cfg->nranks, id, cfg->rank) != ncclSuccess) {
+      delete[] ctx->host_counts;
+      delete ctx;
+      return PIC_ENCCL;
+    }
+    ctx->nccl = comm;
+  }
+  for (int s = 0; s < cfg->n_species; ++s) {
+    if (zero_moments(ctx, s) != PIC_OK) { delete[] ctx->host_counts; delete ctx; return PIC_ECUDA; }
+  }
+  *out = reinterpret_cast<pic_ctx *>(ctx);
+  return PIC_OK;
+}
+
+pic_status pic_set_stream(pic_ctx *p, void *stream) {
+  if (!p) return PIC_EINVAL;
+  C(p)->stream = (cudaStream_t)stream;
+  return PIC_OK;
+}
+
+pic_status pic_set_particles(pic_ctx *p, int32_t s, int64_t n, const double *const xyzuvwq[7],
+                             const int64_t *id) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  if (n < 0) return fail(ctx, PIC_EINVAL, "n < 0");
+  if (n > ctx->sp[s].cap) return fail(ctx, PIC_ERANGE, "n exceeds capacity");
+  if (n > 0) {
+    if (!xyzuvwq) return fail(ctx, PIC_EINVAL, "null particle arrays");
+    for (int k = 0; k < 7; ++k)
+      if (!xyzuvwq[k]) return fail(ctx, PIC_EINVAL, "null particle array");
+  }
+  st = load_particles(ctx, s, n, xyzuvwq, id);
+  if (st != PIC_OK) return st;
+  ctx->sp[s].moved = ctx->sp[s].deposited = false;
+  return PIC_OK;
+}
+
+pic_status pic_count(pic_ctx *p, int32_t s, int64_t *n) {
+  if (!p || !n) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  *n = ctx->sp[s].n;
+  return PIC_OK;
+}
+
+pic_status pic_get_particles(pic_ctx *p, int32_t s, double *const xyzuvwq[7], int64_t *id) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  double *none[7] = {};
+  return unload_particles(ctx, s, xyzuvwq ? xyzuvwq : none, id);
+}
+
+pic_status pic_set_fields(pic_ctx *p, const double *EB) {
+  if (!p || !EB) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  PIC_CUDA(cudaMemcpyAsync(ctx->field, EB, 8 * ctx->field_elems, cudaMemcpyDefault, ctx->stream));
+  ctx->fields_set = true;
+  return PIC_OK;
+}
+
+pic_status pic_mover(pic_ctx *p, int32_t s) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, true);
+  if (st != PIC_OK) return st;
+  if (!ctx->fields_set) return fail(ctx, PIC_ESTATE, "pic_set_fields must precede pic_mover");
+  const int s0 = s < 0 ? 0 : s, s1 = s < 0 ? ctx->cfg.n_species : s + 1;
+  for (int k = s0; k < s1; ++k)
+    if (ctx->sp[k].moved) return fail(ctx, PIC_ESTATE, "pic_mover called twice without pic_exchange");
+  for (int k = s0; k < s1; ++k) {
+    SpeciesStore &sp = ctx->sp[k];
+    bool fused = false;
+    if (use_tiled(ctx)) {
+      st = launch_tiled_step(ctx, k, &fused);
+      if (st != PIC_OK) return st;
+    } else {
+      st = launch_mover_basic(ctx, k);
+      if (st != PIC_OK) return st;
+    }
+    sp.moved = true;
+    sp.deposited = false;
+    sp.fused_deposit = fused;
+  }
+  return PIC_OK;
+}
+
+pic_status pic_moments(pic_ctx *p, int32_t s) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, true);
+  if (st != PIC_OK) return st;
+  const int s0 = s < 0 ? 0 : s, s1 = s < 0 ? ctx->cfg.n_species : s + 1;
+  for (int k = s0; k < s1; ++k)
+    if (ctx->sp[k].deposited) return fail(ctx, PIC_ESTATE, "pic_moments called twice without pic_exchange");
+  for (int k = s0; k < s1; ++k) {
+    SpeciesStore &sp = ctx->sp[k];
+    if (!sp.fused_deposit) {
+      st = zero_moments(ctx, k);
+      if (st != PIC_OK) return st;
+      st = launch_moments_basic(ctx, k);
+      if (st != PIC_OK) return st;
+    }
+    sp.deposited = true;
+    sp.fused_deposit = false;
+  }
+  return PIC_OK;
+}
+
+pic_status pic_exchange(pic_ctx *p) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  for (int k = 0; k < ctx->cfg.n_species; ++k)
+    if (!ctx->sp[k].deposited) return fail(ctx, PIC_ESTATE, "pic_exchange before pic_moments of every species");
+  pic_status st = exchange(ctx);
+  if (st != PIC_OK) return st;
+  for (int k = 0; k < ctx->cfg.n_species; ++k) ctx->sp[k].moved = ctx->sp[k].deposited = false;
+  ctx->cycle++;
+  return PIC_OK;
+}
+
+pic_status pic_cycle(pic_ctx *p) {
+  pic_status st = pic_mover(p, -1);
+  if (st != PIC_OK) return st;
+  st = pic_moments(p, -1);
+  if (st != PIC_OK) return st;
+  return pic_exchange(p);
+}
+
+pic_status pic_moment_shape(const pic_ctx *p, int64_t out[3]) {
+  if (!p || !out) return PIC_EINVAL;
+  const Ctx *ctx = C(p);
+  const pic_config &c = ctx->cfg;
+  out[0] = c.slab_hi - c.slab_lo + ((c.bc[0] == PIC_BC_OPEN && c.slab_hi == c.ncell[0]) ? 1 : 0);
+  out[1] = c.ncell[1] + (c.bc[1] == PIC_BC_OPEN ? 1 : 0);
+  out[2] = c.ncell[2] + (c.bc[2] == PIC_BC_OPEN ? 1 : 0);
+  return PIC_OK;
+}
+
+pic_status pic_get_moments(pic_ctx *p, int32_t s, double *out) {
+  if (!p || !out) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  return pack_moments(ctx, s, out);
+}
+
+pic_status pic_sync(pic_ctx *p, int64_t stats[8]) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  unsigned long long h[ST_N];
+  PIC_CUDA(cudaMemcpy(h, ctx->stats, sizeof(h), cudaMemcpyDeviceToHost));
+  int64_t all[ST_N];
+  for (int k = 0; k < ST_N; ++k) all[k] = (int64_t)h[k] + ctx->hstat[k];
+  if (stats)
+    for (int k = 0; k < ST_N; ++k) stats[k] = all[k];
+  if (all[ST_NONFINITE]) return fail(ctx, PIC_ENONFINITE, "non-finite particle update");
+  if (all[ST_FAR] || all[ST_OVERFLOW] || all[ST_MULTIWRAP])
+    return fail(ctx, PIC_ERANGE, "particle beyond ghost reach, capacity overflow or multiple wrap");
+  return PIC_OK;
+}
+
+pic_status pic_launch_count(const pic_ctx *p, int64_t *n) {
+  if (!p || !n) return PIC_EINVAL;
+  *n = C(p)->launches;
+  return PIC_OK;
+}
+
+const char *pic_last_error(const pic_ctx *p) {
+  if (!p) return "null context";
+  return C(p)->err.c_str();
+}
+
+pic_status pic_destroy(pic_ctx *p) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
+  delete[] ctx->host_counts;
+  delete ctx;
+  return PIC_OK;
+}
+
+}  // extern "C"

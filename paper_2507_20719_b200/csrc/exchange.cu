@@ -1,0 +1,467 @@
+// exchange.cu — ghost-node moment sums, periodic folds, particle compaction and
+// slab migration (pic_exchange), plus particle / moment copy-in and copy-out.
+//
+// Paper mapping (Alg. 1 phase 2): "exiting particles are
+// transferred using MPI".  Here the sender deposits its leavers into ghost node
+// planes before migration; the ghost planes are then summed
+// into their owners with NCCL point-to-point over NVLink (ring-periodic along
+// x when x is periodic), and the leavers travel to the neighbouring slab.
+// The ghost-node sum itself is implied, not stated, by the paper (north_star).
+#include <nccl.h>
+
+#include "pic_internal.cuh"
+
+namespace pic {
+
+#define PIC_NCCL(call)                                                       \
+  do {                                                                       \
+    ncclResult_t r_ = (call);                                                \
+    if (r_ != ncclSuccess)                                                   \
+      return fail(ctx, PIC_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// ------------------------------------------------------------- moment folds --
+// Periodic y / z fold: plane N (the image of plane 0, R18) is added into 0.
+__global__ void fold_axis_kernel(double *mom, int64_t nx, int64_t ny, int64_t nz, int axis,
+                                 int64_t plane) {
+  // iterate over the 2D face (other two axes) x 10 components
+  int64_t nA = axis == 1 ? nx : nx;
+  int64_t nB = axis == 1 ? nz : ny;
+  int64_t total = nA * nB * 10;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = t % nA, b = (t / nA) % nB, m = t / (nA * nB);
+    int64_t src, dst;
+    if (axis == 1) {  // y: a = x, b = z
+      src = (b * ny + (ny - 1)) * nx + a;
+      dst = (b * ny + 0) * nx + a;
+    } else {          // z: a = x, b = y
+      src = ((nz - 1) * ny + b) * nx + a;
+      dst = (0 * ny + b) * nx + a;
+    }
+    mom[m * plane + dst] += mom[m * plane + src];
+    mom[m * plane + src] = 0.0;
+  }
+}
+
+// Copy (mode 0) or add (mode 1) `count` x-planes between a moment array and a
+// contiguous plane buffer [10][count][nz][ny] (x-plane major per component).
+__global__ void xplanes_kernel(double *mom, double *buf, int64_t x0, int64_t count, int64_t nx,
+                               int64_t ny, int64_t nz, int64_t plane, int mode, int to_buf) {
+  int64_t face = ny * nz;
+  int64_t total = face * count * 10;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t yz = t % face, xi = (t / face) % count, m = t / (face * count);
+    int64_t y = yz % ny, z = yz / ny;
+    int64_t node = (z * ny + y) * nx + (x0 + xi);
+    double *pm = mom + m * plane + node;
+    if (to_buf) {
+      buf[t] = *pm;
+    } else {
+      if (mode == 1) *pm += buf[t]; else *pm = buf[t];
+    }
+  }
+}
+
+// Local periodic fold along x (nranks == 1): ghost planes onto their images.
+__global__ void fold_x_local_kernel(double *mom, int64_t N, int G, int64_t nx, int64_t ny,
+                                    int64_t nz, int64_t plane) {
+  // array x-index a holds global node a - G; images: a-G in [N, N+G] -> (a-G-N),
+  // a-G in [-G, -1] -> a-G+N.
+  int64_t face = ny * nz;
+  int64_t nghost = 2 * G + 1;
+  int64_t total = face * 10;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t yz = t % face, m = t / face;
+    double *base = mom + m * plane + yz * nx;
+    for (int64_t k = 0; k < nghost; ++k) {
+      int64_t gidx = (k < G) ? (k - G) : (N + (k - G));  // global node of the ghost
+      int64_t a_src = gidx + G;
+      int64_t a_dst = ((gidx % N) + N) % N + G;
+      base[a_dst] += base[a_src];
+      base[a_src] = 0.0;
+    }
+  }
+}
+
+static unsigned grid_for(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+static pic_status fold_and_ghosts(Ctx *ctx) {
+  const Geom &g = ctx->geom;
+  const int64_t nx = g.m_n[0], ny = g.m_n[1], nz = g.m_n[2];
+  const int S = ctx->cfg.n_species;
+  for (int s = 0; s < S; ++s) {
+    double *mom = ctx->sp[s].mom;
+    if (g.periodic[1])
+      fold_axis_kernel<<<grid_for(nx * nz * 10), 256, 0, ctx->stream>>>(mom, nx, ny, nz, 1, g.m_plane); ++ctx->launches;
+    if (g.periodic[2])
+      fold_axis_kernel<<<grid_for(nx * ny * 10), 256, 0, ctx->stream>>>(mom, nx, ny, nz, 2, g.m_plane); ++ctx->launches;
+    if (ctx->cfg.nranks == 1 && g.periodic[0])
+      fold_x_local_kernel<<<grid_for(ny * nz * 10), 256, 0, ctx->stream>>>(
+          mom, g.ncell[0], g.G, nx, ny, nz, g.m_plane); ++ctx->launches;
+  }
+  PIC_CUDA(cudaGetLastError());
+  if (ctx->cfg.nranks == 1) return PIC_OK;
+
+  // multi-rank: ghost planes along x to the neighbours.
+  const int G = g.G;
+  const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
+  const bool per = g.periodic[0];
+  const int left = (r > 0) ? r - 1 : (per ? P - 1 : -1);
+  const int right = (r < P - 1) ? r + 1 : (per ? 0 : -1);
+  // array x-index of global node X is X - (slab_lo - G)
+  const int64_t nloc = g.slab_hi - g.slab_lo;
+  const int64_t a_right_ghost = G + nloc;   // planes [slab_hi, slab_hi+G] -> G+1 planes
+  const int64_t a_left_ghost = 0;           // planes [slab_lo-G, slab_lo-1] -> G planes
+  const int64_t face = ny * nz * 10;
+  const int64_t nR = (int64_t)(G + 1) * face, nL = (int64_t)G * face;
+  ncclComm_t comm = (ncclComm_t)ctx->nccl;
+  for (int s = 0; s < S; ++s) {
+    double *mom = ctx->sp[s].mom;
+    if (right >= 0)
+      xplanes_kernel<<<grid_for(nR), 256, 0, ctx->stream>>>(mom, ctx->ghost_send[1], a_right_ghost,
+                                                             G + 1, nx, ny, nz, g.m_plane, 0, 1); ++ctx->launches;
+    if (left >= 0)
+      xplanes_kernel<<<grid_for(nL), 256, 0, ctx->stream>>>(mom, ctx->ghost_send[0], a_left_ghost,
+                                                             G, nx, ny, nz, g.m_plane, 0, 1); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+    PIC_NCCL(ncclGroupStart());
+    if (right >= 0) PIC_NCCL(ncclSend(ctx->ghost_send[1], nR, ncclDouble, right, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclSend(ctx->ghost_send[0], nL, ncclDouble, left, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclRecv(ctx->ghost_recv[0], nR, ncclDouble, left, comm, ctx->stream));
+    if (right >= 0) PIC_NCCL(ncclRecv(ctx->ghost_recv[1], nL, ncclDouble, right, comm, ctx->stream));
+    PIC_NCCL(ncclGroupEnd());
+    // from the left neighbour: its planes [its slab_hi, +G] == my [slab_lo, slab_lo+G]
+    if (left >= 0)
+      xplanes_kernel<<<grid_for(nR), 256, 0, ctx->stream>>>(mom, ctx->ghost_recv[0], G, G + 1, nx,
+                                                             ny, nz, g.m_plane, 1, 0); ++ctx->launches;
+    // from the right neighbour: its planes [its slab_lo-G, -1] == my [slab_hi-G, slab_hi-1]
+    if (right >= 0)
+      xplanes_kernel<<<grid_for(nL), 256, 0, ctx->stream>>>(mom, ctx->ghost_recv[1], nloc, G, nx,
+                                                             ny, nz, g.m_plane, 1, 0); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+  }
+  return PIC_OK;
+}
+
+// ---------------------------------------------------------------- migration --
+// Classify by key: 0 stay, 1 left, 2 right, 3 dead; slot from warp-aggregated
+// atomics.  dst[p] = (category << 30) | slot.
+__global__ void classify_kernel(const uint32_t *__restrict__ key, int64_t n, uint32_t *__restrict__ dst,
+                                unsigned long long *__restrict__ counts) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t cat = 3;
+  if (p < n) {
+    uint32_t k = key[p];
+    cat = (k < KEY_FIRST_RESERVED) ? 0u : (k == KEY_LEFT ? 1u : (k == KEY_RIGHT ? 2u : 3u));
+  } else {
+    cat = 4;  // out of range
+  }
+#pragma unroll
+  for (uint32_t c = 0; c < 3; ++c) {
+    unsigned mask = __ballot_sync(0xffffffffu, cat == c);
+    if (!mask) continue;
+    unsigned long long base = 0;
+    int leader = __ffs(mask) - 1;
+    if ((int)lane == leader) base = atomicAdd(&counts[c], (unsigned long long)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (cat == c) {
+      unsigned rank = __popc(mask & ((1u << lane) - 1u));
+      dst[p] = (c << 30) | (uint32_t)(base + rank);
+    }
+  }
+  if (cat == 3) dst[p] = 3u << 30;
+}
+
+// Scatter one fp64 array: stays -> out, leavers -> send buffers (component k).
+__global__ void scatter_kernel(const double *__restrict__ src, const uint32_t *__restrict__ dst,
+                               int64_t n, double *__restrict__ out, double *__restrict__ sendL,
+                               double *__restrict__ sendR, int64_t mig_cap) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t d = dst[p];
+    uint32_t cat = d >> 30, slot = d & 0x3FFFFFFFu;
+    double v = src[p];
+    if (cat == 0) out[slot] = v;
+    else if (cat == 1) { if (slot < mig_cap) sendL[slot] = v; }
+    else if (cat == 2) { if (slot < mig_cap) sendR[slot] = v; }
+  }
+}
+
+// Key of an in-slab particle from its position (cell units).
+__device__ __forceinline__ uint32_t cell_key(const Geom &g, double x, double y, double z) {
+  int64_t cx = (int64_t)floor(x) - g.slab_lo, cy = (int64_t)floor(y), cz = (int64_t)floor(z);
+  return (uint32_t)((cz * g.k_n[1] + cy) * g.k_n[0] + cx);
+}
+
+// Append received particles (component arrays of the recv buffer) at `at`.
+struct Arr7 { double *a[7]; };
+
+__global__ void append_kernel(Geom g, Arr7 arrs, int64_t *__restrict__ id,
+                              uint32_t *__restrict__ key, const double *__restrict__ buf,
+                              int64_t cnt, int64_t mig_cap, int64_t at,
+                              unsigned long long *__restrict__ stats) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      v[k] = buf[k * mig_cap + i];
+      arrs.a[k][at + i] = v[k];
+    }
+    id[at + i] = __double_as_longlong(buf[7 * mig_cap + i]);
+    int64_t cx = (int64_t)floor(v[0]);
+    if (cx < g.slab_lo || cx >= g.slab_hi) {
+      atomicAdd(&stats[ST_FAR], 1ull);
+      key[at + i] = KEY_DEAD;
+    } else {
+      key[at + i] = cell_key(g, v[0], v[1], v[2]);
+    }
+  }
+}
+
+__global__ void add_stat_kernel(unsigned long long *stats, int which, const unsigned long long *src,
+                                int n_src) {
+  unsigned long long t = 0;
+  for (int i = 0; i < n_src; ++i) t += src[i];
+  stats[which] += t;
+}
+
+static pic_status migrate(Ctx *ctx) {
+  const Geom &g = ctx->geom;
+  const int S = ctx->cfg.n_species;
+  const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
+  const bool per = g.periodic[0];
+  const int left = (P > 1) ? ((r > 0) ? r - 1 : (per ? P - 1 : -1)) : -1;
+  const int right = (P > 1) ? ((r < P - 1) ? r + 1 : (per ? 0 : -1)) : -1;
+  ncclComm_t comm = (ncclComm_t)ctx->nccl;
+  unsigned long long *cnt = (unsigned long long *)ctx->dev_counts;  // [S][3]
+  PIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 3 * S, ctx->stream));
+  for (int s = 0; s < S; ++s) {
+    SpeciesStore &sp = ctx->sp[s];
+    if (sp.n == 0) continue;
+    classify_kernel<<<(unsigned)((sp.n + 255) / 256), 256, 0, ctx->stream>>>(sp.key, sp.n, sp.idx,
+                                                                            cnt + 3 * s); ++ctx->launches;
+  }
+  PIC_CUDA(cudaGetLastError());
+  unsigned long long hc[3 * PIC_MAX_SPECIES];
+  PIC_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(unsigned long long) * 3 * S, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int s = 0; s < S; ++s) {
+    if ((int64_t)hc[3 * s + 1] > ctx->mig_cap || (int64_t)hc[3 * s + 2] > ctx->mig_cap)
+      return fail(ctx, PIC_ERANGE, "migration buffer capacity exceeded");
+    if ((hc[3 * s + 1] && left < 0) || (hc[3 * s + 2] && right < 0))
+      return fail(ctx, PIC_ERANGE, "slab leaver with no neighbour");
+  }
+  for (int s = 0; s < S; ++s) {
+    SpeciesStore &sp = ctx->sp[s];
+    if (sp.n == 0 && P == 1) continue;
+    const int64_t n_stay = (int64_t)hc[3 * s], nl = (int64_t)hc[3 * s + 1], nr = (int64_t)hc[3 * s + 2];
+    // permute the 7 fp64 arrays + id through the scratch array
+    for (int k = 0; k < 8; ++k) {
+      double *src = (k < 7) ? sp.a[k] : (double *)sp.id;
+      if (sp.n)
+        scatter_kernel<<<grid_for(sp.n), 256, 0, ctx->stream>>>(
+            src, sp.idx, sp.n, ctx->scratch, ctx->mig_send[0] + k * ctx->mig_cap,
+            ctx->mig_send[1] + k * ctx->mig_cap, ctx->mig_cap); ++ctx->launches;
+      if (k < 7) { sp.a[k] = ctx->scratch; ctx->scratch = src; }
+      else { sp.id = (int64_t *)ctx->scratch; ctx->scratch = src; }
+    }
+    PIC_CUDA(cudaGetLastError());
+    int64_t nrecvL = 0, nrecvR = 0;
+    if (P > 1) {
+      // counts, then payloads (host knows the counts after a sync)
+      int64_t *hcounts = ctx->host_counts;  // [0] sendL [1] sendR [2] recvL [3] recvR
+      int64_t *dcounts = ctx->dev_counts + 3 * PIC_MAX_SPECIES;
+      hcounts[0] = nl; hcounts[1] = nr;
+      PIC_CUDA(cudaMemcpyAsync(dcounts, hcounts, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+      // per-peer order: send-right, send-left, recv-left, recv-right (matches for P == 2)
+      PIC_NCCL(ncclGroupStart());
+      if (right >= 0) PIC_NCCL(ncclSend(dcounts + 1, 1, ncclInt64, right, comm, ctx->stream));
+      if (left >= 0) PIC_NCCL(ncclSend(dcounts + 0, 1, ncclInt64, left, comm, ctx->stream));
+      if (left >= 0) PIC_NCCL(ncclRecv(dcounts + 3, 1, ncclInt64, left, comm, ctx->stream));
+      if (right >= 0) PIC_NCCL(ncclRecv(dcounts + 2, 1, ncclInt64, right, comm, ctx->stream));
+      PIC_NCCL(ncclGroupEnd());
+      // recv from left = what left sent to its right; dcounts[3]; from right -> dcounts[2]
+      PIC_CUDA(cudaMemcpyAsync(hcounts + 2, dcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+      nrecvR = (right >= 0) ? hcounts[2] : 0;
+      nrecvL = (left >= 0) ? hcounts[3] : 0;
+      if (nrecvL > ctx->mig_cap || nrecvR > ctx->mig_cap)
+        return fail(ctx, PIC_ERANGE, "migration receive capacity exceeded");
+      if (n_stay + nrecvL + nrecvR > sp.cap)
+        return fail(ctx, PIC_ERANGE, "particle capacity exceeded after migration");
+      PIC_NCCL(ncclGroupStart());
+      for (int k = 0; k < 8; ++k) {
+        if (right >= 0 && nr) PIC_NCCL(ncclSend(ctx->mig_send[1] + k * ctx->mig_cap, nr, ncclDouble, right, comm, ctx->stream));
+        if (left >= 0 && nl) PIC_NCCL(ncclSend(ctx->mig_send[0] + k * ctx->mig_cap, nl, ncclDouble, left, comm, ctx->stream));
+        if (left >= 0 && nrecvL) PIC_NCCL(ncclRecv(ctx->mig_recv[0] + k * ctx->mig_cap, nrecvL, ncclDouble, left, comm, ctx->stream));
+        if (right >= 0 && nrecvR) PIC_NCCL(ncclRecv(ctx->mig_recv[1] + k * ctx->mig_cap, nrecvR, ncclDouble, right, comm, ctx->stream));
+      }
+      PIC_NCCL(ncclGroupEnd());
+      Arr7 arrs;
+      for (int k = 0; k < 7; ++k) arrs.a[k] = sp.a[k];
+      if (nrecvL)
+        append_kernel<<<grid_for(nrecvL), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key, ctx->mig_recv[0],
+                                                                  nrecvL, ctx->mig_cap, n_stay, ctx->stats); ++ctx->launches;
+      if (nrecvR)
+        append_kernel<<<grid_for(nrecvR), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key, ctx->mig_recv[1],
+                                                                  nrecvR, ctx->mig_cap, n_stay + nrecvL, ctx->stats); ++ctx->launches;
+      PIC_CUDA(cudaGetLastError());
+    }
+    sp.n = n_stay + nrecvL + nrecvR;
+    sp.sorted = false;
+    ctx->hstat[ST_SENT] += nl + nr;
+    ctx->hstat[ST_RECEIVED] += nrecvL + nrecvR;
+  }
+  return PIC_OK;
+}
+
+__global__ void keys_from_positions_kernel(Geom g, const double *__restrict__ X,
+                                           const double *__restrict__ Y, const double *__restrict__ Z,
+                                           uint32_t *__restrict__ key, int64_t n, int64_t from,
+                                           unsigned long long *__restrict__ stats) {
+  for (int64_t p = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    double x = X[p], y = Y[p], z = Z[p];
+    int64_t cx = (int64_t)floor(x), cy = (int64_t)floor(y), cz = (int64_t)floor(z);
+    if (!(cx >= g.slab_lo && cx < g.slab_hi && cy >= 0 && cy < g.ncell[1] && cz >= 0 &&
+          cz < g.ncell[2])) {
+      atomicAdd(&stats[ST_FAR], 1ull);
+      key[p] = KEY_DEAD;
+    } else {
+      key[p] = cell_key(g, x, y, z);
+    }
+  }
+}
+
+pic_status recompute_keys(Ctx *ctx, int s, int64_t from) {
+  SpeciesStore &sp = ctx->sp[s];
+  if (sp.n <= from) return PIC_OK;
+  keys_from_positions_kernel<<<grid_for(sp.n - from), 256, 0, ctx->stream>>>(
+      ctx->geom, sp.a[0], sp.a[1], sp.a[2], sp.key, sp.n, from, ctx->stats); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  return PIC_OK;
+}
+
+static bool needs_compaction(const Ctx *ctx) {
+  if (ctx->cfg.nranks > 1) return true;
+  if (ctx->geom.has_planet) return true;
+  for (int d = 0; d < 3; ++d)
+    if (!ctx->geom.periodic[d]) return true;
+  return false;
+}
+
+pic_status exchange(Ctx *ctx) {
+  pic_status st = fold_and_ghosts(ctx);
+  if (st != PIC_OK) return st;
+  if (needs_compaction(ctx)) {
+    st = migrate(ctx);
+    if (st != PIC_OK) return st;
+    for (int s = 0; s < ctx->cfg.n_species; ++s) {
+      st = recompute_keys(ctx, s, 0);
+      if (st != PIC_OK) return st;
+    }
+  }
+  return PIC_OK;
+}
+
+pic_status zero_moments(Ctx *ctx, int s) {
+  PIC_CUDA(cudaMemsetAsync(ctx->sp[s].mom, 0, sizeof(double) * 10 * ctx->geom.m_plane, ctx->stream));
+  return PIC_OK;
+}
+
+// ------------------------------------------------------------- copy in / out --
+__global__ void pack_moments_kernel(const double *__restrict__ mom, double *__restrict__ out,
+                                    int64_t ox, int64_t nx, int64_t ny, int64_t nz, int64_t mnx,
+                                    int64_t mny, int64_t plane, double invV) {
+  int64_t total = nx * ny * nz * 10;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = t % nx, y = (t / nx) % ny, z = (t / (nx * ny)) % nz, m = t / (nx * ny * nz);
+    out[t] = mom[m * plane + (z * mny + y) * mnx + (ox + x)] * invV;
+  }
+}
+
+pic_status pack_moments(Ctx *ctx, int s, double *out) {
+  const Geom &g = ctx->geom;
+  int64_t shape[3];
+  pic_moment_shape((const pic_ctx *)ctx, shape);
+  const double invV = 1.0 / (g.delta[0] * g.delta[1] * g.delta[2]);
+  const int64_t total = shape[0] * shape[1] * shape[2] * 10;
+  pack_moments_kernel<<<grid_for(total), 256, 0, ctx->stream>>>(
+      ctx->sp[s].mom, ctx->pack, g.G, shape[0], shape[1], shape[2], g.m_n[0], g.m_n[1], g.m_plane, invV); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  PIC_CUDA(cudaMemcpyAsync(out, ctx->pack, sizeof(double) * total, cudaMemcpyDefault, ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PIC_OK;
+}
+
+__global__ void scale_kernel(double *a, int64_t n, double f) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    a[p] = a[p] * f;
+}
+__global__ void divide_kernel(double *a, int64_t n, double d) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    a[p] = a[p] / d;
+}
+__global__ void iota_kernel(int64_t *a, int64_t n) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    a[p] = p;
+}
+
+pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id) {
+  SpeciesStore &sp = ctx->sp[s];
+  for (int k = 0; k < 7; ++k) {
+    if (n) PIC_CUDA(cudaMemcpyAsync(sp.a[k], src[k], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
+    if (k < 3 && n)
+      divide_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.a[k], n, ctx->geom.delta[k]); ++ctx->launches;
+  }
+  if (id) {
+    if (n) PIC_CUDA(cudaMemcpyAsync(sp.id, id, sizeof(int64_t) * n, cudaMemcpyDefault, ctx->stream));
+  } else if (n) {
+    iota_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.id, n); ++ctx->launches;
+  }
+  PIC_CUDA(cudaGetLastError());
+  sp.n = n;
+  sp.sorted = false;
+  pic_status st = recompute_keys(ctx, s, 0);
+  if (st != PIC_OK) return st;
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));  // caller buffers may be pageable
+  return PIC_OK;
+}
+
+pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id) {
+  SpeciesStore &sp = ctx->sp[s];
+  const int64_t n = sp.n;
+  for (int k = 0; k < 7; ++k) {
+    if (!dst[k] || !n) continue;
+    if (k < 3) {
+      PIC_CUDA(cudaMemcpyAsync(ctx->scratch, sp.a[k], sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      scale_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->scratch, n, ctx->geom.delta[k]); ++ctx->launches;
+      PIC_CUDA(cudaGetLastError());
+      PIC_CUDA(cudaMemcpyAsync(dst[k], ctx->scratch, sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
+      PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+      PIC_CUDA(cudaMemcpyAsync(dst[k], sp.a[k], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
+    }
+  }
+  if (id && n) PIC_CUDA(cudaMemcpyAsync(id, sp.id, sizeof(int64_t) * n, cudaMemcpyDefault, ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PIC_OK;
+}
+
+}  // namespace pic

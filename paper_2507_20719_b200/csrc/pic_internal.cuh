@@ -1,0 +1,151 @@
+// pic_internal.cuh — context, store layout and shared device helpers of libpic.
+//
+// Internal representation:
+//   * particle store, per species, SoA fp64: xi_x, xi_y, xi_z (positions in
+//     GLOBAL CELL UNITS, xi_d = x_d / Delta_d), u, v, w (velocity, caller
+//     units), q (charge q_s w_p, R14); int64 id.  One spare fp64 array
+//     (`scratch`) lets the sort / compaction permute one array at a time.
+//   * key (uint32 per particle), written by the mover: the local cell index of
+//     x^{n+1} for live particles that stay, or one of the reserved tail keys
+//     KEY_LEFT / KEY_RIGHT (slab leavers) / KEY_DEAD (removed, R21).
+//   * field window: node-interleaved [kz][ky][kx][6] fp64, exactly the layout
+//     of pic_set_fields (global nodes [slab_lo-G, slab_hi+G] x [-G, Ny+G] x
+//     [-G, Nz+G]).
+//   * moments, per species: 10 x [nzm][nym][nxm] fp64 raw sums
+//     sum_p q {1, v, vv} S (the 1/V of R13 is applied when copying out);
+//     x planes [slab_lo-G, slab_hi+G], y planes [0, Ny], z planes [0, Nz]
+//     (the extra periodic plane is folded by pic_exchange, R18).
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <cuda_runtime.h>
+#include "pic.h"
+
+namespace pic {
+
+constexpr uint32_t KEY_DEAD = 0xFFFFFFFFu;
+constexpr uint32_t KEY_RIGHT = 0xFFFFFFFEu;
+constexpr uint32_t KEY_LEFT = 0xFFFFFFFDu;
+constexpr uint32_t KEY_FIRST_RESERVED = 0xFFFFFFFDu;
+
+// device counters (stats of pic_sync)
+enum Stat {
+  ST_REMOVED = 0, ST_SENT = 1, ST_RECEIVED = 2, ST_FAR = 3, ST_CLAMPED = 4,
+  ST_NONFINITE = 5, ST_OVERFLOW = 6, ST_MULTIWRAP = 7, ST_N = 8
+};
+
+// Geometry passed by value to kernels.
+struct Geom {
+  int64_t ncell[3];       // global cells
+  int32_t periodic[3];
+  double delta[3];        // cell size
+  double inv_delta[3];
+  double dt, c;
+  double planet_c[3];     // planet centre in CELL units
+  double planet_r2;       // radius^2 in physical units (compared in physical units)
+  int32_t has_planet;
+  int64_t slab_lo, slab_hi;
+  int32_t G;
+  int32_t multi_rank;     // nranks > 1 (slab leavers migrate)
+  // field window
+  int64_t f_lo[3];        // global node index of window element 0
+  int64_t f_n[3];         // window nodes per axis
+  // moments
+  int64_t m_lo[3];        // global node index of element 0 of the ghosted arrays
+  int64_t m_n[3];         // ghosted node counts (x, y, z)
+  int64_t m_plane;        // m_n[0]*m_n[1]*m_n[2] (stride between components)
+  // local cell box used for the sort key
+  int64_t k_n[3];         // local cells (slab_hi-slab_lo, Ny, Nz)
+};
+
+struct SpeciesStore {
+  double *a[7] = {};      // xi_x xi_y xi_z u v w q
+  int64_t *id = nullptr;
+  uint32_t *key = nullptr;
+  uint32_t *key_alt = nullptr;
+  uint32_t *idx = nullptr;
+  uint32_t *idx_alt = nullptr;
+  double *mom = nullptr;  // [10][m_plane]
+  int64_t n = 0;          // live particles (host mirror, exact after exchange)
+  int64_t cap = 0;
+  double qom = 0;
+  int32_t n_iter = 3;
+  bool moved = false, deposited = false, fused_deposit = false;
+  bool sorted = false;
+};
+
+struct Ctx {
+  pic_config cfg;
+  Geom geom;
+  cudaStream_t stream = nullptr;
+  SpeciesStore sp[PIC_MAX_SPECIES];
+  double *scratch = nullptr;         // cap_max doubles
+  double *field = nullptr;           // window
+  int64_t field_elems = 0;
+  bool fields_set = false;
+  unsigned long long *stats = nullptr;  // ST_N device counters
+  int64_t *dev_counts = nullptr;     // small device scratch for counts
+  int64_t *host_counts = nullptr;    // pinned? (plain host)
+  // exchange buffers
+  double *ghost_send[2] = {};        // [0] to left, [1] to right
+  double *ghost_recv[2] = {};
+  int64_t ghost_elems = 0;           // per buffer
+  double *mig_send[2] = {};          // [8][mig_cap] per side (7 fp64 + id as fp64 bits)
+  double *mig_recv[2] = {};
+  int64_t mig_cap = 0;
+  double *pack = nullptr;            // moment copy-out staging
+  void *cub_temp = nullptr;
+  size_t cub_bytes = 0;
+  void *nccl = nullptr;              // ncclComm_t
+  int64_t hstat[8] = {};             // host-side counters (sent / received)
+  int64_t launches = 0;              // libpic kernel launches (pic_launch_count)
+  int64_t cycle = 0;
+  int64_t cap_max = 0;
+  std::string err;
+};
+
+// ------------------------------------------------------------ error helpers --
+#define PIC_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) {                                                  \
+      return ::pic::fail(ctx, PIC_ECUDA, std::string(#call) + ": " +          \
+                                             cudaGetErrorString(e_));         \
+    }                                                                         \
+  } while (0)
+
+inline pic_status fail(Ctx *ctx, pic_status s, const std::string &m) {
+  if (ctx) ctx->err = m;
+  return s;
+}
+
+// -------------------------------------------------------------- launchers ----
+// (implemented in the .cu files; all enqueue on ctx->stream)
+pic_status launch_mover_basic(Ctx *ctx, int s);
+pic_status launch_moments_basic(Ctx *ctx, int s);
+pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit);
+pic_status sort_species(Ctx *ctx, int s);
+size_t sort_temp_bytes(int64_t cap);
+pic_status exchange(Ctx *ctx);
+pic_status recompute_keys(Ctx *ctx, int s, int64_t from);
+pic_status zero_moments(Ctx *ctx, int s);
+pic_status pack_moments(Ctx *ctx, int s, double *out);
+pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
+pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id);
+
+// ---------------------------------------------------------- device helpers ---
+// Periodic wrap of a cell-unit coordinate (R10): one wrap, then test.
+__device__ __forceinline__ double wrap_cells(double xi, double n, bool *multi) {
+  if (xi >= n) {
+    xi = xi - n;
+  } else if (xi < 0.0) {
+    xi = xi + n;
+    if (xi == n) xi = 0.0;
+  }
+  if (!(xi >= 0.0 && xi < n)) *multi = true;
+  return xi;
+}
+
+}  // namespace pic

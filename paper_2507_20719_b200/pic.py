@@ -1,0 +1,238 @@
+"""Thin ctypes binding of libpic (include/pic.h).  Argument marshalling only:
+every step of the particle path runs in the CUDA kernels of libpic.so.
+
+The functions keep the C names (pic_init, pic_mover, pic_moments, pic_exchange,
+...).  `Context` is a convenience owner of one pic_ctx plus its torch-allocated
+device workspace.  PyTorch supplies device memory, the stream and (for
+multi-GPU) the process group that broadcasts the NCCL id; nothing else.
+
+If libpic.so is missing or no CUDA device is present this module raises: there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, Optional, Sequence
+
+import torch
+
+from . import inputs as _inputs  # noqa: F401  (re-export convenience for callers)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpic.so")
+
+PIC_MAX_SPECIES = 8
+PIC_NCCL_ID_BYTES = 128
+PIC_OK, PIC_EINVAL, PIC_ECUDA, PIC_ENCCL, PIC_ENOMEM, PIC_ESTATE, PIC_ERANGE, PIC_ENONFINITE = range(8)
+STATUS_NAMES = ["PIC_OK", "PIC_EINVAL", "PIC_ECUDA", "PIC_ENCCL", "PIC_ENOMEM", "PIC_ESTATE",
+                "PIC_ERANGE", "PIC_ENONFINITE"]
+KERNEL_AUTO, KERNEL_BASIC, KERNEL_TILED = 0, 1, 2
+STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "overflow", "multiwrap"]
+EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
+           "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
+           "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
+           "pic_sync", "pic_launch_count", "pic_last_error", "pic_destroy"]
+
+
+class pic_config(C.Structure):
+    _fields_ = [
+        ("ncell", C.c_int64 * 3), ("len", C.c_double * 3), ("bc", C.c_int32 * 3),
+        ("dt", C.c_double), ("c", C.c_double), ("n_species", C.c_int32),
+        ("qom", C.c_double * PIC_MAX_SPECIES), ("n_iter", C.c_int32 * PIC_MAX_SPECIES),
+        ("capacity", C.c_int64 * PIC_MAX_SPECIES),
+        ("planet_center", C.c_double * 3), ("planet_radius", C.c_double),
+        ("rank", C.c_int32), ("nranks", C.c_int32), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64),
+        ("ghost", C.c_int32), ("sort_every", C.c_int32), ("kernel", C.c_int32),
+    ]
+
+
+class PicError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libpic.so; raise if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"libpic.so not built at {path}: run __graft_entry__.build()")
+        lib = C.CDLL(path)
+        P = C.POINTER
+        vp = C.c_void_p
+        lib.pic_abi_version.restype = C.c_int32
+        lib.pic_nccl_id.argtypes = [vp]
+        lib.pic_workspace_bytes.argtypes = [P(pic_config), P(C.c_int64)]
+        lib.pic_init.argtypes = [P(pic_config), vp, vp, C.c_int64, P(vp)]
+        lib.pic_set_stream.argtypes = [vp, vp]
+        lib.pic_set_particles.argtypes = [vp, C.c_int32, C.c_int64, P(vp), vp]
+        lib.pic_count.argtypes = [vp, C.c_int32, P(C.c_int64)]
+        lib.pic_get_particles.argtypes = [vp, C.c_int32, P(vp), vp]
+        lib.pic_set_fields.argtypes = [vp, vp]
+        lib.pic_mover.argtypes = [vp, C.c_int32]
+        lib.pic_moments.argtypes = [vp, C.c_int32]
+        lib.pic_exchange.argtypes = [vp]
+        lib.pic_cycle.argtypes = [vp]
+        lib.pic_moment_shape.argtypes = [vp, P(C.c_int64)]
+        lib.pic_get_moments.argtypes = [vp, C.c_int32, vp]
+        lib.pic_sync.argtypes = [vp, P(C.c_int64)]
+        lib.pic_launch_count.argtypes = [vp, P(C.c_int64)]
+        lib.pic_last_error.argtypes = [vp]
+        lib.pic_last_error.restype = C.c_char_p
+        lib.pic_destroy.argtypes = [vp]
+        for name in EXPORTS:
+            if name not in ("pic_abi_version", "pic_last_error"):
+                getattr(lib, name).restype = C.c_int
+        _lib = lib
+    return _lib
+
+
+def _check(st, ctx=None, what=""):
+    if st != PIC_OK:
+        msg = what
+        if ctx:
+            msg += ": " + load_library().pic_last_error(ctx).decode()
+        raise PicError(st, msg)
+
+
+# ------------------------------------------------------------ C-name layer --
+def pic_nccl_id() -> bytes:
+    buf = (C.c_uint8 * PIC_NCCL_ID_BYTES)()
+    _check(load_library().pic_nccl_id(C.cast(buf, C.c_void_p)), what="pic_nccl_id")
+    return bytes(buf)
+
+
+def pic_workspace_bytes(cfg: pic_config) -> int:
+    out = C.c_int64()
+    _check(load_library().pic_workspace_bytes(C.byref(cfg), C.byref(out)), what="pic_workspace_bytes")
+    return out.value
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, sort_every=0, kernel=KERNEL_AUTO,
+                n_iter=None) -> pic_config:
+    """pic_config from an inputs.Workload (marshalling only)."""
+    cfg = pic_config()
+    lo, hi = w.slab_or_all()
+    for d in range(3):
+        cfg.ncell[d] = w.ncell[d]
+        cfg.len[d] = w.length[d]
+        cfg.bc[d] = w.bc[d]
+        cfg.planet_center[d] = w.planet_center[d]
+    cfg.dt, cfg.c, cfg.planet_radius = w.dt, w.c, w.planet_radius
+    cfg.n_species = len(w.species)
+    for s, sp in enumerate(w.species):
+        cfg.qom[s] = sp.qom
+        cfg.n_iter[s] = n_iter if n_iter is not None else w.n_iter
+        cfg.capacity[s] = capacity[s] if capacity is not None else 0
+    cfg.rank, cfg.nranks, cfg.slab_lo, cfg.slab_hi = rank, nranks, lo, hi
+    cfg.ghost, cfg.sort_every, cfg.kernel = ghost, sort_every, kernel
+    return cfg
+
+
+class Context:
+    """One pic_ctx + its workspace tensor on the current CUDA device."""
+
+    def __init__(self, cfg: pic_config, nccl_id: Optional[bytes] = None, stream=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libpic needs a CUDA device (there is no CPU path)")
+        self.lib = load_library()
+        self.cfg = cfg
+        nbytes = pic_workspace_bytes(cfg)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        h = C.c_void_p()
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (C.c_uint8 * PIC_NCCL_ID_BYTES).from_buffer_copy(nccl_id)
+        st = self.lib.pic_init(C.byref(cfg), C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                               C.c_void_p(self.workspace.data_ptr()), nbytes, C.byref(h))
+        _check(st, what="pic_init")
+        self.h = h
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        _check(self.lib.pic_set_stream(self.h, C.c_void_p(self.stream.cuda_stream)), self.h, "pic_set_stream")
+
+    # -- particles
+    def set_particles(self, s: int, parts: Dict[str, torch.Tensor]):
+        arrs = [parts[k] for k in "xyzuvwq"]
+        n = arrs[0].numel()
+        for a in arrs:
+            assert a.dtype == torch.float64 and a.is_contiguous() and a.numel() == n
+        P7 = (C.c_void_p * 7)(*[a.data_ptr() for a in arrs])
+        idt = parts.get("id")
+        if idt is not None:
+            assert idt.dtype == torch.int64 and idt.is_contiguous() and idt.numel() == n
+        _check(self.lib.pic_set_particles(self.h, s, n, P7, _ptr(idt)), self.h, "pic_set_particles")
+
+    def count(self, s: int) -> int:
+        out = C.c_int64()
+        _check(self.lib.pic_count(self.h, s, C.byref(out)), self.h, "pic_count")
+        return out.value
+
+    def get_particles(self, s: int, device="cuda") -> Dict[str, torch.Tensor]:
+        n = self.count(s)
+        out = {k: torch.empty(n, dtype=torch.float64, device=device) for k in "xyzuvwq"}
+        out["id"] = torch.empty(n, dtype=torch.int64, device=device)
+        P7 = (C.c_void_p * 7)(*[out[k].data_ptr() for k in "xyzuvwq"])
+        _check(self.lib.pic_get_particles(self.h, s, P7, _ptr(out["id"])), self.h, "pic_get_particles")
+        return out
+
+    # -- fields / steps
+    def set_fields(self, EB: torch.Tensor):
+        assert EB.dtype == torch.float64 and EB.is_contiguous()
+        _check(self.lib.pic_set_fields(self.h, _ptr(EB)), self.h, "pic_set_fields")
+
+    def mover(self, s: int = -1):
+        _check(self.lib.pic_mover(self.h, s), self.h, "pic_mover")
+
+    def moments(self, s: int = -1):
+        _check(self.lib.pic_moments(self.h, s), self.h, "pic_moments")
+
+    def exchange(self):
+        _check(self.lib.pic_exchange(self.h), self.h, "pic_exchange")
+
+    def cycle(self):
+        _check(self.lib.pic_cycle(self.h), self.h, "pic_cycle")
+
+    def moment_shape(self):
+        out = (C.c_int64 * 3)()
+        _check(self.lib.pic_moment_shape(self.h, out), self.h, "pic_moment_shape")
+        return tuple(out)
+
+    def get_moments(self, s: int, out: Optional[torch.Tensor] = None, device="cuda") -> torch.Tensor:
+        nx, ny, nz = self.moment_shape()
+        if out is None:
+            out = torch.empty((10, nz, ny, nx), dtype=torch.float64, device=device)
+        _check(self.lib.pic_get_moments(self.h, s, _ptr(out)), self.h, "pic_get_moments")
+        return out
+
+    def sync(self, raise_on_error: bool = True) -> Dict[str, int]:
+        st_arr = (C.c_int64 * 8)()
+        st = self.lib.pic_sync(self.h, st_arr)
+        stats = dict(zip(STAT_NAMES, list(st_arr)))
+        if raise_on_error:
+            _check(st, self.h, f"pic_sync {stats}")
+        return stats
+
+    def launch_count(self) -> int:
+        out = C.c_int64()
+        _check(self.lib.pic_launch_count(self.h, C.byref(out)), self.h, "pic_launch_count")
+        return out.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.pic_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,161 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Same seeded inputs on both sides (paper_2507_20719_b200.inputs), compared by
+particle id with the north_star tolerances (tests/parity_util.py).  Sizes are
+small enough for the oracle to finish in seconds while spanning many cells and
+tiles, with ragged particle counts.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2507_20719_b200 import inputs as I
+from paper_2507_20719_b200 import pic
+import parity_util as PU
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(w, parts, cycles, kernel, ghost=2, sort_every=0, n_iter=None):
+    cap = [int(p["x"].numel() * 1.25) + 64 for p in parts]
+    cfg = pic.make_config(w, capacity=cap, ghost=ghost, sort_every=sort_every, kernel=kernel, n_iter=n_iter)
+    ctx = pic.Context(cfg)
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+    lo, EB = I.field_window(w, ghost, device="cpu")
+    ctx.set_fields(EB.cuda())
+    for _ in range(cycles):
+        ctx.cycle()
+    stats = ctx.sync()
+    out = []
+    for s in range(len(parts)):
+        gp = {k: v.cpu().numpy() for k, v in ctx.get_particles(s).items()}
+        gm = ctx.get_moments(s).cpu().numpy()
+        out.append((gp, gm))
+    ctx.close()
+    return out, stats
+
+
+def check(w, cycles, kernel, ghost=2, sort_every=0, n_iter=None):
+    parts = I.make_species(w, device="cpu")
+    orc = PU.run_oracle(w, parts, cycles, ghost=ghost, n_iter=n_iter)
+    gpu, stats = run_gpu(w, parts, cycles, kernel, ghost, sort_every, n_iter)
+    reports = []
+    for s, sp in enumerate(w.species):
+        rep = {"species": sp.name}
+        ok_p = PU.compare_particles(w, sp, gpu[s][0], orc[s][0], orc[s][1], rep)
+        ok_m = PU.compare_moments(gpu[s][1], orc[s][2], orc[s][3], rep)
+        reports.append(rep)
+        assert ok_p and ok_m, rep
+    return reports, stats
+
+
+KERNELS = [pic.KERNEL_BASIC, pic.KERNEL_TILED]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c1_uniform(kernel):
+    reps, stats = check(I.c1(), 5, kernel, sort_every=1)
+    assert stats["removed"] == 0 and stats["far"] == 0
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c1r_random_fields(kernel):
+    check(I.c1(randomized=True), 5, kernel, sort_every=2)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c2_harris_scaled(kernel):
+    # C2 structure at 1/8 size in x and reduced ppc (oracle in seconds)
+    w = I.c2(nx_per_rank=16, ppc=27)
+    check(w, 3, kernel, sort_every=1)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c4_open_dipole_scaled(kernel):
+    w = I.c4(ncell=(32, 16, 16), ppc=8)
+    reps, stats = check(w, 4, kernel, sort_every=1)
+    assert stats["removed"] > 0
+
+
+@pytest.mark.parametrize("n_iter", [1, 2, 5])
+def test_n_iter_variants(n_iter):
+    check(I.c1(randomized=True), 2, pic.KERNEL_TILED, n_iter=n_iter)
+
+
+def test_ragged_and_empty_species():
+    w = I.c1(randomized=True)
+    parts = I.make_species(w, device="cpu")
+    # ragged: drop a random subset of species 0, empty species 1
+    g = torch.Generator().manual_seed(5)
+    keep = torch.rand(parts[0]["x"].numel(), generator=g) < 0.37
+    parts[0] = {k: v[keep].contiguous() for k, v in parts[0].items()}
+    parts[1] = {k: v[:0].contiguous() for k, v in parts[1].items()}
+    orc = PU.run_oracle(w, parts, 3)
+    gpu, _ = run_gpu(w, parts, 3, pic.KERNEL_TILED, sort_every=1)
+    rep = {}
+    assert PU.compare_particles(w, w.species[0], gpu[0][0], orc[0][0], orc[0][1], rep), rep
+    assert PU.compare_moments(gpu[0][1], orc[0][2], orc[0][3], rep), rep
+    assert gpu[1][0]["x"].size == 0 and not gpu[1][1].any()
+
+
+def test_closed_form_gyration_on_gpu():
+    """P2 on the GPU path directly: |v| conserved and the rotation angle per step."""
+    import math
+    w = I.c1()
+    w.field_params = {"E": (0.0, 0.0, 0.0), "B": (0.0, 0.0, 0.01)}
+    parts = I.make_species(w, device="cpu")
+    gpu, _ = run_gpu(w, parts, 1, pic.KERNEL_TILED, sort_every=1)
+    for s, sp in enumerate(w.species):
+        gp = gpu[s][0]
+        order = np.argsort(gp["id"])
+        p0 = {k: v.numpy() for k, v in parts[s].items()}
+        o0 = np.argsort(p0["id"])
+        v0 = np.stack([p0["u"][o0], p0["v"][o0]], 1)
+        v1 = np.stack([gp["u"][order], gp["v"][order]], 1)
+        th = 2 * math.atan(abs(sp.qom) * 0.01 * w.dt / 2)
+        ang = np.arctan2(v0[:, 0] * v1[:, 1] - v0[:, 1] * v1[:, 0], (v0 * v1).sum(1))
+        assert np.allclose(ang, -math.copysign(th, sp.qom), atol=1e-9)
+        assert np.allclose(np.linalg.norm(v1, axis=1), np.linalg.norm(v0, axis=1), rtol=1e-13)
+
+
+def test_call_order_errors():
+    w = I.c1()
+    parts = I.make_species(w, device="cpu")
+    cfg = pic.make_config(w, capacity=[p["x"].numel() for p in parts])
+    ctx = pic.Context(cfg)
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+    with pytest.raises(pic.PicError) as e:
+        ctx.mover()            # fields not set
+    assert e.value.status == pic.PIC_ESTATE
+    lo, EB = I.field_window(w, 2)
+    ctx.set_fields(EB.cuda())
+    with pytest.raises(pic.PicError) as e:
+        ctx.exchange()         # before moments
+    assert e.value.status == pic.PIC_ESTATE
+    ctx.mover()
+    with pytest.raises(pic.PicError) as e:
+        ctx.mover()            # twice
+    assert e.value.status == pic.PIC_ESTATE
+    ctx.moments()
+    ctx.exchange()
+    ctx.sync()
+    ctx.close()
+
+
+def test_nonfinite_flag():
+    w = I.c1()
+    parts = I.make_species(w, device="cpu")
+    cfg = pic.make_config(w, capacity=[p["x"].numel() for p in parts])
+    ctx = pic.Context(cfg)
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+    lo, EB = I.field_window(w, 2)
+    EB[3, 3, 3, 0] = float("nan")
+    ctx.set_fields(EB.cuda())
+    ctx.cycle()
+    with pytest.raises(pic.PicError) as e:
+        ctx.sync()
+    assert e.value.status == pic.PIC_ENONFINITE
+    ctx.close()
