@@ -50,8 +50,9 @@ pic_status validate(const pic_config *c, std::string *why) {
   if (c->nranks > 1 && c->slab_hi - c->slab_lo < c->ghost + 1) {
     *why = "slab narrower than ghost + 1 cells"; return PIC_EINVAL;
   }
-  const int64_t cells = (c->slab_hi - c->slab_lo) * c->ncell[1] * c->ncell[2];
-  if (cells >= (int64_t)KEY_FIRST_RESERVED) { *why = "too many local cells for 32-bit keys"; return PIC_EINVAL; }
+  const int64_t tcells = ((c->slab_hi - c->slab_lo + TILE - 1) / TILE) * ((c->ncell[1] + TILE - 1) / TILE) *
+                         ((c->ncell[2] + TILE - 1) / TILE) * TILE3;
+  if (tcells >= (int64_t)KEY_FIRST_RESERVED) { *why = "too many local cells for 32-bit keys"; return PIC_EINVAL; }
   if (c->planet_radius < 0) { *why = "planet_radius < 0"; return PIC_EINVAL; }
   if (c->sort_every < 0) { *why = "sort_every < 0"; return PIC_EINVAL; }
   if (c->kernel < 0 || c->kernel > 2) { *why = "bad kernel"; return PIC_EINVAL; }
@@ -88,6 +89,8 @@ void make_geom(const pic_config *c, Geom *g) {
   g->k_n[0] = c->slab_hi - c->slab_lo;
   g->k_n[1] = c->ncell[1];
   g->k_n[2] = c->ncell[2];
+  for (int d = 0; d < 3; ++d) g->nt[d] = (g->k_n[d] + TILE - 1) / TILE;
+  g->ntiles = g->nt[0] * g->nt[1] * g->nt[2];
 }
 
 // Workspace plan; if base != nullptr, assigns pointers into ctx.
@@ -106,12 +109,14 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
     int64_t oid = L.take(8 * cap);
     int64_t okey = L.take(4 * cap), okey2 = L.take(4 * cap), oidx = L.take(4 * cap), oidx2 = L.take(4 * cap);
     int64_t omom = L.take(8 * 10 * g.m_plane);
+    int64_t otile = L.take(4 * (g.ntiles + 1));
     if (base) {
+      ctx->sp[s].tile_start = (uint32_t *)(base + otile);
       SpeciesStore &sp = ctx->sp[s];
       for (int k = 0; k < 7; ++k) sp.a[k] = (double *)(base + o[k]);
       sp.id = (int64_t *)(base + oid);
       sp.key = (uint32_t *)(base + okey);
-      sp.key_alt = (uint32_t *)(base + okey2);
+      sp.key_new = (uint32_t *)(base + okey2);
       sp.idx = (uint32_t *)(base + oidx);
       sp.idx_alt = (uint32_t *)(base + oidx2);
       sp.mom = (double *)(base + omom);

@@ -199,7 +199,7 @@ __global__ void scatter_kernel(const double *__restrict__ src, const uint32_t *_
 // Key of an in-slab particle from its position (cell units).
 __device__ __forceinline__ uint32_t cell_key(const Geom &g, double x, double y, double z) {
   int64_t cx = (int64_t)floor(x) - g.slab_lo, cy = (int64_t)floor(y), cz = (int64_t)floor(z);
-  return (uint32_t)((cz * g.k_n[1] + cy) * g.k_n[0] + cx);
+  return tile_key(g, cx, cy, cz);
 }
 
 // Append received particles (component arrays of the recv buffer) at `at`.
@@ -248,7 +248,7 @@ static pic_status migrate(Ctx *ctx) {
   for (int s = 0; s < S; ++s) {
     SpeciesStore &sp = ctx->sp[s];
     if (sp.n == 0) continue;
-    classify_kernel<<<(unsigned)((sp.n + 255) / 256), 256, 0, ctx->stream>>>(sp.key, sp.n, sp.idx,
+    classify_kernel<<<(unsigned)((sp.n + 255) / 256), 256, 0, ctx->stream>>>(sp.key_new, sp.n, sp.idx,
                                                                             cnt + 3 * s); ++ctx->launches;
   }
   PIC_CUDA(cudaGetLastError());
@@ -312,10 +312,10 @@ static pic_status migrate(Ctx *ctx) {
       Arr7 arrs;
       for (int k = 0; k < 7; ++k) arrs.a[k] = sp.a[k];
       if (nrecvL)
-        append_kernel<<<grid_for(nrecvL), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key, ctx->mig_recv[0],
+        append_kernel<<<grid_for(nrecvL), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0],
                                                                   nrecvL, ctx->mig_cap, n_stay, ctx->stats); ++ctx->launches;
       if (nrecvR)
-        append_kernel<<<grid_for(nrecvR), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key, ctx->mig_recv[1],
+        append_kernel<<<grid_for(nrecvR), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1],
                                                                   nrecvR, ctx->mig_cap, n_stay + nrecvL, ctx->stats); ++ctx->launches;
       PIC_CUDA(cudaGetLastError());
     }
@@ -349,7 +349,7 @@ pic_status recompute_keys(Ctx *ctx, int s, int64_t from) {
   SpeciesStore &sp = ctx->sp[s];
   if (sp.n <= from) return PIC_OK;
   keys_from_positions_kernel<<<grid_for(sp.n - from), 256, 0, ctx->stream>>>(
-      ctx->geom, sp.a[0], sp.a[1], sp.a[2], sp.key, sp.n, from, ctx->stats); ++ctx->launches;
+      ctx->geom, sp.a[0], sp.a[1], sp.a[2], sp.key_new, sp.n, from, ctx->stats); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }

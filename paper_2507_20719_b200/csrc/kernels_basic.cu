@@ -15,41 +15,10 @@
 
 namespace pic {
 
-// Trilinear sample of the 6 field components at a cell-unit position
-// (R11 clamp to the window, R12 weights).  Returns true if clamped.
-__device__ __forceinline__ bool sample_window(const Geom &g, const double *__restrict__ F,
-                                              const double xb[3], double out[6]) {
-  int64_t idx[3];
-  double f[3];
-  bool clamped = false;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    double u = xb[d] - (double)g.f_lo[d];
-    double top = (double)(g.f_n[d] - 1);
-    if (!(u >= 0.0)) { u = 0.0; clamped = true; }
-    if (u > top) { u = top; clamped = true; }
-    double fl = floor(u);
-    if (fl > top - 1.0) fl = top - 1.0;
-    idx[d] = (int64_t)fl;
-    f[d] = u - fl;
-  }
-#pragma unroll
-  for (int m = 0; m < 6; ++m) out[m] = 0.0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
-    double S = (bx ? f[0] : 1.0 - f[0]) * (by ? f[1] : 1.0 - f[1]) * (bz ? f[2] : 1.0 - f[2]);
-    const double *node = F + 6 * (((idx[2] + bz) * g.f_n[1] + (idx[1] + by)) * g.f_n[0] + (idx[0] + bx));
-#pragma unroll
-    for (int m = 0; m < 6; ++m) out[m] = fma(S, __ldg(node + m), out[m]);
-  }
-  return clamped;
-}
-
 __global__ void __launch_bounds__(256) mover_basic_kernel(
     Geom g, double *__restrict__ X, double *__restrict__ Y, double *__restrict__ Z,
     double *__restrict__ U, double *__restrict__ V, double *__restrict__ W,
-    uint32_t *__restrict__ key, const double *__restrict__ F, int64_t n, double ks,
+    uint32_t *__restrict__ key_new, const double *__restrict__ F, int64_t n, double ks,
     double ks_c, int n_iter, unsigned long long *__restrict__ stats) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -83,53 +52,10 @@ __global__ void __launch_bounds__(256) mover_basic_kernel(
     xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
     vnew[d] = fma(2.0, vb[d], -vn[d]);
   }
-  // boundary conditions (R10, R11, R21) and destination key
-  const int64_t cx_pre = (int64_t)floor(xnew[0]);
-  bool dead = false, multi = false;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double N = (double)g.ncell[d];
-    if (g.periodic[d]) {
-      xnew[d] = wrap_cells(xnew[d], N, &multi);
-    } else if (!(xnew[d] >= 0.0 && xnew[d] < N)) {
-      dead = true;
-    }
-  }
-  if (!dead && g.has_planet) {
-    double r2 = 0.0;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double dx = (xnew[d] - g.planet_c[d]) * g.delta[d];
-      r2 += dx * dx;
-    }
-    if (r2 < g.planet_r2) dead = true;
-  }
-  const bool finite = isfinite(vnew[0]) && isfinite(vnew[1]) && isfinite(vnew[2]) &&
-                      isfinite(xnew[0]) && isfinite(xnew[1]) && isfinite(xnew[2]);
-  uint32_t k;
-  if (!finite) {
-    atomicAdd(&stats[ST_NONFINITE], 1ull);
-    k = KEY_DEAD;
-  } else if (multi) {
-    atomicAdd(&stats[ST_MULTIWRAP], 1ull);
-    k = KEY_DEAD;
-  } else if (dead) {
-    atomicAdd(&stats[ST_REMOVED], 1ull);
-    k = KEY_DEAD;
-  } else if (g.multi_rank && cx_pre < g.slab_lo) {
-    k = KEY_LEFT;
-    if (cx_pre < g.slab_lo - g.G) atomicAdd(&stats[ST_FAR], 1ull);
-  } else if (g.multi_rank && cx_pre >= g.slab_hi) {
-    k = KEY_RIGHT;
-    if (cx_pre > g.slab_hi + g.G - 1) atomicAdd(&stats[ST_FAR], 1ull);
-  } else {
-    const int64_t cx = (int64_t)xnew[0], cy = (int64_t)xnew[1], cz = (int64_t)xnew[2];
-    k = (uint32_t)((cz * g.k_n[1] + cy) * g.k_n[0] + (cx - g.slab_lo));
-  }
-  if (clamped) atomicAdd(&stats[ST_CLAMPED], 1ull);
+  const uint32_t k = finish_particle(g, xnew, vnew, clamped, stats);
   X[p] = xnew[0]; Y[p] = xnew[1]; Z[p] = xnew[2];
   U[p] = vnew[0]; V[p] = vnew[1]; W[p] = vnew[2];
-  key[p] = k;
+  key_new[p] = k;
 }
 
 __global__ void __launch_bounds__(256) moments_basic_kernel(
@@ -181,7 +107,7 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   const int threads = 256;
   const int64_t blocks = (S.n + threads - 1) / threads;
   mover_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
-      ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.key, ctx->field, S.n, ks,
+      ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.key_new, ctx->field, S.n, ks,
       ks_c, S.n_iter, ctx->stats); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
@@ -193,7 +119,7 @@ pic_status launch_moments_basic(Ctx *ctx, int s) {
   const int threads = 256;
   const int64_t blocks = (S.n + threads - 1) / threads;
   moments_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
-      ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.a[6], S.key, S.n, S.mom,
+      ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.a[6], S.key_new, S.n, S.mom,
       ctx->stats); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;

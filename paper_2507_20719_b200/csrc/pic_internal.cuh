@@ -58,15 +58,30 @@ struct Geom {
   int64_t m_plane;        // m_n[0]*m_n[1]*m_n[2] (stride between components)
   // local cell box used for the sort key
   int64_t k_n[3];         // local cells (slab_hi-slab_lo, Ny, Nz)
+  int64_t nt[3];          // tiles per axis (ceil(k_n / TILE))
+  int64_t ntiles;
 };
+
+// Cell tiles of TILE^3 cells: the sort key is tile-major,
+//   key = tile * TILE^3 + (lx % T) + T (ly % T) + T^2 (lz % T),
+//   tile = tx + nt_x (ty + nt_y tz),  t_d = l_d / T,
+// with l = local cell (x relative to slab_lo).
+constexpr int TILE = 4;
+constexpr int TILE3 = TILE * TILE * TILE;
+
+__host__ __device__ __forceinline__ uint32_t tile_key(const Geom &g, int64_t lx, int64_t ly, int64_t lz) {
+  const int64_t t = (lx / TILE) + g.nt[0] * ((ly / TILE) + g.nt[1] * (lz / TILE));
+  return (uint32_t)(t * TILE3 + (lx % TILE) + TILE * (ly % TILE) + TILE * TILE * (lz % TILE));
+}
 
 struct SpeciesStore {
   double *a[7] = {};      // xi_x xi_y xi_z u v w q
   int64_t *id = nullptr;
-  uint32_t *key = nullptr;
-  uint32_t *key_alt = nullptr;
+  uint32_t *key = nullptr;        // sort-time keys, in store order (valid while sorted)
+  uint32_t *key_new = nullptr;    // keys of the current positions (mover / recompute)
   uint32_t *idx = nullptr;
   uint32_t *idx_alt = nullptr;
+  uint32_t *tile_start = nullptr; // [ntiles + 1] segment starts of the sorted store
   double *mom = nullptr;  // [10][m_plane]
   int64_t n = 0;          // live particles (host mirror, exact after exchange)
   int64_t cap = 0;
@@ -101,6 +116,8 @@ struct Ctx {
   void *nccl = nullptr;              // ncclComm_t
   int64_t hstat[8] = {};             // host-side counters (sent / received)
   int64_t launches = 0;              // libpic kernel launches (pic_launch_count)
+  alignas(64) unsigned char tmap[128] = {};  // CUtensorMap of the field window (tiled.cu)
+  bool tmap_ok = false;
   int64_t cycle = 0;
   int64_t cap_max = 0;
   std::string err;
@@ -146,6 +163,100 @@ __device__ __forceinline__ double wrap_cells(double xi, double n, bool *multi) {
   }
   if (!(xi >= 0.0 && xi < n)) *multi = true;
   return xi;
+}
+
+// Trilinear sample of the 6 field components of the global window at a
+// cell-unit position (R11 clamp to the window, R12 weights).  Returns true if
+// the position was clamped.
+__device__ __forceinline__ bool sample_window(const Geom &g, const double *__restrict__ F,
+                                              const double xb[3], double out[6]) {
+  int64_t idx[3];
+  double f[3];
+  bool clamped = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double u = xb[d] - (double)g.f_lo[d];
+    double top = (double)(g.f_n[d] - 1);
+    if (!(u >= 0.0)) { u = 0.0; clamped = true; }
+    if (u > top) { u = top; clamped = true; }
+    double fl = floor(u);
+    if (fl > top - 1.0) fl = top - 1.0;
+    idx[d] = (int64_t)fl;
+    f[d] = u - fl;
+  }
+#pragma unroll
+  for (int m = 0; m < 6; ++m) out[m] = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
+    double S = (bx ? f[0] : 1.0 - f[0]) * (by ? f[1] : 1.0 - f[1]) * (bz ? f[2] : 1.0 - f[2]);
+    const double *node = F + 6 * (((idx[2] + bz) * g.f_n[1] + (idx[1] + by)) * g.f_n[0] + (idx[0] + bx));
+#pragma unroll
+    for (int m = 0; m < 6; ++m) out[m] = fma(S, __ldg(node + m), out[m]);
+  }
+  return clamped;
+}
+
+// Boundary conditions (R10, R11, R21) of a pushed particle and its destination
+// key.  xnew: in = pre-wrap position (cell units), out = post-wrap position.
+__device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3], const double vnew[3],
+                                                   bool clamped, unsigned long long *__restrict__ stats) {
+  const int64_t cx_pre = (int64_t)floor(xnew[0]);
+  bool dead = false, multi = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double N = (double)g.ncell[d];
+    if (g.periodic[d]) {
+      xnew[d] = wrap_cells(xnew[d], N, &multi);
+    } else if (!(xnew[d] >= 0.0 && xnew[d] < N)) {
+      dead = true;
+    }
+  }
+  if (!dead && g.has_planet) {
+    double r2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double dx = (xnew[d] - g.planet_c[d]) * g.delta[d];
+      r2 += dx * dx;
+    }
+    if (r2 < g.planet_r2) dead = true;
+  }
+  const bool finite = isfinite(vnew[0]) && isfinite(vnew[1]) && isfinite(vnew[2]) &&
+                      isfinite(xnew[0]) && isfinite(xnew[1]) && isfinite(xnew[2]);
+  uint32_t k;
+  if (!finite) {
+    atomicAdd(&stats[ST_NONFINITE], 1ull);
+    k = KEY_DEAD;
+  } else if (multi) {
+    atomicAdd(&stats[ST_MULTIWRAP], 1ull);
+    k = KEY_DEAD;
+  } else if (dead) {
+    atomicAdd(&stats[ST_REMOVED], 1ull);
+    k = KEY_DEAD;
+  } else if (g.multi_rank && cx_pre < g.slab_lo) {
+    k = KEY_LEFT;
+    if (cx_pre < g.slab_lo - g.G) atomicAdd(&stats[ST_FAR], 1ull);
+  } else if (g.multi_rank && cx_pre >= g.slab_hi) {
+    k = KEY_RIGHT;
+    if (cx_pre > g.slab_hi + g.G - 1) atomicAdd(&stats[ST_FAR], 1ull);
+  } else {
+    const int64_t cx = (int64_t)xnew[0], cy = (int64_t)xnew[1], cz = (int64_t)xnew[2];
+    k = tile_key(g, cx - g.slab_lo, cy, cz);
+  }
+  if (clamped) atomicAdd(&stats[ST_CLAMPED], 1ull);
+  return k;
+}
+
+// Map a global node index to the ghosted moment array (x: ghost planes; y, z:
+// planes [0, N] with periodic images of -1 / N+1 wrapped).  -1 if outside.
+__device__ __forceinline__ int64_t moment_node(const Geom &g, int64_t gx, int64_t gy, int64_t gz) {
+  const int64_t ax = gx - g.m_lo[0];
+  if (ax < 0 || ax >= g.m_n[0]) return -1;
+  const int64_t Ny = g.ncell[1], Nz = g.ncell[2];
+  if (g.periodic[1]) { if (gy < 0) gy += Ny; else if (gy > Ny) gy -= Ny; }
+  if (g.periodic[2]) { if (gz < 0) gz += Nz; else if (gz > Nz) gz -= Nz; }
+  if (gy < 0 || gy > Ny || gz < 0 || gz > Nz) return -1;
+  return (gz * g.m_n[1] + gy) * g.m_n[0] + ax;
 }
 
 }  // namespace pic

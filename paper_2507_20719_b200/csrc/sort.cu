@@ -1,10 +1,12 @@
-// sort.cu — cell sort of the particle store (not a step of
-// the paper, which sorts only for coalescence).
+// sort.cu — tile-major cell sort of the particle store (not
+// a step of the paper, which sorts only for coalescence).
 //
-// key = local cell index of the current position (written by the mover or by
-// recompute_keys); CUB onesweep radix sort of (key, index) over the used key
-// bits; then each of the 8 per-particle arrays is gathered through the single
-// scratch array (8 B/particle of extra memory instead of a second store).
+// key_new = tile-major cell key of the current position (pic_internal.cuh
+// tile_key; written by the mover or recompute_keys).  CUB onesweep radix sort
+// of (key_new, index) -> (key, idx) over the used key bits; each of the 8
+// per-particle arrays is then gathered through the single scratch array (8 B
+// per particle of extra memory instead of a second store); finally the tile
+// segment starts tile_start[t] = lower_bound(key, t * TILE^3).
 #include <cub/device/device_radix_sort.cuh>
 
 #include "pic_internal.cuh"
@@ -21,7 +23,21 @@ __global__ void gather_kernel(const double *__restrict__ src, const uint32_t *__
                               double *__restrict__ dst, int64_t n) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x)
-    dst[p] = src[idx[p]];
+    dst[p] = src[__ldg(idx + p)];
+}
+
+__global__ void tile_start_kernel(const uint32_t *__restrict__ key, int64_t n, int64_t ntiles,
+                                  uint32_t *__restrict__ start) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t target = (uint64_t)t * TILE3;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((uint64_t)key[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    start[t] = (uint32_t)lo;
+  }
 }
 
 size_t sort_temp_bytes(int64_t cap) {
@@ -40,25 +56,28 @@ static unsigned grid_for(int64_t n) {
 pic_status sort_species(Ctx *ctx, int s) {
   SpeciesStore &sp = ctx->sp[s];
   const int64_t n = sp.n;
-  if (n < 2) { sp.sorted = true; return PIC_OK; }
-  int end_bit = 1;
-  const int64_t cells = ctx->geom.k_n[0] * ctx->geom.k_n[1] * ctx->geom.k_n[2];
-  while (end_bit < 32 && (int64_t(1) << end_bit) < cells + 1) ++end_bit;
-  // reserved tail keys (0xFFFFFFFx) need all 32 bits; they only occur between
-  // the mover and the exchange, when the sort is not called.
-  iota_u32_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.idx_alt, n); ++ctx->launches;
-  size_t bytes = ctx->cub_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(ctx->cub_temp, bytes, sp.key, sp.key_alt, sp.idx_alt,
-                                                  sp.idx, (int)n, 0, end_bit, ctx->stream);
-  if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
-  std::swap(sp.key, sp.key_alt);
-  for (int k = 0; k < 8; ++k) {
-    double *src = (k < 7) ? sp.a[k] : (double *)sp.id;
-    gather_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(src, sp.idx, ctx->scratch, n); ++ctx->launches;
-    if (k < 7) sp.a[k] = ctx->scratch;
-    else sp.id = (int64_t *)ctx->scratch;
-    ctx->scratch = src;
+  const int64_t ntiles = ctx->geom.ntiles;
+  if (n >= 2) {
+    int end_bit = 1;
+    while (end_bit < 32 && (int64_t(1) << end_bit) < ntiles * TILE3) ++end_bit;
+    // reserved tail keys (0xFFFFFFFD..F) only exist between the mover and the
+    // exchange; the exchange recomputes the keys of every live particle.
+    iota_u32_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.idx_alt, n); ++ctx->launches;
+    size_t bytes = ctx->cub_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(ctx->cub_temp, bytes, sp.key_new, sp.key, sp.idx_alt,
+                                                    sp.idx, (int)n, 0, end_bit, ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+    for (int k = 0; k < 8; ++k) {
+      double *src = (k < 7) ? sp.a[k] : (double *)sp.id;
+      gather_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(src, sp.idx, ctx->scratch, n); ++ctx->launches;
+      if (k < 7) sp.a[k] = ctx->scratch;
+      else sp.id = (int64_t *)ctx->scratch;
+      ctx->scratch = src;
+    }
+  } else if (n == 1) {
+    PIC_CUDA(cudaMemcpyAsync(sp.key, sp.key_new, 4, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  tile_start_kernel<<<grid_for(ntiles + 1), 256, 0, ctx->stream>>>(sp.key, n, ntiles, sp.tile_start); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   sp.sorted = true;
   return PIC_OK;

@@ -1,19 +1,430 @@
-// tiled.cu — PIC_KERNEL_TILED dispatch: cell sort cadence, then the mover.
-// (The fused tile-staged mover + deposit kernel lands here; until then the
-// tiled family sorts and runs the basic kernels.)
+// tiled.cu — PIC_KERNEL_TILED: cell-sorted, tile-staged, fused mover + deposit.
+//
+// One CTA per tile of TILE^3 cells (the store is sorted tile-major, sort.cu):
+//
+//  1. TMA (cp.async.bulk.tensor.4d, mbarrier) stages the E,B nodes of the tile
+//     plus a one-cell halo, 7^3 nodes x 48 B, from the field window into shared
+//     memory; the CTA pre-scales them by k_s = (q/m) dt/2 and k_s / c so the
+//     mover reads E' = k_s E and a = k_s B / c directly (Eq. 2, R7, R8).
+//  2. Warps split the tile's particle range evenly.  Rounds of 32 consecutive
+//     particles (lane = particle, coalesced SoA loads): n_iter predictor-
+//     corrector iterations of Eq. 2 (R1, R2) with trilinear gathers from shared
+//     memory (R12), then x^{n+1}, v^{n+1}, boundary conditions and the new
+//     sort key (R10, R11, R21).
+//  3. The deposit of the new state (Eq. 3, R13-R18) is fused: each lane turns
+//     its particle into 8 corner weights (hat functions relative to the
+//     particle's sort-time cell c0) and 10 values q{1, v, vv}, written to a
+//     per-warp shared buffer; the warp then re-reads them as 8 corners x 4
+//     particle slots, so each lane accumulates 10 register sums for one corner
+//     node of c0 (no atomics inside a cell).  At every change of c0 the four
+//     slots are reduced with shuffles and added to the tile's shared node
+//     accumulators (7^3 nodes x 10).  Particles that crossed into another cell
+//     deposit their remaining corners ("spills") with shared atomics.
+//  4. The tile's shared accumulators are added to the global ghosted moment
+//     arrays with fp64 atomics (tile faces are shared with neighbour tiles).
+//
+// Sample points or deposit nodes outside the staged 7^3 box fall back to the
+// global field window / global atomics (counted in stats only when beyond the
+// rank's ghost reach).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "pic_internal.cuh"
 
 namespace pic {
+
+constexpr int NB = TILE + 3;            // staged nodes per axis: -1 .. TILE+1
+constexpr int NB3 = NB * NB * NB;       // 343
+constexpr int WARPS = 8;
+constexpr int THREADS = 32 * WARPS;
+constexpr int SGRP = 36;                // doubles per 4-particle group in the S buffer (32 + pad)
+constexpr int WBUF = 8 * SGRP + 32 * 10;  // doubles per warp: S[8][36] + V[32][10]
+constexpr size_t SMEM_BYTES = sizeof(double) * (NB3 * 6 + 10 * NB3 + WARPS * WBUF) + 16;
+
+struct TiledArgs {
+  Geom g;
+  double *X, *Y, *Z, *U, *V, *W;
+  const double *Q;
+  const uint32_t *key;        // sort-time keys (store order)
+  uint32_t *key_new;
+  const uint32_t *tile_start;
+  const double *field;        // global window (fallback sampling)
+  double *mom;                // ghosted moment arrays [10][m_plane]
+  unsigned long long *stats;
+  double ks, ks_c;
+  int n_iter;
+};
+
+// ------------------------------------------------------------- PTX helpers --
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Trilinear gather of the pre-scaled fields from the staged box.  u = position
+// in box node units.  Returns false if the 8 nodes are not all in the box.
+__device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, const double u[3], double out[6]) {
+  double fl[3], f[3];
+  int i[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    fl[d] = floor(u[d]);
+    f[d] = u[d] - fl[d];
+    i[d] = (int)fl[d];
+  }
+  if (!(fl[0] >= 0.0 && fl[0] <= NB - 2 && fl[1] >= 0.0 && fl[1] <= NB - 2 && fl[2] >= 0.0 && fl[2] <= NB - 2))
+    return false;
+  const double gx0 = 1.0 - f[0], gy0 = 1.0 - f[1], gz0 = 1.0 - f[2];
+  const double w00 = gy0 * gz0, w10 = f[1] * gz0, w01 = gy0 * f[2], w11 = f[1] * f[2];
+  const double S[8] = {gx0 * w00, f[0] * w00, gx0 * w10, f[0] * w10,
+                       gx0 * w01, f[0] * w01, gx0 * w11, f[0] * w11};
+#pragma unroll
+  for (int m = 0; m < 6; ++m) out[m] = 0.0;
+  const int base = ((i[2] * NB + i[1]) * NB + i[0]) * 6;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int off = base + 6 * ((c & 1) + NB * ((c >> 1) & 1) + NB * NB * (c >> 2));
+    const double2 a = *reinterpret_cast<const double2 *>(fld + off);
+    const double2 b = *reinterpret_cast<const double2 *>(fld + off + 2);
+    const double2 e = *reinterpret_cast<const double2 *>(fld + off + 4);
+    out[0] = fma(S[c], a.x, out[0]);
+    out[1] = fma(S[c], a.y, out[1]);
+    out[2] = fma(S[c], b.x, out[2]);
+    out[3] = fma(S[c], b.y, out[3]);
+    out[4] = fma(S[c], e.x, out[4]);
+    out[5] = fma(S[c], e.y, out[5]);
+  }
+  return true;
+}
+
+// Add 10 contributions w*val of one node to the tile accumulators (node in box
+// coordinates) or, outside the box, to the global moment arrays.
+__device__ __forceinline__ void deposit_node(const TiledArgs &A, double *__restrict__ acc, int bx, int by, int bz,
+                                             int64_t gx, int64_t gy, int64_t gz, double w, const double val[10]) {
+  if (bx >= 0 && bx < NB && by >= 0 && by < NB && bz >= 0 && bz < NB) {
+    const int node = (bz * NB + by) * NB + bx;
+#pragma unroll
+    for (int m = 0; m < 10; ++m) atomicAdd(acc + m * NB3 + node, w * val[m]);
+  } else {
+    const int64_t node = moment_node(A.g, gx, gy, gz);
+    if (node < 0) {
+      atomicAdd(&A.stats[ST_FAR], 1ull);
+      return;
+    }
+#pragma unroll
+    for (int m = 0; m < 10; ++m) atomicAdd(A.mom + m * A.g.m_plane + node, w * val[m]);
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                           const TiledArgs A) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double *fld = reinterpret_cast<double *>(smem_raw);
+  double *acc = fld + NB3 * 6;
+  double *wbuf = acc + 10 * NB3;
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(wbuf + WARPS * WBUF);
+  const Geom &g = A.g;
+
+  const int tile = blockIdx.x;
+  const uint32_t p0 = A.tile_start[tile], p1 = A.tile_start[tile + 1];
+  if (p0 == p1) return;
+  const int tx = (int)(tile % g.nt[0]);
+  const int ty = (int)((tile / g.nt[0]) % g.nt[1]);
+  const int tz = (int)(tile / (g.nt[0] * g.nt[1]));
+  // global cell (== node) index of the tile origin; box node 0 is origin - 1
+  const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE, oz = (int64_t)tz * TILE;
+  const double bo[3] = {(double)(ox - 1), (double)(oy - 1), (double)(oz - 1)};
+  const int tid = threadIdx.x;
+
+  // ---- 1. stage fields with TMA, zero the accumulators meanwhile
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(mbar, NB3 * 6 * 8);
+    tma_load_4d(fld, &tmap, 0, (int)(ox - 1 - g.f_lo[0]), (int)(oy - 1 - g.f_lo[1]), (int)(oz - 1 - g.f_lo[2]),
+                mbar);
+  }
+  for (int i = tid; i < 10 * NB3; i += THREADS) acc[i] = 0.0;
+  mbar_wait(mbar, 0);
+  for (int i = tid; i < NB3 * 6; i += THREADS) fld[i] *= ((i % 6) < 3) ? A.ks : A.ks_c;
+  __syncthreads();
+
+  // ---- 2./3. warps over contiguous sub-ranges of the tile's particles
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t ntile = p1 - p0;
+  const uint32_t chunk = ((ntile + 32 * WARPS - 1) / (32 * WARPS)) * 32;
+  const uint32_t wbeg = p0 + warp * chunk;
+  const uint32_t wend = min(p1, wbeg + chunk);
+  double *Sb = wbuf + warp * WBUF;       // [8 groups][36]: S[k][j] at grp*36 + k*4 + j
+  double *Vb = Sb + 8 * SGRP;            // [32][10]
+  const int kc = lane & 7, js = lane >> 3;
+  const int kbx = kc & 1, kby = (kc >> 1) & 1, kbz = kc >> 2;
+  const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
+  double accr[10];
+#pragma unroll
+  for (int m = 0; m < 10; ++m) accr[m] = 0.0;
+  int cur = -1;  // local cell (0..63) of the register accumulators, warp-uniform
+
+  auto flush = [&](int c) {
+#pragma unroll
+    for (int m = 0; m < 10; ++m) {
+      accr[m] += __shfl_xor_sync(0xffffffffu, accr[m], 8);
+      accr[m] += __shfl_xor_sync(0xffffffffu, accr[m], 16);
+    }
+    const int cx = c & 3, cy = (c >> 2) & 3, cz = c >> 4;
+    const int node = ((cz + kbz + 1) * NB + (cy + kby + 1)) * NB + (cx + kbx + 1);
+#pragma unroll
+    for (int m = 0; m < 10; ++m) {
+      if ((m & 3) == js && accr[m] != 0.0) atomicAdd(acc + m * NB3 + node, accr[m]);
+      accr[m] = 0.0;
+    }
+  };
+
+  for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
+    const uint32_t p = r0 + lane;
+    const bool act = p < wend;
+    int c0 = 64;  // sentinel: no particle
+    double Sk[8], val[10];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) Sk[k] = 0.0;
+#pragma unroll
+    for (int m = 0; m < 10; ++m) val[m] = 0.0;
+    if (act) {
+      c0 = (int)(A.key[p] & (TILE3 - 1));
+      const double xn[3] = {A.X[p], A.Y[p], A.Z[p]};
+      const double vn[3] = {A.U[p], A.V[p], A.W[p]};
+      const double q = A.Q[p];
+      double xb[3] = {xn[0], xn[1], xn[2]};
+      double vb[3];
+      bool clamped = false;
+      for (int it = 0; it < A.n_iter; ++it) {
+        double EB[6];
+        const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
+        if (!gather_smem(fld, u, EB)) {
+          clamped |= sample_window(g, A.field, xb, EB);
+#pragma unroll
+          for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
+        }
+        // Eq. 2: vt = vn + k E ; a = k B / c ; vb = (vt + vt x a + (vt.a) a) / (1 + a.a)
+        const double vt0 = vn[0] + EB[0], vt1 = vn[1] + EB[1], vt2 = vn[2] + EB[2];
+        const double a0 = EB[3], a1 = EB[4], a2 = EB[5];
+        const double dot = fma(vt0, a0, fma(vt1, a1, vt2 * a2));
+        const double D = fma(a0, a0, fma(a1, a1, fma(a2, a2, 1.0)));
+        const double invD = 1.0 / D;
+        vb[0] = (fma(vt1, a2, fma(-vt2, a1, vt0)) + dot * a0) * invD;
+        vb[1] = (fma(vt2, a0, fma(-vt0, a2, vt1)) + dot * a1) * invD;
+        vb[2] = (fma(vt0, a1, fma(-vt1, a0, vt2)) + dot * a2) * invD;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
+      }
+      double xnew[3], vnew[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
+        vnew[d] = fma(2.0, vb[d], -vn[d]);
+      }
+      const double xdep[3] = {xnew[0], xnew[1], xnew[2]};  // pre-wrap: deposit position
+      const uint32_t knew = finish_particle(g, xnew, vnew, clamped, A.stats);
+      A.X[p] = xnew[0]; A.Y[p] = xnew[1]; A.Z[p] = xnew[2];
+      A.U[p] = vnew[0]; A.V[p] = vnew[1]; A.W[p] = vnew[2];
+      A.key_new[p] = knew;
+      if (knew != KEY_DEAD) {
+        // values q {1, v, vv} (Eq. 3, R16 order)
+        const double qu = q * vnew[0], qv = q * vnew[1], qw = q * vnew[2];
+        val[0] = q; val[1] = qu; val[2] = qv; val[3] = qw;
+        val[4] = qu * vnew[0]; val[5] = qu * vnew[1]; val[6] = qu * vnew[2];
+        val[7] = qv * vnew[1]; val[8] = qv * vnew[2]; val[9] = qw * vnew[2];
+        // hat weights of the two nodes of c0 per axis
+        const int c0x = c0 & 3, c0y = (c0 >> 2) & 3, c0z = c0 >> 4;
+        const double r[3] = {xdep[0] - (double)(ox + c0x), xdep[1] - (double)(oy + c0y),
+                             xdep[2] - (double)(oz + c0z)};
+        double hw0[3], hw1[3];
+        bool inside = true;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          hw0[d] = fmax(0.0, 1.0 - fabs(r[d]));
+          hw1[d] = fmax(0.0, 1.0 - fabs(r[d] - 1.0));
+          inside &= (r[d] >= 0.0) && (r[d] < 1.0);
+        }
+        const double w00 = hw0[1] * hw0[2], w10 = hw1[1] * hw0[2], w01 = hw0[1] * hw1[2], w11 = hw1[1] * hw1[2];
+        Sk[0] = hw0[0] * w00; Sk[1] = hw1[0] * w00; Sk[2] = hw0[0] * w10; Sk[3] = hw1[0] * w10;
+        Sk[4] = hw0[0] * w01; Sk[5] = hw1[0] * w01; Sk[6] = hw0[0] * w11; Sk[7] = hw1[0] * w11;
+        if (!inside) {
+          // spill: corners of the new cell outside c0's corner set
+          const double fl[3] = {floor(xdep[0]), floor(xdep[1]), floor(xdep[2])};
+          const double f[3] = {xdep[0] - fl[0], xdep[1] - fl[1], xdep[2] - fl[2]};
+          const int64_t c1[3] = {(int64_t)fl[0], (int64_t)fl[1], (int64_t)fl[2]};
+          const int64_t cc0[3] = {ox + c0x, oy + c0y, oz + c0z};
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            const int b[3] = {c & 1, (c >> 1) & 1, c >> 2};
+            int64_t n[3];
+            bool in_set = true;
+            double w = 1.0;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              n[d] = c1[d] + b[d];
+              in_set &= (n[d] == cc0[d] || n[d] == cc0[d] + 1);
+              w *= b[d] ? f[d] : 1.0 - f[d];
+            }
+            if (in_set || w == 0.0) continue;
+            deposit_node(A, acc, (int)(n[0] - ox + 1), (int)(n[1] - oy + 1), (int)(n[2] - oz + 1), n[0], n[1],
+                         n[2], w, val);
+          }
+        }
+      }
+    }
+    // stage S (corner-major per 4-particle group) and the 10 values
+    {
+      const int grp = lane >> 2, j = lane & 3;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Sb[grp * SGRP + k * 4 + j] = Sk[k];
+#pragma unroll
+      for (int m = 0; m < 10; m += 2)
+        *reinterpret_cast<double2 *>(Vb + lane * 10 + m) = make_double2(val[m], val[m + 1]);
+    }
+    __syncwarp();
+    const uint32_t navail = min(32u, wend - r0);
+    for (int grp = 0; grp < 8; ++grp) {
+      if ((uint32_t)(grp * 4) >= navail) break;
+      const int cj = __shfl_sync(0xffffffffu, c0, grp * 4 + js);
+      int v = (int)__reduce_min_sync(0xffffffffu, (unsigned)cj);
+      const double s = Sb[grp * SGRP + kc * 4 + js];
+      const double *vv = Vb + (grp * 4 + js) * 10;
+      double vals[10];
+#pragma unroll
+      for (int m = 0; m < 10; m += 2) {
+        const double2 t = *reinterpret_cast<const double2 *>(vv + m);
+        vals[m] = t.x;
+        vals[m + 1] = t.y;
+      }
+      while (v < 64) {
+        if (v != cur) {
+          if (cur >= 0) flush(cur);
+          cur = v;
+        }
+        const double sw = (cj == v) ? s : 0.0;
+#pragma unroll
+        for (int m = 0; m < 10; ++m) accr[m] = fma(sw, vals[m], accr[m]);
+        v = (int)__reduce_min_sync(0xffffffffu, (unsigned)(cj > v ? cj : 64));
+      }
+    }
+    __syncwarp();
+  }
+  if (cur >= 0) flush(cur);
+  __syncthreads();
+
+  // ---- 4. tile accumulators -> global moments
+  for (int i = tid; i < NB3; i += THREADS) {
+    const int bx = i % NB, by = (i / NB) % NB, bz = i / (NB * NB);
+    double vsum = 0.0;
+#pragma unroll
+    for (int m = 0; m < 10; ++m) vsum += fabs(acc[m * NB3 + i]);
+    if (vsum == 0.0) continue;
+    const int64_t node = moment_node(g, ox - 1 + bx, oy - 1 + by, oz - 1 + bz);
+    if (node < 0) {
+      atomicAdd(&A.stats[ST_FAR], 1ull);
+      continue;
+    }
+#pragma unroll
+    for (int m = 0; m < 10; ++m) {
+      const double a = acc[m * NB3 + i];
+      if (a != 0.0) atomicAdd(A.mom + m * g.m_plane + node, a);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- host --
+static pic_status make_tmap(Ctx *ctx) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+      return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const Geom &g = ctx->geom;
+  CUtensorMap *map = reinterpret_cast<CUtensorMap *>(ctx->tmap);
+  cuuint64_t dims[4] = {6, (cuuint64_t)g.f_n[0], (cuuint64_t)g.f_n[1], (cuuint64_t)g.f_n[2]};
+  cuuint64_t strides[3] = {48, (cuuint64_t)(48 * g.f_n[0]), (cuuint64_t)(48 * g.f_n[0] * g.f_n[1])};
+  cuuint32_t box[4] = {6, NB, NB, NB};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)ctx->field, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
+  ctx->tmap_ok = true;
+  return PIC_OK;
+}
 
 pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   *did_deposit = false;
   SpeciesStore &sp = ctx->sp[s];
   const int se = ctx->cfg.sort_every;
-  if (se > 0 && (ctx->cycle % se == 0 || !sp.sorted)) {
+  if (!sp.sorted || (se > 0 && ctx->cycle % se == 0)) {
     pic_status st = sort_species(ctx, s);
     if (st != PIC_OK) return st;
   }
-  return launch_mover_basic(ctx, s);
+  if (!ctx->tmap_ok) {
+    pic_status st = make_tmap(ctx);
+    if (st != PIC_OK) return st;
+    PIC_CUDA(cudaFuncSetAttribute(tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+  }
+  pic_status st = zero_moments(ctx, s);
+  if (st != PIC_OK) return st;
+  if (sp.n == 0) {
+    *did_deposit = true;
+    return PIC_OK;
+  }
+  TiledArgs A;
+  A.g = ctx->geom;
+  A.X = sp.a[0]; A.Y = sp.a[1]; A.Z = sp.a[2]; A.U = sp.a[3]; A.V = sp.a[4]; A.W = sp.a[5]; A.Q = sp.a[6];
+  A.key = sp.key;
+  A.key_new = sp.key_new;
+  A.tile_start = sp.tile_start;
+  A.field = ctx->field;
+  A.mom = sp.mom;
+  A.stats = ctx->stats;
+  A.ks = sp.qom * (ctx->geom.dt * 0.5);
+  A.ks_c = A.ks / ctx->geom.c;
+  A.n_iter = sp.n_iter;
+  tiled_kernel<<<(unsigned)ctx->geom.ntiles, THREADS, SMEM_BYTES, ctx->stream>>>(
+      *reinterpret_cast<const CUtensorMap *>(ctx->tmap), A); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  *did_deposit = true;
+  return PIC_OK;
 }
 
 }  // namespace pic
