@@ -1,0 +1,29 @@
+"""Multi-GPU parity (P14, decomposition invariance): launches tests/mr_parity.py
+under torchrun on 2 (and 4 when available) GPUs of this box."""
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_multirank_parity(nproc):
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "rep.json")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + nproc * 7),
+               os.path.join(HERE, "mr_parity.py"), "--out", out]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+        rep = json.load(open(out))
+        assert rep["ok"], rep
+        assert any(x["sent"] > 0 for x in rep["reports"])
