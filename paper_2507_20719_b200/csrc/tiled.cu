@@ -12,14 +12,15 @@
 //     memory (R12), then x^{n+1}, v^{n+1}, boundary conditions and the new
 //     sort key (R10, R11, R21).
 //  3. The deposit of the new state (Eq. 3, R13-R18) is fused: each lane turns
-//     its particle into 8 corner weights (hat functions relative to the
-//     particle's sort-time cell c0) and 10 values q{1, v, vv}, written to a
-//     per-warp shared buffer; the warp then re-reads them as 8 corners x 4
-//     particle slots, so each lane accumulates 10 register sums for one corner
-//     node of c0 (no atomics inside a cell).  At every change of c0 the four
-//     slots are reduced with shuffles and added to the tile's shared node
-//     accumulators (7^3 nodes x 10).  Particles that crossed into another cell
-//     deposit their remaining corners ("spills") with shared atomics.
+//     its particle into the 8 trilinear corner weights of its new cell c1 and
+//     the 10 values q{1, v, vv}, written to a per-warp shared buffer; the warp
+//     re-reads them as 8 corners x 4 particle slots.
+//     Pass A (particles still in their sort-time cell c0, the vast majority):
+//     each lane accumulates 10 register sums for one corner node of c0 across
+//     rounds (no atomics inside a cell); when c0 changes the four slots are
+//     reduced with shuffles and added to the tile's shared node accumulators
+//     (7^3 nodes x 10).  Pass B (cell crossers, c1 != c0): 4 crossers per step,
+//     one corner node per lane, added with shared-memory atomics.
 //  4. The tile's shared accumulators are added to the global ghosted moment
 //     arrays with fp64 atomics (tile faces are shared with neighbour tiles).
 //
@@ -38,7 +39,7 @@ constexpr int NB3 = NB * NB * NB;       // 343
 constexpr int WARPS = 8;
 constexpr int THREADS = 32 * WARPS;
 constexpr int SGRP = 36;                // doubles per 4-particle group in the S buffer (32 + pad)
-constexpr int WBUF = 8 * SGRP + 32 * 10;  // doubles per warp: S[8][36] + V[32][10]
+constexpr int WBUF = 8 * SGRP + 32 * 10 + 16;  // doubles per warp: S[8][36] + V[32][10] + 32 ints
 constexpr size_t SMEM_BYTES = sizeof(double) * (NB3 * 6 + 10 * NB3 + WARPS * WBUF) + 16;
 
 struct TiledArgs {
@@ -88,6 +89,17 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, i
       : "memory");
 }
 
+// 1/D for D >= 1 (D = 1 + |a|^2 of Eq. 2): MUFU.RCP64H seed + two Newton steps
+// (error well below 1 ulp of the 1e-12 parity budget; no IEEE slow path).
+__device__ __forceinline__ double rcp_ge1(double D) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
+  double e = fma(-D, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-D, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Trilinear gather of the pre-scaled fields from the staged box.  u = position
 // in box node units.  Returns false if the 8 nodes are not all in the box.
 __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, const double u[3], double out[6]) {
@@ -122,25 +134,6 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
     out[5] = fma(S[c], e.y, out[5]);
   }
   return true;
-}
-
-// Add 10 contributions w*val of one node to the tile accumulators (node in box
-// coordinates) or, outside the box, to the global moment arrays.
-__device__ __forceinline__ void deposit_node(const TiledArgs &A, double *__restrict__ acc, int bx, int by, int bz,
-                                             int64_t gx, int64_t gy, int64_t gz, double w, const double val[10]) {
-  if (bx >= 0 && bx < NB && by >= 0 && by < NB && bz >= 0 && bz < NB) {
-    const int node = (bz * NB + by) * NB + bx;
-#pragma unroll
-    for (int m = 0; m < 10; ++m) atomicAdd(acc + m * NB3 + node, w * val[m]);
-  } else {
-    const int64_t node = moment_node(A.g, gx, gy, gz);
-    if (node < 0) {
-      atomicAdd(&A.stats[ST_FAR], 1ull);
-      return;
-    }
-#pragma unroll
-    for (int m = 0; m < 10; ++m) atomicAdd(A.mom + m * A.g.m_plane + node, w * val[m]);
-  }
 }
 
 __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -210,15 +203,20 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
     }
   };
 
+  int *cl = reinterpret_cast<int *>(Vb + 32 * 10);  // crosser -> lane table (32 ints)
+
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    int c0 = 64;  // sentinel: no particle
+    int c0 = 0;          // sort-time local cell (0..63)
+    int c1b = -1;        // new cell in box coordinates (bx + NB (by + NB bz)) of a crosser
+    bool alive = false, crosser = false;
     double Sk[8], val[10];
 #pragma unroll
     for (int k = 0; k < 8; ++k) Sk[k] = 0.0;
 #pragma unroll
     for (int m = 0; m < 10; ++m) val[m] = 0.0;
+    int64_t c1g[3] = {0, 0, 0};
     if (act) {
       c0 = (int)(A.key[p] & (TILE3 - 1));
       const double xn[3] = {A.X[p], A.Y[p], A.Z[p]};
@@ -240,10 +238,10 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
         const double a0 = EB[3], a1 = EB[4], a2 = EB[5];
         const double dot = fma(vt0, a0, fma(vt1, a1, vt2 * a2));
         const double D = fma(a0, a0, fma(a1, a1, fma(a2, a2, 1.0)));
-        const double invD = 1.0 / D;
-        vb[0] = (fma(vt1, a2, fma(-vt2, a1, vt0)) + dot * a0) * invD;
-        vb[1] = (fma(vt2, a0, fma(-vt0, a2, vt1)) + dot * a1) * invD;
-        vb[2] = (fma(vt0, a1, fma(-vt1, a0, vt2)) + dot * a2) * invD;
+        const double invD = rcp_ge1(D);
+        vb[0] = fma(dot, a0, fma(vt1, a2, fma(-vt2, a1, vt0))) * invD;
+        vb[1] = fma(dot, a1, fma(vt2, a0, fma(-vt0, a2, vt1))) * invD;
+        vb[2] = fma(dot, a2, fma(vt0, a1, fma(-vt1, a0, vt2))) * invD;
 #pragma unroll
         for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
       }
@@ -259,52 +257,33 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
       A.U[p] = vnew[0]; A.V[p] = vnew[1]; A.W[p] = vnew[2];
       A.key_new[p] = knew;
       if (knew != KEY_DEAD) {
+        alive = true;
         // values q {1, v, vv} (Eq. 3, R16 order)
         const double qu = q * vnew[0], qv = q * vnew[1], qw = q * vnew[2];
         val[0] = q; val[1] = qu; val[2] = qv; val[3] = qw;
         val[4] = qu * vnew[0]; val[5] = qu * vnew[1]; val[6] = qu * vnew[2];
         val[7] = qv * vnew[1]; val[8] = qv * vnew[2]; val[9] = qw * vnew[2];
-        // hat weights of the two nodes of c0 per axis
-        const int c0x = c0 & 3, c0y = (c0 >> 2) & 3, c0z = c0 >> 4;
-        const double r[3] = {xdep[0] - (double)(ox + c0x), xdep[1] - (double)(oy + c0y),
-                             xdep[2] - (double)(oz + c0z)};
-        double hw0[3], hw1[3];
-        bool inside = true;
+        // trilinear weights of the 8 corners of the new cell c1 (R12)
+        double f[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          hw0[d] = fmax(0.0, 1.0 - fabs(r[d]));
-          hw1[d] = fmax(0.0, 1.0 - fabs(r[d] - 1.0));
-          inside &= (r[d] >= 0.0) && (r[d] < 1.0);
+          const double fl = floor(xdep[d]);
+          f[d] = xdep[d] - fl;
+          c1g[d] = (int64_t)fl;
         }
-        const double w00 = hw0[1] * hw0[2], w10 = hw1[1] * hw0[2], w01 = hw0[1] * hw1[2], w11 = hw1[1] * hw1[2];
-        Sk[0] = hw0[0] * w00; Sk[1] = hw1[0] * w00; Sk[2] = hw0[0] * w10; Sk[3] = hw1[0] * w10;
-        Sk[4] = hw0[0] * w01; Sk[5] = hw1[0] * w01; Sk[6] = hw0[0] * w11; Sk[7] = hw1[0] * w11;
-        if (!inside) {
-          // spill: corners of the new cell outside c0's corner set
-          const double fl[3] = {floor(xdep[0]), floor(xdep[1]), floor(xdep[2])};
-          const double f[3] = {xdep[0] - fl[0], xdep[1] - fl[1], xdep[2] - fl[2]};
-          const int64_t c1[3] = {(int64_t)fl[0], (int64_t)fl[1], (int64_t)fl[2]};
-          const int64_t cc0[3] = {ox + c0x, oy + c0y, oz + c0z};
-#pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
-            const int b[3] = {c & 1, (c >> 1) & 1, c >> 2};
-            int64_t n[3];
-            bool in_set = true;
-            double w = 1.0;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              n[d] = c1[d] + b[d];
-              in_set &= (n[d] == cc0[d] || n[d] == cc0[d] + 1);
-              w *= b[d] ? f[d] : 1.0 - f[d];
-            }
-            if (in_set || w == 0.0) continue;
-            deposit_node(A, acc, (int)(n[0] - ox + 1), (int)(n[1] - oy + 1), (int)(n[2] - oz + 1), n[0], n[1],
-                         n[2], w, val);
-          }
+        const double gx = 1.0 - f[0], gy = 1.0 - f[1], gz = 1.0 - f[2];
+        const double w00 = gy * gz, w10 = f[1] * gz, w01 = gy * f[2], w11 = f[1] * f[2];
+        Sk[0] = gx * w00; Sk[1] = f[0] * w00; Sk[2] = gx * w10; Sk[3] = f[0] * w10;
+        Sk[4] = gx * w01; Sk[5] = f[0] * w01; Sk[6] = gx * w11; Sk[7] = f[0] * w11;
+        crosser = (c1g[0] != ox + (c0 & 3)) || (c1g[1] != oy + ((c0 >> 2) & 3)) || (c1g[2] != oz + (c0 >> 4));
+        if (crosser) {
+          const int64_t bx = c1g[0] - ox + 1, by = c1g[1] - oy + 1, bz = c1g[2] - oz + 1;
+          c1b = (bx >= 0 && bx <= NB - 2 && by >= 0 && by <= NB - 2 && bz >= 0 && bz <= NB - 2)
+                    ? (int)((bz * NB + by) * NB + bx) : -2;   // -2: outside the box
         }
       }
     }
-    // stage S (corner-major per 4-particle group) and the 10 values
+    // stage S (corner-major per 4-particle group) and the 10 values, lane order
     {
       const int grp = lane >> 2, j = lane & 3;
 #pragma unroll
@@ -313,30 +292,87 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
       for (int m = 0; m < 10; m += 2)
         *reinterpret_cast<double2 *>(Vb + lane * 10 + m) = make_double2(val[m], val[m + 1]);
     }
+    const unsigned xmask = __ballot_sync(0xffffffffu, crosser);
+    if (crosser) cl[__popc(xmask & ((1u << lane) - 1u))] = lane;
     __syncwarp();
-    const uint32_t navail = min(32u, wend - r0);
-    for (int grp = 0; grp < 8; ++grp) {
-      if ((uint32_t)(grp * 4) >= navail) break;
-      const int cj = __shfl_sync(0xffffffffu, c0, grp * 4 + js);
-      int v = (int)__reduce_min_sync(0xffffffffu, (unsigned)cj);
-      const double s = Sb[grp * SGRP + kc * 4 + js];
-      const double *vv = Vb + (grp * 4 + js) * 10;
-      double vals[10];
+
+    // ---- pass B: cell crossers, 4 per step, each lane one corner node, shared atomics
+    const int ncross = __popc(xmask);
+    for (int r = 0; r < ncross; r += 4) {
+      const int rr = r + js;
+      const int src = (rr < ncross) ? cl[rr] : -1;
+      const int cb = __shfl_sync(0xffffffffu, c1b, src < 0 ? 0 : src);
+      if (src >= 0) {
+        const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
+        const double *vv = Vb + src * 10;
+        if (s != 0.0 && cb >= 0) {
+          const int node = cb + kbx + NB * (kby + NB * kbz);
 #pragma unroll
-      for (int m = 0; m < 10; m += 2) {
-        const double2 t = *reinterpret_cast<const double2 *>(vv + m);
-        vals[m] = t.x;
-        vals[m + 1] = t.y;
-      }
-      while (v < 64) {
-        if (v != cur) {
-          if (cur >= 0) flush(cur);
-          cur = v;
+          for (int m = 0; m < 10; ++m) atomicAdd(acc + m * NB3 + node, s * vv[m]);
         }
-        const double sw = (cj == v) ? s : 0.0;
+      }
+      // crossers outside the staged box: global atomics (rare; far movers)
+      const int64_t gx = __shfl_sync(0xffffffffu, c1g[0], src < 0 ? 0 : src);
+      const int64_t gy = __shfl_sync(0xffffffffu, c1g[1], src < 0 ? 0 : src);
+      const int64_t gz = __shfl_sync(0xffffffffu, c1g[2], src < 0 ? 0 : src);
+      if (src >= 0 && cb == -2) {
+        const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
+        if (s != 0.0) {
+          const int64_t node = moment_node(g, gx + kbx, gy + kby, gz + kbz);
+          if (node < 0) {
+            atomicAdd(&A.stats[ST_FAR], 1ull);
+          } else {
 #pragma unroll
-        for (int m = 0; m < 10; ++m) accr[m] = fma(sw, vals[m], accr[m]);
-        v = (int)__reduce_min_sync(0xffffffffu, (unsigned)(cj > v ? cj : 64));
+            for (int m = 0; m < 10; ++m) atomicAdd(A.mom + m * g.m_plane + node, s * Vb[src * 10 + m]);
+          }
+        }
+      }
+    }
+
+    // ---- pass A: particles still in their sort-time cell, register accumulation
+    const unsigned amask = __ballot_sync(0xffffffffu, alive && !crosser);
+    if (amask) {
+      const bool uniform = __all_sync(0xffffffffu, !(alive && !crosser) || c0 == cur);
+      if (uniform) {
+        // fast path: every pass-A particle of the round is in the current cell
+        for (int grp = 0; grp < 8; ++grp) {
+          if (((amask >> (grp * 4)) & 0xFu) == 0u) continue;
+          const bool mine = (amask >> (grp * 4 + js)) & 1u;
+          const double s = mine ? Sb[grp * SGRP + kc * 4 + js] : 0.0;
+          const double *vv = Vb + (grp * 4 + js) * 10;
+#pragma unroll
+          for (int m = 0; m < 10; m += 2) {
+            const double2 t = *reinterpret_cast<const double2 *>(vv + m);
+            accr[m] = fma(s, t.x, accr[m]);
+            accr[m + 1] = fma(s, t.y, accr[m + 1]);
+          }
+        }
+      } else {
+        const int ca = (alive && !crosser) ? c0 : 64;
+        for (int grp = 0; grp < 8; ++grp) {
+          if (((amask >> (grp * 4)) & 0xFu) == 0u) continue;
+          const int cj = __shfl_sync(0xffffffffu, ca, grp * 4 + js);
+          int v = (int)__reduce_min_sync(0xffffffffu, (unsigned)cj);
+          const double s = Sb[grp * SGRP + kc * 4 + js];
+          const double *vv = Vb + (grp * 4 + js) * 10;
+          double vals[10];
+#pragma unroll
+          for (int m = 0; m < 10; m += 2) {
+            const double2 t = *reinterpret_cast<const double2 *>(vv + m);
+            vals[m] = t.x;
+            vals[m + 1] = t.y;
+          }
+          while (v < 64) {
+            if (v != cur) {
+              if (cur >= 0) flush(cur);
+              cur = v;
+            }
+            const double sw = (cj == v) ? s : 0.0;
+#pragma unroll
+            for (int m = 0; m < 10; ++m) accr[m] = fma(sw, vals[m], accr[m]);
+            v = (int)__reduce_min_sync(0xffffffffu, (unsigned)(cj > v ? cj : 64));
+          }
+        }
       }
     }
     __syncwarp();
