@@ -296,34 +296,31 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
     if (crosser) cl[__popc(xmask & ((1u << lane) - 1u))] = lane;
     __syncwarp();
 
-    // ---- pass B: cell crossers, 4 per step, each lane one corner node, shared atomics
+    // ---- pass B: cell crossers, one at a time; lane = (corner kc, value group
+    // js) so the 32 lanes add distinct (node, component) pairs: the shared CAS
+    // atomics never conflict inside the warp.
     const int ncross = __popc(xmask);
-    for (int r = 0; r < ncross; r += 4) {
-      const int rr = r + js;
-      const int src = (rr < ncross) ? cl[rr] : -1;
-      const int cb = __shfl_sync(0xffffffffu, c1b, src < 0 ? 0 : src);
-      if (src >= 0) {
-        const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
-        const double *vv = Vb + src * 10;
-        if (s != 0.0 && cb >= 0) {
+    for (int r = 0; r < ncross; ++r) {
+      const int src = cl[r];
+      const int cb = __shfl_sync(0xffffffffu, c1b, src);
+      const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
+      const double *vv = Vb + src * 10;
+      if (cb >= 0) {
+        if (s != 0.0) {
           const int node = cb + kbx + NB * (kby + NB * kbz);
-#pragma unroll
-          for (int m = 0; m < 10; ++m) atomicAdd(acc + m * NB3 + node, s * vv[m]);
+          for (int m = js; m < 10; m += 4) atomicAdd(acc + m * NB3 + node, s * vv[m]);
         }
-      }
-      // crossers outside the staged box: global atomics (rare; far movers)
-      const int64_t gx = __shfl_sync(0xffffffffu, c1g[0], src < 0 ? 0 : src);
-      const int64_t gy = __shfl_sync(0xffffffffu, c1g[1], src < 0 ? 0 : src);
-      const int64_t gz = __shfl_sync(0xffffffffu, c1g[2], src < 0 ? 0 : src);
-      if (src >= 0 && cb == -2) {
-        const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
+      } else {
+        // crosser outside the staged box: global atomics (far movers, rare)
+        const int64_t gx = __shfl_sync(0xffffffffu, c1g[0], src);
+        const int64_t gy = __shfl_sync(0xffffffffu, c1g[1], src);
+        const int64_t gz = __shfl_sync(0xffffffffu, c1g[2], src);
         if (s != 0.0) {
           const int64_t node = moment_node(g, gx + kbx, gy + kby, gz + kbz);
           if (node < 0) {
-            atomicAdd(&A.stats[ST_FAR], 1ull);
+            if (js == 0) atomicAdd(&A.stats[ST_FAR], 1ull);
           } else {
-#pragma unroll
-            for (int m = 0; m < 10; ++m) atomicAdd(A.mom + m * g.m_plane + node, s * Vb[src * 10 + m]);
+            for (int m = js; m < 10; m += 4) atomicAdd(A.mom + m * g.m_plane + node, s * vv[m]);
           }
         }
       }
