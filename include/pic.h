@@ -90,7 +90,8 @@ typedef struct {
   int64_t slab_lo, slab_hi;      /* this rank owns x-cells [slab_lo, slab_hi)     */
   int32_t ghost;                 /* G >= 1: field-window ghost nodes per side and
                                     moment ghost node planes per x-side (R22)     */
-  int32_t sort_every;            /* cycles between cell sorts (0 = never)         */
+  int32_t sort_every;            /* reserved (the cell order is rebuilt every cycle
+                                    by the counting sort; value ignored)          */
   int32_t kernel;                /* pic_kernel                                    */
 } pic_config;
 

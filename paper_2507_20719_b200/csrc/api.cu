@@ -91,6 +91,7 @@ void make_geom(const pic_config *c, Geom *g) {
   g->k_n[2] = c->ncell[2];
   for (int d = 0; d < 3; ++d) g->nt[d] = (g->k_n[d] + TILE - 1) / TILE;
   g->ntiles = g->nt[0] * g->nt[1] * g->nt[2];
+  g->ncells = g->ntiles * TILE3;
 }
 
 // Workspace plan; if base != nullptr, assigns pointers into ctx.
@@ -101,31 +102,38 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   cap_max = std::max<int64_t>(cap_max, 1);
   const int64_t mig_cap = std::max<int64_t>(cap_max / 4, 4096);
   for (int s = 0; s < c->n_species; ++s) {
-    // every per-particle array has cap_max slots: the sort and the compaction
-    // rotate arrays through the shared scratch array (R20: order is free)
-    const int64_t cap = cap_max;
-    int64_t o[7];
-    for (int k = 0; k < 7; ++k) o[k] = L.take(8 * cap);
-    int64_t oid = L.take(8 * cap);
-    int64_t okey = L.take(4 * cap), okey2 = L.take(4 * cap), oidx = L.take(4 * cap), oidx2 = L.take(4 * cap);
+    // two buffers of the SoA store (the mover gathers A[perm[q]] into B[q]),
+    // plus the order metadata of the counting sort (order.cu)
+    const int64_t cap = std::max<int64_t>(c->capacity[s], 1);
+    int64_t oa[7], ob[7];
+    for (int k = 0; k < 7; ++k) oa[k] = L.take(8 * cap);
+    for (int k = 0; k < 7; ++k) ob[k] = L.take(8 * cap);
+    int64_t oid = L.take(8 * cap), oidb = L.take(8 * cap);
+    int64_t okn = L.take(4 * cap), ork = L.take(4 * cap), opm = L.take(4 * cap), okey = L.take(4 * cap);
+    int64_t occ = L.take(4 * (g.ncells + 1)), oco = L.take(4 * (g.ncells + 1));
+    int64_t onraw = L.take(8);
     int64_t omom = L.take(8 * 10 * g.m_plane);
-    int64_t otile = L.take(4 * (g.ntiles + 1));
     if (base) {
-      ctx->sp[s].tile_start = (uint32_t *)(base + otile);
       SpeciesStore &sp = ctx->sp[s];
-      for (int k = 0; k < 7; ++k) sp.a[k] = (double *)(base + o[k]);
+      for (int k = 0; k < 7; ++k) {
+        sp.a[k] = (double *)(base + oa[k]);
+        sp.b[k] = (double *)(base + ob[k]);
+      }
       sp.id = (int64_t *)(base + oid);
+      sp.id_b = (int64_t *)(base + oidb);
+      sp.key_new = (uint32_t *)(base + okn);
+      sp.rank = (uint32_t *)(base + ork);
+      sp.perm = (uint32_t *)(base + opm);
       sp.key = (uint32_t *)(base + okey);
-      sp.key_new = (uint32_t *)(base + okey2);
-      sp.idx = (uint32_t *)(base + oidx);
-      sp.idx_alt = (uint32_t *)(base + oidx2);
+      sp.cell_count = (uint32_t *)(base + occ);
+      sp.cell_off = (uint32_t *)(base + oco);
+      sp.d_nraw = (int64_t *)(base + onraw);
       sp.mom = (double *)(base + omom);
       sp.cap = c->capacity[s];
       sp.qom = c->qom[s];
       sp.n_iter = c->n_iter[s];
     }
   }
-  int64_t oscr = L.take(8 * cap_max);
   int64_t field_elems = g.f_n[0] * g.f_n[1] * g.f_n[2] * 6;
   int64_t ofield = L.take(8 * field_elems);
   int64_t ostats = L.take(8 * ST_N);
@@ -141,7 +149,6 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   int64_t opack = L.take(8 * pack_elems);
   int64_t ocub = L.take((int64_t)cub_bytes);
   if (base) {
-    ctx->scratch = (double *)(base + oscr);
     ctx->field = (double *)(base + ofield);
     ctx->field_elems = field_elems;
     ctx->stats = (unsigned long long *)(base + ostats);
@@ -199,9 +206,7 @@ pic_status pic_workspace_bytes(const pic_config *cfg, int64_t *bytes) {
   if (!bytes) return PIC_EINVAL;
   Geom g;
   make_geom(cfg, &g);
-  int64_t cap_max = 1;
-  for (int s = 0; s < cfg->n_species; ++s) cap_max = std::max<int64_t>(cap_max, cfg->capacity[s]);
-  *bytes = plan(cfg, g, nullptr, nullptr, sort_temp_bytes(cap_max));
+  *bytes = plan(cfg, g, nullptr, nullptr, order_temp_bytes(g.ncells));
   return PIC_OK;
 }
 
@@ -217,9 +222,7 @@ pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
   if (!ctx) return PIC_ENOMEM;
   ctx->cfg = *cfg;
   make_geom(cfg, &ctx->geom);
-  int64_t cap_max = 1;
-  for (int s = 0; s < cfg->n_species; ++s) cap_max = std::max<int64_t>(cap_max, cfg->capacity[s]);
-  const size_t cub_bytes = sort_temp_bytes(cap_max);
+  const size_t cub_bytes = order_temp_bytes(ctx->geom.ncells);
   const int64_t need = plan(cfg, ctx->geom, nullptr, nullptr, cub_bytes);
   if (bytes < need) {
     delete ctx;
@@ -280,9 +283,8 @@ pic_status pic_count(pic_ctx *p, int32_t s, int64_t *n) {
   Ctx *ctx = C(p);
   pic_status st = check_species(ctx, s, false);
   if (st != PIC_OK) return st;
-  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-  *n = ctx->sp[s].n;
-  return PIC_OK;
+  if (!ctx->sp[s].order_valid) return fail(ctx, PIC_ESTATE, "pic_count between pic_mover and pic_exchange");
+  return live_count(ctx, s, n);
 }
 
 pic_status pic_get_particles(pic_ctx *p, int32_t s, double *const xyzuvwq[7], int64_t *id) {
@@ -290,6 +292,8 @@ pic_status pic_get_particles(pic_ctx *p, int32_t s, double *const xyzuvwq[7], in
   Ctx *ctx = C(p);
   pic_status st = check_species(ctx, s, false);
   if (st != PIC_OK) return st;
+  if (!ctx->sp[s].order_valid)
+    return fail(ctx, PIC_ESTATE, "pic_get_particles between pic_mover and pic_exchange");
   double *none[7] = {};
   return unload_particles(ctx, s, xyzuvwq ? xyzuvwq : none, id);
 }
@@ -310,7 +314,8 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
   if (!ctx->fields_set) return fail(ctx, PIC_ESTATE, "pic_set_fields must precede pic_mover");
   const int s0 = s < 0 ? 0 : s, s1 = s < 0 ? ctx->cfg.n_species : s + 1;
   for (int k = s0; k < s1; ++k)
-    if (ctx->sp[k].moved) return fail(ctx, PIC_ESTATE, "pic_mover called twice without pic_exchange");
+    if (ctx->sp[k].moved || !ctx->sp[k].order_valid)
+      return fail(ctx, PIC_ESTATE, "pic_mover called twice without pic_exchange");
   for (int k = s0; k < s1; ++k) {
     SpeciesStore &sp = ctx->sp[k];
     bool fused = false;

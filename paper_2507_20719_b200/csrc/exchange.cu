@@ -152,47 +152,41 @@ static pic_status fold_and_ghosts(Ctx *ctx) {
 }
 
 // ---------------------------------------------------------------- migration --
-// Classify by key: 0 stay, 1 left, 2 right, 3 dead; slot from warp-aggregated
-// atomics.  dst[p] = (category << 30) | slot.
-__global__ void classify_kernel(const uint32_t *__restrict__ key, int64_t n, uint32_t *__restrict__ dst,
-                                unsigned long long *__restrict__ counts) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const unsigned lane = threadIdx.x & 31;
-  uint32_t cat = 3;
-  if (p < n) {
-    uint32_t k = key[p];
-    cat = (k < KEY_FIRST_RESERVED) ? 0u : (k == KEY_LEFT ? 1u : (k == KEY_RIGHT ? 2u : 3u));
-  } else {
-    cat = 4;  // out of range
-  }
-#pragma unroll
-  for (uint32_t c = 0; c < 3; ++c) {
-    unsigned mask = __ballot_sync(0xffffffffu, cat == c);
-    if (!mask) continue;
-    unsigned long long base = 0;
-    int leader = __ffs(mask) - 1;
-    if ((int)lane == leader) base = atomicAdd(&counts[c], (unsigned long long)__popc(mask));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (cat == c) {
-      unsigned rank = __popc(mask & ((1u << lane) - 1u));
-      dst[p] = (c << 30) | (uint32_t)(base + rank);
-    }
-  }
-  if (cat == 3) dst[p] = 3u << 30;
-}
+// Slab leavers (keys LEFT / RIGHT written by the mover) are packed from the A
+// positions into the send buffers [8][mig_cap] (7 fp64 + id bits); slots come
+// from warp-aggregated atomics.  No compaction of the stayers is needed: the
+// next cell order (order.cu) only contains counted particles.
+struct Arr7 { double *a[7]; };
 
-// Scatter one fp64 array: stays -> out, leavers -> send buffers (component k).
-__global__ void scatter_kernel(const double *__restrict__ src, const uint32_t *__restrict__ dst,
-                               int64_t n, double *__restrict__ out, double *__restrict__ sendL,
-                               double *__restrict__ sendR, int64_t mig_cap) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t d = dst[p];
-    uint32_t cat = d >> 30, slot = d & 0x3FFFFFFFu;
-    double v = src[p];
-    if (cat == 0) out[slot] = v;
-    else if (cat == 1) { if (slot < mig_cap) sendL[slot] = v; }
-    else if (cat == 2) { if (slot < mig_cap) sendR[slot] = v; }
+__global__ void pack_leavers_kernel(Arr7 A, const int64_t *__restrict__ id, const uint32_t *__restrict__ key,
+                                    const int64_t *__restrict__ d_nraw, double *__restrict__ sendL,
+                                    double *__restrict__ sendR, int64_t mig_cap,
+                                    unsigned long long *__restrict__ counts) {
+  const int64_t n = *d_nraw;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t p = base + threadIdx.x;
+    const uint32_t k = p < n ? key[p] : KEY_DEAD;
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const bool mine = k == (side == 0 ? KEY_LEFT : KEY_RIGHT);
+      const unsigned mask = __ballot_sync(0xffffffffu, mine);
+      if (!mask) continue;
+      const int leader = __ffs(mask) - 1;
+      unsigned long long slot0 = 0;
+      if ((int)lane == leader) slot0 = atomicAdd(&counts[side], (unsigned long long)__popc(mask));
+      slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+      if (mine) {
+        const int64_t slot = (int64_t)slot0 + __popc(mask & ((1u << lane) - 1u));
+        if (slot < mig_cap) {
+          double *buf = side == 0 ? sendL : sendR;
+#pragma unroll
+          for (int c = 0; c < 7; ++c) buf[c * mig_cap + slot] = A.a[c][p];
+          buf[7 * mig_cap + slot] = __longlong_as_double(id[p]);
+        }
+      }
+    }
   }
 }
 
@@ -203,11 +197,8 @@ __device__ __forceinline__ uint32_t cell_key(const Geom &g, double x, double y, 
 }
 
 // Append received particles (component arrays of the recv buffer) at `at`.
-struct Arr7 { double *a[7]; };
-
-__global__ void append_kernel(Geom g, Arr7 arrs, int64_t *__restrict__ id,
-                              uint32_t *__restrict__ key, const double *__restrict__ buf,
-                              int64_t cnt, int64_t mig_cap, int64_t at,
+__global__ void append_kernel(Geom g, Arr7 arrs, int64_t *__restrict__ id, uint32_t *__restrict__ key,
+                              const double *__restrict__ buf, int64_t cnt, int64_t mig_cap, int64_t at,
                               unsigned long long *__restrict__ stats) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -228,115 +219,91 @@ __global__ void append_kernel(Geom g, Arr7 arrs, int64_t *__restrict__ id,
   }
 }
 
-__global__ void add_stat_kernel(unsigned long long *stats, int which, const unsigned long long *src,
-                                int n_src) {
-  unsigned long long t = 0;
-  for (int i = 0; i < n_src; ++i) t += src[i];
-  stats[which] += t;
-}
+__global__ void set_scalar_kernel(int64_t *dst, int64_t v) { *dst = v; }
 
 static pic_status migrate(Ctx *ctx) {
   const Geom &g = ctx->geom;
   const int S = ctx->cfg.n_species;
   const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
   const bool per = g.periodic[0];
-  const int left = (P > 1) ? ((r > 0) ? r - 1 : (per ? P - 1 : -1)) : -1;
-  const int right = (P > 1) ? ((r < P - 1) ? r + 1 : (per ? 0 : -1)) : -1;
+  const int left = (r > 0) ? r - 1 : (per ? P - 1 : -1);
+  const int right = (r < P - 1) ? r + 1 : (per ? 0 : -1);
   ncclComm_t comm = (ncclComm_t)ctx->nccl;
-  unsigned long long *cnt = (unsigned long long *)ctx->dev_counts;  // [S][3]
-  PIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 3 * S, ctx->stream));
+  unsigned long long *cnt = (unsigned long long *)ctx->dev_counts;  // [S][2] leavers L/R, [S] nraw
+  int64_t *hc = ctx->host_counts;
   for (int s = 0; s < S; ++s) {
     SpeciesStore &sp = ctx->sp[s];
-    if (sp.n == 0) continue;
-    classify_kernel<<<(unsigned)((sp.n + 255) / 256), 256, 0, ctx->stream>>>(sp.key_new, sp.n, sp.idx,
-                                                                            cnt + 3 * s); ++ctx->launches;
-  }
-  PIC_CUDA(cudaGetLastError());
-  unsigned long long hc[3 * PIC_MAX_SPECIES];
-  PIC_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(unsigned long long) * 3 * S, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (int s = 0; s < S; ++s) {
-    if ((int64_t)hc[3 * s + 1] > ctx->mig_cap || (int64_t)hc[3 * s + 2] > ctx->mig_cap)
-      return fail(ctx, PIC_ERANGE, "migration buffer capacity exceeded");
-    if ((hc[3 * s + 1] && left < 0) || (hc[3 * s + 2] && right < 0))
-      return fail(ctx, PIC_ERANGE, "slab leaver with no neighbour");
-  }
-  for (int s = 0; s < S; ++s) {
-    SpeciesStore &sp = ctx->sp[s];
-    if (sp.n == 0 && P == 1) continue;
-    const int64_t n_stay = (int64_t)hc[3 * s], nl = (int64_t)hc[3 * s + 1], nr = (int64_t)hc[3 * s + 2];
-    // permute the 7 fp64 arrays + id through the scratch array
-    for (int k = 0; k < 8; ++k) {
-      double *src = (k < 7) ? sp.a[k] : (double *)sp.id;
-      if (sp.n)
-        scatter_kernel<<<grid_for(sp.n), 256, 0, ctx->stream>>>(
-            src, sp.idx, sp.n, ctx->scratch, ctx->mig_send[0] + k * ctx->mig_cap,
-            ctx->mig_send[1] + k * ctx->mig_cap, ctx->mig_cap); ++ctx->launches;
-      if (k < 7) { sp.a[k] = ctx->scratch; ctx->scratch = src; }
-      else { sp.id = (int64_t *)ctx->scratch; ctx->scratch = src; }
-    }
-    PIC_CUDA(cudaGetLastError());
-    int64_t nrecvL = 0, nrecvR = 0;
-    if (P > 1) {
-      // counts, then payloads (host knows the counts after a sync)
-      int64_t *hcounts = ctx->host_counts;  // [0] sendL [1] sendR [2] recvL [3] recvR
-      int64_t *dcounts = ctx->dev_counts + 3 * PIC_MAX_SPECIES;
-      hcounts[0] = nl; hcounts[1] = nr;
-      PIC_CUDA(cudaMemcpyAsync(dcounts, hcounts, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-      // per-peer order: send-right, send-left, recv-left, recv-right (matches for P == 2)
-      PIC_NCCL(ncclGroupStart());
-      if (right >= 0) PIC_NCCL(ncclSend(dcounts + 1, 1, ncclInt64, right, comm, ctx->stream));
-      if (left >= 0) PIC_NCCL(ncclSend(dcounts + 0, 1, ncclInt64, left, comm, ctx->stream));
-      if (left >= 0) PIC_NCCL(ncclRecv(dcounts + 3, 1, ncclInt64, left, comm, ctx->stream));
-      if (right >= 0) PIC_NCCL(ncclRecv(dcounts + 2, 1, ncclInt64, right, comm, ctx->stream));
-      PIC_NCCL(ncclGroupEnd());
-      // recv from left = what left sent to its right; dcounts[3]; from right -> dcounts[2]
-      PIC_CUDA(cudaMemcpyAsync(hcounts + 2, dcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                               ctx->stream));
-      PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-      nrecvR = (right >= 0) ? hcounts[2] : 0;
-      nrecvL = (left >= 0) ? hcounts[3] : 0;
-      if (nrecvL > ctx->mig_cap || nrecvR > ctx->mig_cap)
-        return fail(ctx, PIC_ERANGE, "migration receive capacity exceeded");
-      if (n_stay + nrecvL + nrecvR > sp.cap)
-        return fail(ctx, PIC_ERANGE, "particle capacity exceeded after migration");
-      PIC_NCCL(ncclGroupStart());
-      for (int k = 0; k < 8; ++k) {
-        if (right >= 0 && nr) PIC_NCCL(ncclSend(ctx->mig_send[1] + k * ctx->mig_cap, nr, ncclDouble, right, comm, ctx->stream));
-        if (left >= 0 && nl) PIC_NCCL(ncclSend(ctx->mig_send[0] + k * ctx->mig_cap, nl, ncclDouble, left, comm, ctx->stream));
-        if (left >= 0 && nrecvL) PIC_NCCL(ncclRecv(ctx->mig_recv[0] + k * ctx->mig_cap, nrecvL, ncclDouble, left, comm, ctx->stream));
-        if (right >= 0 && nrecvR) PIC_NCCL(ncclRecv(ctx->mig_recv[1] + k * ctx->mig_cap, nrecvR, ncclDouble, right, comm, ctx->stream));
-      }
-      PIC_NCCL(ncclGroupEnd());
-      Arr7 arrs;
-      for (int k = 0; k < 7; ++k) arrs.a[k] = sp.a[k];
-      if (nrecvL)
-        append_kernel<<<grid_for(nrecvL), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0],
-                                                                  nrecvL, ctx->mig_cap, n_stay, ctx->stats); ++ctx->launches;
-      if (nrecvR)
-        append_kernel<<<grid_for(nrecvR), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1],
-                                                                  nrecvR, ctx->mig_cap, n_stay + nrecvL, ctx->stats); ++ctx->launches;
+    PIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2, ctx->stream));
+    if (sp.n_raw > 0) {
+      Arr7 A;
+      for (int k = 0; k < 7; ++k) A.a[k] = sp.a[k];
+      pack_leavers_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(
+          A, sp.id, sp.key_new, sp.d_nraw, ctx->mig_send[0], ctx->mig_send[1], ctx->mig_cap, cnt); ++ctx->launches;
       PIC_CUDA(cudaGetLastError());
     }
-    sp.n = n_stay + nrecvL + nrecvR;
-    sp.sorted = false;
+    // leaver counts and the number of A positions, to the host
+    PIC_CUDA(cudaMemcpyAsync(hc, cnt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    PIC_CUDA(cudaMemcpyAsync(hc + 2, sp.d_nraw, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t nl = hc[0], nr = hc[1], nraw = hc[2];
+    if (nl > ctx->mig_cap || nr > ctx->mig_cap) return fail(ctx, PIC_ERANGE, "migration buffer capacity exceeded");
+    if ((nl && left < 0) || (nr && right < 0)) return fail(ctx, PIC_ERANGE, "slab leaver with no neighbour");
+    // counts, then payloads; per-peer order send-right, send-left, recv-left,
+    // recv-right (matches when left == right, P == 2)
+    int64_t *dcounts = ctx->dev_counts + 8;   // [0] to L, [1] to R, [2] from R, [3] from L
+    hc[4] = nl;
+    hc[5] = nr;
+    PIC_CUDA(cudaMemcpyAsync(dcounts, hc + 4, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    PIC_NCCL(ncclGroupStart());
+    if (right >= 0) PIC_NCCL(ncclSend(dcounts + 1, 1, ncclInt64, right, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclSend(dcounts + 0, 1, ncclInt64, left, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclRecv(dcounts + 3, 1, ncclInt64, left, comm, ctx->stream));
+    if (right >= 0) PIC_NCCL(ncclRecv(dcounts + 2, 1, ncclInt64, right, comm, ctx->stream));
+    PIC_NCCL(ncclGroupEnd());
+    PIC_CUDA(cudaMemcpyAsync(hc + 6, dcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t nrecvR = (right >= 0) ? hc[6] : 0;
+    const int64_t nrecvL = (left >= 0) ? hc[7] : 0;
+    if (nrecvL > ctx->mig_cap || nrecvR > ctx->mig_cap)
+      return fail(ctx, PIC_ERANGE, "migration receive capacity exceeded");
+    if (nraw + nrecvL + nrecvR > sp.cap)
+      return fail(ctx, PIC_ERANGE, "particle capacity exceeded after migration");
+    PIC_NCCL(ncclGroupStart());
+    for (int k = 0; k < 8; ++k) {
+      if (right >= 0 && nr) PIC_NCCL(ncclSend(ctx->mig_send[1] + k * ctx->mig_cap, nr, ncclDouble, right, comm, ctx->stream));
+      if (left >= 0 && nl) PIC_NCCL(ncclSend(ctx->mig_send[0] + k * ctx->mig_cap, nl, ncclDouble, left, comm, ctx->stream));
+      if (left >= 0 && nrecvL) PIC_NCCL(ncclRecv(ctx->mig_recv[0] + k * ctx->mig_cap, nrecvL, ncclDouble, left, comm, ctx->stream));
+      if (right >= 0 && nrecvR) PIC_NCCL(ncclRecv(ctx->mig_recv[1] + k * ctx->mig_cap, nrecvR, ncclDouble, right, comm, ctx->stream));
+    }
+    PIC_NCCL(ncclGroupEnd());
+    Arr7 arrs;
+    for (int k = 0; k < 7; ++k) arrs.a[k] = sp.a[k];
+    if (nrecvL)
+      append_kernel<<<grid_for(nrecvL), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0], nrecvL,
+                                                                ctx->mig_cap, nraw, ctx->stats); ++ctx->launches;
+    if (nrecvR)
+      append_kernel<<<grid_for(nrecvR), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1], nrecvR,
+                                                                ctx->mig_cap, nraw + nrecvL, ctx->stats); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+    const int64_t nnew = nraw + nrecvL + nrecvR;
+    set_scalar_kernel<<<1, 1, 0, ctx->stream>>>(sp.d_nraw, nnew); ++ctx->launches;
+    pic_status st = count_positions(ctx, s, nraw, nnew);
+    if (st != PIC_OK) return st;
+    sp.n_raw = nnew;
     ctx->hstat[ST_SENT] += nl + nr;
     ctx->hstat[ST_RECEIVED] += nrecvL + nrecvR;
   }
   return PIC_OK;
 }
 
-__global__ void keys_from_positions_kernel(Geom g, const double *__restrict__ X,
-                                           const double *__restrict__ Y, const double *__restrict__ Z,
-                                           uint32_t *__restrict__ key, int64_t n, int64_t from,
-                                           unsigned long long *__restrict__ stats) {
-  for (int64_t p = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+__global__ void keys_from_positions_kernel(Geom g, const double *__restrict__ X, const double *__restrict__ Y,
+                                           const double *__restrict__ Z, uint32_t *__restrict__ key, int64_t from,
+                                           int64_t to, unsigned long long *__restrict__ stats) {
+  for (int64_t p = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < to;
        p += (int64_t)gridDim.x * blockDim.x) {
     double x = X[p], y = Y[p], z = Z[p];
     int64_t cx = (int64_t)floor(x), cy = (int64_t)floor(y), cz = (int64_t)floor(z);
-    if (!(cx >= g.slab_lo && cx < g.slab_hi && cy >= 0 && cy < g.ncell[1] && cz >= 0 &&
-          cz < g.ncell[2])) {
+    if (!(cx >= g.slab_lo && cx < g.slab_hi && cy >= 0 && cy < g.ncell[1] && cz >= 0 && cz < g.ncell[2])) {
       atomicAdd(&stats[ST_FAR], 1ull);
       key[p] = KEY_DEAD;
     } else {
@@ -345,33 +312,25 @@ __global__ void keys_from_positions_kernel(Geom g, const double *__restrict__ X,
   }
 }
 
-pic_status recompute_keys(Ctx *ctx, int s, int64_t from) {
+pic_status recompute_keys(Ctx *ctx, int s, int64_t from, int64_t to) {
   SpeciesStore &sp = ctx->sp[s];
-  if (sp.n <= from) return PIC_OK;
-  keys_from_positions_kernel<<<grid_for(sp.n - from), 256, 0, ctx->stream>>>(
-      ctx->geom, sp.a[0], sp.a[1], sp.a[2], sp.key_new, sp.n, from, ctx->stats); ++ctx->launches;
+  if (to <= from) return PIC_OK;
+  keys_from_positions_kernel<<<grid_for(to - from), 256, 0, ctx->stream>>>(ctx->geom, sp.a[0], sp.a[1], sp.a[2],
+                                                                           sp.key_new, from, to, ctx->stats); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
-}
-
-static bool needs_compaction(const Ctx *ctx) {
-  if (ctx->cfg.nranks > 1) return true;
-  if (ctx->geom.has_planet) return true;
-  for (int d = 0; d < 3; ++d)
-    if (!ctx->geom.periodic[d]) return true;
-  return false;
 }
 
 pic_status exchange(Ctx *ctx) {
   pic_status st = fold_and_ghosts(ctx);
   if (st != PIC_OK) return st;
-  if (needs_compaction(ctx)) {
+  if (ctx->cfg.nranks > 1) {
     st = migrate(ctx);
     if (st != PIC_OK) return st;
-    for (int s = 0; s < ctx->cfg.n_species; ++s) {
-      st = recompute_keys(ctx, s, 0);
-      if (st != PIC_OK) return st;
-    }
+  }
+  for (int s = 0; s < ctx->cfg.n_species; ++s) {
+    st = build_order(ctx, s);
+    if (st != PIC_OK) return st;
   }
   return PIC_OK;
 }
@@ -407,11 +366,6 @@ pic_status pack_moments(Ctx *ctx, int s, double *out) {
   return PIC_OK;
 }
 
-__global__ void scale_kernel(double *a, int64_t n, double f) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x)
-    a[p] = a[p] * f;
-}
 __global__ void divide_kernel(double *a, int64_t n, double d) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x)
@@ -422,13 +376,27 @@ __global__ void iota_kernel(int64_t *a, int64_t n) {
        p += (int64_t)gridDim.x * blockDim.x)
     a[p] = p;
 }
+// out[q] = src[perm[q]] * scale  (q < live count)
+__global__ void gather_scaled_kernel(const double *__restrict__ src, const uint32_t *__restrict__ perm,
+                                     const uint32_t *__restrict__ nlive, double *__restrict__ out, double scale) {
+  const int64_t n = *nlive;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = src[perm[q]] * scale;
+}
+__global__ void gather_i64_kernel(const int64_t *__restrict__ src, const uint32_t *__restrict__ perm,
+                                  const uint32_t *__restrict__ nlive, int64_t *__restrict__ out) {
+  const int64_t n = *nlive;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = src[perm[q]];
+}
 
 pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id) {
   SpeciesStore &sp = ctx->sp[s];
   for (int k = 0; k < 7; ++k) {
     if (n) PIC_CUDA(cudaMemcpyAsync(sp.a[k], src[k], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
-    if (k < 3 && n)
+    if (k < 3 && n) {
       divide_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.a[k], n, ctx->geom.delta[k]); ++ctx->launches;
+    }
   }
   if (id) {
     if (n) PIC_CUDA(cudaMemcpyAsync(sp.id, id, sizeof(int64_t) * n, cudaMemcpyDefault, ctx->stream));
@@ -436,30 +404,52 @@ pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7]
     iota_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.id, n); ++ctx->launches;
   }
   PIC_CUDA(cudaGetLastError());
-  sp.n = n;
-  sp.sorted = false;
-  pic_status st = recompute_keys(ctx, s, 0);
+  sp.n_raw = n;
+  set_scalar_kernel<<<1, 1, 0, ctx->stream>>>(sp.d_nraw, n); ++ctx->launches;
+  pic_status st = recompute_keys(ctx, s, 0, n);
   if (st != PIC_OK) return st;
+  st = zero_cell_counts(ctx, s);
+  if (st != PIC_OK) return st;
+  st = count_positions(ctx, s, 0, n);
+  if (st != PIC_OK) return st;
+  st = build_order(ctx, s);
+  if (st != PIC_OK) return st;
+  uint32_t nlive = 0;
+  PIC_CUDA(cudaMemcpyAsync(&nlive, sp.cell_off + ctx->geom.ncells, 4, cudaMemcpyDeviceToHost, ctx->stream));
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));  // caller buffers may be pageable
+  sp.n = nlive;
+  return PIC_OK;
+}
+
+pic_status live_count(Ctx *ctx, int s, int64_t *n) {
+  SpeciesStore &sp = ctx->sp[s];
+  uint32_t nlive = 0;
+  PIC_CUDA(cudaMemcpyAsync(&nlive, sp.cell_off + ctx->geom.ncells, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  sp.n = nlive;
+  *n = nlive;
   return PIC_OK;
 }
 
 pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id) {
   SpeciesStore &sp = ctx->sp[s];
-  const int64_t n = sp.n;
+  int64_t n = 0;
+  pic_status st = live_count(ctx, s, &n);
+  if (st != PIC_OK) return st;
+  const uint32_t *nl = sp.cell_off + ctx->geom.ncells;
+  // buffer B is free between cycles: gather into it, then copy out
   for (int k = 0; k < 7; ++k) {
     if (!dst[k] || !n) continue;
-    if (k < 3) {
-      PIC_CUDA(cudaMemcpyAsync(ctx->scratch, sp.a[k], sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
-      scale_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->scratch, n, ctx->geom.delta[k]); ++ctx->launches;
-      PIC_CUDA(cudaGetLastError());
-      PIC_CUDA(cudaMemcpyAsync(dst[k], ctx->scratch, sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
-      PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-    } else {
-      PIC_CUDA(cudaMemcpyAsync(dst[k], sp.a[k], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
-    }
+    gather_scaled_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.a[k], sp.perm, nl, sp.b[k],
+                                                               k < 3 ? ctx->geom.delta[k] : 1.0); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+    PIC_CUDA(cudaMemcpyAsync(dst[k], sp.b[k], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
   }
-  if (id && n) PIC_CUDA(cudaMemcpyAsync(id, sp.id, sizeof(int64_t) * n, cudaMemcpyDefault, ctx->stream));
+  if (id && n) {
+    gather_i64_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.id, sp.perm, nl, sp.id_b); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+    PIC_CUDA(cudaMemcpyAsync(id, sp.id_b, sizeof(int64_t) * n, cudaMemcpyDefault, ctx->stream));
+  }
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));
   return PIC_OK;
 }

@@ -4,67 +4,92 @@
 //                  sample at x^n (R1), fixed n_iter (R2), trilinear gather from
 //                  the global field window (R12), boundary conditions (R10,
 //                  R11, R21) and the destination key of the new position.
+//                  Reads A[perm[q]], writes B[q] and ranks the particle for
+//                  the next cell order (order.cu).
 //   moments_basic  Eq. 3: 10 moments x 8 corners per
 //                  particle, global fp64 atomics (RED.E.ADD.F64) into the
 //                  ghosted node arrays.
 //
-// This family is the simple reference path on the GPU (and the far-flyer /
-// odd-config fallback of the tiled path): correct for every config, no sort
-// needed, but the deposit costs 80 global atomics per particle.
+// This family is the simple reference path on the GPU: correct for every
+// config, but the deposit costs 80 global atomics per particle.
 #include "pic_internal.cuh"
 
 namespace pic {
 
-__global__ void __launch_bounds__(256) mover_basic_kernel(
-    Geom g, double *__restrict__ X, double *__restrict__ Y, double *__restrict__ Z,
-    double *__restrict__ U, double *__restrict__ V, double *__restrict__ W,
-    uint32_t *__restrict__ key_new, const double *__restrict__ F, int64_t n, double ks,
-    double ks_c, int n_iter, unsigned long long *__restrict__ stats) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const double xn[3] = {X[p], Y[p], Z[p]};
-  const double vn[3] = {U[p], V[p], W[p]};
-  const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1],
-                       0.5 * g.dt * g.inv_delta[2]};
-  double xb[3] = {xn[0], xn[1], xn[2]};
-  double vb[3] = {vn[0], vn[1], vn[2]};
-  bool clamped = false;
-  for (int it = 0; it < n_iter; ++it) {
-    double EB[6];
-    clamped |= sample_window(g, F, xb, EB);
-    double vt[3], a[3];
+struct MoverArgs {
+  Geom g;
+  const double *src[7];
+  const int64_t *src_id;
+  double *dst[7];
+  int64_t *dst_id;
+  const uint32_t *perm;
+  const uint32_t *cell_off;   // cell_off[ncells] = number of particles to move
+  uint32_t *key_new, *rank, *cell_count;
+  int64_t *d_nraw;
+  const double *F;
+  unsigned long long *stats;
+  double ks, ks_c;
+  int n_iter;
+};
+
+__global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
+  const Geom &g = A.g;
+  const int64_t n = A.cell_off[g.ncells];
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q == 0) *A.d_nraw = n;
+  if ((int64_t)blockIdx.x * blockDim.x >= n) return;   // whole warps leave together
+  const bool act = q < n;
+  uint32_t k = KEY_DEAD;
+  if (act) {
+    const uint32_t p = A.perm[q];
+    const double xn[3] = {A.src[0][p], A.src[1][p], A.src[2][p]};
+    const double vn[3] = {A.src[3][p], A.src[4][p], A.src[5][p]};
+    const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
+    double xb[3] = {xn[0], xn[1], xn[2]};
+    double vb[3] = {vn[0], vn[1], vn[2]};
+    bool clamped = false;
+    for (int it = 0; it < A.n_iter; ++it) {
+      double EB[6];
+      clamped |= sample_window(g, A.F, xb, EB);
+      double vt[3], a[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) { vt[d] = fma(ks, EB[d], vn[d]); a[d] = ks_c * EB[3 + d]; }
-    const double cr0 = vt[1] * a[2] - vt[2] * a[1];
-    const double cr1 = vt[2] * a[0] - vt[0] * a[2];
-    const double cr2 = vt[0] * a[1] - vt[1] * a[0];
-    const double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
-    const double invD = 1.0 / (1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2]));
-    vb[0] = (vt[0] + cr0 + dot * a[0]) * invD;
-    vb[1] = (vt[1] + cr1 + dot * a[1]) * invD;
-    vb[2] = (vt[2] + cr2 + dot * a[2]) * invD;
+      for (int d = 0; d < 3; ++d) { vt[d] = fma(A.ks, EB[d], vn[d]); a[d] = A.ks_c * EB[3 + d]; }
+      const double cr0 = vt[1] * a[2] - vt[2] * a[1];
+      const double cr1 = vt[2] * a[0] - vt[0] * a[2];
+      const double cr2 = vt[0] * a[1] - vt[1] * a[0];
+      const double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
+      const double invD = 1.0 / (1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2]));
+      vb[0] = (vt[0] + cr0 + dot * a[0]) * invD;
+      vb[1] = (vt[1] + cr1 + dot * a[1]) * invD;
+      vb[2] = (vt[2] + cr2 + dot * a[2]) * invD;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
+      for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
+    }
+    double xnew[3], vnew[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
+      vnew[d] = fma(2.0, vb[d], -vn[d]);
+    }
+    k = finish_particle(g, xnew, vnew, clamped, A.stats);
+    A.dst[0][q] = xnew[0]; A.dst[1][q] = xnew[1]; A.dst[2][q] = xnew[2];
+    A.dst[3][q] = vnew[0]; A.dst[4][q] = vnew[1]; A.dst[5][q] = vnew[2];
+    A.dst[6][q] = A.src[6][p];
+    A.dst_id[q] = A.src_id[p];
+    A.key_new[q] = k;
   }
-  double xnew[3], vnew[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
-    vnew[d] = fma(2.0, vb[d], -vn[d]);
-  }
-  const uint32_t k = finish_particle(g, xnew, vnew, clamped, stats);
-  X[p] = xnew[0]; Y[p] = xnew[1]; Z[p] = xnew[2];
-  U[p] = vnew[0]; V[p] = vnew[1]; W[p] = vnew[2];
-  key_new[p] = k;
+  const bool counted = act && k < KEY_FIRST_RESERVED;
+  const uint32_t r = count_rank(A.cell_count, k, counted);
+  if (counted) A.rank[q] = r;
 }
 
 __global__ void __launch_bounds__(256) moments_basic_kernel(
     Geom g, const double *__restrict__ X, const double *__restrict__ Y,
     const double *__restrict__ Z, const double *__restrict__ U, const double *__restrict__ V,
     const double *__restrict__ W, const double *__restrict__ Q, const uint32_t *__restrict__ key,
-    int64_t n, double *__restrict__ mom, unsigned long long *__restrict__ stats) {
+    const int64_t *__restrict__ d_nraw, double *__restrict__ mom, unsigned long long *__restrict__ stats) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
+  if (p >= *d_nraw) return;
   const uint32_t k = key[p];
   if (k == KEY_DEAD) return;
   double xi[3] = {X[p], Y[p], Z[p]};
@@ -91,7 +116,7 @@ __global__ void __launch_bounds__(256) moments_basic_kernel(
   const double val[10] = {q, qu, qv, qw, qu * u, qu * v, qu * w, qv * v, qv * w, qw * w};
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
+    const int bx = c & 1, by = (c >> 1) & 1, bz = c >> 2;
     const double S = (bx ? f[0] : 1.0 - f[0]) * (by ? f[1] : 1.0 - f[1]) * (bz ? f[2] : 1.0 - f[2]);
     const int64_t node = ((idx[2] + bz) * g.m_n[1] + (idx[1] + by)) * g.m_n[0] + (idx[0] + bx);
 #pragma unroll
@@ -101,25 +126,40 @@ __global__ void __launch_bounds__(256) moments_basic_kernel(
 
 pic_status launch_mover_basic(Ctx *ctx, int s) {
   SpeciesStore &S = ctx->sp[s];
-  if (S.n == 0) return PIC_OK;
-  const double ks = S.qom * (ctx->geom.dt * 0.5);
-  const double ks_c = ks / ctx->geom.c;
+  pic_status st = zero_cell_counts(ctx, s);
+  if (st != PIC_OK) return st;
+  MoverArgs A;
+  A.g = ctx->geom;
+  for (int k = 0; k < 7; ++k) { A.src[k] = S.a[k]; A.dst[k] = S.b[k]; }
+  A.src_id = S.id;
+  A.dst_id = S.id_b;
+  A.perm = S.perm;
+  A.cell_off = S.cell_off;
+  A.key_new = S.key_new;
+  A.rank = S.rank;
+  A.cell_count = S.cell_count;
+  A.d_nraw = S.d_nraw;
+  A.F = ctx->field;
+  A.stats = ctx->stats;
+  A.ks = S.qom * (ctx->geom.dt * 0.5);
+  A.ks_c = A.ks / ctx->geom.c;
+  A.n_iter = S.n_iter;
   const int threads = 256;
-  const int64_t blocks = (S.n + threads - 1) / threads;
-  mover_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
-      ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.key_new, ctx->field, S.n, ks,
-      ks_c, S.n_iter, ctx->stats); ++ctx->launches;
+  const int64_t blocks = std::max<int64_t>(1, (S.n_raw + threads - 1) / threads);
+  mover_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
+  S.swap_buffers();
+  S.order_valid = false;
   return PIC_OK;
 }
 
 pic_status launch_moments_basic(Ctx *ctx, int s) {
   SpeciesStore &S = ctx->sp[s];
-  if (S.n == 0) return PIC_OK;
+  if (S.n_raw == 0) return PIC_OK;
   const int threads = 256;
-  const int64_t blocks = (S.n + threads - 1) / threads;
+  const int64_t blocks = (S.n_raw + threads - 1) / threads;
   moments_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
-      ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.a[6], S.key_new, S.n, S.mom,
+      ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.a[6], S.key_new, S.d_nraw, S.mom,
       ctx->stats); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;

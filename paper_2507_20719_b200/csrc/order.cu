@@ -1,0 +1,90 @@
+// order.cu — cell order of the particle store by a counting sort through an
+// indirection (not a step of the paper, which sorts only
+// for coalescence).
+//
+// The mover ranks every particle that stays on this rank within its new cell
+// (count_rank, warp-aggregated atomics on cell_count) while it moves; the
+// exchange ranks received particles the same way.  build_order then turns the
+// counts into cell offsets (exclusive scan) and scatters perm[cell_off[k] +
+// rank] = position, key[...] = k.  The next mover gathers its inputs through
+// perm and writes them in that order, so no separate permutation pass over the
+// particle data is ever needed (≈ 16 B / particle of order metadata instead of
+// a radix sort + gather of all arrays).  Removed particles and slab leavers are
+// not counted and so drop out of the next order.
+#include <cub/device/device_scan.cuh>
+
+#include "pic_internal.cuh"
+
+namespace pic {
+
+static unsigned grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+size_t order_temp_bytes(int64_t ncells) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                (int)(ncells + 1));
+  return bytes + 1024;
+}
+
+__global__ void count_kernel(const uint32_t *__restrict__ key_new, uint32_t *__restrict__ rank,
+                             uint32_t *__restrict__ cell_count, int64_t from, int64_t to) {
+  // grid-stride loop with whole warps (count_rank is warp-collective)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = from + (int64_t)blockIdx.x * blockDim.x; base < to; base += stride) {
+    const int64_t p = base + threadIdx.x;
+    const bool act = p < to;
+    const uint32_t k = act ? key_new[p] : KEY_DEAD;
+    const bool counted = act && k < KEY_FIRST_RESERVED;
+    const uint32_t r = count_rank(cell_count, k, counted);
+    if (counted) rank[p] = r;
+  }
+}
+
+__global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t *__restrict__ rank,
+                            const uint32_t *__restrict__ cell_off, const int64_t *__restrict__ d_nraw,
+                            uint32_t *__restrict__ perm, uint32_t *__restrict__ key) {
+  const int64_t n = *d_nraw;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = key_new[p];
+    if (k >= KEY_FIRST_RESERVED) continue;
+    const uint32_t q = cell_off[k] + rank[p];
+    perm[q] = (uint32_t)p;
+    key[q] = k;
+  }
+}
+
+pic_status zero_cell_counts(Ctx *ctx, int s) {
+  PIC_CUDA(cudaMemsetAsync(ctx->sp[s].cell_count, 0, sizeof(uint32_t) * (ctx->geom.ncells + 1), ctx->stream));
+  return PIC_OK;
+}
+
+pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to) {
+  SpeciesStore &sp = ctx->sp[s];
+  if (to <= from) return PIC_OK;
+  count_kernel<<<grid_for(to - from), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_count, from, to); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  return PIC_OK;
+}
+
+// Exclusive scan of the counts and the perm / key scatter (positions [0, d_nraw)).
+pic_status build_order(Ctx *ctx, int s) {
+  SpeciesStore &sp = ctx->sp[s];
+  const int64_t nc = ctx->geom.ncells;
+  size_t bytes = ctx->cub_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(ctx->cub_temp, bytes, sp.cell_count, sp.cell_off, (int)(nc + 1),
+                                                ctx->stream);
+  if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("scan: ") + cudaGetErrorString(e));
+  if (sp.n_raw > 0) {
+    perm_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_off, sp.d_nraw, sp.perm,
+                                                             sp.key); ++ctx->launches;
+  }
+  PIC_CUDA(cudaGetLastError());
+  sp.order_valid = true;
+  return PIC_OK;
+}
+
+}  // namespace pic

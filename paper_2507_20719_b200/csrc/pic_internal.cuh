@@ -1,13 +1,14 @@
 // pic_internal.cuh — context, store layout and shared device helpers of libpic.
 //
 // Internal representation:
-//   * particle store, per species, SoA fp64: xi_x, xi_y, xi_z (positions in
-//     GLOBAL CELL UNITS, xi_d = x_d / Delta_d), u, v, w (velocity, caller
-//     units), q (charge q_s w_p, R14); int64 id.  One spare fp64 array
-//     (`scratch`) lets the sort / compaction permute one array at a time.
-//   * key (uint32 per particle), written by the mover: the local cell index of
-//     x^{n+1} for live particles that stay, or one of the reserved tail keys
-//     KEY_LEFT / KEY_RIGHT (slab leavers) / KEY_DEAD (removed, R21).
+//   * particle store, per species, SoA fp64 in two buffers (A = state, B =
+//     mover destination): xi_x, xi_y, xi_z (positions in GLOBAL CELL UNITS,
+//     xi_d = x_d / Delta_d), u, v, w (velocity, caller units), q (charge
+//     q_s w_p, R14); int64 id.  The cell order is an indirection (perm) built
+//     by a counting sort (order.cu, SpeciesStore below).
+//   * key_new (uint32 per particle), written by the mover: the tile-major cell
+//     key of x^{n+1} for live particles that stay, or one of the reserved tail
+//     keys KEY_LEFT / KEY_RIGHT (slab leavers) / KEY_DEAD (removed, R21).
 //   * field window: node-interleaved [kz][ky][kx][6] fp64, exactly the layout
 //     of pic_set_fields (global nodes [slab_lo-G, slab_hi+G] x [-G, Ny+G] x
 //     [-G, Nz+G]).
@@ -16,6 +17,7 @@
 //     x planes [slab_lo-G, slab_hi+G], y planes [0, Ny], z planes [0, Nz]
 //     (the extra periodic plane is folded by pic_exchange, R18).
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -60,6 +62,7 @@ struct Geom {
   int64_t k_n[3];         // local cells (slab_hi-slab_lo, Ny, Nz)
   int64_t nt[3];          // tiles per axis (ceil(k_n / TILE))
   int64_t ntiles;
+  int64_t ncells;         // ntiles * TILE^3 (key range)
 };
 
 // Cell tiles of TILE^3 cells: the sort key is tile-major,
@@ -74,21 +77,38 @@ __host__ __device__ __forceinline__ uint32_t tile_key(const Geom &g, int64_t lx,
   return (uint32_t)(t * TILE3 + (lx % TILE) + TILE * (ly % TILE) + TILE * TILE * (lz % TILE));
 }
 
+// Particle store of one species.  Buffer A holds the state at
+// positions [0, n_raw); the cell order of the live particles is an indirection:
+// perm[q] = A-position of the q-th particle in tile-major cell order, key[q] its
+// key, cell_off[c] the first q of cell c (exclusive scan of cell_count, built by
+// a counting sort whose ranks the mover produces while it moves).  The movers
+// gather A[perm[q]] and write B[q] (then A <-> B), so the store comes out of
+// every cycle already in the order of the next one.  Dead particles and slab
+// leavers are simply not counted, which drops them from the next order.
 struct SpeciesStore {
-  double *a[7] = {};      // xi_x xi_y xi_z u v w q
+  double *a[7] = {};      // A: xi_x xi_y xi_z u v w q
   int64_t *id = nullptr;
-  uint32_t *key = nullptr;        // sort-time keys, in store order (valid while sorted)
-  uint32_t *key_new = nullptr;    // keys of the current positions (mover / recompute)
-  uint32_t *idx = nullptr;
-  uint32_t *idx_alt = nullptr;
-  uint32_t *tile_start = nullptr; // [ntiles + 1] segment starts of the sorted store
+  double *b[7] = {};      // B: mover destination
+  int64_t *id_b = nullptr;
+  uint32_t *key_new = nullptr;    // [cap] key of the particle at A-position p
+  uint32_t *rank = nullptr;       // [cap] rank of A-position p within its cell
+  uint32_t *perm = nullptr;       // [cap] q -> A-position (cell order)
+  uint32_t *key = nullptr;        // [cap] key[q] = key_new[perm[q]]
+  uint32_t *cell_count = nullptr; // [ncells + 1]
+  uint32_t *cell_off = nullptr;   // [ncells + 1]; cell_off[ncells] = live count
+  int64_t *d_nraw = nullptr;      // device scalar: number of A positions
   double *mom = nullptr;  // [10][m_plane]
-  int64_t n = 0;          // live particles (host mirror, exact after exchange)
+  int64_t n_raw = 0;      // host upper bound of the A positions in use
+  int64_t n = 0;          // host mirror of the live count (exact after pic_count / sync)
   int64_t cap = 0;
   double qom = 0;
   int32_t n_iter = 3;
   bool moved = false, deposited = false, fused_deposit = false;
-  bool sorted = false;
+  bool order_valid = false;
+  void swap_buffers() {
+    for (int k = 0; k < 7; ++k) { double *t = a[k]; a[k] = b[k]; b[k] = t; }
+    int64_t *t = id; id = id_b; id_b = t;
+  }
 };
 
 struct Ctx {
@@ -96,7 +116,6 @@ struct Ctx {
   Geom geom;
   cudaStream_t stream = nullptr;
   SpeciesStore sp[PIC_MAX_SPECIES];
-  double *scratch = nullptr;         // cap_max doubles
   double *field = nullptr;           // window
   int64_t field_elems = 0;
   bool fields_set = false;
@@ -143,14 +162,17 @@ inline pic_status fail(Ctx *ctx, pic_status s, const std::string &m) {
 pic_status launch_mover_basic(Ctx *ctx, int s);
 pic_status launch_moments_basic(Ctx *ctx, int s);
 pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit);
-pic_status sort_species(Ctx *ctx, int s);
-size_t sort_temp_bytes(int64_t cap);
+size_t order_temp_bytes(int64_t ncells);
+pic_status zero_cell_counts(Ctx *ctx, int s);
+pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to);
+pic_status build_order(Ctx *ctx, int s);
 pic_status exchange(Ctx *ctx);
-pic_status recompute_keys(Ctx *ctx, int s, int64_t from);
+pic_status recompute_keys(Ctx *ctx, int s, int64_t from, int64_t to);
 pic_status zero_moments(Ctx *ctx, int s);
 pic_status pack_moments(Ctx *ctx, int s, double *out);
 pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
 pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id);
+pic_status live_count(Ctx *ctx, int s, int64_t *n);
 
 // ---------------------------------------------------------- device helpers ---
 // Periodic wrap of a cell-unit coordinate (R10): one wrap, then test.
@@ -245,6 +267,20 @@ __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3
   }
   if (clamped) atomicAdd(&stats[ST_CLAMPED], 1ull);
   return k;
+}
+
+// Rank of a live particle within its cell for the counting sort: the lanes of
+// a warp holding the same key share one global atomicAdd.  All 32 lanes must
+// call it; `counted == false` lanes get no rank.
+__device__ __forceinline__ uint32_t count_rank(uint32_t *__restrict__ cell_count, uint32_t k, bool counted) {
+  const unsigned kk = counted ? k : 0xFFFFFFFFu;
+  const unsigned peers = __match_any_sync(0xffffffffu, kk);
+  const unsigned lane = threadIdx.x & 31u;
+  const int leader = __ffs(peers) - 1;
+  uint32_t base = 0;
+  if (counted && (int)lane == leader) base = atomicAdd(cell_count + k, (unsigned)__popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
 }
 
 // Map a global node index to the ghosted moment array (x: ghost planes; y, z:

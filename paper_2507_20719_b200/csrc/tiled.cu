@@ -44,11 +44,15 @@ constexpr size_t SMEM_BYTES = sizeof(double) * (NB3 * 6 + 10 * NB3 + WARPS * WBU
 
 struct TiledArgs {
   Geom g;
-  double *X, *Y, *Z, *U, *V, *W;
-  const double *Q;
-  const uint32_t *key;        // sort-time keys (store order)
-  uint32_t *key_new;
-  const uint32_t *tile_start;
+  const double *src[7];       // buffer A (read through perm)
+  const int64_t *src_id;
+  double *dst[7];             // buffer B (written in cell order)
+  int64_t *dst_id;
+  const uint32_t *perm;       // q -> A-position
+  const uint32_t *key;        // key[q]: sort-time key (cell c0 of x^n)
+  const uint32_t *cell_off;   // tile t covers q in [cell_off[64 t], cell_off[64 (t+1)])
+  uint32_t *key_new, *rank, *cell_count;
+  int64_t *d_nraw;
   const double *field;        // global window (fallback sampling)
   double *mom;                // ghosted moment arrays [10][m_plane]
   unsigned long long *stats;
@@ -146,7 +150,8 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
   const Geom &g = A.g;
 
   const int tile = blockIdx.x;
-  const uint32_t p0 = A.tile_start[tile], p1 = A.tile_start[tile + 1];
+  if (tile == 0 && threadIdx.x == 0) *A.d_nraw = A.cell_off[g.ncells];
+  const uint32_t p0 = A.cell_off[(int64_t)tile * TILE3], p1 = A.cell_off[(int64_t)(tile + 1) * TILE3];
   if (p0 == p1) return;
   const int tx = (int)(tile % g.nt[0]);
   const int ty = (int)((tile / g.nt[0]) % g.nt[1]);
@@ -217,11 +222,15 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
 #pragma unroll
     for (int m = 0; m < 10; ++m) val[m] = 0.0;
     int64_t c1g[3] = {0, 0, 0};
+    uint32_t knew_l = KEY_DEAD;
     if (act) {
       c0 = (int)(A.key[p] & (TILE3 - 1));
-      const double xn[3] = {A.X[p], A.Y[p], A.Z[p]};
-      const double vn[3] = {A.U[p], A.V[p], A.W[p]};
-      const double q = A.Q[p];
+      const uint32_t sp_ = A.perm[p];
+      const double xn[3] = {A.src[0][sp_], A.src[1][sp_], A.src[2][sp_]};
+      const double vn[3] = {A.src[3][sp_], A.src[4][sp_], A.src[5][sp_]};
+      const double q = A.src[6][sp_];
+      A.dst[6][p] = q;
+      A.dst_id[p] = A.src_id[sp_];
       double xb[3] = {xn[0], xn[1], xn[2]};
       double vb[3];
       bool clamped = false;
@@ -253,9 +262,10 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
       }
       const double xdep[3] = {xnew[0], xnew[1], xnew[2]};  // pre-wrap: deposit position
       const uint32_t knew = finish_particle(g, xnew, vnew, clamped, A.stats);
-      A.X[p] = xnew[0]; A.Y[p] = xnew[1]; A.Z[p] = xnew[2];
-      A.U[p] = vnew[0]; A.V[p] = vnew[1]; A.W[p] = vnew[2];
+      A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
+      A.dst[3][p] = vnew[0]; A.dst[4][p] = vnew[1]; A.dst[5][p] = vnew[2];
       A.key_new[p] = knew;
+      knew_l = knew;
       if (knew != KEY_DEAD) {
         alive = true;
         // values q {1, v, vv} (Eq. 3, R16 order)
@@ -282,6 +292,12 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
                     ? (int)((bz * NB + by) * NB + bx) : -2;   // -2: outside the box
         }
       }
+    }
+    // rank for the next cell order (order.cu); leavers and removed are not counted
+    {
+      const bool counted = act && knew_l < KEY_FIRST_RESERVED;
+      const uint32_t r = count_rank(A.cell_count, knew_l, counted);
+      if (counted) A.rank[p] = r;
     }
     // stage S (corner-major per 4-particle group) and the 10 values, lane order
     {
@@ -425,11 +441,6 @@ static pic_status make_tmap(Ctx *ctx) {
 pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   *did_deposit = false;
   SpeciesStore &sp = ctx->sp[s];
-  const int se = ctx->cfg.sort_every;
-  if (!sp.sorted || (se > 0 && ctx->cycle % se == 0)) {
-    pic_status st = sort_species(ctx, s);
-    if (st != PIC_OK) return st;
-  }
   if (!ctx->tmap_ok) {
     pic_status st = make_tmap(ctx);
     if (st != PIC_OK) return st;
@@ -437,16 +448,20 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   }
   pic_status st = zero_moments(ctx, s);
   if (st != PIC_OK) return st;
-  if (sp.n == 0) {
-    *did_deposit = true;
-    return PIC_OK;
-  }
+  st = zero_cell_counts(ctx, s);
+  if (st != PIC_OK) return st;
   TiledArgs A;
   A.g = ctx->geom;
-  A.X = sp.a[0]; A.Y = sp.a[1]; A.Z = sp.a[2]; A.U = sp.a[3]; A.V = sp.a[4]; A.W = sp.a[5]; A.Q = sp.a[6];
+  for (int k = 0; k < 7; ++k) { A.src[k] = sp.a[k]; A.dst[k] = sp.b[k]; }
+  A.src_id = sp.id;
+  A.dst_id = sp.id_b;
+  A.perm = sp.perm;
   A.key = sp.key;
+  A.cell_off = sp.cell_off;
   A.key_new = sp.key_new;
-  A.tile_start = sp.tile_start;
+  A.rank = sp.rank;
+  A.cell_count = sp.cell_count;
+  A.d_nraw = sp.d_nraw;
   A.field = ctx->field;
   A.mom = sp.mom;
   A.stats = ctx->stats;
@@ -456,6 +471,8 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   tiled_kernel<<<(unsigned)ctx->geom.ntiles, THREADS, SMEM_BYTES, ctx->stream>>>(
       *reinterpret_cast<const CUtensorMap *>(ctx->tmap), A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
+  sp.swap_buffers();
+  sp.order_valid = false;
   *did_deposit = true;
   return PIC_OK;
 }
