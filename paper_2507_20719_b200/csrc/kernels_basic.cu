@@ -23,6 +23,7 @@ struct MoverArgs {
   double *dst[7];
   int64_t *dst_id;
   const uint32_t *perm;
+  const uint32_t *key;        // key[q]: cell of x^n (stayer test)
   const uint32_t *cell_off;   // cell_off[ncells] = number of particles to move
   uint32_t *key_new, *rank, *cell_count;
   int64_t *d_nraw;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
     A.key_new[q] = k;
   }
   const bool counted = act && k < KEY_FIRST_RESERVED;
-  const uint32_t r = count_rank(A.cell_count, k, counted);
+  const uint32_t r = count_rank(A.cell_count, g.ncells, k, counted, !act || k != A.key[q]);
   if (counted) A.rank[q] = r;
 }
 
@@ -134,6 +135,7 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   A.src_id = S.id;
   A.dst_id = S.id_b;
   A.perm = S.perm;
+  A.key = S.key;
   A.cell_off = S.cell_off;
   A.key_new = S.key_new;
   A.rank = S.rank;

@@ -31,7 +31,7 @@ size_t order_temp_bytes(int64_t ncells) {
 }
 
 __global__ void count_kernel(const uint32_t *__restrict__ key_new, uint32_t *__restrict__ rank,
-                             uint32_t *__restrict__ cell_count, int64_t from, int64_t to) {
+                             uint32_t *__restrict__ cell_count, int64_t ncells, int64_t from, int64_t to) {
   // grid-stride loop with whole warps (count_rank is warp-collective)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = from + (int64_t)blockIdx.x * blockDim.x; base < to; base += stride) {
@@ -39,33 +39,41 @@ __global__ void count_kernel(const uint32_t *__restrict__ key_new, uint32_t *__r
     const bool act = p < to;
     const uint32_t k = act ? key_new[p] : KEY_DEAD;
     const bool counted = act && k < KEY_FIRST_RESERVED;
-    const uint32_t r = count_rank(cell_count, k, counted);
+    const uint32_t r = count_rank(cell_count, ncells, k, counted, true);
     if (counted) rank[p] = r;
   }
 }
 
+__global__ void total_kernel(const uint32_t *__restrict__ cell_count, uint32_t *__restrict__ tot, int64_t ncells) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= ncells; c += (int64_t)gridDim.x * blockDim.x)
+    tot[c] = cell_count[c] + cell_count[ncells + 1 + c];
+}
+
 __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t *__restrict__ rank,
-                            const uint32_t *__restrict__ cell_off, const int64_t *__restrict__ d_nraw,
-                            uint32_t *__restrict__ perm, uint32_t *__restrict__ key) {
+                            const uint32_t *__restrict__ cell_off, const uint32_t *__restrict__ cell_count,
+                            const int64_t *__restrict__ d_nraw, uint32_t *__restrict__ perm,
+                            uint32_t *__restrict__ key) {
   const int64_t n = *d_nraw;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = key_new[p];
     if (k >= KEY_FIRST_RESERVED) continue;
-    const uint32_t q = cell_off[k] + rank[p];
+    const uint32_t r = rank[p];
+    const uint32_t q = cell_off[k] + ((r & RANK_ARRIVAL) ? cell_count[k] + (r & ~RANK_ARRIVAL) : r);
     perm[q] = (uint32_t)p;
     key[q] = k;
   }
 }
 
 pic_status zero_cell_counts(Ctx *ctx, int s) {
-  PIC_CUDA(cudaMemsetAsync(ctx->sp[s].cell_count, 0, sizeof(uint32_t) * (ctx->geom.ncells + 1), ctx->stream));
+  PIC_CUDA(cudaMemsetAsync(ctx->sp[s].cell_count, 0, sizeof(uint32_t) * 2 * (ctx->geom.ncells + 1), ctx->stream));
   return PIC_OK;
 }
 
 pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to) {
   SpeciesStore &sp = ctx->sp[s];
   if (to <= from) return PIC_OK;
-  count_kernel<<<grid_for(to - from), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_count, from, to); ++ctx->launches;
+  count_kernel<<<grid_for(to - from), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_count,
+                                                              ctx->geom.ncells, from, to); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }
@@ -74,13 +82,14 @@ pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to) {
 pic_status build_order(Ctx *ctx, int s) {
   SpeciesStore &sp = ctx->sp[s];
   const int64_t nc = ctx->geom.ncells;
+  total_kernel<<<grid_for(nc + 1), 256, 0, ctx->stream>>>(sp.cell_count, sp.cell_tot, nc); ++ctx->launches;
   size_t bytes = ctx->cub_bytes;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(ctx->cub_temp, bytes, sp.cell_count, sp.cell_off, (int)(nc + 1),
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(ctx->cub_temp, bytes, sp.cell_tot, sp.cell_off, (int)(nc + 1),
                                                 ctx->stream);
   if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("scan: ") + cudaGetErrorString(e));
   if (sp.n_raw > 0) {
-    perm_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_off, sp.d_nraw, sp.perm,
-                                                             sp.key); ++ctx->launches;
+    perm_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_off, sp.cell_count,
+                                                             sp.d_nraw, sp.perm, sp.key); ++ctx->launches;
   }
   PIC_CUDA(cudaGetLastError());
   sp.order_valid = true;

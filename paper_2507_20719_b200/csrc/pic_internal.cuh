@@ -94,7 +94,8 @@ struct SpeciesStore {
   uint32_t *rank = nullptr;       // [cap] rank of A-position p within its cell
   uint32_t *perm = nullptr;       // [cap] q -> A-position (cell order)
   uint32_t *key = nullptr;        // [cap] key[q] = key_new[perm[q]]
-  uint32_t *cell_count = nullptr; // [ncells + 1]
+  uint32_t *cell_count = nullptr; // [2][ncells + 1]: stayers (kept their cell), arrivals
+  uint32_t *cell_tot = nullptr;   // [ncells + 1] stayers + arrivals (scan input)
   uint32_t *cell_off = nullptr;   // [ncells + 1]; cell_off[ncells] = live count
   int64_t *d_nraw = nullptr;      // device scalar: number of A positions
   double *mom = nullptr;  // [10][m_plane]
@@ -270,17 +271,24 @@ __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3
 }
 
 // Rank of a live particle within its cell for the counting sort: the lanes of
-// a warp holding the same key share one global atomicAdd.  All 32 lanes must
-// call it; `counted == false` lanes get no rank.
-__device__ __forceinline__ uint32_t count_rank(uint32_t *__restrict__ cell_count, uint32_t k, bool counted) {
-  const unsigned kk = counted ? k : 0xFFFFFFFFu;
+// a warp holding the same key share one global atomicAdd.  Particles that kept
+// their cell ("stayers") and arrivals are counted separately so that, in the
+// next order, every cell lists its stayers first, in their previous order (a
+// contiguous run of the previous store: coalesced gathers), then its arrivals;
+// arrivals carry bit 31 in the rank.  All 32 lanes must call it; `counted ==
+// false` lanes get no rank.
+constexpr uint32_t RANK_ARRIVAL = 0x80000000u;
+__device__ __forceinline__ uint32_t count_rank(uint32_t *__restrict__ cell_count, int64_t ncells, uint32_t k,
+                                               bool counted, bool arrival) {
+  const unsigned kk = counted ? (k | (arrival ? RANK_ARRIVAL : 0u)) : 0xFFFFFFFFu;
   const unsigned peers = __match_any_sync(0xffffffffu, kk);
   const unsigned lane = threadIdx.x & 31u;
   const int leader = __ffs(peers) - 1;
   uint32_t base = 0;
-  if (counted && (int)lane == leader) base = atomicAdd(cell_count + k, (unsigned)__popc(peers));
+  if (counted && (int)lane == leader)
+    base = atomicAdd(cell_count + (arrival ? ncells + 1 : 0) + k, (unsigned)__popc(peers));
   base = __shfl_sync(0xffffffffu, base, leader);
-  return base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+  return (base + (uint32_t)__popc(peers & ((1u << lane) - 1u))) | (arrival ? RANK_ARRIVAL : 0u);
 }
 
 // Map a global node index to the ghosted moment array (x: ghost planes; y, z:

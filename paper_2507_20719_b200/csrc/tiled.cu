@@ -213,6 +213,13 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
+    // prefetch the next round's gathered sources into L1 while this round computes
+    if (p + 32 < wend) {
+      const uint32_t pn = A.perm[p + 32];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + pn));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src_id + pn));
+    }
     int c0 = 0;          // sort-time local cell (0..63)
     int c1b = -1;        // new cell in box coordinates (bx + NB (by + NB bz)) of a crosser
     bool alive = false, crosser = false;
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
     // rank for the next cell order (order.cu); leavers and removed are not counted
     {
       const bool counted = act && knew_l < KEY_FIRST_RESERVED;
-      const uint32_t r = count_rank(A.cell_count, knew_l, counted);
+      const uint32_t r = count_rank(A.cell_count, g.ncells, knew_l, counted, !act || knew_l != A.key[p]);
       if (counted) A.rank[p] = r;
     }
     // stage S (corner-major per 4-particle group) and the 10 values, lane order
