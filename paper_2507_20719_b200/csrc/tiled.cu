@@ -104,6 +104,27 @@ __device__ __forceinline__ double rcp_ge1(double D) {
   return fma(r, e, r);
 }
 
+// N independent fp64 additions into shared memory with compare-and-swap
+// (sm_100 has no native shared fp64 add): the N CAS chains are issued together
+// so their latencies overlap.  Bit i of `valid` enables entry i.
+template <int N>
+__device__ __forceinline__ void smem_add_batch(double *const *addr, const double *val, unsigned valid) {
+  unsigned long long cur[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) cur[i] = ((valid >> i) & 1u) ? *reinterpret_cast<unsigned long long *>(addr[i]) : 0ull;
+  while (valid) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if ((valid >> i) & 1u) {
+        const unsigned long long want = __double_as_longlong(__longlong_as_double(cur[i]) + val[i]);
+        const unsigned long long got = atomicCAS(reinterpret_cast<unsigned long long *>(addr[i]), cur[i], want);
+        if (got == cur[i]) valid &= ~(1u << i);
+        else cur[i] = got;
+      }
+    }
+  }
+}
+
 // Trilinear gather of the pre-scaled fields from the staged box.  u = position
 // in box node units.  Returns false if the 8 nodes are not all in the box.
 __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, const double u[3], double out[6]) {
@@ -201,11 +222,23 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
     }
     const int cx = c & 3, cy = (c >> 2) & 3, cz = c >> 4;
     const int node = ((cz + kbz + 1) * NB + (cy + kby + 1)) * NB + (cx + kbx + 1);
+    double *ad[3];
+    double vl[3];
+    unsigned valid = 0;
 #pragma unroll
-    for (int m = 0; m < 10; ++m) {
-      if ((m & 3) == js && accr[m] != 0.0) atomicAdd(acc + m * NB3 + node, accr[m]);
-      accr[m] = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      const int m = js + 4 * i;
+      ad[i] = acc + (m < 10 ? m : 0) * NB3 + node;
+      double v = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < 10; ++mm)
+        if (mm == m) v = accr[mm];
+      vl[i] = v;
+      if (m < 10 && v != 0.0) valid |= 1u << i;
     }
+    smem_add_batch<3>(ad, vl, valid);
+#pragma unroll
+    for (int m = 0; m < 10; ++m) accr[m] = 0.0;
   };
 
   int *cl = reinterpret_cast<int *>(Vb + 32 * 10);  // crosser -> lane table (32 ints)
@@ -228,7 +261,6 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
     for (int k = 0; k < 8; ++k) Sk[k] = 0.0;
 #pragma unroll
     for (int m = 0; m < 10; ++m) val[m] = 0.0;
-    int64_t c1g[3] = {0, 0, 0};
     uint32_t knew_l = KEY_DEAD;
     if (act) {
       c0 = (int)(A.key[p] & (TILE3 - 1));
@@ -282,6 +314,7 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
         val[7] = qv * vnew[1]; val[8] = qv * vnew[2]; val[9] = qw * vnew[2];
         // trilinear weights of the 8 corners of the new cell c1 (R12)
         double f[3];
+        int64_t c1g[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           const double fl = floor(xdep[d]);
@@ -323,30 +356,59 @@ __global__ void __launch_bounds__(THREADS, 2) tiled_kernel(const __grid_constant
     // js) so the 32 lanes add distinct (node, component) pairs: the shared CAS
     // atomics never conflict inside the warp.
     const int ncross = __popc(xmask);
-    for (int r = 0; r < ncross; ++r) {
-      const int src = cl[r];
-      const int cb = __shfl_sync(0xffffffffu, c1b, src);
-      const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
-      const double *vv = Vb + src * 10;
-      if (cb >= 0) {
-        if (s != 0.0) {
-          const int node = cb + kbx + NB * (kby + NB * kbz);
-          for (int m = js; m < 10; m += 4) atomicAdd(acc + m * NB3 + node, s * vv[m]);
-        }
-      } else {
-        // crosser outside the staged box: global atomics (far movers, rare)
-        const int64_t gx = __shfl_sync(0xffffffffu, c1g[0], src);
-        const int64_t gy = __shfl_sync(0xffffffffu, c1g[1], src);
-        const int64_t gz = __shfl_sync(0xffffffffu, c1g[2], src);
-        if (s != 0.0) {
-          const int64_t node = moment_node(g, gx + kbx, gy + kby, gz + kbz);
-          if (node < 0) {
-            if (js == 0) atomicAdd(&A.stats[ST_FAR], 1ull);
-          } else {
-            for (int m = js; m < 10; m += 4) atomicAdd(A.mom + m * g.m_plane + node, s * vv[m]);
-          }
+    // crossers outside the staged box (far movers, rare): global atomics
+    if (__any_sync(0xffffffffu, crosser && c1b < 0)) {
+      for (int r = 0; r < ncross; ++r) {
+        const int src = cl[r];
+        const int cb = __shfl_sync(0xffffffffu, c1b, src);
+        if (cb >= 0) continue;
+        // re-derive the (pre-wrap) cell of the crosser from what the mover stored
+        const uint32_t qs = r0 + src;
+        double xs = A.dst[0][qs];
+        const uint32_t ks_ = A.key_new[qs];
+        if (ks_ == KEY_LEFT && xs >= (double)g.slab_hi) xs -= (double)g.ncell[0];
+        if (ks_ == KEY_RIGHT && xs < (double)g.slab_lo) xs += (double)g.ncell[0];
+        if (g.periodic[0] && !g.multi_rank && xs < (double)(ox - 1)) xs += (double)g.ncell[0];
+        if (g.periodic[0] && !g.multi_rank && xs >= (double)(ox + TILE + 1)) xs -= (double)g.ncell[0];
+        const int64_t gx = (int64_t)floor(xs);
+        const int64_t gy = (int64_t)floor(A.dst[1][qs]);
+        const int64_t gz = (int64_t)floor(A.dst[2][qs]);
+        const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
+        const double *vv = Vb + src * 10;
+        const int64_t node = moment_node(g, gx + kbx, gy + kby, gz + kbz);
+        if (node < 0) {
+          if (js == 0 && s != 0.0) atomicAdd(&A.stats[ST_FAR], 1ull);
+        } else {
+          for (int m = js; m < 10; m += 4) atomicAdd(A.mom + m * g.m_plane + node, s * vv[m]);
         }
       }
+    }
+    // two crossers per step: up to 6 independent shared CAS chains per lane
+    for (int r = 0; r < ncross; r += 2) {
+      double *ad[6];
+      double vl[6];
+      unsigned valid = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (r + t < ncross) {
+          const int src = cl[r + t];
+          const int cb = __shfl_sync(0xffffffffu, c1b, src);
+          const double s = Sb[(src >> 2) * SGRP + kc * 4 + (src & 3)];
+          const double *vv = Vb + src * 10;
+          const int node = cb + kbx + NB * (kby + NB * kbz);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int m = js + 4 * i;
+            ad[3 * t + i] = acc + m * NB3 + node;
+            vl[3 * t + i] = (m < 10) ? s * vv[m] : 0.0;
+            if (cb >= 0 && m < 10) valid |= 1u << (3 * t + i);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 3; ++i) { ad[3 * t + i] = acc; vl[3 * t + i] = 0.0; }
+        }
+      }
+      smem_add_batch<6>(ad, vl, valid);
     }
 
     // ---- pass A: particles still in their sort-time cell, register accumulation
