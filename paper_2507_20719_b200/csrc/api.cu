@@ -284,7 +284,7 @@ pic_status pic_count(pic_ctx *p, int32_t s, int64_t *n) {
   Ctx *ctx = C(p);
   pic_status st = check_species(ctx, s, false);
   if (st != PIC_OK) return st;
-  if (!ctx->sp[s].order_valid) return fail(ctx, PIC_ESTATE, "pic_count between pic_mover and pic_exchange");
+  if (ctx->sp[s].moved) return fail(ctx, PIC_ESTATE, "pic_count between pic_mover and pic_exchange");
   return live_count(ctx, s, n);
 }
 
@@ -293,7 +293,7 @@ pic_status pic_get_particles(pic_ctx *p, int32_t s, double *const xyzuvwq[7], in
   Ctx *ctx = C(p);
   pic_status st = check_species(ctx, s, false);
   if (st != PIC_OK) return st;
-  if (!ctx->sp[s].order_valid)
+  if (ctx->sp[s].moved)
     return fail(ctx, PIC_ESTATE, "pic_get_particles between pic_mover and pic_exchange");
   double *none[7] = {};
   return unload_particles(ctx, s, xyzuvwq ? xyzuvwq : none, id);
@@ -329,7 +329,6 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
     }
     sp.moved = true;
     sp.deposited = false;
-    sp.fused_deposit = fused;
   }
   return PIC_OK;
 }
@@ -344,14 +343,16 @@ pic_status pic_moments(pic_ctx *p, int32_t s) {
     if (ctx->sp[k].deposited) return fail(ctx, PIC_ESTATE, "pic_moments called twice without pic_exchange");
   for (int k = s0; k < s1; ++k) {
     SpeciesStore &sp = ctx->sp[k];
-    if (!sp.fused_deposit) {
+    if (use_tiled(ctx)) {
+      st = launch_tiled_deposit(ctx, k);
+      if (st != PIC_OK) return st;
+    } else {
       st = zero_moments(ctx, k);
       if (st != PIC_OK) return st;
       st = launch_moments_basic(ctx, k);
       if (st != PIC_OK) return st;
     }
     sp.deposited = true;
-    sp.fused_deposit = false;
   }
   return PIC_OK;
 }

@@ -327,10 +327,11 @@ pic_status exchange(Ctx *ctx) {
   if (ctx->cfg.nranks > 1) {
     st = migrate(ctx);
     if (st != PIC_OK) return st;
-  }
-  for (int s = 0; s < ctx->cfg.n_species; ++s) {
-    st = build_order(ctx, s);
-    if (st != PIC_OK) return st;
+    // received particles were appended and counted: rebuild the order
+    for (int s = 0; s < ctx->cfg.n_species; ++s) {
+      st = build_order(ctx, s);
+      if (st != PIC_OK) return st;
+    }
   }
   return PIC_OK;
 }

@@ -88,11 +88,13 @@ __global__ void __launch_bounds__(256) moments_basic_kernel(
     Geom g, const double *__restrict__ X, const double *__restrict__ Y,
     const double *__restrict__ Z, const double *__restrict__ U, const double *__restrict__ V,
     const double *__restrict__ W, const double *__restrict__ Q, const uint32_t *__restrict__ key,
-    const int64_t *__restrict__ d_nraw, double *__restrict__ mom, unsigned long long *__restrict__ stats) {
+    const int64_t *__restrict__ d_nraw, double *__restrict__ mom, unsigned long long *__restrict__ stats,
+    bool leavers_only) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= *d_nraw) return;
   const uint32_t k = key[p];
   if (k == KEY_DEAD) return;
+  if (leavers_only && k != KEY_LEFT && k != KEY_RIGHT) return;
   double xi[3] = {X[p], Y[p], Z[p]};
   // slab leavers deposit at their unwrapped position (ghost planes, R15)
   const double Nx = (double)g.ncell[0];
@@ -151,18 +153,17 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   mover_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   S.swap_buffers();
-  S.order_valid = false;
-  return PIC_OK;
+  return build_order(ctx, s);
 }
 
-pic_status launch_moments_basic(Ctx *ctx, int s) {
+pic_status launch_moments_basic(Ctx *ctx, int s, bool leavers_only) {
   SpeciesStore &S = ctx->sp[s];
   if (S.n_raw == 0) return PIC_OK;
   const int threads = 256;
   const int64_t blocks = (S.n_raw + threads - 1) / threads;
   moments_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
       ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.a[6], S.key_new, S.d_nraw, S.mom,
-      ctx->stats); ++ctx->launches;
+      ctx->stats, leavers_only); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }
