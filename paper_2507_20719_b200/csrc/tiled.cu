@@ -155,7 +155,10 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
 }
 
 // ----------------------------------------------------------------- mover ----
-__global__ void __launch_bounds__(THREADS, 3) mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap,
+#ifndef PIC_MOVER_MINB
+#define PIC_MOVER_MINB 3
+#endif
+__global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                  const MoverTArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *fld = reinterpret_cast<double *>(smem_raw);
@@ -197,19 +200,27 @@ __global__ void __launch_bounds__(THREADS, 3) mover_tiled_kernel(const __grid_co
   const uint32_t wend = min(p1, wbeg + chunk);
   const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
 
+  // perm/key one round ahead, sources of the next round prefetched into L1
+  uint32_t p_nx = 0, k_nx = 0;
+  if (wbeg + lane < wend) {
+    p_nx = A.perm[wbeg + lane];
+    k_nx = A.key[wbeg + lane];
+  }
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
+    const uint32_t sp_ = p_nx, kold_ = k_nx;
     if (p + 32 < wend) {
-      const uint32_t pn = A.perm[p + 32];
+      p_nx = A.perm[p + 32];
+      k_nx = A.key[p + 32];
+    }
+    if (act) {
 #pragma unroll
-      for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + pn));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src_id + pn));
+      for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + sp_));
     }
     uint32_t knew = KEY_DEAD, kold = 0;
     if (act) {
-      kold = A.key[p];
-      const uint32_t sp_ = A.perm[p];
+      kold = kold_;
       const double xn[3] = {A.src[0][sp_], A.src[1][sp_], A.src[2][sp_]};
       const double vn[3] = {A.src[3][sp_], A.src[4][sp_], A.src[5][sp_]};
       double xb[3] = {xn[0], xn[1], xn[2]};
@@ -300,13 +311,38 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
     }
   };
 
+  // two-stage software pipeline: the sources of round r+1 and the perm/key of
+  // round r+2 are in flight while round r is reduced
+  uint32_t k_nx = 0, p_nx = 0, k_n2 = 0, p_n2 = 0;
+  double s_nx[7];
+  {
+    const uint32_t p = wbeg + lane;
+    if (p < wend) {
+      k_nx = A.key[p];
+      p_nx = A.perm[p];
+    }
+    if (p + 32 < wend) {
+      k_n2 = A.key[p + 32];
+      p_n2 = A.perm[p + 32];
+    }
+#pragma unroll
+    for (int k = 0; k < 7; ++k) s_nx[k] = (p < wend) ? A.src[k][p_nx] : 0.0;
+  }
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    if (p + 32 < wend) {
-      const uint32_t pn = A.perm[p + 32];
+    const uint32_t k_cur = k_nx;
+    double s_cur[7];
 #pragma unroll
-      for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + pn));
+    for (int k = 0; k < 7; ++k) s_cur[k] = s_nx[k];
+    // advance the pipeline
+    k_nx = k_n2;
+    p_nx = p_n2;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) s_nx[k] = (p + 32 < wend) ? A.src[k][p_nx] : 0.0;
+    if (p + 64 < wend) {
+      k_n2 = A.key[p + 64];
+      p_n2 = A.perm[p + 64];
     }
     int c = 64;  // sentinel: no particle
     double Sk[8], val[10];
@@ -315,10 +351,9 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
 #pragma unroll
     for (int m = 0; m < 10; ++m) val[m] = 0.0;
     if (act) {
-      c = (int)(A.key[p] & (TILE3 - 1));
-      const uint32_t sp_ = A.perm[p];
-      const double x = A.src[0][sp_], y = A.src[1][sp_], z = A.src[2][sp_];
-      const double u = A.src[3][sp_], v = A.src[4][sp_], w = A.src[5][sp_], q = A.src[6][sp_];
+      c = (int)(k_cur & (TILE3 - 1));
+      const double x = s_cur[0], y = s_cur[1], z = s_cur[2];
+      const double u = s_cur[3], v = s_cur[4], w = s_cur[5], q = s_cur[6];
       // values q {1, v, vv} (Eq. 3, R16 order)
       const double qu = q * u, qv = q * v, qw = q * w;
       val[0] = q; val[1] = qu; val[2] = qv; val[3] = qw;

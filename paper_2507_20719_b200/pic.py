@@ -20,7 +20,7 @@ import torch
 from . import inputs as _inputs  # noqa: F401  (re-export convenience for callers)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpic.so")
+LIB_PATH = os.environ.get("PIC_LIB", os.path.join(HERE, "libpic.so"))
 
 PIC_MAX_SPECIES = 8
 PIC_NCCL_ID_BYTES = 128
