@@ -200,27 +200,44 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
   const uint32_t wend = min(p1, wbeg + chunk);
   const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
 
-  // perm/key one round ahead, sources of the next round prefetched into L1
-  uint32_t p_nx = 0, k_nx = 0;
+  // Software pipeline: perm/key two rounds ahead, the next round's sources
+  // prefetched into L1, and the counting-sort rank of a round taken at the
+  // start of the next one so the global atomic's latency overlaps compute.
+  uint32_t p_nx = 0, k_nx = 0, p_n2 = 0, k_n2 = 0;
   if (wbeg + lane < wend) {
     p_nx = A.perm[wbeg + lane];
     k_nx = A.key[wbeg + lane];
   }
+  if (wbeg + 32 + lane < wend) {
+    p_n2 = A.perm[wbeg + 32 + lane];
+    k_n2 = A.key[wbeg + 32 + lane];
+  }
+  uint32_t pr_p = 0, pr_k = KEY_DEAD;
+  bool pr_counted = false, pr_arrival = false;
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    const uint32_t sp_ = p_nx, kold_ = k_nx;
+    const uint32_t sp_ = p_nx, kold = k_nx;
+    p_nx = p_n2;
+    k_nx = k_n2;
+    if (p + 64 < wend) {
+      p_n2 = A.perm[p + 64];
+      k_n2 = A.key[p + 64];
+    }
     if (p + 32 < wend) {
-      p_nx = A.perm[p + 32];
-      k_nx = A.key[p + 32];
-    }
-    if (act) {
 #pragma unroll
-      for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + sp_));
+      for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + p_nx));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src_id + p_nx));
     }
-    uint32_t knew = KEY_DEAD, kold = 0;
+    // rank of the previous round (order.cu); leavers and removed are not counted
+    {
+      const uint32_t r = count_rank(A.cell_count, g.ncells, pr_k, pr_counted, pr_arrival);
+      if (pr_counted) A.rank[pr_p] = r;
+    }
+    uint32_t knew = KEY_DEAD;
     if (act) {
-      kold = kold_;
+      const double qv = A.src[6][sp_];
+      const int64_t idv = A.src_id[sp_];
       const double xn[3] = {A.src[0][sp_], A.src[1][sp_], A.src[2][sp_]};
       const double vn[3] = {A.src[3][sp_], A.src[4][sp_], A.src[5][sp_]};
       double xb[3] = {xn[0], xn[1], xn[2]};
@@ -255,14 +272,18 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
       knew = finish_particle(g, xnew, vnew, clamped, A.stats);
       A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
       A.dst[3][p] = vnew[0]; A.dst[4][p] = vnew[1]; A.dst[5][p] = vnew[2];
-      A.dst[6][p] = A.src[6][sp_];
-      A.dst_id[p] = A.src_id[sp_];
+      A.dst[6][p] = qv;
+      A.dst_id[p] = idv;
       A.key_new[p] = knew;
     }
-    // rank for the next cell order (order.cu); leavers and removed are not counted
-    const bool counted = act && knew < KEY_FIRST_RESERVED;
-    const uint32_t r = count_rank(A.cell_count, g.ncells, knew, counted, knew != kold);
-    if (counted) A.rank[p] = r;
+    pr_p = p;
+    pr_k = knew;
+    pr_counted = act && knew < KEY_FIRST_RESERVED;
+    pr_arrival = knew != kold;
+  }
+  {
+    const uint32_t r = count_rank(A.cell_count, g.ncells, pr_k, pr_counted, pr_arrival);
+    if (pr_counted) A.rank[pr_p] = r;
   }
 }
 
