@@ -292,6 +292,34 @@ __device__ __forceinline__ uint32_t count_rank(uint32_t *__restrict__ cell_count
   return (base + (uint32_t)__popc(peers & ((1u << lane) - 1u))) | (arrival ? RANK_ARRIVAL : 0u);
 }
 
+// The same rank in two halves, so that the atomic's return latency can be
+// hidden behind unrelated work: count_rank_issue starts the warp-aggregated
+// atomic, count_rank_finish (called later by all 32 lanes) completes the rank.
+struct RankTicket {
+  uint32_t base;      // atomic result (leader lanes), consumed in finish
+  unsigned peers;
+  int leader;
+  bool counted, arrival;
+};
+__device__ __forceinline__ RankTicket count_rank_issue(uint32_t *__restrict__ cell_count, int64_t ncells,
+                                                       uint32_t k, bool counted, bool arrival) {
+  RankTicket t;
+  const unsigned kk = counted ? (k | (arrival ? RANK_ARRIVAL : 0u)) : 0xFFFFFFFFu;
+  t.peers = __match_any_sync(0xffffffffu, kk);
+  t.leader = __ffs(t.peers) - 1;
+  t.counted = counted;
+  t.arrival = arrival;
+  t.base = 0;
+  if (counted && (int)(threadIdx.x & 31u) == t.leader)
+    t.base = atomicAdd(cell_count + (arrival ? ncells + 1 : 0) + k, (unsigned)__popc(t.peers));
+  return t;
+}
+__device__ __forceinline__ uint32_t count_rank_finish(const RankTicket &t) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t base = __shfl_sync(0xffffffffu, t.base, t.leader);
+  return (base + (uint32_t)__popc(t.peers & ((1u << lane) - 1u))) | (t.arrival ? RANK_ARRIVAL : 0u);
+}
+
 // Map a global node index to the ghosted moment array (x: ghost planes; y, z:
 // planes [0, N] with periodic images of -1 / N+1 wrapped).  -1 if outside.
 __device__ __forceinline__ int64_t moment_node(const Geom &g, int64_t gx, int64_t gy, int64_t gz) {

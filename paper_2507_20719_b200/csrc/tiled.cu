@@ -156,7 +156,7 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
 
 // ----------------------------------------------------------------- mover ----
 #ifndef PIC_MOVER_MINB
-#define PIC_MOVER_MINB 3
+#define PIC_MOVER_MINB 2
 #endif
 __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                  const MoverTArgs A) {
@@ -212,8 +212,10 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
     p_n2 = A.perm[wbeg + 32 + lane];
     k_n2 = A.key[wbeg + 32 + lane];
   }
-  uint32_t pr_p = 0, pr_k = KEY_DEAD;
-  bool pr_counted = false, pr_arrival = false;
+  // rank ticket of the previous round: its atomic flies while this round computes
+  RankTicket tk;
+  tk.base = 0; tk.peers = 0; tk.leader = 0; tk.counted = false; tk.arrival = false;
+  uint32_t pr_p = 0;
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
@@ -228,11 +230,6 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
 #pragma unroll
       for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + p_nx));
       asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src_id + p_nx));
-    }
-    // rank of the previous round (order.cu); leavers and removed are not counted
-    {
-      const uint32_t r = count_rank(A.cell_count, g.ncells, pr_k, pr_counted, pr_arrival);
-      if (pr_counted) A.rank[pr_p] = r;
     }
     uint32_t knew = KEY_DEAD;
     if (act) {
@@ -276,14 +273,18 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
       A.dst_id[p] = idv;
       A.key_new[p] = knew;
     }
+    // complete the previous round's rank, then start this round's (order.cu);
+    // leavers and removed particles are not counted
+    if (r0 != wbeg) {
+      const uint32_t r = count_rank_finish(tk);
+      if (tk.counted) A.rank[pr_p] = r;
+    }
+    tk = count_rank_issue(A.cell_count, g.ncells, knew, act && knew < KEY_FIRST_RESERVED, knew != kold);
     pr_p = p;
-    pr_k = knew;
-    pr_counted = act && knew < KEY_FIRST_RESERVED;
-    pr_arrival = knew != kold;
   }
-  {
-    const uint32_t r = count_rank(A.cell_count, g.ncells, pr_k, pr_counted, pr_arrival);
-    if (pr_counted) A.rank[pr_p] = r;
+  if (wbeg < wend) {
+    const uint32_t r = count_rank_finish(tk);
+    if (tk.counted) A.rank[pr_p] = r;
   }
 }
 
