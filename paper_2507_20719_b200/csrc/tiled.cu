@@ -42,7 +42,7 @@ constexpr int MB = TILE + 1;            // deposit nodes per axis: 0 .. TILE
 constexpr int MB3 = MB * MB * MB;       // 125
 constexpr int WARPS = 8;
 constexpr int THREADS = 32 * WARPS;
-constexpr size_t MOVER_SMEM = sizeof(double) * NB3 * 6 + 16;
+constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + WARPS * 2 * 8 * 32) + 16;
 constexpr int SGRP = 36;                        // doubles per 4-particle group in the S buffer (32 + pad)
 constexpr int WBUF = 8 * SGRP + 32 * 10;        // doubles per warp: S[8][36] + V[32][10]
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (10 * MB3 + WARPS * WBUF);
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
                                                                  const MoverTArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *fld = reinterpret_cast<double *>(smem_raw);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(fld + NB3 * 6);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(fld + NB3 * 6 + WARPS * 2 * 8 * 32);
   const Geom &g = A.g;
 
   const int tile = blockIdx.x;
@@ -200,43 +200,68 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
   const uint32_t wend = min(p1, wbeg + chunk);
   const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
 
-  // Software pipeline: perm/key two rounds ahead, the next round's sources
-  // prefetched into L1, and the counting-sort rank of a round taken at the
-  // start of the next one so the global atomic's latency overlaps compute.
-  uint32_t p_nx = 0, k_nx = 0, p_n2 = 0, k_n2 = 0;
+  // Software pipeline: perm/key two rounds ahead; the next round's sources are
+  // gathered with cp.async (LDGSTS) into a per-warp shared double buffer while
+  // this round computes; the counting-sort rank of a round is completed during
+  // the next one so the global atomic's latency overlaps compute.
+  double *stg = fld + NB3 * 6 + (size_t)warp * (2 * 8 * 32);   // [2][8][32]
+  uint32_t p_nx = 0, k_nx = 0, p_n2 = 0, k_n2 = 0, k_cur = 0;
   if (wbeg + lane < wend) {
     p_nx = A.perm[wbeg + lane];
     k_nx = A.key[wbeg + lane];
   }
+  uint32_t p_n1 = 0, k_n1 = 0;
   if (wbeg + 32 + lane < wend) {
-    p_n2 = A.perm[wbeg + 32 + lane];
-    k_n2 = A.key[wbeg + 32 + lane];
+    p_n1 = A.perm[wbeg + 32 + lane];
+    k_n1 = A.key[wbeg + 32 + lane];
   }
+  if (wbeg + 64 + lane < wend) {
+    p_n2 = A.perm[wbeg + 64 + lane];
+    k_n2 = A.key[wbeg + 64 + lane];
+  }
+  auto stage_round = [&](int buf, uint32_t src_idx, bool valid) {
+    if (valid) {
+      double *d = stg + buf * (8 * 32) + lane;
+#pragma unroll
+      for (int k = 0; k < 7; ++k)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
+                     : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 7 * 32)), "l"(A.src_id + src_idx)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage_round(0, p_nx, wbeg + lane < wend);
+  k_cur = k_nx;
+  p_nx = p_n1;   // round 1
+  k_nx = k_n1;
   // rank ticket of the previous round: its atomic flies while this round computes
   RankTicket tk;
   tk.base = 0; tk.peers = 0; tk.leader = 0; tk.counted = false; tk.arrival = false;
   uint32_t pr_p = 0;
+  int buf = 0;
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    const uint32_t sp_ = p_nx, kold = k_nx;
-    p_nx = p_n2;
+    const uint32_t kold = k_cur;
+    // stage round r+1, then advance perm/key
+    stage_round(buf ^ 1, p_nx, p + 32 < wend);
+    k_cur = k_nx;
+    p_nx = p_n2;   // round r+2
     k_nx = k_n2;
-    if (p + 64 < wend) {
-      p_n2 = A.perm[p + 64];
-      k_n2 = A.key[p + 64];
+    if (p + 96 < wend) {   // round r+3
+      p_n2 = A.perm[p + 96];
+      k_n2 = A.key[p + 96];
     }
-    if (p + 32 < wend) {
-#pragma unroll
-      for (int k = 0; k < 7; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src[k] + p_nx));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(A.src_id + p_nx));
-    }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    const double *sv = stg + buf * (8 * 32) + lane;
+    buf ^= 1;
     uint32_t knew = KEY_DEAD;
     if (act) {
-      const double qv = A.src[6][sp_];
-      const int64_t idv = A.src_id[sp_];
-      const double xn[3] = {A.src[0][sp_], A.src[1][sp_], A.src[2][sp_]};
-      const double vn[3] = {A.src[3][sp_], A.src[4][sp_], A.src[5][sp_]};
+      const double qv = sv[6 * 32];
+      const int64_t idv = __double_as_longlong(sv[7 * 32]);
+      const double xn[3] = {sv[0], sv[32], sv[64]};
+      const double vn[3] = {sv[96], sv[128], sv[160]};
       double xb[3] = {xn[0], xn[1], xn[2]};
       double vb[3];
       bool clamped = false;
