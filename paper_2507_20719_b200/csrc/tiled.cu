@@ -42,9 +42,10 @@ constexpr int MB = TILE + 1;            // deposit nodes per axis: 0 .. TILE
 constexpr int MB3 = MB * MB * MB;       // 125
 constexpr int WARPS = 8;
 constexpr int THREADS = 32 * WARPS;
-constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + WARPS * 2 * 8 * 32) + 16;
+constexpr int MOVER_WARP_STAGE = 2 * 8 * 32 + 4 * 2 * 32 / 2;   // doubles: sources [2][8][32] + perm/key ring [4][2][32] u32
+constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + WARPS * MOVER_WARP_STAGE) + 16;
 constexpr int SGRP = 36;                        // doubles per 4-particle group in the S buffer (32 + pad)
-constexpr int WBUF = 8 * SGRP + 32 * 10;        // doubles per warp: S[8][36] + V[32][10]
+constexpr int WBUF = 8 * SGRP + 32 * 10 + 2 * 7 * 32 + 4 * 2 * 32 / 2;  // doubles per warp: S[8][36] + V[32][10] + staging
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (10 * MB3 + WARPS * WBUF);
 
 struct MoverTArgs {
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
                                                                  const MoverTArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *fld = reinterpret_cast<double *>(smem_raw);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(fld + NB3 * 6 + WARPS * 2 * 8 * 32);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(fld + NB3 * 6 + WARPS * MOVER_WARP_STAGE);
   const Geom &g = A.g;
 
   const int tile = blockIdx.x;
@@ -200,28 +201,27 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
   const uint32_t wend = min(p1, wbeg + chunk);
   const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
 
-  // Software pipeline: perm/key two rounds ahead; the next round's sources are
-  // gathered with cp.async (LDGSTS) into a per-warp shared double buffer while
-  // this round computes; the counting-sort rank of a round is completed during
-  // the next one so the global atomic's latency overlaps compute.
-  double *stg = fld + NB3 * 6 + (size_t)warp * (2 * 8 * 32);   // [2][8][32]
-  uint32_t p_nx = 0, k_nx = 0, p_n2 = 0, k_n2 = 0, k_cur = 0;
-  if (wbeg + lane < wend) {
-    p_nx = A.perm[wbeg + lane];
-    k_nx = A.key[wbeg + lane];
-  }
-  uint32_t p_n1 = 0, k_n1 = 0;
-  if (wbeg + 32 + lane < wend) {
-    p_n1 = A.perm[wbeg + 32 + lane];
-    k_n1 = A.key[wbeg + 32 + lane];
-  }
-  if (wbeg + 64 + lane < wend) {
-    p_n2 = A.perm[wbeg + 64 + lane];
-    k_n2 = A.key[wbeg + 64 + lane];
-  }
-  auto stage_round = [&](int buf, uint32_t src_idx, bool valid) {
-    if (valid) {
-      double *d = stg + buf * (8 * 32) + lane;
+  // Software pipeline through shared memory (cp.async / LDGSTS, no register
+  // dependencies): in round r the warp gathers the sources of round r+1 into a
+  // double buffer and fetches perm/key of round r+3 into a 4-slot ring, one
+  // commit group per round; "wait_group 1" then guarantees round r's sources.
+  // The counting-sort rank of a round completes during the next one, so the
+  // global atomic's latency overlaps compute.
+  double *stg = fld + NB3 * 6 + (size_t)warp * MOVER_WARP_STAGE;   // [2][8][32] doubles
+  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + 2 * 8 * 32);    // [4][2][32] (perm, key)
+  auto fetch_pk = [&](uint32_t rr) {   // perm/key of the round starting at rr
+    const uint32_t q = rr + lane;
+    if (q < wend) {
+      uint32_t *slot = pk + (((rr - wbeg) >> 5) & 3) * 64 + lane;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(A.perm + q) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 32)), "l"(A.key + q) : "memory");
+    }
+  };
+  auto fetch_src = [&](uint32_t rr) {  // sources of the round starting at rr (perm already in the ring)
+    const uint32_t q = rr + lane;
+    if (q < wend) {
+      const uint32_t src_idx = pk[(((rr - wbeg) >> 5) & 3) * 64 + lane];
+      double *d = stg + (((rr - wbeg) >> 5) & 1) * (8 * 32) + lane;
 #pragma unroll
       for (int k = 0; k < 7; ++k)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
@@ -229,33 +229,27 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 7 * 32)), "l"(A.src_id + src_idx)
                    : "memory");
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  stage_round(0, p_nx, wbeg + lane < wend);
-  k_cur = k_nx;
-  p_nx = p_n1;   // round 1
-  k_nx = k_n1;
+  fetch_pk(wbeg);
+  fetch_pk(wbeg + 32);
+  fetch_pk(wbeg + 64);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  fetch_src(wbeg);
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // rank ticket of the previous round: its atomic flies while this round computes
   RankTicket tk;
   tk.base = 0; tk.peers = 0; tk.leader = 0; tk.counted = false; tk.arrival = false;
   uint32_t pr_p = 0;
-  int buf = 0;
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    const uint32_t kold = k_cur;
-    // stage round r+1, then advance perm/key
-    stage_round(buf ^ 1, p_nx, p + 32 < wend);
-    k_cur = k_nx;
-    p_nx = p_n2;   // round r+2
-    k_nx = k_n2;
-    if (p + 96 < wend) {   // round r+3
-      p_n2 = A.perm[p + 96];
-      k_n2 = A.key[p + 96];
-    }
+    const uint32_t kold = act ? pk[(((r0 - wbeg) >> 5) & 3) * 64 + 32 + lane] : 0u;
+    fetch_src(r0 + 32);
+    fetch_pk(r0 + 96);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");
-    const double *sv = stg + buf * (8 * 32) + lane;
-    buf ^= 1;
+    const double *sv = stg + (((r0 - wbeg) >> 5) & 1) * (8 * 32) + lane;
     uint32_t knew = KEY_DEAD;
     if (act) {
       const double qv = sv[6 * 32];
@@ -358,39 +352,49 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
     }
   };
 
-  // two-stage software pipeline: the sources of round r+1 and the perm/key of
-  // round r+2 are in flight while round r is reduced
-  uint32_t k_nx = 0, p_nx = 0, k_n2 = 0, p_n2 = 0;
-  double s_nx[7];
-  {
-    const uint32_t p = wbeg + lane;
-    if (p < wend) {
-      k_nx = A.key[p];
-      p_nx = A.perm[p];
+  // Software pipeline through shared memory (cp.async), as in the mover:
+  // sources of round r+1 into a double buffer, perm/key of round r+3 into a
+  // 4-slot ring, one commit group per round.
+  double *stg = Vb + 32 * 10;                                       // [2][7][32] doubles
+  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + 2 * 7 * 32);    // [4][2][32] (perm, key)
+  auto fetch_pk = [&](uint32_t rr) {
+    const uint32_t q = rr + lane;
+    if (q < wend) {
+      uint32_t *slot = pk + (((rr - wbeg) >> 5) & 3) * 64 + lane;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(A.perm + q) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 32)), "l"(A.key + q) : "memory");
     }
-    if (p + 32 < wend) {
-      k_n2 = A.key[p + 32];
-      p_n2 = A.perm[p + 32];
-    }
+  };
+  auto fetch_src = [&](uint32_t rr) {
+    const uint32_t q = rr + lane;
+    if (q < wend) {
+      const uint32_t src_idx = pk[(((rr - wbeg) >> 5) & 3) * 64 + lane];
+      double *d = stg + (((rr - wbeg) >> 5) & 1) * (7 * 32) + lane;
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s_nx[k] = (p < wend) ? A.src[k][p_nx] : 0.0;
-  }
+      for (int k = 0; k < 7; ++k)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
+                     : "memory");
+    }
+  };
+  fetch_pk(wbeg);
+  fetch_pk(wbeg + 32);
+  fetch_pk(wbeg + 64);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  fetch_src(wbeg);
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    const uint32_t k_cur = k_nx;
+    const uint32_t k_cur = act ? pk[(((r0 - wbeg) >> 5) & 3) * 64 + 32 + lane] : 0u;
+    fetch_src(r0 + 32);
+    fetch_pk(r0 + 96);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    const double *sv = stg + (((r0 - wbeg) >> 5) & 1) * (7 * 32) + lane;
     double s_cur[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s_cur[k] = s_nx[k];
-    // advance the pipeline
-    k_nx = k_n2;
-    p_nx = p_n2;
-#pragma unroll
-    for (int k = 0; k < 7; ++k) s_nx[k] = (p + 32 < wend) ? A.src[k][p_nx] : 0.0;
-    if (p + 64 < wend) {
-      k_n2 = A.key[p + 64];
-      p_n2 = A.perm[p + 64];
-    }
+    for (int k = 0; k < 7; ++k) s_cur[k] = act ? sv[k * 32] : 0.0;
     int c = 64;  // sentinel: no particle
     double Sk[8], val[10];
 #pragma unroll
