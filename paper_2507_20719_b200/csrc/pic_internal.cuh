@@ -221,51 +221,61 @@ __device__ __forceinline__ bool sample_window(const Geom &g, const double *__res
   return clamped;
 }
 
+// Tile-major key of a local cell (lx relative to slab_lo), 32-bit arithmetic
+// (valid while the key range fits 32 bits, which pic_init checks; TILE == 4).
+__device__ __forceinline__ uint32_t tile_key32(const Geom &g, uint32_t lx, uint32_t ly, uint32_t lz) {
+  static_assert(TILE == 4, "tile_key32 assumes 4^3 tiles");
+  const uint32_t t = (lx >> 2) + (uint32_t)g.nt[0] * ((ly >> 2) + (uint32_t)g.nt[1] * (lz >> 2));
+  return t * TILE3 + (lx & 3u) + 4u * (ly & 3u) + 16u * (lz & 3u);
+}
+
 // Boundary conditions (R10, R11, R21) of a pushed particle and its destination
 // key.  xnew: in = pre-wrap position (cell units), out = post-wrap position.
+// Non-finite values fail the range tests, so the finiteness check only runs on
+// the rare flagged path.
 __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3], const double vnew[3],
                                                    bool clamped, unsigned long long *__restrict__ stats) {
-  const int64_t cx_pre = (int64_t)floor(xnew[0]);
-  bool dead = false, multi = false;
+  const double x_pre = xnew[0];
+  bool bad = false, out = false;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const double N = (double)g.ncell[d];
+    const double x = xnew[d];
     if (g.periodic[d]) {
-      xnew[d] = wrap_cells(xnew[d], N, &multi);
-    } else if (!(xnew[d] >= 0.0 && xnew[d] < N)) {
-      dead = true;
+      // R10: x >= L -> x - L; x < 0 -> x + L (and L -> 0); more than one wrap is bad
+      const bool neg = x < 0.0;
+      double y = (x >= N) ? x - N : (neg ? x + N : x);
+      y = (neg && y == N) ? 0.0 : y;
+      bad |= !(y >= 0.0 && y < N);
+      xnew[d] = y;
+    } else {
+      out |= !(x >= 0.0 && x < N);   // left through an open face (or non-finite)
     }
   }
-  if (!dead && g.has_planet) {
+  if (g.has_planet && !bad && !out) {
     double r2 = 0.0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const double dx = (xnew[d] - g.planet_c[d]) * g.delta[d];
       r2 += dx * dx;
     }
-    if (r2 < g.planet_r2) dead = true;
+    out = r2 < g.planet_r2;
   }
-  const bool finite = isfinite(vnew[0]) && isfinite(vnew[1]) && isfinite(vnew[2]) &&
-                      isfinite(xnew[0]) && isfinite(xnew[1]) && isfinite(xnew[2]);
   uint32_t k;
-  if (!finite) {
-    atomicAdd(&stats[ST_NONFINITE], 1ull);
+  if (bad || out) {
+    const bool finite = isfinite(vnew[0]) && isfinite(vnew[1]) && isfinite(vnew[2]) &&
+                        isfinite(xnew[0]) && isfinite(xnew[1]) && isfinite(xnew[2]);
+    atomicAdd(&stats[!finite ? ST_NONFINITE : (bad ? ST_MULTIWRAP : ST_REMOVED)], 1ull);
     k = KEY_DEAD;
-  } else if (multi) {
-    atomicAdd(&stats[ST_MULTIWRAP], 1ull);
-    k = KEY_DEAD;
-  } else if (dead) {
-    atomicAdd(&stats[ST_REMOVED], 1ull);
-    k = KEY_DEAD;
-  } else if (g.multi_rank && cx_pre < g.slab_lo) {
+  } else if (g.multi_rank && x_pre < (double)g.slab_lo) {
     k = KEY_LEFT;
-    if (cx_pre < g.slab_lo - g.G) atomicAdd(&stats[ST_FAR], 1ull);
-  } else if (g.multi_rank && cx_pre >= g.slab_hi) {
+    if (x_pre < (double)(g.slab_lo - g.G)) atomicAdd(&stats[ST_FAR], 1ull);
+  } else if (g.multi_rank && x_pre >= (double)g.slab_hi) {
     k = KEY_RIGHT;
-    if (cx_pre > g.slab_hi + g.G - 1) atomicAdd(&stats[ST_FAR], 1ull);
+    if (x_pre >= (double)(g.slab_hi + g.G)) atomicAdd(&stats[ST_FAR], 1ull);
   } else {
-    const int64_t cx = (int64_t)xnew[0], cy = (int64_t)xnew[1], cz = (int64_t)xnew[2];
-    k = tile_key(g, cx - g.slab_lo, cy, cz);
+    const int cx = (int)xnew[0], cy = (int)xnew[1], cz = (int)xnew[2];
+    k = tile_key32(g, (uint32_t)(cx - (int)g.slab_lo), (uint32_t)cy, (uint32_t)cz);
   }
   if (clamped) atomicAdd(&stats[ST_CLAMPED], 1ull);
   return k;

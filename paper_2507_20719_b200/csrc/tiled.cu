@@ -45,7 +45,7 @@ constexpr int THREADS = 32 * WARPS;
 constexpr int MOVER_WARP_STAGE = 2 * 8 * 32 + 4 * 2 * 32 / 2;   // doubles: sources [2][8][32] + perm/key ring [4][2][32] u32
 constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + WARPS * MOVER_WARP_STAGE) + 16;
 constexpr int SGRP = 36;                        // doubles per 4-particle group in the S buffer (32 + pad)
-constexpr int WBUF = 8 * SGRP + 32 * 10 + 2 * 7 * 32 + 4 * 2 * 32 / 2;  // doubles per warp: S[8][36] + V[32][10] + staging
+constexpr int WBUF = 8 * SGRP + 32 * 10;        // doubles per warp: S[8][36] + V[32][10]
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (10 * MB3 + WARPS * WBUF);
 
 struct MoverTArgs {
@@ -130,7 +130,8 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
     f[d] = u[d] - fl[d];
     i[d] = (int)fl[d];
   }
-  if (!(fl[0] >= 0.0 && fl[0] <= NB - 2 && fl[1] >= 0.0 && fl[1] <= NB - 2 && fl[2] >= 0.0 && fl[2] <= NB - 2))
+  if (!((unsigned)i[0] <= (unsigned)(NB - 2) && (unsigned)i[1] <= (unsigned)(NB - 2) &&
+        (unsigned)i[2] <= (unsigned)(NB - 2)))
     return false;
   const double gx0 = 1.0 - f[0], gy0 = 1.0 - f[1], gz0 = 1.0 - f[2];
   const double w00 = gy0 * gz0, w10 = f[1] * gz0, w01 = gy0 * f[2], w11 = f[1] * f[2];
@@ -159,6 +160,9 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
 #ifndef PIC_MOVER_MINB
 #define PIC_MOVER_MINB 2
 #endif
+// NIT > 0: the iteration count is a compile-time constant (fully unrolled);
+// NIT == 0: runtime A.n_iter.
+template <int NIT>
 __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                  const MoverTArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -259,7 +263,9 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
       double xb[3] = {xn[0], xn[1], xn[2]};
       double vb[3];
       bool clamped = false;
-      for (int it = 0; it < A.n_iter; ++it) {
+      const int n_iter = NIT > 0 ? NIT : A.n_iter;
+#pragma unroll
+      for (int it = 0; it < n_iter; ++it) {
         double EB[6];
         const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
         if (!gather_smem(fld, u, EB)) {
@@ -352,49 +358,39 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
     }
   };
 
-  // Software pipeline through shared memory (cp.async), as in the mover:
-  // sources of round r+1 into a double buffer, perm/key of round r+3 into a
-  // 4-slot ring, one commit group per round.
-  double *stg = Vb + 32 * 10;                                       // [2][7][32] doubles
-  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + 2 * 7 * 32);    // [4][2][32] (perm, key)
-  auto fetch_pk = [&](uint32_t rr) {
-    const uint32_t q = rr + lane;
-    if (q < wend) {
-      uint32_t *slot = pk + (((rr - wbeg) >> 5) & 3) * 64 + lane;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(A.perm + q) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 32)), "l"(A.key + q) : "memory");
+  // two-stage software pipeline: the sources of round r+1 and the perm/key of
+  // round r+2 are in flight while round r is reduced
+  uint32_t k_nx = 0, p_nx = 0, k_n2 = 0, p_n2 = 0;
+  double s_nx[7];
+  {
+    const uint32_t p = wbeg + lane;
+    if (p < wend) {
+      k_nx = A.key[p];
+      p_nx = A.perm[p];
     }
-  };
-  auto fetch_src = [&](uint32_t rr) {
-    const uint32_t q = rr + lane;
-    if (q < wend) {
-      const uint32_t src_idx = pk[(((rr - wbeg) >> 5) & 3) * 64 + lane];
-      double *d = stg + (((rr - wbeg) >> 5) & 1) * (7 * 32) + lane;
+    if (p + 32 < wend) {
+      k_n2 = A.key[p + 32];
+      p_n2 = A.perm[p + 32];
+    }
 #pragma unroll
-      for (int k = 0; k < 7; ++k)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
-                     : "memory");
-    }
-  };
-  fetch_pk(wbeg);
-  fetch_pk(wbeg + 32);
-  fetch_pk(wbeg + 64);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  fetch_src(wbeg);
-  asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int k = 0; k < 7; ++k) s_nx[k] = (p < wend) ? A.src[k][p_nx] : 0.0;
+  }
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    const uint32_t k_cur = act ? pk[(((r0 - wbeg) >> 5) & 3) * 64 + 32 + lane] : 0u;
-    fetch_src(r0 + 32);
-    fetch_pk(r0 + 96);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    const double *sv = stg + (((r0 - wbeg) >> 5) & 1) * (7 * 32) + lane;
+    const uint32_t k_cur = k_nx;
     double s_cur[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s_cur[k] = act ? sv[k * 32] : 0.0;
+    for (int k = 0; k < 7; ++k) s_cur[k] = s_nx[k];
+    // advance the pipeline
+    k_nx = k_n2;
+    p_nx = p_n2;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) s_nx[k] = (p + 32 < wend) ? A.src[k][p_nx] : 0.0;
+    if (p + 64 < wend) {
+      k_n2 = A.key[p + 64];
+      p_n2 = A.perm[p + 64];
+    }
     int c = 64;  // sentinel: no particle
     double Sk[8], val[10];
 #pragma unroll
@@ -517,7 +513,11 @@ static pic_status make_tmap(Ctx *ctx) {
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
   PIC_CUDA(cudaFuncSetAttribute(deposit_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)DEPOSIT_SMEM));
   ctx->tmap_ok = true;
@@ -552,8 +552,16 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   A.ks = sp.qom * (ctx->geom.dt * 0.5);
   A.ks_c = A.ks / ctx->geom.c;
   A.n_iter = sp.n_iter;
-  mover_tiled_kernel<<<(unsigned)ctx->geom.ntiles, THREADS, MOVER_SMEM, ctx->stream>>>(
-      *reinterpret_cast<const CUtensorMap *>(ctx->tmap), A); ++ctx->launches;
+  const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap);
+  const unsigned grid = (unsigned)ctx->geom.ntiles;
+  switch (sp.n_iter) {
+    case 1: mover_tiled_kernel<1><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
+    case 2: mover_tiled_kernel<2><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
+    case 3: mover_tiled_kernel<3><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
+    case 4: mover_tiled_kernel<4><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
+    default: mover_tiled_kernel<0><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
+  }
+  ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   sp.swap_buffers();
   return build_order(ctx, s);
