@@ -32,6 +32,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "pic_internal.cuh"
 
 namespace pic {
@@ -43,7 +46,6 @@ constexpr int MB3 = MB * MB * MB;       // 125
 constexpr int WARPS = 8;
 constexpr int THREADS = 32 * WARPS;
 constexpr int MOVER_WARP_STAGE = 2 * 8 * 32 + 4 * 2 * 32 / 2;   // doubles: sources [2][8][32] + perm/key ring [4][2][32] u32
-constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + WARPS * MOVER_WARP_STAGE) + 16;
 constexpr int SGRP = 36;                        // doubles per 4-particle group in the S buffer (32 + pad)
 constexpr int WBUF = 8 * SGRP + 32 * 10;        // doubles per warp: S[8][36] + V[32][10]
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (10 * MB3 + WARPS * WBUF);
@@ -156,18 +158,66 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
   return true;
 }
 
+// Per-cell polynomial form of the trilinear interpolant (the same function as
+// the 8-weight form of R12, re-associated): for each of the 6 components the
+// cell holds [c000 c001 c010 c011 c100 c101 c110 c111] with
+//   W(f) = c000 + fz c001 + fy (c010 + fz c011) + fx (c100 + fz c101 + fy (c110 + fz c111)),
+// i.e. 7 FMA per component instead of 8 weights + 8 FMA.  NC^3 cells of the
+// staged box (tile cells -1 .. TILE).
+constexpr int NC = TILE + 2;
+constexpr int NC3 = NC * NC * NC;   // 216
+__device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, const double u[3], double out[6]) {
+  double f[3];
+  int i[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double fl = floor(u[d]);
+    f[d] = u[d] - fl;
+    i[d] = (int)fl;
+  }
+  if (!((unsigned)i[0] < (unsigned)NC && (unsigned)i[1] < (unsigned)NC && (unsigned)i[2] < (unsigned)NC))
+    return false;
+  const double *c = coef + ((i[2] * NC + i[1]) * NC + i[0]) * 48;
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    const double2 c0 = *reinterpret_cast<const double2 *>(c + 8 * m);
+    const double2 c1 = *reinterpret_cast<const double2 *>(c + 8 * m + 2);
+    const double2 c2 = *reinterpret_cast<const double2 *>(c + 8 * m + 4);
+    const double2 c3 = *reinterpret_cast<const double2 *>(c + 8 * m + 6);
+    const double a = fma(f[2], c0.y, c0.x), b = fma(f[2], c1.y, c1.x);
+    const double cc = fma(f[2], c2.y, c2.x), dd = fma(f[2], c3.y, c3.x);
+    out[m] = fma(f[0], fma(f[1], dd, cc), fma(f[1], b, a));
+  }
+  return true;
+}
+
 // ----------------------------------------------------------------- mover ----
 #ifndef PIC_MOVER_MINB
 #define PIC_MOVER_MINB 2
 #endif
 // NIT > 0: the iteration count is a compile-time constant (fully unrolled);
 // NIT == 0: runtime A.n_iter.
-template <int NIT>
-__global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                                 const MoverTArgs A) {
+// COEF: per-cell polynomial gather, 16 warps per CTA (the coefficient table
+// is 83 KB; the TMA node box is staged in the per-warp staging area and turned
+// into coefficients before the main loop).  !COEF: node gather, 8 warps.
+template <bool COEF> struct MoverShape {
+  static constexpr int WARPS_ = COEF ? 16 : 8;
+  static constexpr int THREADS_ = 32 * WARPS_;
+  static constexpr int TABLE = COEF ? NC3 * 48 : NB3 * 6;         // doubles before the staging area
+  static constexpr size_t SMEM = sizeof(double) * (TABLE + WARPS_ * MOVER_WARP_STAGE) + 16;
+  static constexpr int MINB = COEF ? 1 : PIC_MOVER_MINB;
+};
+
+template <int NIT, bool COEF>
+__global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::MINB)
+    mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap, const MoverTArgs A) {
+  constexpr int MW = MoverShape<COEF>::WARPS_;
+  constexpr int MT = MoverShape<COEF>::THREADS_;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double *fld = reinterpret_cast<double *>(smem_raw);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(fld + NB3 * 6 + WARPS * MOVER_WARP_STAGE);
+  double *table = reinterpret_cast<double *>(smem_raw);            // node box (!COEF) or coefficients
+  double *stage_base = table + MoverShape<COEF>::TABLE;
+  double *fld = COEF ? stage_base : table;                         // TMA destination (node box)
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_base + MW * MOVER_WARP_STAGE);
   const Geom &g = A.g;
 
   const int tile = blockIdx.x;
@@ -194,13 +244,34 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
                 mbar);
   }
   mbar_wait(mbar, 0);
-  for (int i = tid; i < NB3 * 6; i += THREADS) fld[i] *= ((i % 6) < 3) ? A.ks : A.ks_c;
+  if (COEF) {
+    // polynomial coefficients of every staged cell, pre-scaled by k_s, k_s/c
+    for (int t = tid; t < NC3 * 6; t += MT) {
+      const int m = t % 6, cell = t / 6;
+      const int cx = cell % NC, cy = (cell / NC) % NC, cz = cell / (NC * NC);
+      auto n = [&](int a, int b, int c) { return fld[(((cz + c) * NB + (cy + b)) * NB + (cx + a)) * 6 + m]; };
+      const double sc = m < 3 ? A.ks : A.ks_c;
+      const double n000 = n(0, 0, 0), n001 = n(0, 0, 1), n010 = n(0, 1, 0), n011 = n(0, 1, 1);
+      const double n100 = n(1, 0, 0), n101 = n(1, 0, 1), n110 = n(1, 1, 0), n111 = n(1, 1, 1);
+      double *c = table + cell * 48 + 8 * m;
+      c[0] = sc * n000;
+      c[1] = sc * (n001 - n000);
+      c[2] = sc * (n010 - n000);
+      c[3] = sc * ((n011 - n010) - (n001 - n000));
+      c[4] = sc * (n100 - n000);
+      c[5] = sc * ((n101 - n100) - (n001 - n000));
+      c[6] = sc * ((n110 - n100) - (n010 - n000));
+      c[7] = sc * (((n111 - n110) - (n101 - n100)) - ((n011 - n010) - (n001 - n000)));
+    }
+  } else {
+    for (int i = tid; i < NB3 * 6; i += MT) fld[i] *= ((i % 6) < 3) ? A.ks : A.ks_c;
+  }
   __syncthreads();
 
   // ---- 2. warps over contiguous sub-ranges of the tile's particles
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t ntile = p1 - p0;
-  const uint32_t chunk = ((ntile + 32 * WARPS - 1) / (32 * WARPS)) * 32;
+  const uint32_t chunk = ((ntile + 32 * MW - 1) / (32 * MW)) * 32;
   const uint32_t wbeg = p0 + warp * chunk;
   const uint32_t wend = min(p1, wbeg + chunk);
   const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
@@ -211,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
   // commit group per round; "wait_group 1" then guarantees round r's sources.
   // The counting-sort rank of a round completes during the next one, so the
   // global atomic's latency overlaps compute.
-  double *stg = fld + NB3 * 6 + (size_t)warp * MOVER_WARP_STAGE;   // [2][8][32] doubles
+  double *stg = stage_base + (size_t)warp * MOVER_WARP_STAGE;      // [2][8][32] doubles
   uint32_t *pk = reinterpret_cast<uint32_t *>(stg + 2 * 8 * 32);    // [4][2][32] (perm, key)
   auto fetch_pk = [&](uint32_t rr) {   // perm/key of the round starting at rr
     const uint32_t q = rr + lane;
@@ -268,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, PIC_MOVER_MINB) mover_tiled_kernel(co
       for (int it = 0; it < n_iter; ++it) {
         double EB[6];
         const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
-        if (!gather_smem(fld, u, EB)) {
+        if (!(COEF ? gather_coef(table, u, EB) : gather_smem(table, u, EB))) {
           clamped |= sample_window(g, A.field, xb, EB);
 #pragma unroll
           for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
@@ -513,11 +584,13 @@ static pic_status make_tmap(Ctx *ctx) {
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM));
+#define PIC_SET_SMEM(NIT, C)                                                                           \
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                (int)MoverShape<C>::SMEM))
+  PIC_SET_SMEM(0, true); PIC_SET_SMEM(1, true); PIC_SET_SMEM(2, true); PIC_SET_SMEM(3, true); PIC_SET_SMEM(4, true);
+  PIC_SET_SMEM(0, false); PIC_SET_SMEM(1, false); PIC_SET_SMEM(2, false); PIC_SET_SMEM(3, false);
+  PIC_SET_SMEM(4, false);
+#undef PIC_SET_SMEM
   PIC_CUDA(cudaFuncSetAttribute(deposit_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)DEPOSIT_SMEM));
   ctx->tmap_ok = true;
@@ -554,13 +627,23 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   A.n_iter = sp.n_iter;
   const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap);
   const unsigned grid = (unsigned)ctx->geom.ntiles;
+  static const bool coef = [] {
+    const char *e = getenv("PIC_MOVER_GATHER");
+    return !(e && strcmp(e, "nodes") == 0);
+  }();
+#define PIC_LAUNCH(NIT)                                                                                     \
+  if (coef)                                                                                                 \
+    mover_tiled_kernel<NIT, true><<<grid, MoverShape<true>::THREADS_, MoverShape<true>::SMEM, ctx->stream>>>(tm, A); \
+  else                                                                                                      \
+    mover_tiled_kernel<NIT, false><<<grid, MoverShape<false>::THREADS_, MoverShape<false>::SMEM, ctx->stream>>>(tm, A);
   switch (sp.n_iter) {
-    case 1: mover_tiled_kernel<1><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
-    case 2: mover_tiled_kernel<2><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
-    case 3: mover_tiled_kernel<3><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
-    case 4: mover_tiled_kernel<4><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
-    default: mover_tiled_kernel<0><<<grid, THREADS, MOVER_SMEM, ctx->stream>>>(tm, A); break;
+    case 1: PIC_LAUNCH(1); break;
+    case 2: PIC_LAUNCH(2); break;
+    case 3: PIC_LAUNCH(3); break;
+    case 4: PIC_LAUNCH(4); break;
+    default: PIC_LAUNCH(0); break;
   }
+#undef PIC_LAUNCH
   ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   sp.swap_buffers();
