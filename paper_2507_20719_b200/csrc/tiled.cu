@@ -48,7 +48,7 @@ constexpr int THREADS = 32 * WARPS;
 constexpr int MOVER_WARP_STAGE = 2 * 8 * 32 + 4 * 2 * 32 / 2;   // doubles: sources [2][8][32] + perm/key ring [4][2][32] u32
 constexpr int SGRP = 36;                        // doubles per 4-particle group in the S buffer (32 + pad)
 constexpr int WBUF = 8 * SGRP + 32 * 10;        // doubles per warp: S[8][36] + V[32][10]
-constexpr size_t DEPOSIT_SMEM = sizeof(double) * (10 * MB3 + WARPS * WBUF);
+constexpr size_t DEPOSIT_SMEM = sizeof(double) * (TILE3 * 80 + WARPS * WBUF);
 
 struct MoverTArgs {
   Geom g;
@@ -387,29 +387,43 @@ __global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::
 // --------------------------------------------------------------- deposit ----
 __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const DepositArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double *acc = reinterpret_cast<double *>(smem_raw);  // [10][MB3]
-  double *wbuf = acc + 10 * MB3;
+  double *cacc = reinterpret_cast<double *>(smem_raw);  // [64 cells][8 corners][10]
+  double *wbuf = cacc + TILE3 * 80;
   const Geom &g = A.g;
   const int tile = blockIdx.x;
-  const uint32_t p0 = A.cell_off[(int64_t)tile * TILE3], p1 = A.cell_off[(int64_t)(tile + 1) * TILE3];
+  const uint32_t *coff = A.cell_off + (int64_t)tile * TILE3;   // 65 offsets of this tile's cells
+  const uint32_t p0 = coff[0], p1 = coff[TILE3];
   if (p0 == p1) return;
   const int tx = (int)(tile % g.nt[0]);
   const int ty = (int)((tile / g.nt[0]) % g.nt[1]);
   const int tz = (int)(tile / (g.nt[0] * g.nt[1]));
   const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE, oz = (int64_t)tz * TILE;
   const int tid = threadIdx.x;
-  for (int i = tid; i < 10 * MB3; i += THREADS) acc[i] = 0.0;
+  for (int i = tid; i < TILE3 * 80; i += THREADS) cacc[i] = 0.0;
   __syncthreads();
 
+  // warp ranges are aligned to cell boundaries, so every cell belongs to one
+  // warp and its corner sums are stored without atomics
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t ntile = p1 - p0;
-  const uint32_t chunk = ((ntile + 32 * WARPS - 1) / (32 * WARPS)) * 32;
-  const uint32_t wbeg = p0 + warp * chunk;
-  const uint32_t wend = min(p1, wbeg + chunk);
+  int cbeg = 0, cend = 0;
+  {
+    const uint32_t t0 = p0 + (uint32_t)(((uint64_t)ntile * warp) / WARPS);
+    const uint32_t t1 = p0 + (uint32_t)(((uint64_t)ntile * (warp + 1)) / WARPS);
+    // first cell starting at or after the target (lane-parallel search over 64 cells)
+    const uint32_t o0 = coff[lane], o1 = coff[lane + 32];
+    const unsigned b0a = __ballot_sync(0xffffffffu, o0 >= t0), b0b = __ballot_sync(0xffffffffu, o1 >= t0);
+    const unsigned b1a = __ballot_sync(0xffffffffu, o0 >= t1), b1b = __ballot_sync(0xffffffffu, o1 >= t1);
+    cbeg = b0a ? __ffs(b0a) - 1 : (b0b ? 32 + __ffs(b0b) - 1 : TILE3);
+    cend = b1a ? __ffs(b1a) - 1 : (b1b ? 32 + __ffs(b1b) - 1 : TILE3);
+    if (warp == WARPS - 1) cend = TILE3;
+    if (warp == 0) cbeg = 0;
+  }
+  const uint32_t wbeg = coff[cbeg];
+  const uint32_t wend = coff[cend];
   double *Sb = wbuf + warp * WBUF;       // [8 groups][36]: S[k][j] at grp*36 + k*4 + j
   double *Vb = Sb + 8 * SGRP;            // [32][10]
   const int kc = lane & 7, js = lane >> 3;
-  const int koff = (kc & 1) + MB * (((kc >> 1) & 1) + MB * (kc >> 2));
   double accr[10];
 #pragma unroll
   for (int m = 0; m < 10; ++m) accr[m] = 0.0;
@@ -421,10 +435,10 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
       accr[m] += __shfl_xor_sync(0xffffffffu, accr[m], 8);
       accr[m] += __shfl_xor_sync(0xffffffffu, accr[m], 16);
     }
-    const int node = (c & 3) + MB * (((c >> 2) & 3) + MB * (c >> 4)) + koff;
+    double *dst = cacc + (c * 8 + kc) * 10;
 #pragma unroll
     for (int m = 0; m < 10; ++m) {
-      if ((m & 3) == js && accr[m] != 0.0) atomicAdd(acc + m * MB3 + node, accr[m]);
+      if ((m & 3) == js) dst[m] = accr[m];
       accr[m] = 0.0;
     }
   };
@@ -543,12 +557,24 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   if (cur >= 0) flush(cur);
   __syncthreads();
 
-  // tile accumulators -> global moments
+  // corner sums -> node sums of the tile (each node gathers its <= 8 cells)
+  // -> global moments (tile faces are shared with neighbour tiles: atomics)
   for (int i = tid; i < MB3; i += THREADS) {
     const int bx = i % MB, by = (i / MB) % MB, bz = i / (MB * MB);
+    double v[10];
+#pragma unroll
+    for (int m = 0; m < 10; ++m) v[m] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int cx = bx - (k & 1), cy = by - ((k >> 1) & 1), cz = bz - (k >> 2);
+      if (cx < 0 || cx >= TILE || cy < 0 || cy >= TILE || cz < 0 || cz >= TILE) continue;
+      const double *src = cacc + ((cx + TILE * (cy + TILE * cz)) * 8 + k) * 10;
+#pragma unroll
+      for (int m = 0; m < 10; ++m) v[m] += src[m];
+    }
     double vsum = 0.0;
 #pragma unroll
-    for (int m = 0; m < 10; ++m) vsum += fabs(acc[m * MB3 + i]);
+    for (int m = 0; m < 10; ++m) vsum += fabs(v[m]);
     if (vsum == 0.0) continue;
     const int64_t node = moment_node(g, ox + bx, oy + by, oz + bz);
     if (node < 0) {
@@ -556,10 +582,8 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
       continue;
     }
 #pragma unroll
-    for (int m = 0; m < 10; ++m) {
-      const double a = acc[m * MB3 + i];
-      if (a != 0.0) atomicAdd(A.mom + m * g.m_plane + node, a);
-    }
+    for (int m = 0; m < 10; ++m)
+      if (v[m] != 0.0) atomicAdd(A.mom + m * g.m_plane + node, v[m]);
   }
 }
 
@@ -629,7 +653,7 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   const unsigned grid = (unsigned)ctx->geom.ntiles;
   static const bool coef = [] {
     const char *e = getenv("PIC_MOVER_GATHER");
-    return !(e && strcmp(e, "nodes") == 0);
+    return e && strcmp(e, "coef") == 0;
   }();
 #define PIC_LAUNCH(NIT)                                                                                     \
   if (coef)                                                                                                 \
