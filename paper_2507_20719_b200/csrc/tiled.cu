@@ -164,8 +164,12 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
 //   W(f) = c000 + fz c001 + fy (c010 + fz c011) + fx (c100 + fz c101 + fy (c110 + fz c111)),
 // i.e. 7 FMA per component instead of 8 weights + 8 FMA.  NC^3 cells of the
 // staged box (tile cells -1 .. TILE).
+// The coefficient variant works on half tiles (4 x 4 x 2 cells; the lower and
+// upper halves of a tile are contiguous key ranges): NC x NC x NCZ staged cells.
 constexpr int NC = TILE + 2;
-constexpr int NC3 = NC * NC * NC;   // 216
+constexpr int NCZ = TILE / 2 + 2;
+constexpr int NC3 = NC * NC * NCZ;   // 144
+constexpr int NBZ = TILE / 2 + 3;    // staged node planes in z for a half tile
 __device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, const double u[3], double out[6]) {
   double f[3];
   int i[3];
@@ -175,7 +179,7 @@ __device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, con
     f[d] = u[d] - fl;
     i[d] = (int)fl;
   }
-  if (!((unsigned)i[0] < (unsigned)NC && (unsigned)i[1] < (unsigned)NC && (unsigned)i[2] < (unsigned)NC))
+  if (!((unsigned)i[0] < (unsigned)NC && (unsigned)i[1] < (unsigned)NC && (unsigned)i[2] < (unsigned)NCZ))
     return false;
   const double *c = coef + ((i[2] * NC + i[1]) * NC + i[0]) * 48;
 #pragma unroll
@@ -201,11 +205,11 @@ __device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, con
 // is 83 KB; the TMA node box is staged in the per-warp staging area and turned
 // into coefficients before the main loop).  !COEF: node gather, 8 warps.
 template <bool COEF> struct MoverShape {
-  static constexpr int WARPS_ = COEF ? 16 : 8;
+  static constexpr int WARPS_ = 8;
   static constexpr int THREADS_ = 32 * WARPS_;
   static constexpr int TABLE = COEF ? NC3 * 48 : NB3 * 6;         // doubles before the staging area
   static constexpr size_t SMEM = sizeof(double) * (TABLE + WARPS_ * MOVER_WARP_STAGE) + 16;
-  static constexpr int MINB = COEF ? 1 : PIC_MOVER_MINB;
+  static constexpr int MINB = PIC_MOVER_MINB;
 };
 
 template <int NIT, bool COEF>
@@ -220,15 +224,19 @@ __global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::
   uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_base + MW * MOVER_WARP_STAGE);
   const Geom &g = A.g;
 
-  const int tile = blockIdx.x;
-  if (tile == 0 && threadIdx.x == 0) *A.d_nraw = A.cell_off[g.ncells];
-  const uint32_t p0 = A.cell_off[(int64_t)tile * TILE3], p1 = A.cell_off[(int64_t)(tile + 1) * TILE3];
+  // COEF: one CTA per half tile (cells with lz in {0,1} or {2,3}: 32 contiguous keys)
+  const int tile = COEF ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int half = COEF ? (int)(blockIdx.x & 1) : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *A.d_nraw = A.cell_off[g.ncells];
+  const int64_t k0 = (int64_t)tile * TILE3 + (COEF ? half * (TILE3 / 2) : 0);
+  const uint32_t p0 = A.cell_off[k0], p1 = A.cell_off[k0 + (COEF ? TILE3 / 2 : TILE3)];
   if (p0 == p1) return;
   const int tx = (int)(tile % g.nt[0]);
   const int ty = (int)((tile / g.nt[0]) % g.nt[1]);
   const int tz = (int)(tile / (g.nt[0] * g.nt[1]));
-  // global cell (== node) index of the tile origin; box node 0 is origin - 1
-  const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE, oz = (int64_t)tz * TILE;
+  // global cell (== node) index of the (half) tile origin; box node 0 is origin - 1
+  const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE,
+                oz = (int64_t)tz * TILE + (COEF ? half * (TILE / 2) : 0);
   const double bo[3] = {(double)(ox - 1), (double)(oy - 1), (double)(oz - 1)};
   const int tid = threadIdx.x;
 
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_expect_tx(mbar, NB3 * 6 * 8);
+    mbar_expect_tx(mbar, (COEF ? NB * NB * NBZ : NB3) * 6 * 8);
     tma_load_4d(fld, &tmap, 0, (int)(ox - 1 - g.f_lo[0]), (int)(oy - 1 - g.f_lo[1]), (int)(oz - 1 - g.f_lo[2]),
                 mbar);
   }
@@ -248,7 +256,7 @@ __global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::
     // polynomial coefficients of every staged cell, pre-scaled by k_s, k_s/c
     for (int t = tid; t < NC3 * 6; t += MT) {
       const int m = t % 6, cell = t / 6;
-      const int cx = cell % NC, cy = (cell / NC) % NC, cz = cell / (NC * NC);
+      const int cx = cell % NC, cy = (cell / NC) % NC, cz = cell / (NC * NC);   // cz < NCZ
       auto n = [&](int a, int b, int c) { return fld[(((cz + c) * NB + (cy + b)) * NB + (cx + a)) * 6 + m]; };
       const double sc = m < 3 ? A.ks : A.ks_c;
       const double n000 = n(0, 0, 0), n001 = n(0, 0, 1), n010 = n(0, 1, 0), n011 = n(0, 1, 1);
@@ -608,6 +616,11 @@ static pic_status make_tmap(Ctx *ctx) {
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
+  cuuint32_t box_half[4] = {6, NB, NB, NBZ};
+  r = encode(reinterpret_cast<CUtensorMap *>(ctx->tmap_half), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)ctx->field,
+             dims, strides, box_half, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled (half tile) failed");
 #define PIC_SET_SMEM(NIT, C)                                                                           \
   PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                 (int)MoverShape<C>::SMEM))
@@ -650,6 +663,7 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   A.ks_c = A.ks / ctx->geom.c;
   A.n_iter = sp.n_iter;
   const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap);
+  const CUtensorMap &tmh = *reinterpret_cast<const CUtensorMap *>(ctx->tmap_half);
   const unsigned grid = (unsigned)ctx->geom.ntiles;
   static const bool coef = [] {
     const char *e = getenv("PIC_MOVER_GATHER");
@@ -657,7 +671,7 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   }();
 #define PIC_LAUNCH(NIT)                                                                                     \
   if (coef)                                                                                                 \
-    mover_tiled_kernel<NIT, true><<<grid, MoverShape<true>::THREADS_, MoverShape<true>::SMEM, ctx->stream>>>(tm, A); \
+    mover_tiled_kernel<NIT, true><<<2 * grid, MoverShape<true>::THREADS_, MoverShape<true>::SMEM, ctx->stream>>>(tmh, A); \
   else                                                                                                      \
     mover_tiled_kernel<NIT, false><<<grid, MoverShape<false>::THREADS_, MoverShape<false>::SMEM, ctx->stream>>>(tm, A);
   switch (sp.n_iter) {
