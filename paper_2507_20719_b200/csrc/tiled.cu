@@ -170,6 +170,7 @@ constexpr int NC = TILE + 2;
 constexpr int NCZ = TILE / 2 + 2;
 constexpr int NC3 = NC * NC * NCZ;   // 144
 constexpr int NBZ = TILE / 2 + 3;    // staged node planes in z for a half tile
+constexpr int CSTRIDE = 50;         // doubles per cell: 48 + 2 pad (consecutive cells on different banks)
 __device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, const double u[3], double out[6]) {
   double f[3];
   int i[3];
@@ -181,7 +182,7 @@ __device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, con
   }
   if (!((unsigned)i[0] < (unsigned)NC && (unsigned)i[1] < (unsigned)NC && (unsigned)i[2] < (unsigned)NCZ))
     return false;
-  const double *c = coef + ((i[2] * NC + i[1]) * NC + i[0]) * 48;
+  const double *c = coef + ((i[2] * NC + i[1]) * NC + i[0]) * CSTRIDE;
 #pragma unroll
   for (int m = 0; m < 6; ++m) {
     const double2 c0 = *reinterpret_cast<const double2 *>(c + 8 * m);
@@ -207,7 +208,7 @@ __device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, con
 template <bool COEF> struct MoverShape {
   static constexpr int WARPS_ = 8;
   static constexpr int THREADS_ = 32 * WARPS_;
-  static constexpr int TABLE = COEF ? NC3 * 48 : NB3 * 6;         // doubles before the staging area
+  static constexpr int TABLE = COEF ? NC3 * CSTRIDE : NB3 * 6;    // doubles before the staging area
   static constexpr size_t SMEM = sizeof(double) * (TABLE + WARPS_ * MOVER_WARP_STAGE) + 16;
   static constexpr int MINB = PIC_MOVER_MINB;
 };
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::
       const double sc = m < 3 ? A.ks : A.ks_c;
       const double n000 = n(0, 0, 0), n001 = n(0, 0, 1), n010 = n(0, 1, 0), n011 = n(0, 1, 1);
       const double n100 = n(1, 0, 0), n101 = n(1, 0, 1), n110 = n(1, 1, 0), n111 = n(1, 1, 1);
-      double *c = table + cell * 48 + 8 * m;
+      double *c = table + cell * CSTRIDE + 8 * m;
       c[0] = sc * n000;
       c[1] = sc * (n001 - n000);
       c[2] = sc * (n010 - n000);
