@@ -519,45 +519,30 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
         *reinterpret_cast<double2 *>(Vb + lane * 10 + m) = make_double2(val[m], val[m + 1]);
     }
     __syncwarp();
+    // runs of equal cells in the round (the order is sorted, so a round holds
+    // a few contiguous runs); each run accumulates into the register sums of
+    // its cell, the sums being flushed when the cell changes
     const unsigned navail = min(32u, wend - r0);
-    const int clo = __shfl_sync(0xffffffffu, c, 0);
-    const int chi = __shfl_sync(0xffffffffu, c, (int)navail - 1);
-    if (clo == chi && clo == cur) {
-      // fast path: the whole round belongs to the current cell
-      for (int grp = 0; grp < 8; ++grp) {
-        if ((unsigned)(grp * 4) >= navail) break;
-        const double s = Sb[grp * SGRP + kc * 4 + js];
-        const double *vv = Vb + (grp * 4 + js) * 10;
+    const int cprev = __shfl_up_sync(0xffffffffu, c, 1);
+    unsigned starts = __ballot_sync(0xffffffffu, (unsigned)lane < navail && (lane == 0 || c != cprev));
+    while (starts) {
+      const int b = __ffs(starts) - 1;
+      starts &= starts - 1;
+      const int e = starts ? __ffs(starts) - 1 : (int)navail;
+      const int rc = __shfl_sync(0xffffffffu, c, b);
+      if (rc != cur) {
+        if (cur >= 0) flush(cur);
+        cur = rc;
+      }
+      for (int grp = b >> 2; grp * 4 < e; ++grp) {
+        const int idx = grp * 4 + js;
+        const double s = (idx >= b && idx < e) ? Sb[grp * SGRP + kc * 4 + js] : 0.0;
+        const double *vv = Vb + idx * 10;
 #pragma unroll
         for (int m = 0; m < 10; m += 2) {
           const double2 t = *reinterpret_cast<const double2 *>(vv + m);
           accr[m] = fma(s, t.x, accr[m]);
           accr[m + 1] = fma(s, t.y, accr[m + 1]);
-        }
-      }
-    } else {
-      for (int grp = 0; grp < 8; ++grp) {
-        if ((unsigned)(grp * 4) >= navail) break;
-        const int cj = __shfl_sync(0xffffffffu, c, grp * 4 + js);
-        int v = (int)__reduce_min_sync(0xffffffffu, (unsigned)cj);
-        const double s = Sb[grp * SGRP + kc * 4 + js];
-        const double *vv = Vb + (grp * 4 + js) * 10;
-        double vals[10];
-#pragma unroll
-        for (int m = 0; m < 10; m += 2) {
-          const double2 t = *reinterpret_cast<const double2 *>(vv + m);
-          vals[m] = t.x;
-          vals[m + 1] = t.y;
-        }
-        while (v < 64) {
-          if (v != cur) {
-            if (cur >= 0) flush(cur);
-            cur = v;
-          }
-          const double sw = (cj == v) ? s : 0.0;
-#pragma unroll
-          for (int m = 0; m < 10; ++m) accr[m] = fma(sw, vals[m], accr[m]);
-          v = (int)__reduce_min_sync(0xffffffffu, (unsigned)(cj > v ? cj : 64));
         }
       }
     }
