@@ -137,7 +137,6 @@ struct Ctx {
   int64_t hstat[8] = {};             // host-side counters (sent / received)
   int64_t launches = 0;              // libpic kernel launches (pic_launch_count)
   alignas(64) unsigned char tmap[128] = {};  // CUtensorMap of the field window (tiled.cu)
-  alignas(64) unsigned char tmap_half[128] = {};  // same, half-tile box (coefficient mover)
   bool tmap_ok = false;
   int64_t cycle = 0;
   int64_t cap_max = 0;

@@ -158,86 +158,36 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
   return true;
 }
 
-// Per-cell polynomial form of the trilinear interpolant (the same function as
-// the 8-weight form of R12, re-associated): for each of the 6 components the
-// cell holds [c000 c001 c010 c011 c100 c101 c110 c111] with
-//   W(f) = c000 + fz c001 + fy (c010 + fz c011) + fx (c100 + fz c101 + fy (c110 + fz c111)),
-// i.e. 7 FMA per component instead of 8 weights + 8 FMA.  NC^3 cells of the
-// staged box (tile cells -1 .. TILE).
-// The coefficient variant works on half tiles (4 x 4 x 2 cells; the lower and
-// upper halves of a tile are contiguous key ranges): NC x NC x NCZ staged cells.
-constexpr int NC = TILE + 2;
-constexpr int NCZ = TILE / 2 + 2;
-constexpr int NC3 = NC * NC * NCZ;   // 144
-constexpr int NBZ = TILE / 2 + 3;    // staged node planes in z for a half tile
-constexpr int CSTRIDE = 50;         // doubles per cell: 48 + 2 pad (consecutive cells on different banks)
-__device__ __forceinline__ bool gather_coef(const double *__restrict__ coef, const double u[3], double out[6]) {
-  double f[3];
-  int i[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double fl = floor(u[d]);
-    f[d] = u[d] - fl;
-    i[d] = (int)fl;
-  }
-  if (!((unsigned)i[0] < (unsigned)NC && (unsigned)i[1] < (unsigned)NC && (unsigned)i[2] < (unsigned)NCZ))
-    return false;
-  const double *c = coef + ((i[2] * NC + i[1]) * NC + i[0]) * CSTRIDE;
-#pragma unroll
-  for (int m = 0; m < 6; ++m) {
-    const double2 c0 = *reinterpret_cast<const double2 *>(c + 8 * m);
-    const double2 c1 = *reinterpret_cast<const double2 *>(c + 8 * m + 2);
-    const double2 c2 = *reinterpret_cast<const double2 *>(c + 8 * m + 4);
-    const double2 c3 = *reinterpret_cast<const double2 *>(c + 8 * m + 6);
-    const double a = fma(f[2], c0.y, c0.x), b = fma(f[2], c1.y, c1.x);
-    const double cc = fma(f[2], c2.y, c2.x), dd = fma(f[2], c3.y, c3.x);
-    out[m] = fma(f[0], fma(f[1], dd, cc), fma(f[1], b, a));
-  }
-  return true;
-}
-
 // ----------------------------------------------------------------- mover ----
 #ifndef PIC_MOVER_MINB
 #define PIC_MOVER_MINB 2
 #endif
 // NIT > 0: the iteration count is a compile-time constant (fully unrolled);
 // NIT == 0: runtime A.n_iter.
-// COEF: per-cell polynomial gather, 16 warps per CTA (the coefficient table
-// is 83 KB; the TMA node box is staged in the per-warp staging area and turned
-// into coefficients before the main loop).  !COEF: node gather, 8 warps.
-template <bool COEF> struct MoverShape {
-  static constexpr int WARPS_ = 8;
-  static constexpr int THREADS_ = 32 * WARPS_;
-  static constexpr int TABLE = COEF ? NC3 * CSTRIDE : NB3 * 6;    // doubles before the staging area
-  static constexpr size_t SMEM = sizeof(double) * (TABLE + WARPS_ * MOVER_WARP_STAGE) + 16;
-  static constexpr int MINB = PIC_MOVER_MINB;
-};
+constexpr int MOVER_WARPS = 8;
+constexpr int MOVER_THREADS = 32 * MOVER_WARPS;
+constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + MOVER_WARPS * MOVER_WARP_STAGE) + 16;
 
-template <int NIT, bool COEF>
-__global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::MINB)
+template <int NIT>
+__global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap, const MoverTArgs A) {
-  constexpr int MW = MoverShape<COEF>::WARPS_;
-  constexpr int MT = MoverShape<COEF>::THREADS_;
+  constexpr int MW = MOVER_WARPS;
+  constexpr int MT = MOVER_THREADS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double *table = reinterpret_cast<double *>(smem_raw);            // node box (!COEF) or coefficients
-  double *stage_base = table + MoverShape<COEF>::TABLE;
-  double *fld = COEF ? stage_base : table;                         // TMA destination (node box)
+  double *fld = reinterpret_cast<double *>(smem_raw);              // staged node box
+  double *stage_base = fld + NB3 * 6;
   uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_base + MW * MOVER_WARP_STAGE);
   const Geom &g = A.g;
 
-  // COEF: one CTA per half tile (cells with lz in {0,1} or {2,3}: 32 contiguous keys)
-  const int tile = COEF ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int half = COEF ? (int)(blockIdx.x & 1) : 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *A.d_nraw = A.cell_off[g.ncells];
-  const int64_t k0 = (int64_t)tile * TILE3 + (COEF ? half * (TILE3 / 2) : 0);
-  const uint32_t p0 = A.cell_off[k0], p1 = A.cell_off[k0 + (COEF ? TILE3 / 2 : TILE3)];
+  const int tile = blockIdx.x;
+  if (tile == 0 && threadIdx.x == 0) *A.d_nraw = A.cell_off[g.ncells];
+  const uint32_t p0 = A.cell_off[(int64_t)tile * TILE3], p1 = A.cell_off[(int64_t)(tile + 1) * TILE3];
   if (p0 == p1) return;
   const int tx = (int)(tile % g.nt[0]);
   const int ty = (int)((tile / g.nt[0]) % g.nt[1]);
   const int tz = (int)(tile / (g.nt[0] * g.nt[1]));
-  // global cell (== node) index of the (half) tile origin; box node 0 is origin - 1
-  const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE,
-                oz = (int64_t)tz * TILE + (COEF ? half * (TILE / 2) : 0);
+  // global cell (== node) index of the tile origin; box node 0 is origin - 1
+  const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE, oz = (int64_t)tz * TILE;
   const double bo[3] = {(double)(ox - 1), (double)(oy - 1), (double)(oz - 1)};
   const int tid = threadIdx.x;
 
@@ -248,31 +198,12 @@ __global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_expect_tx(mbar, (COEF ? NB * NB * NBZ : NB3) * 6 * 8);
+    mbar_expect_tx(mbar, NB3 * 6 * 8);
     tma_load_4d(fld, &tmap, 0, (int)(ox - 1 - g.f_lo[0]), (int)(oy - 1 - g.f_lo[1]), (int)(oz - 1 - g.f_lo[2]),
                 mbar);
   }
   mbar_wait(mbar, 0);
-  if (COEF) {
-    // polynomial coefficients of every staged cell, pre-scaled by k_s, k_s/c
-    for (int t = tid; t < NC3 * 6; t += MT) {
-      const int m = t % 6, cell = t / 6;
-      const int cx = cell % NC, cy = (cell / NC) % NC, cz = cell / (NC * NC);   // cz < NCZ
-      auto n = [&](int a, int b, int c) { return fld[(((cz + c) * NB + (cy + b)) * NB + (cx + a)) * 6 + m]; };
-      const double sc = m < 3 ? A.ks : A.ks_c;
-      const double n000 = n(0, 0, 0), n001 = n(0, 0, 1), n010 = n(0, 1, 0), n011 = n(0, 1, 1);
-      const double n100 = n(1, 0, 0), n101 = n(1, 0, 1), n110 = n(1, 1, 0), n111 = n(1, 1, 1);
-      double *c = table + cell * CSTRIDE + 8 * m;
-      c[0] = sc * n000;
-      c[1] = sc * (n001 - n000);
-      c[2] = sc * (n010 - n000);
-      c[3] = sc * ((n011 - n010) - (n001 - n000));
-      c[4] = sc * (n100 - n000);
-      c[5] = sc * ((n101 - n100) - (n001 - n000));
-      c[6] = sc * ((n110 - n100) - (n010 - n000));
-      c[7] = sc * (((n111 - n110) - (n101 - n100)) - ((n011 - n010) - (n001 - n000)));
-    }
-  } else {
+  {
     for (int i = tid; i < NB3 * 6; i += MT) fld[i] *= ((i % 6) < 3) ? A.ks : A.ks_c;
   }
   __syncthreads();
@@ -348,7 +279,7 @@ __global__ void __launch_bounds__(MoverShape<COEF>::THREADS_, MoverShape<COEF>::
       for (int it = 0; it < n_iter; ++it) {
         double EB[6];
         const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
-        if (!(COEF ? gather_coef(table, u, EB) : gather_smem(table, u, EB))) {
+        if (!gather_smem(fld, u, EB)) {
           clamped |= sample_window(g, A.field, xb, EB);
 #pragma unroll
           for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
@@ -534,15 +465,31 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
         if (cur >= 0) flush(cur);
         cur = rc;
       }
-      for (int grp = b >> 2; grp * 4 < e; ++grp) {
-        const int idx = grp * 4 + js;
-        const double s = (idx >= b && idx < e) ? Sb[grp * SGRP + kc * 4 + js] : 0.0;
-        const double *vv = Vb + idx * 10;
+      if (b == 0 && e == 32) {
+        // the whole round is one cell: straight-line, loads of all groups in flight
 #pragma unroll
-        for (int m = 0; m < 10; m += 2) {
-          const double2 t = *reinterpret_cast<const double2 *>(vv + m);
-          accr[m] = fma(s, t.x, accr[m]);
-          accr[m + 1] = fma(s, t.y, accr[m + 1]);
+        for (int grp = 0; grp < 8; ++grp) {
+          const double s = Sb[grp * SGRP + kc * 4 + js];
+          const double *vv = Vb + (grp * 4 + js) * 10;
+#pragma unroll
+          for (int m = 0; m < 10; m += 2) {
+            const double2 t = *reinterpret_cast<const double2 *>(vv + m);
+            accr[m] = fma(s, t.x, accr[m]);
+            accr[m + 1] = fma(s, t.y, accr[m + 1]);
+          }
+        }
+      } else {
+#pragma unroll 2
+        for (int grp = b >> 2; grp * 4 < e; ++grp) {
+          const int idx = grp * 4 + js;
+          const double s = (idx >= b && idx < e) ? Sb[grp * SGRP + kc * 4 + js] : 0.0;
+          const double *vv = Vb + idx * 10;
+#pragma unroll
+          for (int m = 0; m < 10; m += 2) {
+            const double2 t = *reinterpret_cast<const double2 *>(vv + m);
+            accr[m] = fma(s, t.x, accr[m]);
+            accr[m + 1] = fma(s, t.y, accr[m + 1]);
+          }
         }
       }
     }
@@ -602,17 +549,9 @@ static pic_status make_tmap(Ctx *ctx) {
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
-  cuuint32_t box_half[4] = {6, NB, NB, NBZ};
-  r = encode(reinterpret_cast<CUtensorMap *>(ctx->tmap_half), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)ctx->field,
-             dims, strides, box_half, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled (half tile) failed");
-#define PIC_SET_SMEM(NIT, C)                                                                           \
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                (int)MoverShape<C>::SMEM))
-  PIC_SET_SMEM(0, true); PIC_SET_SMEM(1, true); PIC_SET_SMEM(2, true); PIC_SET_SMEM(3, true); PIC_SET_SMEM(4, true);
-  PIC_SET_SMEM(0, false); PIC_SET_SMEM(1, false); PIC_SET_SMEM(2, false); PIC_SET_SMEM(3, false);
-  PIC_SET_SMEM(4, false);
+#define PIC_SET_SMEM(NIT) \
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM))
+  PIC_SET_SMEM(0); PIC_SET_SMEM(1); PIC_SET_SMEM(2); PIC_SET_SMEM(3); PIC_SET_SMEM(4);
 #undef PIC_SET_SMEM
   PIC_CUDA(cudaFuncSetAttribute(deposit_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)DEPOSIT_SMEM));
@@ -649,17 +588,9 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   A.ks_c = A.ks / ctx->geom.c;
   A.n_iter = sp.n_iter;
   const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap);
-  const CUtensorMap &tmh = *reinterpret_cast<const CUtensorMap *>(ctx->tmap_half);
   const unsigned grid = (unsigned)ctx->geom.ntiles;
-  static const bool coef = [] {
-    const char *e = getenv("PIC_MOVER_GATHER");
-    return e && strcmp(e, "coef") == 0;
-  }();
-#define PIC_LAUNCH(NIT)                                                                                     \
-  if (coef)                                                                                                 \
-    mover_tiled_kernel<NIT, true><<<2 * grid, MoverShape<true>::THREADS_, MoverShape<true>::SMEM, ctx->stream>>>(tmh, A); \
-  else                                                                                                      \
-    mover_tiled_kernel<NIT, false><<<grid, MoverShape<false>::THREADS_, MoverShape<false>::SMEM, ctx->stream>>>(tm, A);
+#define PIC_LAUNCH(NIT) \
+  mover_tiled_kernel<NIT><<<grid, MOVER_THREADS, MOVER_SMEM, ctx->stream>>>(tm, A)
   switch (sp.n_iter) {
     case 1: PIC_LAUNCH(1); break;
     case 2: PIC_LAUNCH(2); break;
