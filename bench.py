@@ -246,7 +246,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = ctx.launch_count()
-    updates = 0
+    ctx.profile(True)        # CUDA events around each phase, on the libpic stream
     barrier()
     with ClockSampler(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
@@ -263,6 +263,8 @@ def main():
         end.record(stream)
         barrier()
     launches = ctx.launch_count() - launches0
+    prof = ctx.profile_read()
+    ctx.profile(False)
     stats = ctx.sync()
     t_ms = start.elapsed_time(end)
     mover_ms = [a.elapsed_time(b) for a, b, c in ev]
@@ -276,21 +278,45 @@ def main():
     total_updates = float(tot.item()) * args.steps
     value = total_updates / (t_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (the mover launch, fused with the
-    # deposit in the tiled family): algorithmic bytes / its event-timed duration
+    # ---- roofline of the dominant kernel: the mover kernel (Eq. 2).  achieved =
+    # its algorithmic bytes (read x, v: 48 B; write x, v: 48 B; plus the field
+    # share 48 B per node / particles per cell) x particles / its event-timed
+    # duration (pic_profile: CUDA events on the libpic stream around the mover
+    # launches inside the timed region).  The whole step's fraction uses the
+    # north_star figure 104 B + grid share.
     peak, peak_kind = measured_peaks()
-    fused = args.kernel in (0, 2)
     n_sp = len(w.species)
     ppc = w.species[0].ppc
     grid_share = (48.0 + 80.0 * n_sp) / (ppc * n_sp)
-    b_mover = (B_ALG_PARTICLE + grid_share) if fused else (96.0 + 48.0 / (ppc * n_sp))
-    mover_avg = sum(mover_ms) / len(mover_ms)
-    achieved = n_alive * b_mover / (mover_avg / 1e3) / 1e9
-    roof = {"bound": "hbm", "kernel": "tiled fused mover+deposit" if fused else "mover_basic",
+    b_mover = 96.0 + 48.0 / (ppc * n_sp)
+    b_deposit = 56.0 + 80.0 / ppc
+    mover_ms_step = prof["mover"][0] / args.steps
+    deposit_ms_step = prof["deposit"][0] / args.steps
+    mover_launch_ms = prof["mover"][0] / max(1, prof["mover"][1])
+    achieved = n_alive * b_mover / (mover_ms_step / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("config") == args.config:
+                # ncu --set full capture of one mover launch (one species): DRAM bytes per
+                # particle update, scaled to this launch's particles
+                traffic = tj["mover_bytes_per_update"] * n_alive / n_sp
+        except Exception:
+            traffic = None
+    kname = "mover_tiled_kernel" if args.kernel in (0, 2) else "mover_basic_kernel"
+    roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None,
-            "bytes_per_update": b_mover, "launch_ms": mover_avg,
-            "step_frac": (value / world) * (B_ALG_PARTICLE + grid_share) / (peak * 1e9)}
+            "frac": achieved / peak, "traffic": traffic,
+            "bytes_per_update": b_mover, "launch_ms": mover_launch_ms,
+            "launches_per_step": prof["mover"][1] / args.steps,
+            "step_frac": (value / world) * (B_ALG_PARTICLE + grid_share) / (peak * 1e9),
+            "step_bytes_per_update": B_ALG_PARTICLE + grid_share,
+            "deposit": {"kernel": "deposit_tiled_kernel" if args.kernel in (0, 2) else "moments_basic_kernel",
+                        "bytes_per_update": b_deposit, "ms_per_step": deposit_ms_step,
+                        "achieved": n_alive * b_deposit / (deposit_ms_step / 1e3) / 1e9 if deposit_ms_step else None}}
+    mover_avg = sum(mover_ms) / len(mover_ms)
 
     # ---- e2e through the public API with host buffers (paper's discrete-GPU
     # cycle: fields host->device, moments device->host)
@@ -346,7 +372,8 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "phase_ms": {"mover": mover_avg, "moments+exchange": sum(rest_ms) / len(rest_ms)},
+            "phase_ms": {"mover+order": mover_avg, "moments+exchange": sum(rest_ms) / len(rest_ms),
+                         "kernels_per_step": {k: v[0] / args.steps for k, v in prof.items()}},
             "stats": stats,
         }
         print(json.dumps(line), flush=True)

@@ -186,6 +186,16 @@ PIC_API pic_status pic_sync(pic_ctx *ctx, int64_t stats[8]);
  * (the bench's gpu_launches evidence).                                       */
 PIC_API pic_status pic_launch_count(const pic_ctx *ctx, int64_t *n);
 
+/* Kernel timing with CUDA events recorded on the context stream around the
+ * launches of each phase.  pic_profile(ctx, 1) resets and enables it (events
+ * cost nothing measurable), 0 disables it.  pic_profile_read synchronises the
+ * stream and returns accumulated milliseconds and launch counts:
+ *   ms[0] mover kernels (Eq. 2), ms[1] order build (scan + perm scatter),
+ *   ms[2] deposit kernels (Eq. 3), ms[3] exchange (folds, ghost sums, migration)
+ *   launches[0..3] the number of timed intervals of each phase.               */
+PIC_API pic_status pic_profile(pic_ctx *ctx, int32_t enable);
+PIC_API pic_status pic_profile_read(pic_ctx *ctx, double ms[4], int64_t launches[4]);
+
 /* Human-readable text of the last error on this context (never NULL).       */
 PIC_API const char *pic_last_error(const pic_ctx *ctx);
 

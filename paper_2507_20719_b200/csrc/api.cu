@@ -343,15 +343,16 @@ pic_status pic_moments(pic_ctx *p, int32_t s) {
     if (ctx->sp[k].deposited) return fail(ctx, PIC_ESTATE, "pic_moments called twice without pic_exchange");
   for (int k = s0; k < s1; ++k) {
     SpeciesStore &sp = ctx->sp[k];
-    if (use_tiled(ctx)) {
-      st = launch_tiled_deposit(ctx, k);
-      if (st != PIC_OK) return st;
-    } else {
-      st = zero_moments(ctx, k);
-      if (st != PIC_OK) return st;
-      st = launch_moments_basic(ctx, k);
-      if (st != PIC_OK) return st;
+    {
+      PhaseTimer t(ctx, 2);
+      if (use_tiled(ctx)) {
+        st = launch_tiled_deposit(ctx, k);
+      } else {
+        st = zero_moments(ctx, k);
+        if (st == PIC_OK) st = launch_moments_basic(ctx, k);
+      }
     }
+    if (st != PIC_OK) return st;
     sp.deposited = true;
   }
   return PIC_OK;
@@ -362,7 +363,11 @@ pic_status pic_exchange(pic_ctx *p) {
   Ctx *ctx = C(p);
   for (int k = 0; k < ctx->cfg.n_species; ++k)
     if (!ctx->sp[k].deposited) return fail(ctx, PIC_ESTATE, "pic_exchange before pic_moments of every species");
-  pic_status st = exchange(ctx);
+  pic_status st;
+  {
+    PhaseTimer t(ctx, 3);
+    st = exchange(ctx);
+  }
   if (st != PIC_OK) return st;
   for (int k = 0; k < ctx->cfg.n_species; ++k) ctx->sp[k].moved = ctx->sp[k].deposited = false;
   ctx->cycle++;
@@ -417,6 +422,37 @@ pic_status pic_launch_count(const pic_ctx *p, int64_t *n) {
   return PIC_OK;
 }
 
+pic_status pic_profile(pic_ctx *p, int32_t enable) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto &v : ctx->prof_ev)
+    for (auto &e : v) {
+      ctx->prof_pool.push_back(e.first);
+      ctx->prof_pool.push_back(e.second);
+    }
+  for (auto &v : ctx->prof_ev) v.clear();
+  ctx->prof_on = enable != 0;
+  return PIC_OK;
+}
+
+pic_status pic_profile_read(pic_ctx *p, double ms[4], int64_t launches[4]) {
+  if (!p || !ms || !launches) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < 4; ++k) {
+    double t = 0.0;
+    for (auto &e : ctx->prof_ev[k]) {
+      float f = 0.f;
+      PIC_CUDA(cudaEventElapsedTime(&f, e.first, e.second));
+      t += f;
+    }
+    ms[k] = t;
+    launches[k] = (int64_t)ctx->prof_ev[k].size();
+  }
+  return PIC_OK;
+}
+
 const char *pic_last_error(const pic_ctx *p) {
   if (!p) return "null context";
   return C(p)->err.c_str();
@@ -426,6 +462,12 @@ pic_status pic_destroy(pic_ctx *p) {
   if (!p) return PIC_EINVAL;
   Ctx *ctx = C(p);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
+  for (auto &v : ctx->prof_ev)
+    for (auto &e : v) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
   delete[] ctx->host_counts;
   delete ctx;
   return PIC_OK;

@@ -150,9 +150,13 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   A.n_iter = S.n_iter;
   const int threads = 256;
   const int64_t blocks = std::max<int64_t>(1, (S.n_raw + threads - 1) / threads);
-  mover_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(A); ++ctx->launches;
+  {
+    PhaseTimer t(ctx, 0);
+    mover_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(A); ++ctx->launches;
+  }
   PIC_CUDA(cudaGetLastError());
   S.swap_buffers();
+  PhaseTimer t(ctx, 1);
   return build_order(ctx, s);
 }
 

@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 #include <cuda_runtime.h>
 #include "pic.h"
 
@@ -141,6 +142,40 @@ struct Ctx {
   int64_t cycle = 0;
   int64_t cap_max = 0;
   std::string err;
+  // pic_profile: CUDA event pairs per phase (0 mover, 1 order, 2 deposit, 3 exchange)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];
+  cudaEvent_t prof_event() {
+    if (!prof_pool.empty()) {
+      cudaEvent_t e = prof_pool.back();
+      prof_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+// Records an event pair around a phase when profiling is on (RAII).
+struct PhaseTimer {
+  Ctx *ctx;
+  int phase;
+  cudaEvent_t start = nullptr;
+  PhaseTimer(Ctx *c, int ph) : ctx(c), phase(ph) {
+    if (ctx->prof_on) {
+      start = ctx->prof_event();
+      cudaEventRecord(start, ctx->stream);
+    }
+  }
+  ~PhaseTimer() {
+    if (start) {
+      cudaEvent_t stop = ctx->prof_event();
+      cudaEventRecord(stop, ctx->stream);
+      ctx->prof_ev[phase].emplace_back(start, stop);
+    }
+  }
 };
 
 // ------------------------------------------------------------ error helpers --

@@ -591,17 +591,21 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   const unsigned grid = (unsigned)ctx->geom.ntiles;
 #define PIC_LAUNCH(NIT) \
   mover_tiled_kernel<NIT><<<grid, MOVER_THREADS, MOVER_SMEM, ctx->stream>>>(tm, A)
-  switch (sp.n_iter) {
-    case 1: PIC_LAUNCH(1); break;
-    case 2: PIC_LAUNCH(2); break;
-    case 3: PIC_LAUNCH(3); break;
-    case 4: PIC_LAUNCH(4); break;
-    default: PIC_LAUNCH(0); break;
+  {
+    PhaseTimer t(ctx, 0);
+    switch (sp.n_iter) {
+      case 1: PIC_LAUNCH(1); break;
+      case 2: PIC_LAUNCH(2); break;
+      case 3: PIC_LAUNCH(3); break;
+      case 4: PIC_LAUNCH(4); break;
+      default: PIC_LAUNCH(0); break;
+    }
   }
 #undef PIC_LAUNCH
   ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   sp.swap_buffers();
+  PhaseTimer t(ctx, 1);
   return build_order(ctx, s);
 }
 

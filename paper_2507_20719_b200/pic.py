@@ -32,7 +32,7 @@ STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "ove
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_launch_count", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -82,6 +82,8 @@ def load_library(path: str = LIB_PATH):
         lib.pic_get_moments.argtypes = [vp, C.c_int32, vp]
         lib.pic_sync.argtypes = [vp, P(C.c_int64)]
         lib.pic_launch_count.argtypes = [vp, P(C.c_int64)]
+        lib.pic_profile.argtypes = [vp, C.c_int32]
+        lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
         lib.pic_last_error.restype = C.c_char_p
         lib.pic_destroy.argtypes = [vp]
@@ -225,6 +227,16 @@ class Context:
         out = C.c_int64()
         _check(self.lib.pic_launch_count(self.h, C.byref(out)), self.h, "pic_launch_count")
         return out.value
+
+    def profile(self, enable: bool = True):
+        _check(self.lib.pic_profile(self.h, 1 if enable else 0), self.h, "pic_profile")
+
+    def profile_read(self):
+        """{phase: (ms, launches)} for mover, order, deposit, exchange."""
+        ms = (C.c_double * 4)()
+        n = (C.c_int64 * 4)()
+        _check(self.lib.pic_profile_read(self.h, ms, n), self.h, "pic_profile_read")
+        return {k: (ms[i], n[i]) for i, k in enumerate(("mover", "order", "deposit", "exchange"))}
 
     def close(self):
         if getattr(self, "h", None):
