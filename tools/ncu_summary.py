@@ -30,8 +30,12 @@ KEYS = [
 ]
 
 
+LAUNCH = 0
+
+
 def ncu_csv(rep, *args):
-    out = subprocess.check_output(["ncu", "-i", rep, "--csv"] + list(args), stderr=subprocess.DEVNULL).decode()
+    out = subprocess.check_output(["ncu", "-i", rep, "--csv", "--launch-skip", str(LAUNCH), "--launch-count", "1"]
+                                  + list(args), stderr=subprocess.DEVNULL).decode()
     return list(csv.reader(io.StringIO(out)))
 
 
@@ -41,7 +45,10 @@ def main():
     ap.add_argument("out_prefix")
     ap.add_argument("--particles", type=float, required=True, help="particles processed by the profiled launch")
     ap.add_argument("--title", default="")
+    ap.add_argument("--launch", type=int, default=0, help="index of the profiled launch in the report")
     a = ap.parse_args()
+    global LAUNCH
+    LAUNCH = a.launch
     rows = ncu_csv(a.rep, "--page", "raw")
     h, units, vals = rows[0], rows[1], rows[2]
     kname = vals[h.index("Kernel Name")] if "Kernel Name" in h else "?"
