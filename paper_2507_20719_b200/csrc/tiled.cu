@@ -45,7 +45,10 @@ constexpr int MB = TILE + 1;            // deposit nodes per axis: 0 .. TILE
 constexpr int MB3 = MB * MB * MB;       // 125
 constexpr int WARPS = 8;
 constexpr int THREADS = 32 * WARPS;
-constexpr int MOVER_WARP_STAGE = 2 * 8 * 32 + 4 * 2 * 32 / 2;   // doubles: sources [2][8][32] + perm/key ring [4][2][32] u32
+constexpr int SRC_STAGES = 3;    // mover: rounds of gathered sources in flight (ring)
+constexpr int PK_SLOTS = 6;      // mover: perm/key ring slots
+constexpr int PK_AHEAD = 5;      // mover: perm/key fetched this many rounds ahead
+constexpr int MOVER_WARP_STAGE = SRC_STAGES * 8 * 32 + PK_SLOTS * 2 * 32 / 2;  // doubles per warp
 constexpr int SGRP = 36;                        // doubles per 4-particle group in the S buffer (32 + pad)
 constexpr int WBUF = 8 * SGRP + 32 * 10;        // doubles per warp: S[8][36] + V[32][10]
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (TILE3 * 80 + WARPS * WBUF);
@@ -217,26 +220,26 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
   const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
 
   // Software pipeline through shared memory (cp.async / LDGSTS, no register
-  // dependencies): in round r the warp gathers the sources of round r+1 into a
-  // double buffer and fetches perm/key of round r+3 into a 4-slot ring, one
-  // commit group per round; "wait_group 1" then guarantees round r's sources.
+  // dependencies): in round r the warp gathers the sources of round r+2 into a
+  // 3-deep buffer ring and fetches perm/key of round r+5 into a 6-slot ring, one
+  // commit group per round; "wait_group 2" then guarantees round r's sources.
   // The counting-sort rank of a round completes during the next one, so the
   // global atomic's latency overlaps compute.
-  double *stg = stage_base + (size_t)warp * MOVER_WARP_STAGE;      // [2][8][32] doubles
-  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + 2 * 8 * 32);    // [4][2][32] (perm, key)
-  auto fetch_pk = [&](uint32_t rr) {   // perm/key of the round starting at rr
-    const uint32_t q = rr + lane;
+  double *stg = stage_base + (size_t)warp * MOVER_WARP_STAGE;          // [3][8][32] doubles
+  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + SRC_STAGES * 8 * 32);  // [6][2][32] (perm, key)
+  auto fetch_pk = [&](int ri) {        // perm/key of round ri
+    const uint32_t q = wbeg + 32u * ri + lane;
     if (q < wend) {
-      uint32_t *slot = pk + (((rr - wbeg) >> 5) & 3) * 64 + lane;
+      uint32_t *slot = pk + (ri % PK_SLOTS) * 64 + lane;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(A.perm + q) : "memory");
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 32)), "l"(A.key + q) : "memory");
     }
   };
-  auto fetch_src = [&](uint32_t rr) {  // sources of the round starting at rr (perm already in the ring)
-    const uint32_t q = rr + lane;
+  auto fetch_src = [&](int ri) {       // sources of round ri (its perm is already in the ring)
+    const uint32_t q = wbeg + 32u * ri + lane;
     if (q < wend) {
-      const uint32_t src_idx = pk[(((rr - wbeg) >> 5) & 3) * 64 + lane];
-      double *d = stg + (((rr - wbeg) >> 5) & 1) * (8 * 32) + lane;
+      const uint32_t src_idx = pk[(ri % PK_SLOTS) * 64 + lane];
+      double *d = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
 #pragma unroll
       for (int k = 0; k < 7; ++k)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
@@ -245,26 +248,27 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
                    : "memory");
     }
   };
-  fetch_pk(wbeg);
-  fetch_pk(wbeg + 32);
-  fetch_pk(wbeg + 64);
+  for (int ri = 0; ri < PK_AHEAD; ++ri) fetch_pk(ri);
   asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  fetch_src(wbeg);
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int ri = 0; ri < SRC_STAGES - 1; ++ri) {
+    fetch_src(ri);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   // rank ticket of the previous round: its atomic flies while this round computes
   RankTicket tk;
   tk.base = 0; tk.peers = 0; tk.leader = 0; tk.counted = false; tk.arrival = false;
   uint32_t pr_p = 0;
-  for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
+  int ri = 0;
+  for (uint32_t r0 = wbeg; r0 < wend; r0 += 32, ++ri) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    const uint32_t kold = act ? pk[(((r0 - wbeg) >> 5) & 3) * 64 + 32 + lane] : 0u;
-    fetch_src(r0 + 32);
-    fetch_pk(r0 + 96);
+    const uint32_t kold = act ? pk[(ri % PK_SLOTS) * 64 + 32 + lane] : 0u;
+    fetch_src(ri + SRC_STAGES - 1);
+    fetch_pk(ri + PK_AHEAD);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    const double *sv = stg + (((r0 - wbeg) >> 5) & 1) * (8 * 32) + lane;
+    asm volatile("cp.async.wait_group %0;" ::"n"(SRC_STAGES - 1) : "memory");
+    const double *sv = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
     uint32_t knew = KEY_DEAD;
     if (act) {
       const double qv = sv[6 * 32];
