@@ -100,7 +100,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   int64_t cap_max = 0;
   for (int s = 0; s < c->n_species; ++s) cap_max = std::max<int64_t>(cap_max, c->capacity[s]);
   cap_max = std::max<int64_t>(cap_max, 1);
-  const int64_t mig_cap = std::max<int64_t>(cap_max / 4, 4096);
+  const int64_t mig_cap = std::max<int64_t>(cap_max / 64, 65536);   // slab leavers per side per species
   for (int s = 0; s < c->n_species; ++s) {
     // two buffers of the SoA store (the mover gathers A[perm[q]] into B[q]),
     // plus the order metadata of the counting sort (order.cu)
@@ -143,9 +143,9 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   const int64_t ghost_elems = (int64_t)(c->ghost + 1) * face;
   int64_t og[4];
   const bool multi = c->nranks > 1;
-  for (int k = 0; k < 4; ++k) og[k] = L.take(multi ? 8 * ghost_elems : 8);
+  for (int k = 0; k < 4; ++k) og[k] = L.take(multi ? 8 * ghost_elems * c->n_species : 8);
   int64_t om[4];
-  for (int k = 0; k < 4; ++k) om[k] = L.take(multi || k < 2 ? 8 * 8 * mig_cap : 8);
+  for (int k = 0; k < 4; ++k) om[k] = L.take(multi ? 8 * 8 * mig_cap * c->n_species : 8);
   const int64_t pack_elems = (g.k_n[0] + 1) * g.m_n[1] * g.m_n[2] * 10;
   int64_t opack = L.take(8 * pack_elems);
   int64_t ocub = L.take((int64_t)cub_bytes);
@@ -230,7 +230,7 @@ pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
     return PIC_ENOMEM;
   }
   plan(cfg, ctx->geom, ctx, (char *)workspace, cub_bytes);
-  ctx->host_counts = new int64_t[16]();
+  ctx->host_counts = new int64_t[64]();
   cudaError_t e = cudaMemset(ctx->stats, 0, 8 * ST_N);
   if (e != cudaSuccess) { delete[] ctx->host_counts; delete ctx; return PIC_ECUDA; }
   e = cudaMemset(ctx->field, 0, 8 * ctx->field_elems);

@@ -123,31 +123,39 @@ static pic_status fold_and_ghosts(Ctx *ctx) {
   const int64_t face = ny * nz * 10;
   const int64_t nR = (int64_t)(G + 1) * face, nL = (int64_t)G * face;
   ncclComm_t comm = (ncclComm_t)ctx->nccl;
+  const int64_t gs = ctx->ghost_elems;   // per-species stride in the ghost buffers
   for (int s = 0; s < S; ++s) {
     double *mom = ctx->sp[s].mom;
     if (right >= 0)
-      xplanes_kernel<<<grid_for(nR), 256, 0, ctx->stream>>>(mom, ctx->ghost_send[1], a_right_ghost,
+      xplanes_kernel<<<grid_for(nR), 256, 0, ctx->stream>>>(mom, ctx->ghost_send[1] + s * gs, a_right_ghost,
                                                              G + 1, nx, ny, nz, g.m_plane, 0, 1); ++ctx->launches;
     if (left >= 0)
-      xplanes_kernel<<<grid_for(nL), 256, 0, ctx->stream>>>(mom, ctx->ghost_send[0], a_left_ghost,
+      xplanes_kernel<<<grid_for(nL), 256, 0, ctx->stream>>>(mom, ctx->ghost_send[0] + s * gs, a_left_ghost,
                                                              G, nx, ny, nz, g.m_plane, 0, 1); ++ctx->launches;
-    PIC_CUDA(cudaGetLastError());
-    PIC_NCCL(ncclGroupStart());
-    if (right >= 0) PIC_NCCL(ncclSend(ctx->ghost_send[1], nR, ncclDouble, right, comm, ctx->stream));
-    if (left >= 0) PIC_NCCL(ncclSend(ctx->ghost_send[0], nL, ncclDouble, left, comm, ctx->stream));
-    if (left >= 0) PIC_NCCL(ncclRecv(ctx->ghost_recv[0], nR, ncclDouble, left, comm, ctx->stream));
-    if (right >= 0) PIC_NCCL(ncclRecv(ctx->ghost_recv[1], nL, ncclDouble, right, comm, ctx->stream));
-    PIC_NCCL(ncclGroupEnd());
+  }
+  PIC_CUDA(cudaGetLastError());
+  // one NCCL group for every species; per-peer order send-right, send-left,
+  // recv-left, recv-right (matches when left == right, P == 2)
+  PIC_NCCL(ncclGroupStart());
+  for (int s = 0; s < S; ++s) {
+    if (right >= 0) PIC_NCCL(ncclSend(ctx->ghost_send[1] + s * gs, nR, ncclDouble, right, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclSend(ctx->ghost_send[0] + s * gs, nL, ncclDouble, left, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclRecv(ctx->ghost_recv[0] + s * gs, nR, ncclDouble, left, comm, ctx->stream));
+    if (right >= 0) PIC_NCCL(ncclRecv(ctx->ghost_recv[1] + s * gs, nL, ncclDouble, right, comm, ctx->stream));
+  }
+  PIC_NCCL(ncclGroupEnd());
+  for (int s = 0; s < S; ++s) {
+    double *mom = ctx->sp[s].mom;
     // from the left neighbour: its planes [its slab_hi, +G] == my [slab_lo, slab_lo+G]
     if (left >= 0)
-      xplanes_kernel<<<grid_for(nR), 256, 0, ctx->stream>>>(mom, ctx->ghost_recv[0], G, G + 1, nx,
+      xplanes_kernel<<<grid_for(nR), 256, 0, ctx->stream>>>(mom, ctx->ghost_recv[0] + s * gs, G, G + 1, nx,
                                                              ny, nz, g.m_plane, 1, 0); ++ctx->launches;
     // from the right neighbour: its planes [its slab_lo-G, -1] == my [slab_hi-G, slab_hi-1]
     if (right >= 0)
-      xplanes_kernel<<<grid_for(nL), 256, 0, ctx->stream>>>(mom, ctx->ghost_recv[1], nloc, G, nx,
+      xplanes_kernel<<<grid_for(nL), 256, 0, ctx->stream>>>(mom, ctx->ghost_recv[1] + s * gs, nloc, G, nx,
                                                              ny, nz, g.m_plane, 1, 0); ++ctx->launches;
-    PIC_CUDA(cudaGetLastError());
   }
+  PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }
 
@@ -229,69 +237,87 @@ static pic_status migrate(Ctx *ctx) {
   const int left = (r > 0) ? r - 1 : (per ? P - 1 : -1);
   const int right = (r < P - 1) ? r + 1 : (per ? 0 : -1);
   ncclComm_t comm = (ncclComm_t)ctx->nccl;
-  unsigned long long *cnt = (unsigned long long *)ctx->dev_counts;  // [S][2] leavers L/R, [S] nraw
+  const int64_t mc = ctx->mig_cap;
+  const int64_t ms = 8 * mc;                 // per-species stride in the migration buffers
+  // device scratch: [0, 2S) leaver counts L/R per species (unsigned long long),
+  // [2S, 3S) A-positions per species, then the NCCL count messages
+  unsigned long long *cnt = (unsigned long long *)ctx->dev_counts;
+  int64_t *dsend = ctx->dev_counts + 3 * PIC_MAX_SPECIES;        // [S][2]  to L, to R
+  int64_t *drecv = dsend + 2 * PIC_MAX_SPECIES;                  // [S][2]  from R, from L
   int64_t *hc = ctx->host_counts;
+  PIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * S, ctx->stream));
   for (int s = 0; s < S; ++s) {
     SpeciesStore &sp = ctx->sp[s];
-    PIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2, ctx->stream));
     if (sp.n_raw > 0) {
       Arr7 A;
       for (int k = 0; k < 7; ++k) A.a[k] = sp.a[k];
       pack_leavers_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(
-          A, sp.id, sp.key_new, sp.d_nraw, ctx->mig_send[0], ctx->mig_send[1], ctx->mig_cap, cnt); ++ctx->launches;
-      PIC_CUDA(cudaGetLastError());
+          A, sp.id, sp.key_new, sp.d_nraw, ctx->mig_send[0] + s * ms, ctx->mig_send[1] + s * ms, mc,
+          cnt + 2 * s); ++ctx->launches;
     }
-    // leaver counts and the number of A positions, to the host
-    PIC_CUDA(cudaMemcpyAsync(hc, cnt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    PIC_CUDA(cudaMemcpyAsync(hc + 2, sp.d_nraw, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-    const int64_t nl = hc[0], nr = hc[1], nraw = hc[2];
-    if (nl > ctx->mig_cap || nr > ctx->mig_cap) return fail(ctx, PIC_ERANGE, "migration buffer capacity exceeded");
-    if ((nl && left < 0) || (nr && right < 0)) return fail(ctx, PIC_ERANGE, "slab leaver with no neighbour");
-    // counts, then payloads; per-peer order send-right, send-left, recv-left,
-    // recv-right (matches when left == right, P == 2)
-    int64_t *dcounts = ctx->dev_counts + 8;   // [0] to L, [1] to R, [2] from R, [3] from L
-    hc[4] = nl;
-    hc[5] = nr;
-    PIC_CUDA(cudaMemcpyAsync(dcounts, hc + 4, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-    PIC_NCCL(ncclGroupStart());
-    if (right >= 0) PIC_NCCL(ncclSend(dcounts + 1, 1, ncclInt64, right, comm, ctx->stream));
-    if (left >= 0) PIC_NCCL(ncclSend(dcounts + 0, 1, ncclInt64, left, comm, ctx->stream));
-    if (left >= 0) PIC_NCCL(ncclRecv(dcounts + 3, 1, ncclInt64, left, comm, ctx->stream));
-    if (right >= 0) PIC_NCCL(ncclRecv(dcounts + 2, 1, ncclInt64, right, comm, ctx->stream));
-    PIC_NCCL(ncclGroupEnd());
-    PIC_CUDA(cudaMemcpyAsync(hc + 6, dcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-    const int64_t nrecvR = (right >= 0) ? hc[6] : 0;
-    const int64_t nrecvL = (left >= 0) ? hc[7] : 0;
-    if (nrecvL > ctx->mig_cap || nrecvR > ctx->mig_cap)
-      return fail(ctx, PIC_ERANGE, "migration receive capacity exceeded");
-    if (nraw + nrecvL + nrecvR > sp.cap)
+    PIC_CUDA(cudaMemcpyAsync((int64_t *)cnt + 2 * S + s, sp.d_nraw, sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  }
+  PIC_CUDA(cudaGetLastError());
+  // send counts of every species in one NCCL group (the leaver counts are
+  // already on the device); per-peer order send-right, send-left, recv-left,
+  // recv-right (matches when left == right, P == 2)
+  PIC_NCCL(ncclGroupStart());
+  for (int s = 0; s < S; ++s) {
+    if (right >= 0) PIC_NCCL(ncclSend((int64_t *)cnt + 2 * s + 1, 1, ncclInt64, right, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclSend((int64_t *)cnt + 2 * s + 0, 1, ncclInt64, left, comm, ctx->stream));
+    if (left >= 0) PIC_NCCL(ncclRecv(drecv + 2 * s + 1, 1, ncclInt64, left, comm, ctx->stream));
+    if (right >= 0) PIC_NCCL(ncclRecv(drecv + 2 * s + 0, 1, ncclInt64, right, comm, ctx->stream));
+  }
+  PIC_NCCL(ncclGroupEnd());
+  // one host synchronisation for every count
+  PIC_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 3 * S, cudaMemcpyDeviceToHost, ctx->stream));
+  PIC_CUDA(cudaMemcpyAsync(hc + 3 * S, drecv, sizeof(int64_t) * 2 * S, cudaMemcpyDeviceToHost, ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  (void)dsend;
+  int64_t nl[PIC_MAX_SPECIES], nr[PIC_MAX_SPECIES], nraw[PIC_MAX_SPECIES];
+  int64_t recvL[PIC_MAX_SPECIES], recvR[PIC_MAX_SPECIES];
+  for (int s = 0; s < S; ++s) {
+    nl[s] = hc[2 * s];
+    nr[s] = hc[2 * s + 1];
+    nraw[s] = hc[2 * S + s];
+    recvR[s] = (right >= 0) ? hc[3 * S + 2 * s + 0] : 0;
+    recvL[s] = (left >= 0) ? hc[3 * S + 2 * s + 1] : 0;
+    if (nl[s] > mc || nr[s] > mc) return fail(ctx, PIC_ERANGE, "migration buffer capacity exceeded");
+    if ((nl[s] && left < 0) || (nr[s] && right < 0)) return fail(ctx, PIC_ERANGE, "slab leaver with no neighbour");
+    if (recvL[s] > mc || recvR[s] > mc) return fail(ctx, PIC_ERANGE, "migration receive capacity exceeded");
+    if (nraw[s] + recvL[s] + recvR[s] > ctx->sp[s].cap)
       return fail(ctx, PIC_ERANGE, "particle capacity exceeded after migration");
-    PIC_NCCL(ncclGroupStart());
+  }
+  // payloads of every species in one NCCL group
+  PIC_NCCL(ncclGroupStart());
+  for (int s = 0; s < S; ++s)
     for (int k = 0; k < 8; ++k) {
-      if (right >= 0 && nr) PIC_NCCL(ncclSend(ctx->mig_send[1] + k * ctx->mig_cap, nr, ncclDouble, right, comm, ctx->stream));
-      if (left >= 0 && nl) PIC_NCCL(ncclSend(ctx->mig_send[0] + k * ctx->mig_cap, nl, ncclDouble, left, comm, ctx->stream));
-      if (left >= 0 && nrecvL) PIC_NCCL(ncclRecv(ctx->mig_recv[0] + k * ctx->mig_cap, nrecvL, ncclDouble, left, comm, ctx->stream));
-      if (right >= 0 && nrecvR) PIC_NCCL(ncclRecv(ctx->mig_recv[1] + k * ctx->mig_cap, nrecvR, ncclDouble, right, comm, ctx->stream));
+      const int64_t o = s * ms + k * mc;
+      if (right >= 0 && nr[s]) PIC_NCCL(ncclSend(ctx->mig_send[1] + o, nr[s], ncclDouble, right, comm, ctx->stream));
+      if (left >= 0 && nl[s]) PIC_NCCL(ncclSend(ctx->mig_send[0] + o, nl[s], ncclDouble, left, comm, ctx->stream));
+      if (left >= 0 && recvL[s]) PIC_NCCL(ncclRecv(ctx->mig_recv[0] + o, recvL[s], ncclDouble, left, comm, ctx->stream));
+      if (right >= 0 && recvR[s]) PIC_NCCL(ncclRecv(ctx->mig_recv[1] + o, recvR[s], ncclDouble, right, comm, ctx->stream));
     }
-    PIC_NCCL(ncclGroupEnd());
+  PIC_NCCL(ncclGroupEnd());
+  for (int s = 0; s < S; ++s) {
+    SpeciesStore &sp = ctx->sp[s];
     Arr7 arrs;
     for (int k = 0; k < 7; ++k) arrs.a[k] = sp.a[k];
-    if (nrecvL)
-      append_kernel<<<grid_for(nrecvL), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0], nrecvL,
-                                                                ctx->mig_cap, nraw, ctx->stats); ++ctx->launches;
-    if (nrecvR)
-      append_kernel<<<grid_for(nrecvR), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1], nrecvR,
-                                                                ctx->mig_cap, nraw + nrecvL, ctx->stats); ++ctx->launches;
+    if (recvL[s])
+      append_kernel<<<grid_for(recvL[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0] + s * ms,
+                                                                  recvL[s], mc, nraw[s], ctx->stats); ++ctx->launches;
+    if (recvR[s])
+      append_kernel<<<grid_for(recvR[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1] + s * ms,
+                                                                  recvR[s], mc, nraw[s] + recvL[s], ctx->stats); ++ctx->launches;
     PIC_CUDA(cudaGetLastError());
-    const int64_t nnew = nraw + nrecvL + nrecvR;
+    const int64_t nnew = nraw[s] + recvL[s] + recvR[s];
     set_scalar_kernel<<<1, 1, 0, ctx->stream>>>(sp.d_nraw, nnew); ++ctx->launches;
-    pic_status st = count_positions(ctx, s, nraw, nnew);
+    pic_status st = count_positions(ctx, s, nraw[s], nnew);
     if (st != PIC_OK) return st;
-    sp.n_raw = nnew;
-    ctx->hstat[ST_SENT] += nl + nr;
-    ctx->hstat[ST_RECEIVED] += nrecvL + nrecvR;
+    sp.n_raw = std::max(sp.n_raw, nnew);
+    ctx->hstat[ST_SENT] += nl[s] + nr[s];
+    ctx->hstat[ST_RECEIVED] += recvL[s] + recvR[s];
   }
   return PIC_OK;
 }

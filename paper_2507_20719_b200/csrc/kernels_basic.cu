@@ -100,31 +100,8 @@ __global__ void __launch_bounds__(256) moments_basic_kernel(
   const double Nx = (double)g.ncell[0];
   if (k == KEY_LEFT && xi[0] >= (double)g.slab_hi) xi[0] -= Nx;
   if (k == KEY_RIGHT && xi[0] < (double)g.slab_lo) xi[0] += Nx;
-  int64_t idx[3];
-  double f[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double u = xi[d] - (double)g.m_lo[d];
-    const double fl = floor(u);
-    idx[d] = (int64_t)fl;
-    f[d] = u - fl;
-  }
-  if (idx[0] < 0 || idx[0] > g.m_n[0] - 2 || idx[1] < 0 || idx[1] > g.m_n[1] - 2 ||
-      idx[2] < 0 || idx[2] > g.m_n[2] - 2) {
-    atomicAdd(&stats[ST_FAR], 1ull);
-    return;
-  }
-  const double q = Q[p], u = U[p], v = V[p], w = W[p];
-  const double qu = q * u, qv = q * v, qw = q * w;
-  const double val[10] = {q, qu, qv, qw, qu * u, qu * v, qu * w, qv * v, qv * w, qw * w};
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int bx = c & 1, by = (c >> 1) & 1, bz = c >> 2;
-    const double S = (bx ? f[0] : 1.0 - f[0]) * (by ? f[1] : 1.0 - f[1]) * (bz ? f[2] : 1.0 - f[2]);
-    const int64_t node = ((idx[2] + bz) * g.m_n[1] + (idx[1] + by)) * g.m_n[0] + (idx[0] + bx);
-#pragma unroll
-    for (int m = 0; m < 10; ++m) atomicAdd(mom + m * g.m_plane + node, S * val[m]);
-  }
+  const double v3[3] = {U[p], V[p], W[p]};
+  if (!deposit_global(g, mom, xi, Q[p], v3)) atomicAdd(&stats[ST_FAR], 1ull);
 }
 
 pic_status launch_mover_basic(Ctx *ctx, int s) {

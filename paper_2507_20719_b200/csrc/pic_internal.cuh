@@ -107,6 +107,7 @@ struct SpeciesStore {
   int32_t n_iter = 3;
   bool moved = false, deposited = false, fused_deposit = false;
   bool order_valid = false;
+  bool mom_primed = false;         // mover zeroed the moments and deposited its slab leavers
   void swap_buffers() {
     for (int k = 0; k < 7; ++k) { double *t = a[k]; a[k] = b[k]; b[k] = t; }
     int64_t *t = id; id = id_b; id_b = t;
@@ -363,6 +364,37 @@ __device__ __forceinline__ uint32_t count_rank_finish(const RankTicket &t) {
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t base = __shfl_sync(0xffffffffu, t.base, t.leader);
   return (base + (uint32_t)__popc(t.peers & ((1u << lane) - 1u))) | (t.arrival ? RANK_ARRIVAL : 0u);
+}
+
+// Eq. 3 deposit of one particle with global fp64 atomics (80 RED), at a
+// cell-unit position relative to the ghosted moment arrays.  Used for the basic
+// family and for slab leavers, which the tiled mover deposits into the ghost
+// planes before they migrate (R15).  Returns false if the stencil is outside.
+__device__ __forceinline__ bool deposit_global(const Geom &g, double *__restrict__ mom, const double xi[3], double q,
+                                               const double v[3]) {
+  int64_t idx[3];
+  double f[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double u = xi[d] - (double)g.m_lo[d];
+    const double fl = floor(u);
+    idx[d] = (int64_t)fl;
+    f[d] = u - fl;
+  }
+  if (idx[0] < 0 || idx[0] > g.m_n[0] - 2 || idx[1] < 0 || idx[1] > g.m_n[1] - 2 || idx[2] < 0 ||
+      idx[2] > g.m_n[2] - 2)
+    return false;
+  const double qu = q * v[0], qv = q * v[1], qw = q * v[2];
+  const double val[10] = {q, qu, qv, qw, qu * v[0], qu * v[1], qu * v[2], qv * v[1], qv * v[2], qw * v[2]};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int bx = c & 1, by = (c >> 1) & 1, bz = c >> 2;
+    const double S = (bx ? f[0] : 1.0 - f[0]) * (by ? f[1] : 1.0 - f[1]) * (bz ? f[2] : 1.0 - f[2]);
+    const int64_t node = ((idx[2] + bz) * g.m_n[1] + (idx[1] + by)) * g.m_n[0] + (idx[0] + bx);
+#pragma unroll
+    for (int m = 0; m < 10; ++m) atomicAdd(mom + m * g.m_plane + node, S * val[m]);
+  }
+  return true;
 }
 
 // Map a global node index to the ghosted moment array (x: ghost planes; y, z:

@@ -65,6 +65,7 @@ struct MoverTArgs {
   uint32_t *key_new, *rank, *cell_count;
   int64_t *d_nraw;
   const double *field;        // global window (fallback sampling)
+  double *mom;                // ghosted moments (slab leavers, deposited by the mover)
   unsigned long long *stats;
   double ks, ks_c;
   int n_iter;
@@ -306,7 +307,14 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
         xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
         vnew[d] = fma(2.0, vb[d], -vn[d]);
       }
+      const double x_pre = xnew[0];
       knew = finish_particle(g, xnew, vnew, clamped, A.stats);
+      if (g.multi_rank && (knew == KEY_LEFT || knew == KEY_RIGHT)) {
+        // slab leaver: deposit into the x ghost planes now, before it migrates
+        // (R15); x unwrapped, y and z wrapped (the moment arrays hold planes [0, N])
+        const double xdep[3] = {x_pre, xnew[1], xnew[2]};
+        if (!deposit_global(g, A.mom, xdep, qv, vnew)) atomicAdd(&A.stats[ST_FAR], 1ull);
+      }
       A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
       A.dst[3][p] = vnew[0]; A.dst[4][p] = vnew[1]; A.dst[5][p] = vnew[2];
       A.dst[6][p] = qv;
@@ -574,6 +582,9 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   }
   pic_status st = zero_cell_counts(ctx, s);
   if (st != PIC_OK) return st;
+  st = zero_moments(ctx, s);   // the mover deposits slab leavers (multi-rank)
+  if (st != PIC_OK) return st;
+  sp.mom_primed = true;
   MoverTArgs A;
   A.g = ctx->geom;
   for (int k = 0; k < 7; ++k) { A.src[k] = sp.a[k]; A.dst[k] = sp.b[k]; }
@@ -587,6 +598,7 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   A.cell_count = sp.cell_count;
   A.d_nraw = sp.d_nraw;
   A.field = ctx->field;
+  A.mom = sp.mom;
   A.stats = ctx->stats;
   A.ks = sp.qom * (ctx->geom.dt * 0.5);
   A.ks_c = A.ks / ctx->geom.c;
@@ -622,8 +634,11 @@ pic_status launch_tiled_deposit(Ctx *ctx, int s) {
     pic_status st = make_tmap(ctx);
     if (st != PIC_OK) return st;
   }
-  pic_status st = zero_moments(ctx, s);
-  if (st != PIC_OK) return st;
+  if (!sp.mom_primed) {
+    pic_status st = zero_moments(ctx, s);
+    if (st != PIC_OK) return st;
+  }
+  sp.mom_primed = false;
   DepositArgs A;
   A.g = ctx->geom;
   for (int k = 0; k < 7; ++k) A.src[k] = sp.a[k];
@@ -634,7 +649,6 @@ pic_status launch_tiled_deposit(Ctx *ctx, int s) {
   A.stats = ctx->stats;
   deposit_tiled_kernel<<<(unsigned)ctx->geom.ntiles, THREADS, DEPOSIT_SMEM, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
-  if (ctx->cfg.nranks > 1) return launch_moments_basic(ctx, s, /*leavers_only=*/true);
   return PIC_OK;
 }
 
