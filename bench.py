@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
     ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
-    ap.add_argument("--sort-every", type=int, default=1)
+    ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
     ap.add_argument("--ghost", type=int, default=2)
     ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
@@ -217,7 +217,7 @@ def main():
     cap = [int(n * 1.08) + 65536 for n in n_local]
     nccl_id = decomp.broadcast_nccl_id(pic.pic_nccl_id) if world > 1 else None
     cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
-                          sort_every=args.sort_every, kernel=args.kernel)
+                          transport=args.transport, kernel=args.kernel)
     stream = torch.cuda.current_stream()
     ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
     for s, p in enumerate(parts):
@@ -265,6 +265,11 @@ def main():
     launches = ctx.launch_count() - launches0
     prof = ctx.profile_read()
     ctx.profile(False)
+    kps = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
+    kps_ranks = [kps]
+    if world > 1:
+        kps_ranks = [None] * world
+        dist.all_gather_object(kps_ranks, kps)
     stats = ctx.sync()
     t_ms = start.elapsed_time(end)
     mover_ms = [a.elapsed_time(b) for a, b, c in ev]
@@ -364,7 +369,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": desc, "particles_per_gpu": n_alive, "cells_per_gpu": list(w.ncell[1:]),
-                       "kernel": ["auto", "basic", "tiled"][args.kernel], "sort_every": args.sort_every,
+                       "kernel": ["auto", "basic", "tiled"][args.kernel], "transport": (["nccl", "peer"][int(ctx.peer)] if world > 1 else None),
                        "l2": "inputs (%.2f GB per GPU) exceed the 126 MB L2; no flush" % (n_alive * 64 / 1e9),
                        "parallelism": f"x-slabs{world}"},
             "roofline": roof,
@@ -373,7 +378,8 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "phase_ms": {"mover+order": mover_avg, "moments+exchange": sum(rest_ms) / len(rest_ms),
-                         "kernels_per_step": {k: v[0] / args.steps for k, v in prof.items()}},
+                         "kernels_per_step": kps,
+                         **({"kernels_per_step_ranks": kps_ranks} if world > 1 else {})},
             "stats": stats,
         }
         print(json.dumps(line), flush=True)

@@ -26,7 +26,8 @@
  *    flags and surfaced by the next pic_sync / pic_exchange.
  *  - Per cycle the call order is pic_mover -> pic_moments -> pic_exchange
  *    (for each species, mover before moments); other orders return
- *    PIC_ESTATE.  pic_exchange is COLLECTIVE over the nranks of the config.
+ *    PIC_ESTATE.  With nranks > 1, pic_mover and pic_exchange are COLLECTIVE
+ *    over the nranks of the config (every rank calls them with the same s).
  */
 #ifndef PIC_H
 #define PIC_H
@@ -43,7 +44,7 @@
 extern "C" {
 #endif
 
-#define PIC_ABI_VERSION 1
+#define PIC_ABI_VERSION 2
 #define PIC_MAX_SPECIES 8
 #define PIC_NCCL_ID_BYTES 128
 #define PIC_N_MOMENTS 10  /* rho, Jx, Jy, Jz, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz (R16) */
@@ -72,6 +73,18 @@ typedef enum {
   PIC_KERNEL_TILED = 2     /* cell-sorted, tile-staged fused mover + deposit   */
 } pic_kernel;
 
+/* Multi-rank transport (pic_config.transport).                              */
+typedef enum {
+  PIC_TRANSPORT_AUTO = 0,  /* peer memory when every rank can map its slab
+                              neighbours' workspaces (CUDA IPC), else NCCL     */
+  PIC_TRANSPORT_NCCL = 1,  /* NCCL point-to-point messages, host sync for the
+                              migration counts                                 */
+  PIC_TRANSPORT_PEER = 2   /* the mover writes slab leavers into the
+                              neighbour's buffer over NVLink and ghost planes
+                              are read from peer memory; pic_init fails if the
+                              neighbours cannot be mapped                      */
+} pic_transport;
+
 typedef struct {
   /* Global grid: cells [0, ncell) per axis, origin 0, Delta_d = len_d/ncell_d. */
   int64_t ncell[3];
@@ -90,8 +103,7 @@ typedef struct {
   int64_t slab_lo, slab_hi;      /* this rank owns x-cells [slab_lo, slab_hi)     */
   int32_t ghost;                 /* G >= 1: field-window ghost nodes per side and
                                     moment ghost node planes per x-side (R22)     */
-  int32_t sort_every;            /* reserved (the cell order is rebuilt every cycle
-                                    by the counting sort; value ignored)          */
+  int32_t transport;             /* pic_transport (nranks > 1)                    */
   int32_t kernel;                /* pic_kernel                                    */
 } pic_config;
 
@@ -148,8 +160,11 @@ PIC_API pic_status pic_get_particles(pic_ctx *ctx, int32_t s, double *const xyzu
 PIC_API pic_status pic_set_fields(pic_ctx *ctx, const double *EB);
 
 /* Advance species s (-1 = all) one cycle with Eq. 2 (R1-R3, R7-R9), then
- * apply the boundary conditions (R10, R11, R21).  The library may fuse the
- * moment deposit of the new state into this pass.                            */
+ * apply the boundary conditions (R10, R11, R21).  With nranks > 1 this call
+ * is COLLECTIVE: particles that left the slab migrate to their new owner rank
+ * ("exiting particles are transferred using MPI"),
+ * which blocks the host once for the message counts.  Ends by building the
+ * cell order of the new state that pic_moments deposits over.                */
 PIC_API pic_status pic_mover(pic_ctx *ctx, int32_t s);
 
 /* Gather rho_s, J_s, Pi_s (Eq. 3, R12-R18) of the current state of species s
@@ -157,9 +172,9 @@ PIC_API pic_status pic_mover(pic_ctx *ctx, int32_t s);
  * final after pic_exchange).                                                 */
 PIC_API pic_status pic_moments(pic_ctx *ctx, int32_t s);
 
-/* COLLECTIVE.  Sum ghost-node moment planes into their owners (periodic fold
- * when nranks == 1) and migrate particles that left the slab to their new
- * owner rank (R21).  Surfaces latched device errors.                         */
+/* COLLECTIVE when nranks > 1.  Sum ghost-node moment planes into their owners
+ * (periodic folds along y, z, and along x when nranks == 1).  Surfaces
+ * latched device errors.                                                     */
 PIC_API pic_status pic_exchange(pic_ctx *ctx);
 
 /* Shorthand for one full cycle: pic_mover(-1), pic_moments(-1),
@@ -182,6 +197,10 @@ PIC_API pic_status pic_get_moments(pic_ctx *ctx, int32_t s, double *out);
  * Returns the first latched device error as a status.                        */
 PIC_API pic_status pic_sync(pic_ctx *ctx, int64_t stats[8]);
 
+/* Transport in use: PIC_TRANSPORT_PEER or PIC_TRANSPORT_NCCL when nranks > 1
+ * (AUTO resolved at pic_init), PIC_TRANSPORT_AUTO for a single rank.        */
+PIC_API pic_status pic_get_transport(const pic_ctx *ctx, int32_t *out);
+
 /* Number of libpic kernel launches enqueued on this context since pic_init
  * (the bench's gpu_launches evidence).                                       */
 PIC_API pic_status pic_launch_count(const pic_ctx *ctx, int64_t *n);
@@ -191,10 +210,14 @@ PIC_API pic_status pic_launch_count(const pic_ctx *ctx, int64_t *n);
  * cost nothing measurable), 0 disables it.  pic_profile_read synchronises the
  * stream and returns accumulated milliseconds and launch counts:
  *   ms[0] mover kernels (Eq. 2), ms[1] order build (scan + perm scatter),
- *   ms[2] deposit kernels (Eq. 3), ms[3] exchange (folds, ghost sums, migration)
- *   launches[0..3] the number of timed intervals of each phase.               */
+ *   ms[2] deposit kernels (Eq. 3), ms[3] pic_exchange (folds, ghost sums),
+ *   ms[4] migration up to the count message (pack + NCCL counts),
+ *   ms[5] migration after the host learnt the counts (payload + append);
+ *   the host wait between ms[4] and ms[5] is in neither.
+ *   launches[k] the number of timed intervals of each phase.                 */
+#define PIC_PROF_PHASES 6
 PIC_API pic_status pic_profile(pic_ctx *ctx, int32_t enable);
-PIC_API pic_status pic_profile_read(pic_ctx *ctx, double ms[4], int64_t launches[4]);
+PIC_API pic_status pic_profile_read(pic_ctx *ctx, double ms[PIC_PROF_PHASES], int64_t launches[PIC_PROF_PHASES]);
 
 /* Human-readable text of the last error on this context (never NULL).       */
 PIC_API const char *pic_last_error(const pic_ctx *ctx);

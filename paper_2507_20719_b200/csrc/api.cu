@@ -54,7 +54,7 @@ pic_status validate(const pic_config *c, std::string *why) {
                          ((c->ncell[2] + TILE - 1) / TILE) * TILE3;
   if (tcells >= (int64_t)KEY_FIRST_RESERVED) { *why = "too many local cells for 32-bit keys"; return PIC_EINVAL; }
   if (c->planet_radius < 0) { *why = "planet_radius < 0"; return PIC_EINVAL; }
-  if (c->sort_every < 0) { *why = "sort_every < 0"; return PIC_EINVAL; }
+  if (c->transport < PIC_TRANSPORT_AUTO || c->transport > PIC_TRANSPORT_PEER) { *why = "bad transport"; return PIC_EINVAL; }
   if (c->kernel < 0 || c->kernel > 2) { *why = "bad kernel"; return PIC_EINVAL; }
   return PIC_OK;
 }
@@ -139,6 +139,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   int64_t ofield = L.take(8 * field_elems);
   int64_t ostats = L.take(8 * ST_N);
   int64_t ocounts = L.take(8 * 64);
+  int64_t opeer = L.take(sizeof(PeerCtl));
   const int64_t face = g.m_n[1] * g.m_n[2] * 10;
   const int64_t ghost_elems = (int64_t)(c->ghost + 1) * face;
   int64_t og[4];
@@ -154,6 +155,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
     ctx->field_elems = field_elems;
     ctx->stats = (unsigned long long *)(base + ostats);
     ctx->dev_counts = (int64_t *)(base + ocounts);
+    ctx->peer_ctl = (PeerCtl *)(base + opeer);
     ctx->ghost_send[0] = (double *)(base + og[0]);
     ctx->ghost_send[1] = (double *)(base + og[1]);
     ctx->ghost_recv[0] = (double *)(base + og[2]);
@@ -230,25 +232,33 @@ pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
     return PIC_ENOMEM;
   }
   plan(cfg, ctx->geom, ctx, (char *)workspace, cub_bytes);
-  ctx->host_counts = new int64_t[64]();
-  cudaError_t e = cudaMemset(ctx->stats, 0, 8 * ST_N);
-  if (e != cudaSuccess) { delete[] ctx->host_counts; delete ctx; return PIC_ECUDA; }
+  ctx->workspace = workspace;
+  cudaError_t e = cudaHostAlloc((void **)&ctx->host_counts, 64 * sizeof(int64_t), cudaHostAllocDefault);
+  if (e != cudaSuccess) { delete ctx; return PIC_ECUDA; }
+  e = cudaMemset(ctx->stats, 0, 8 * ST_N);
+  if (e != cudaSuccess) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_ECUDA; }
   e = cudaMemset(ctx->field, 0, 8 * ctx->field_elems);
-  if (e != cudaSuccess) { delete[] ctx->host_counts; delete ctx; return PIC_ECUDA; }
+  if (e != cudaSuccess) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_ECUDA; }
   if (cfg->nranks > 1) {
-    if (!nccl_id) { delete[] ctx->host_counts; delete ctx; return PIC_EINVAL; }
+    if (!nccl_id) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_EINVAL; }
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof(id));
     ncclComm_t comm;
     if (ncclCommInitRank(&comm, cfg->nranks, id, cfg->rank) != ncclSuccess) {
-      delete[] ctx->host_counts;
+      cudaFreeHost(ctx->host_counts);
       delete ctx;
       return PIC_ENCCL;
     }
     ctx->nccl = comm;
+    if (peer_setup(ctx) != PIC_OK) {
+      ncclCommDestroy(comm);
+      cudaFreeHost(ctx->host_counts);
+      delete ctx;
+      return PIC_ECUDA;
+    }
   }
   for (int s = 0; s < cfg->n_species; ++s) {
-    if (zero_moments(ctx, s) != PIC_OK) { delete[] ctx->host_counts; delete ctx; return PIC_ECUDA; }
+    if (zero_moments(ctx, s) != PIC_OK) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_ECUDA; }
   }
   *out = reinterpret_cast<pic_ctx *>(ctx);
   return PIC_OK;
@@ -318,17 +328,23 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
     if (ctx->sp[k].moved || !ctx->sp[k].order_valid)
       return fail(ctx, PIC_ESTATE, "pic_mover called twice without pic_exchange");
   for (int k = s0; k < s1; ++k) {
-    SpeciesStore &sp = ctx->sp[k];
-    bool fused = false;
-    if (use_tiled(ctx)) {
-      st = launch_tiled_step(ctx, k, &fused);
-      if (st != PIC_OK) return st;
-    } else {
-      st = launch_mover_basic(ctx, k);
-      if (st != PIC_OK) return st;
-    }
-    sp.moved = true;
-    sp.deposited = false;
+    st = use_tiled(ctx) ? launch_tiled_step(ctx, k) : launch_mover_basic(ctx, k);
+    if (st != PIC_OK) return st;
+    ctx->sp[k].moved = true;
+    ctx->sp[k].deposited = false;
+  }
+  // slab leavers go to their neighbour right after the mover (Alg. 1: the
+  // particle communication follows the push), every species in one NCCL group
+  // per message; the receiver deposits them like its own particles
+  if (ctx->cfg.nranks > 1) {
+    st = ctx->peer ? peer_migrate(ctx, s0, s1) : migrate(ctx, s0, s1);
+    if (st != PIC_OK) return st;
+  }
+  // the next cell order (stayers, in-slab arrivals, migrated arrivals)
+  for (int k = s0; k < s1; ++k) {
+    PhaseTimer t(ctx, 1);
+    st = build_order(ctx, k);
+    if (st != PIC_OK) return st;
   }
   return PIC_OK;
 }
@@ -366,7 +382,7 @@ pic_status pic_exchange(pic_ctx *p) {
   pic_status st;
   {
     PhaseTimer t(ctx, 3);
-    st = exchange(ctx);
+    st = ctx->peer ? peer_exchange(ctx) : exchange(ctx);
   }
   if (st != PIC_OK) return st;
   for (int k = 0; k < ctx->cfg.n_species; ++k) ctx->sp[k].moved = ctx->sp[k].deposited = false;
@@ -410,9 +426,21 @@ pic_status pic_sync(pic_ctx *p, int64_t stats[8]) {
   for (int k = 0; k < ST_N; ++k) all[k] = (int64_t)h[k] + ctx->hstat[k];
   if (stats)
     for (int k = 0; k < ST_N; ++k) stats[k] = all[k];
+  if (ctx->peer) {
+    unsigned long long perr = 0;
+    PIC_CUDA(cudaMemcpy(&perr, &ctx->peer_ctl->err, sizeof(perr), cudaMemcpyDeviceToHost));
+    if (perr) return fail(ctx, PIC_ENCCL, "peer barrier timed out (a neighbour rank stopped)");
+  }
   if (all[ST_NONFINITE]) return fail(ctx, PIC_ENONFINITE, "non-finite particle update");
   if (all[ST_FAR] || all[ST_OVERFLOW] || all[ST_MULTIWRAP])
     return fail(ctx, PIC_ERANGE, "particle beyond ghost reach, capacity overflow or multiple wrap");
+  return PIC_OK;
+}
+
+pic_status pic_get_transport(const pic_ctx *p, int32_t *out) {
+  if (!p || !out) return PIC_EINVAL;
+  const Ctx *ctx = C(p);
+  *out = ctx->cfg.nranks < 2 ? PIC_TRANSPORT_AUTO : (ctx->peer ? PIC_TRANSPORT_PEER : PIC_TRANSPORT_NCCL);
   return PIC_OK;
 }
 
@@ -436,11 +464,11 @@ pic_status pic_profile(pic_ctx *p, int32_t enable) {
   return PIC_OK;
 }
 
-pic_status pic_profile_read(pic_ctx *p, double ms[4], int64_t launches[4]) {
+pic_status pic_profile_read(pic_ctx *p, double ms[PIC_PROF_PHASES], int64_t launches[PIC_PROF_PHASES]) {
   if (!p || !ms || !launches) return PIC_EINVAL;
   Ctx *ctx = C(p);
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < PIC_PROF_PHASES; ++k) {
     double t = 0.0;
     for (auto &e : ctx->prof_ev[k]) {
       float f = 0.f;
@@ -461,6 +489,7 @@ const char *pic_last_error(const pic_ctx *p) {
 pic_status pic_destroy(pic_ctx *p) {
   if (!p) return PIC_EINVAL;
   Ctx *ctx = C(p);
+  peer_close(ctx);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
   for (auto &v : ctx->prof_ev)
     for (auto &e : v) {
@@ -468,7 +497,7 @@ pic_status pic_destroy(pic_ctx *p) {
       cudaEventDestroy(e.second);
     }
   for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
-  delete[] ctx->host_counts;
+  cudaFreeHost(ctx->host_counts);
   delete ctx;
   return PIC_OK;
 }

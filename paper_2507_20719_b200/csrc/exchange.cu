@@ -1,12 +1,14 @@
-// exchange.cu — ghost-node moment sums, periodic folds, particle compaction and
-// slab migration (pic_exchange), plus particle / moment copy-in and copy-out.
+// exchange.cu — slab migration (inside pic_mover), ghost-node moment sums and
+// periodic folds (pic_exchange), plus particle / moment copy-in and copy-out.
 //
 // Paper mapping (Alg. 1 phase 2): "exiting particles are
-// transferred using MPI".  Here the sender deposits its leavers into ghost node
-// planes before migration; the ghost planes are then summed
-// into their owners with NCCL point-to-point over NVLink (ring-periodic along
-// x when x is periodic), and the leavers travel to the neighbouring slab.
-// The ghost-node sum itself is implied, not stated, by the paper (north_star).
+// transferred using MPI".  Here slab leavers travel to the neighbouring slab
+// right after the mover, before the order for the deposit is built, so every
+// particle is deposited once, by its owner.  The x ghost planes (the stencil
+// of the owner's last cell reaches node slab_hi) are then summed into their
+// owners with NCCL point-to-point over NVLink (ring-periodic along x when x is
+// periodic).  The ghost-node sum itself is implied, not stated, by the paper
+// (north_star).
 #include <nccl.h>
 
 #include "pic_internal.cuh"
@@ -22,15 +24,15 @@ namespace pic {
 
 // ------------------------------------------------------------- moment folds --
 // Periodic y / z fold: plane N (the image of plane 0, R18) is added into 0.
+// x planes [x0, x0 + nA) of arrays with nx planes.
 __global__ void fold_axis_kernel(double *mom, int64_t nx, int64_t ny, int64_t nz, int axis,
-                                 int64_t plane) {
+                                 int64_t plane, int64_t x0, int64_t nA) {
   // iterate over the 2D face (other two axes) x 10 components
-  int64_t nA = axis == 1 ? nx : nx;
   int64_t nB = axis == 1 ? nz : ny;
   int64_t total = nA * nB * 10;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t a = t % nA, b = (t / nA) % nB, m = t / (nA * nB);
+    int64_t a = x0 + t % nA, b = (t / nA) % nB, m = t / (nA * nB);
     int64_t src, dst;
     if (axis == 1) {  // y: a = x, b = z
       src = (b * ny + (ny - 1)) * nx + a;
@@ -93,6 +95,16 @@ static unsigned grid_for(int64_t total) {
   return (unsigned)b;
 }
 
+pic_status launch_fold_axis(Ctx *ctx, int s, int axis, int64_t x0, int64_t nxr) {
+  const Geom &g = ctx->geom;
+  const int64_t nx = g.m_n[0], ny = g.m_n[1], nz = g.m_n[2];
+  const int64_t other = axis == 1 ? nz : ny;
+  fold_axis_kernel<<<grid_for(nxr * other * 10), 256, 0, ctx->stream>>>(ctx->sp[s].mom, nx, ny, nz, axis, g.m_plane,
+                                                                        x0, nxr); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  return PIC_OK;
+}
+
 static pic_status fold_and_ghosts(Ctx *ctx) {
   const Geom &g = ctx->geom;
   const int64_t nx = g.m_n[0], ny = g.m_n[1], nz = g.m_n[2];
@@ -100,9 +112,9 @@ static pic_status fold_and_ghosts(Ctx *ctx) {
   for (int s = 0; s < S; ++s) {
     double *mom = ctx->sp[s].mom;
     if (g.periodic[1])
-      fold_axis_kernel<<<grid_for(nx * nz * 10), 256, 0, ctx->stream>>>(mom, nx, ny, nz, 1, g.m_plane); ++ctx->launches;
+      fold_axis_kernel<<<grid_for(nx * nz * 10), 256, 0, ctx->stream>>>(mom, nx, ny, nz, 1, g.m_plane, 0, nx); ++ctx->launches;
     if (g.periodic[2])
-      fold_axis_kernel<<<grid_for(nx * ny * 10), 256, 0, ctx->stream>>>(mom, nx, ny, nz, 2, g.m_plane); ++ctx->launches;
+      fold_axis_kernel<<<grid_for(nx * ny * 10), 256, 0, ctx->stream>>>(mom, nx, ny, nz, 2, g.m_plane, 0, nx); ++ctx->launches;
     if (ctx->cfg.nranks == 1 && g.periodic[0])
       fold_x_local_kernel<<<grid_for(ny * nz * 10), 256, 0, ctx->stream>>>(
           mom, g.ncell[0], g.G, nx, ny, nz, g.m_plane); ++ctx->launches;
@@ -161,7 +173,8 @@ static pic_status fold_and_ghosts(Ctx *ctx) {
 
 // ---------------------------------------------------------------- migration --
 // Slab leavers (keys LEFT / RIGHT written by the mover) are packed from the A
-// positions into the send buffers [8][mig_cap] (7 fp64 + id bits); slots come
+// positions into the send buffers as records of 8 words (x y z u v w q, id
+// bits), so one message per neighbour and species carries them; slots come
 // from warp-aggregated atomics.  No compaction of the stayers is needed: the
 // next cell order (order.cu) only contains counted particles.
 struct Arr7 { double *a[7]; };
@@ -188,10 +201,10 @@ __global__ void pack_leavers_kernel(Arr7 A, const int64_t *__restrict__ id, cons
       if (mine) {
         const int64_t slot = (int64_t)slot0 + __popc(mask & ((1u << lane) - 1u));
         if (slot < mig_cap) {
-          double *buf = side == 0 ? sendL : sendR;
+          double *rec = (side == 0 ? sendL : sendR) + slot * MIG_REC;
 #pragma unroll
-          for (int c = 0; c < 7; ++c) buf[c * mig_cap + slot] = A.a[c][p];
-          buf[7 * mig_cap + slot] = __longlong_as_double(id[p]);
+          for (int c = 0; c < 7; ++c) rec[c] = A.a[c][p];
+          rec[7] = __longlong_as_double(id[p]);
         }
       }
     }
@@ -204,19 +217,20 @@ __device__ __forceinline__ uint32_t cell_key(const Geom &g, double x, double y, 
   return tile_key(g, cx, cy, cz);
 }
 
-// Append received particles (component arrays of the recv buffer) at `at`.
+// Append received records at `at` (component arrays, ids, keys).
 __global__ void append_kernel(Geom g, Arr7 arrs, int64_t *__restrict__ id, uint32_t *__restrict__ key,
-                              const double *__restrict__ buf, int64_t cnt, int64_t mig_cap, int64_t at,
+                              const double *__restrict__ buf, int64_t cnt, int64_t at,
                               unsigned long long *__restrict__ stats) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (int64_t)gridDim.x * blockDim.x) {
+    const double *rec = buf + i * MIG_REC;
     double v[7];
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
-      v[k] = buf[k * mig_cap + i];
+      v[k] = rec[k];
       arrs.a[k][at + i] = v[k];
     }
-    id[at + i] = __double_as_longlong(buf[7 * mig_cap + i]);
+    id[at + i] = __double_as_longlong(rec[7]);
     int64_t cx = (int64_t)floor(v[0]);
     if (cx < g.slab_lo || cx >= g.slab_hi) {
       atomicAdd(&stats[ST_FAR], 1ull);
@@ -229,55 +243,57 @@ __global__ void append_kernel(Geom g, Arr7 arrs, int64_t *__restrict__ id, uint3
 
 __global__ void set_scalar_kernel(int64_t *dst, int64_t v) { *dst = v; }
 
-static pic_status migrate(Ctx *ctx) {
+// Migration of species [s0, s1) (collective): pack, one NCCL group with the
+// counts of every species, one host synchronisation, one NCCL group with the
+// payloads, append + rank the arrivals into the cell counts (order.cu).
+pic_status migrate(Ctx *ctx, int s0, int s1) {
   const Geom &g = ctx->geom;
-  const int S = ctx->cfg.n_species;
+  const int S = ctx->cfg.n_species;   // count-scratch layout stride
   const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
   const bool per = g.periodic[0];
   const int left = (r > 0) ? r - 1 : (per ? P - 1 : -1);
   const int right = (r < P - 1) ? r + 1 : (per ? 0 : -1);
   ncclComm_t comm = (ncclComm_t)ctx->nccl;
   const int64_t mc = ctx->mig_cap;
-  const int64_t ms = 8 * mc;                 // per-species stride in the migration buffers
+  const int64_t ms = MIG_REC * mc;           // per-species stride in the migration buffers
   // device scratch: [0, 2S) leaver counts L/R per species (unsigned long long),
-  // [2S, 3S) A-positions per species, then the NCCL count messages
+  // [2S, 3S) A-positions per species, [3S, 5S) received counts from R, from L
   unsigned long long *cnt = (unsigned long long *)ctx->dev_counts;
-  int64_t *dsend = ctx->dev_counts + 3 * PIC_MAX_SPECIES;        // [S][2]  to L, to R
-  int64_t *drecv = dsend + 2 * PIC_MAX_SPECIES;                  // [S][2]  from R, from L
+  int64_t *drecv = ctx->dev_counts + 3 * S;
   int64_t *hc = ctx->host_counts;
-  PIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * S, ctx->stream));
-  for (int s = 0; s < S; ++s) {
-    SpeciesStore &sp = ctx->sp[s];
-    if (sp.n_raw > 0) {
-      Arr7 A;
-      for (int k = 0; k < 7; ++k) A.a[k] = sp.a[k];
-      pack_leavers_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(
-          A, sp.id, sp.key_new, sp.d_nraw, ctx->mig_send[0] + s * ms, ctx->mig_send[1] + s * ms, mc,
-          cnt + 2 * s); ++ctx->launches;
+  {
+    PhaseTimer t(ctx, 4);
+    PIC_CUDA(cudaMemsetAsync(cnt + 2 * s0, 0, sizeof(unsigned long long) * 2 * (s1 - s0), ctx->stream));
+    for (int s = s0; s < s1; ++s) {
+      SpeciesStore &sp = ctx->sp[s];
+      if (sp.n_raw > 0) {
+        Arr7 A;
+        for (int k = 0; k < 7; ++k) A.a[k] = sp.a[k];
+        pack_leavers_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(
+            A, sp.id, sp.key_new, sp.d_nraw, ctx->mig_send[0] + s * ms, ctx->mig_send[1] + s * ms, mc,
+            cnt + 2 * s); ++ctx->launches;
+      }
+      PIC_CUDA(cudaMemcpyAsync((int64_t *)cnt + 2 * S + s, sp.d_nraw, sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
     }
-    PIC_CUDA(cudaMemcpyAsync((int64_t *)cnt + 2 * S + s, sp.d_nraw, sizeof(int64_t), cudaMemcpyDeviceToDevice,
-                             ctx->stream));
+    PIC_CUDA(cudaGetLastError());
+    // per-peer order send-right, send-left, recv-left, recv-right (matches
+    // when left == right, P == 2)
+    PIC_NCCL(ncclGroupStart());
+    for (int s = s0; s < s1; ++s) {
+      if (right >= 0) PIC_NCCL(ncclSend((int64_t *)cnt + 2 * s + 1, 1, ncclInt64, right, comm, ctx->stream));
+      if (left >= 0) PIC_NCCL(ncclSend((int64_t *)cnt + 2 * s + 0, 1, ncclInt64, left, comm, ctx->stream));
+      if (left >= 0) PIC_NCCL(ncclRecv(drecv + 2 * s + 1, 1, ncclInt64, left, comm, ctx->stream));
+      if (right >= 0) PIC_NCCL(ncclRecv(drecv + 2 * s + 0, 1, ncclInt64, right, comm, ctx->stream));
+    }
+    PIC_NCCL(ncclGroupEnd());
+    PIC_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 5 * S, cudaMemcpyDeviceToHost, ctx->stream));
   }
-  PIC_CUDA(cudaGetLastError());
-  // send counts of every species in one NCCL group (the leaver counts are
-  // already on the device); per-peer order send-right, send-left, recv-left,
-  // recv-right (matches when left == right, P == 2)
-  PIC_NCCL(ncclGroupStart());
-  for (int s = 0; s < S; ++s) {
-    if (right >= 0) PIC_NCCL(ncclSend((int64_t *)cnt + 2 * s + 1, 1, ncclInt64, right, comm, ctx->stream));
-    if (left >= 0) PIC_NCCL(ncclSend((int64_t *)cnt + 2 * s + 0, 1, ncclInt64, left, comm, ctx->stream));
-    if (left >= 0) PIC_NCCL(ncclRecv(drecv + 2 * s + 1, 1, ncclInt64, left, comm, ctx->stream));
-    if (right >= 0) PIC_NCCL(ncclRecv(drecv + 2 * s + 0, 1, ncclInt64, right, comm, ctx->stream));
-  }
-  PIC_NCCL(ncclGroupEnd());
-  // one host synchronisation for every count
-  PIC_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 3 * S, cudaMemcpyDeviceToHost, ctx->stream));
-  PIC_CUDA(cudaMemcpyAsync(hc + 3 * S, drecv, sizeof(int64_t) * 2 * S, cudaMemcpyDeviceToHost, ctx->stream));
+  // the one host synchronisation of the cycle
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));
-  (void)dsend;
   int64_t nl[PIC_MAX_SPECIES], nr[PIC_MAX_SPECIES], nraw[PIC_MAX_SPECIES];
   int64_t recvL[PIC_MAX_SPECIES], recvR[PIC_MAX_SPECIES];
-  for (int s = 0; s < S; ++s) {
+  for (int s = s0; s < s1; ++s) {
     nl[s] = hc[2 * s];
     nr[s] = hc[2 * s + 1];
     nraw[s] = hc[2 * S + s];
@@ -289,27 +305,27 @@ static pic_status migrate(Ctx *ctx) {
     if (nraw[s] + recvL[s] + recvR[s] > ctx->sp[s].cap)
       return fail(ctx, PIC_ERANGE, "particle capacity exceeded after migration");
   }
-  // payloads of every species in one NCCL group
+  PhaseTimer t(ctx, 5);
+  // payloads of every species in one NCCL group, one message per neighbour
   PIC_NCCL(ncclGroupStart());
-  for (int s = 0; s < S; ++s)
-    for (int k = 0; k < 8; ++k) {
-      const int64_t o = s * ms + k * mc;
-      if (right >= 0 && nr[s]) PIC_NCCL(ncclSend(ctx->mig_send[1] + o, nr[s], ncclDouble, right, comm, ctx->stream));
-      if (left >= 0 && nl[s]) PIC_NCCL(ncclSend(ctx->mig_send[0] + o, nl[s], ncclDouble, left, comm, ctx->stream));
-      if (left >= 0 && recvL[s]) PIC_NCCL(ncclRecv(ctx->mig_recv[0] + o, recvL[s], ncclDouble, left, comm, ctx->stream));
-      if (right >= 0 && recvR[s]) PIC_NCCL(ncclRecv(ctx->mig_recv[1] + o, recvR[s], ncclDouble, right, comm, ctx->stream));
-    }
+  for (int s = s0; s < s1; ++s) {
+    const int64_t o = s * ms;
+    if (right >= 0 && nr[s]) PIC_NCCL(ncclSend(ctx->mig_send[1] + o, MIG_REC * nr[s], ncclDouble, right, comm, ctx->stream));
+    if (left >= 0 && nl[s]) PIC_NCCL(ncclSend(ctx->mig_send[0] + o, MIG_REC * nl[s], ncclDouble, left, comm, ctx->stream));
+    if (left >= 0 && recvL[s]) PIC_NCCL(ncclRecv(ctx->mig_recv[0] + o, MIG_REC * recvL[s], ncclDouble, left, comm, ctx->stream));
+    if (right >= 0 && recvR[s]) PIC_NCCL(ncclRecv(ctx->mig_recv[1] + o, MIG_REC * recvR[s], ncclDouble, right, comm, ctx->stream));
+  }
   PIC_NCCL(ncclGroupEnd());
-  for (int s = 0; s < S; ++s) {
+  for (int s = s0; s < s1; ++s) {
     SpeciesStore &sp = ctx->sp[s];
     Arr7 arrs;
     for (int k = 0; k < 7; ++k) arrs.a[k] = sp.a[k];
     if (recvL[s])
       append_kernel<<<grid_for(recvL[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0] + s * ms,
-                                                                  recvL[s], mc, nraw[s], ctx->stats); ++ctx->launches;
+                                                                  recvL[s], nraw[s], ctx->stats); ++ctx->launches;
     if (recvR[s])
       append_kernel<<<grid_for(recvR[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1] + s * ms,
-                                                                  recvR[s], mc, nraw[s] + recvL[s], ctx->stats); ++ctx->launches;
+                                                                  recvR[s], nraw[s] + recvL[s], ctx->stats); ++ctx->launches;
     PIC_CUDA(cudaGetLastError());
     const int64_t nnew = nraw[s] + recvL[s] + recvR[s];
     set_scalar_kernel<<<1, 1, 0, ctx->stream>>>(sp.d_nraw, nnew); ++ctx->launches;
@@ -347,20 +363,7 @@ pic_status recompute_keys(Ctx *ctx, int s, int64_t from, int64_t to) {
   return PIC_OK;
 }
 
-pic_status exchange(Ctx *ctx) {
-  pic_status st = fold_and_ghosts(ctx);
-  if (st != PIC_OK) return st;
-  if (ctx->cfg.nranks > 1) {
-    st = migrate(ctx);
-    if (st != PIC_OK) return st;
-    // received particles were appended and counted: rebuild the order
-    for (int s = 0; s < ctx->cfg.n_species; ++s) {
-      st = build_order(ctx, s);
-      if (st != PIC_OK) return st;
-    }
-  }
-  return PIC_OK;
-}
+pic_status exchange(Ctx *ctx) { return fold_and_ghosts(ctx); }
 
 pic_status zero_moments(Ctx *ctx, int s) {
   PIC_CUDA(cudaMemsetAsync(ctx->sp[s].mom, 0, sizeof(double) * 10 * ctx->geom.m_plane, ctx->stream));

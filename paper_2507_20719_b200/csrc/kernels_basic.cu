@@ -5,7 +5,8 @@
 //                  the global field window (R12), boundary conditions (R10,
 //                  R11, R21) and the destination key of the new position.
 //                  Reads A[perm[q]], writes B[q] and ranks the particle for
-//                  the next cell order (order.cu).
+//                  the next cell order (order.cu, built by pic_mover after
+//                  the slab migration).
 //   moments_basic  Eq. 3: 10 moments x 8 corners per
 //                  particle, global fp64 atomics (RED.E.ADD.F64) into the
 //                  ghosted node arrays.
@@ -31,6 +32,8 @@ struct MoverArgs {
   unsigned long long *stats;
   double ks, ks_c;
   int n_iter;
+  int peer;                   // slab leavers go straight into the neighbours' buffers (peer.cu)
+  PeerOut po;
 };
 
 __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
@@ -82,24 +85,20 @@ __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
   const bool counted = act && k < KEY_FIRST_RESERVED;
   const uint32_t r = count_rank(A.cell_count, g.ncells, k, counted, !act || k != A.key[q]);
   if (counted) A.rank[q] = r;
+  if (A.peer && __any_sync(0xffffffffu, k == KEY_LEFT || k == KEY_RIGHT))
+    send_leavers_peer(A.po, k, A.dst, A.dst_id, q, A.stats);
 }
 
 __global__ void __launch_bounds__(256) moments_basic_kernel(
     Geom g, const double *__restrict__ X, const double *__restrict__ Y,
     const double *__restrict__ Z, const double *__restrict__ U, const double *__restrict__ V,
     const double *__restrict__ W, const double *__restrict__ Q, const uint32_t *__restrict__ key,
-    const int64_t *__restrict__ d_nraw, double *__restrict__ mom, unsigned long long *__restrict__ stats,
-    bool leavers_only) {
+    const int64_t *__restrict__ d_nraw, double *__restrict__ mom, unsigned long long *__restrict__ stats) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= *d_nraw) return;
-  const uint32_t k = key[p];
-  if (k == KEY_DEAD) return;
-  if (leavers_only && k != KEY_LEFT && k != KEY_RIGHT) return;
-  double xi[3] = {X[p], Y[p], Z[p]};
-  // slab leavers deposit at their unwrapped position (ghost planes, R15)
-  const double Nx = (double)g.ncell[0];
-  if (k == KEY_LEFT && xi[0] >= (double)g.slab_hi) xi[0] -= Nx;
-  if (k == KEY_RIGHT && xi[0] < (double)g.slab_lo) xi[0] += Nx;
+  // removed particles and slab leavers (deposited by their new owner) skip
+  if (key[p] >= KEY_FIRST_RESERVED) return;
+  const double xi[3] = {X[p], Y[p], Z[p]};
   const double v3[3] = {U[p], V[p], W[p]};
   if (!deposit_global(g, mom, xi, Q[p], v3)) atomicAdd(&stats[ST_FAR], 1ull);
 }
@@ -125,6 +124,8 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   A.ks = S.qom * (ctx->geom.dt * 0.5);
   A.ks_c = A.ks / ctx->geom.c;
   A.n_iter = S.n_iter;
+  A.peer = ctx->peer;
+  A.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
   const int threads = 256;
   const int64_t blocks = std::max<int64_t>(1, (S.n_raw + threads - 1) / threads);
   {
@@ -133,18 +134,17 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   }
   PIC_CUDA(cudaGetLastError());
   S.swap_buffers();
-  PhaseTimer t(ctx, 1);
-  return build_order(ctx, s);
+  return PIC_OK;
 }
 
-pic_status launch_moments_basic(Ctx *ctx, int s, bool leavers_only) {
+pic_status launch_moments_basic(Ctx *ctx, int s) {
   SpeciesStore &S = ctx->sp[s];
   if (S.n_raw == 0) return PIC_OK;
   const int threads = 256;
   const int64_t blocks = (S.n_raw + threads - 1) / threads;
   moments_basic_kernel<<<(unsigned)blocks, threads, 0, ctx->stream>>>(
       ctx->geom, S.a[0], S.a[1], S.a[2], S.a[3], S.a[4], S.a[5], S.a[6], S.key_new, S.d_nraw, S.mom,
-      ctx->stats, leavers_only); ++ctx->launches;
+      ctx->stats); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }

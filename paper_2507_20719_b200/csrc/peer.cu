@@ -1,0 +1,390 @@
+// peer.cu — multi-rank transport over NVLink peer memory (PIC_TRANSPORT_PEER).
+//
+// The paper moves exiting particles with MPI after the push and sums the
+// moments of shared nodes (Alg. 1 phase 2).  On one
+// B200 node every rank can map its slab neighbours' workspaces (CUDA IPC over
+// NVLink / NVSwitch), so both exchanges become stores into peer memory issued
+// by the kernels that produce the data:
+//
+//   migration   the mover itself writes every slab leaver's record into the
+//               neighbour's receive buffer (send_leavers_peer, pic_internal.cuh;
+//               one remote atomic per warp and side reserves the slots).  A
+//               flag barrier (release / acquire at system scope) then tells the
+//               receiver that its buffer is complete; arrive_kernel appends and
+//               ranks the arrivals into the cell counts of the next order, with
+//               no host round trip for the counts.
+//   ghost sums  after the deposit and a second flag barrier, each rank reads
+//               its left neighbour's ghost node plane x = slab_hi (== my
+//               slab_lo) from peer memory and adds it into its own plane
+//               (ghost_pull_kernel); the periodic y / z folds then run over the
+//               owned planes only, so the plane a neighbour reads is never
+//               modified concurrently.
+//
+// Ordering: every barrier is a release store of a monotonically increasing
+// epoch into both neighbours' flag words after a system-scope fence, and an
+// acquire spin on the own flags (bounded: a neighbour that never arrives sets
+// the peer error word instead of hanging the GPU; pic_sync reports it).
+// Reuse safety: a receive buffer is refilled only by the neighbour's next
+// mover, which starts after the second barrier of this cycle, i.e. after the
+// arrivals were consumed; a ghost plane is re-zeroed only after the first
+// barrier of the next cycle, i.e. after the neighbour pulled it.
+#include <nccl.h>
+
+#include <cuda.h>
+#include <cstring>
+
+#include "pic_internal.cuh"
+
+namespace pic {
+
+#define PIC_NCCL(call)                                                       \
+  do {                                                                       \
+    ncclResult_t r_ = (call);                                                \
+    if (r_ != ncclSuccess)                                                   \
+      return fail(ctx, PIC_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// What a rank tells its neighbours about its workspace (offsets from the base
+// of the CUDA allocation that holds it).
+struct PeerDesc {
+  cudaIpcMemHandle_t handle;
+  int64_t ok;                  // this rank could export its workspace
+  int64_t ctl_off;             // PeerCtl
+  int64_t recv_off[2];         // receive records: [0] from the left, [1] from the right
+  int64_t mom_off[PIC_MAX_SPECIES];
+  int64_t mig_cap;             // records per side and species
+  int64_t m_plane, m_nx;       // moment array plane stride and x extent
+  int64_t ghost_x;             // array x index of node slab_hi (the plane the right neighbour pulls)
+};
+
+static unsigned grid_for(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// ----------------------------------------------------------------- setup ----
+pic_status peer_setup(Ctx *ctx) {
+  const pic_config &c = ctx->cfg;
+  const Geom &g = ctx->geom;
+  if (c.nranks < 2 || c.transport == PIC_TRANSPORT_NCCL) return PIC_OK;
+  const int r = c.rank, P = c.nranks;
+  const bool per = g.periodic[0];
+  const int left = (r > 0) ? r - 1 : (per ? P - 1 : -1);
+  const int right = (r < P - 1) ? r + 1 : (per ? 0 : -1);
+
+  PeerDesc mine;
+  memset(&mine, 0, sizeof(mine));
+  // base of the allocation holding the workspace (driver API through the runtime)
+  using GetRange = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  char *ws = reinterpret_cast<char *>(ctx->workspace);
+  if (get_range && get_range(&base, &size, (CUdeviceptr)ws) == CUDA_SUCCESS &&
+      cudaIpcGetMemHandle(&mine.handle, (void *)base) == cudaSuccess) {
+    mine.ok = 1;
+  }
+  cudaGetLastError();
+  char *b = reinterpret_cast<char *>(base);
+  mine.ctl_off = reinterpret_cast<char *>(ctx->peer_ctl) - b;
+  mine.recv_off[0] = reinterpret_cast<char *>(ctx->mig_recv[0]) - b;
+  mine.recv_off[1] = reinterpret_cast<char *>(ctx->mig_recv[1]) - b;
+  for (int s = 0; s < c.n_species; ++s) mine.mom_off[s] = reinterpret_cast<char *>(ctx->sp[s].mom) - b;
+  mine.mig_cap = ctx->mig_cap;
+  mine.m_plane = g.m_plane;
+  mine.m_nx = g.m_n[0];
+  mine.ghost_x = g.G + (g.slab_hi - g.slab_lo);
+
+  // neighbours' descriptors: NCCL point-to-point through a device staging area
+  char *stage = reinterpret_cast<char *>(ctx->pack);
+  const size_t D = sizeof(PeerDesc);
+  PIC_CUDA(cudaMemcpy(stage, &mine, D, cudaMemcpyHostToDevice));
+  ncclComm_t comm = (ncclComm_t)ctx->nccl;
+  PIC_NCCL(ncclGroupStart());
+  if (right >= 0) PIC_NCCL(ncclSend(stage, D, ncclChar, right, comm, ctx->stream));
+  if (left >= 0) PIC_NCCL(ncclSend(stage, D, ncclChar, left, comm, ctx->stream));
+  if (left >= 0) PIC_NCCL(ncclRecv(stage + D, D, ncclChar, left, comm, ctx->stream));
+  if (right >= 0) PIC_NCCL(ncclRecv(stage + 2 * D, D, ncclChar, right, comm, ctx->stream));
+  PIC_NCCL(ncclGroupEnd());
+  PeerDesc nb[2];
+  memset(nb, 0, sizeof(nb));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (left >= 0) PIC_CUDA(cudaMemcpy(&nb[0], stage + D, D, cudaMemcpyDeviceToHost));
+  if (right >= 0) PIC_CUDA(cudaMemcpy(&nb[1], stage + 2 * D, D, cudaMemcpyDeviceToHost));
+
+  // map them (once when left == right)
+  int ok = mine.ok ? 1 : 0;
+  char *mapped[2] = {nullptr, nullptr};
+  for (int side = 0; side < 2 && ok; ++side) {
+    const int peer = side == 0 ? left : right;
+    if (peer < 0) continue;
+    if (!nb[side].ok) { ok = 0; break; }
+    if (side == 1 && right == left) { mapped[1] = mapped[0]; nb[1] = nb[0]; continue; }
+    void *ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, nb[side].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    mapped[side] = reinterpret_cast<char *>(ptr);
+  }
+  // every rank must agree on the transport
+  int *dok = reinterpret_cast<int *>(stage);
+  PIC_CUDA(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  PIC_NCCL(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, comm, ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  int all_ok = 0;
+  PIC_CUDA(cudaMemcpy(&all_ok, dok, sizeof(int), cudaMemcpyDeviceToHost));
+  if (!all_ok) {
+    for (int side = 0; side < 2; ++side)
+      if (mapped[side] && !(side == 1 && mapped[1] == mapped[0])) cudaIpcCloseMemHandle(mapped[side]);
+    if (c.transport == PIC_TRANSPORT_PEER)
+      return fail(ctx, PIC_ECUDA, "peer transport requested but a neighbour workspace cannot be mapped");
+    return PIC_OK;   // AUTO: NCCL transport
+  }
+  for (int side = 0; side < 2; ++side) {
+    Ctx::PeerLink &L = ctx->link[side];
+    L.mapped = mapped[side];
+    if (!mapped[side]) continue;
+    L.owns_mapping = !(side == 1 && mapped[1] == mapped[0]);
+    // I am the neighbour's right (side 0) or left (side 1) neighbour
+    const int from = side == 0 ? 1 : 0;
+    PeerCtl *pc = reinterpret_cast<PeerCtl *>(mapped[side] + nb[side].ctl_off);
+    L.flag = &pc->flag[from];
+    L.cnt = &pc->cnt[from][0];
+    L.recv = reinterpret_cast<double *>(mapped[side] + nb[side].recv_off[from]);
+    L.mig_cap = nb[side].mig_cap;
+    for (int s = 0; s < c.n_species; ++s) L.mom[s] = reinterpret_cast<double *>(mapped[side] + nb[side].mom_off[s]);
+    L.m_plane = nb[side].m_plane;
+    L.m_nx = nb[side].m_nx;
+    L.ghost_x = nb[side].ghost_x;
+  }
+  PIC_CUDA(cudaMemset(ctx->peer_ctl, 0, sizeof(PeerCtl)));
+  PIC_CUDA(cudaDeviceSynchronize());
+  ctx->peer = true;
+  return PIC_OK;
+}
+
+void peer_close(Ctx *ctx) {
+  for (int side = 0; side < 2; ++side)
+    if (ctx->link[side].mapped && ctx->link[side].owns_mapping) cudaIpcCloseMemHandle(ctx->link[side].mapped);
+}
+
+PeerOut peer_out(const Ctx *ctx, int s) {
+  PeerOut po;
+  for (int side = 0; side < 2; ++side) {
+    const Ctx::PeerLink &L = ctx->link[side];
+    po.buf[side] = L.mapped ? L.recv + (int64_t)s * MIG_REC * L.mig_cap : nullptr;
+    po.cnt[side] = L.mapped ? L.cnt + s : nullptr;
+    po.cap[side] = L.mapped ? L.mig_cap : 0;
+  }
+  return po;
+}
+
+// --------------------------------------------------------------- barrier ----
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long long *left_flag,
+                                    unsigned long long *right_flag, unsigned long long epoch,
+                                    unsigned long long *err) {
+  __threadfence_system();
+  if (left_flag) st_release_sys(left_flag, epoch);
+  if (right_flag) st_release_sys(right_flag, epoch);
+  const unsigned long long t0 = global_ns();
+  // own_flag[0] is written by the left neighbour, own_flag[1] by the right one
+  while ((left_flag && ld_acquire_sys(own_flag) < epoch) || (right_flag && ld_acquire_sys(own_flag + 1) < epoch)) {
+    if (global_ns() - t0 > 20ull * 1000 * 1000 * 1000) {   // 20 s: a neighbour is gone
+      atomicAdd(err, 1ull);
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
+static pic_status barrier(Ctx *ctx) {
+  ++ctx->peer_epoch;
+  peer_barrier_kernel<<<1, 1, 0, ctx->stream>>>(ctx->peer_ctl->flag, ctx->link[0].flag, ctx->link[1].flag,
+                                                ctx->peer_epoch, &ctx->peer_ctl->err); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  return PIC_OK;
+}
+
+// -------------------------------------------------------------- arrivals ----
+struct ArriveArgs {
+  Geom g;
+  double *a[PIC_MAX_SPECIES][7];
+  int64_t *id[PIC_MAX_SPECIES];
+  uint32_t *key_new[PIC_MAX_SPECIES], *rank[PIC_MAX_SPECIES], *cell_count[PIC_MAX_SPECIES];
+  int64_t *d_nraw[PIC_MAX_SPECIES];
+  int64_t cap[PIC_MAX_SPECIES];
+  const double *recv[2];           // own receive records, [from][species][MIG_REC * mig_cap]
+  int64_t mig_cap;
+  PeerCtl *ctl;
+  unsigned long long *stats;
+  int s0;
+};
+
+// blockIdx.y = species - s0.  Arrival i < n_from_left comes from the left
+// buffer, the rest from the right one; appended at d_nraw + i and ranked into
+// the cell counts as an arrival (order.cu).
+__global__ void arrive_kernel(const ArriveArgs A) {
+  const int s = A.s0 + blockIdx.y;
+  const int64_t c0 = min((int64_t)A.ctl->cnt[0][s], A.mig_cap), c1 = min((int64_t)A.ctl->cnt[1][s], A.mig_cap);
+  const int64_t n = c0 + c1, base = *A.d_nraw[s];
+  const Geom &g = A.g;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < n; w0 += stride) {
+    const int64_t i = w0 + threadIdx.x;
+    uint32_t k = KEY_DEAD;
+    const int64_t at = base + i;
+    const bool act = i < n;
+    if (act) {
+      const double *rec = i < c0 ? A.recv[0] + ((int64_t)s * A.mig_cap + i) * MIG_REC
+                                 : A.recv[1] + ((int64_t)s * A.mig_cap + (i - c0)) * MIG_REC;
+      double v[7];
+#pragma unroll
+      for (int c = 0; c < 7; ++c) v[c] = rec[c];
+      const int64_t idv = __double_as_longlong(rec[7]);
+      const int64_t cx = (int64_t)floor(v[0]), cy = (int64_t)floor(v[1]), cz = (int64_t)floor(v[2]);
+      if (at >= A.cap[s]) {
+        atomicAdd(&A.stats[ST_OVERFLOW], 1ull);
+      } else {
+        if (cx >= g.slab_lo && cx < g.slab_hi && cy >= 0 && cy < g.ncell[1] && cz >= 0 && cz < g.ncell[2]) {
+          k = tile_key(g, cx - g.slab_lo, cy, cz);
+        } else {
+          atomicAdd(&A.stats[ST_FAR], 1ull);
+        }
+#pragma unroll
+        for (int c = 0; c < 7; ++c) A.a[s][c][at] = v[c];
+        A.id[s][at] = idv;
+        A.key_new[s][at] = k;
+      }
+    }
+    const bool counted = act && k < KEY_FIRST_RESERVED;
+    const uint32_t r = count_rank(A.cell_count[s], g.ncells, k, counted, true);
+    if (counted) A.rank[s][at] = r;
+  }
+}
+
+__global__ void arrive_finish_kernel(const ArriveArgs A, int S) {
+  const int s = A.s0 + threadIdx.x;
+  if (threadIdx.x >= S) return;
+  const int64_t c0 = min((int64_t)A.ctl->cnt[0][s], A.mig_cap), c1 = min((int64_t)A.ctl->cnt[1][s], A.mig_cap);
+  const int64_t n = c0 + c1;
+  *A.d_nraw[s] = min(*A.d_nraw[s] + n, A.cap[s]);
+  atomicAdd(&A.stats[ST_RECEIVED], (unsigned long long)n);
+  A.ctl->cnt[0][s] = 0;
+  A.ctl->cnt[1][s] = 0;
+}
+
+// After the movers of species [s0, s1): barrier, append + rank the arrivals.
+pic_status peer_migrate(Ctx *ctx, int s0, int s1) {
+  {
+    PhaseTimer t(ctx, 4);
+    pic_status st = barrier(ctx);
+    if (st != PIC_OK) return st;
+  }
+  PhaseTimer t(ctx, 5);
+  ArriveArgs A;
+  A.g = ctx->geom;
+  for (int s = s0; s < s1; ++s) {
+    SpeciesStore &sp = ctx->sp[s];
+    for (int k = 0; k < 7; ++k) A.a[s][k] = sp.a[k];
+    A.id[s] = sp.id;
+    A.key_new[s] = sp.key_new;
+    A.rank[s] = sp.rank;
+    A.cell_count[s] = sp.cell_count;
+    A.d_nraw[s] = sp.d_nraw;
+    A.cap[s] = sp.cap;
+    // the host no longer knows the live count exactly: keep an upper bound for grid sizes
+    sp.n_raw = std::min<int64_t>(sp.cap, sp.n_raw + 2 * ctx->mig_cap);
+  }
+  A.recv[0] = ctx->mig_recv[0];
+  A.recv[1] = ctx->mig_recv[1];
+  A.mig_cap = ctx->mig_cap;
+  A.ctl = ctx->peer_ctl;
+  A.stats = ctx->stats;
+  A.s0 = s0;
+  dim3 grid(148, s1 - s0);
+  arrive_kernel<<<grid, 256, 0, ctx->stream>>>(A); ++ctx->launches;
+  arrive_finish_kernel<<<1, 32, 0, ctx->stream>>>(A, s1 - s0); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  return PIC_OK;
+}
+
+// ------------------------------------------------------------ ghost sums ----
+struct PullArgs {
+  double *mine[PIC_MAX_SPECIES];
+  const double *theirs[PIC_MAX_SPECIES];
+  int64_t face_yz, my_plane, my_nx, my_x, their_plane, their_nx, their_x;
+};
+
+// my plane x = slab_lo (array index G) += left neighbour's plane x = its slab_hi
+__global__ void ghost_pull_kernel(const PullArgs A) {
+  const int s = blockIdx.y;
+  const int64_t total = A.face_yz * 10;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t yz = t % A.face_yz, m = t / A.face_yz;
+    A.mine[s][m * A.my_plane + yz * A.my_nx + A.my_x] += A.theirs[s][m * A.their_plane + yz * A.their_nx + A.their_x];
+  }
+}
+
+pic_status launch_fold_axis(Ctx *ctx, int s, int axis, int64_t x0, int64_t nxr);
+
+pic_status peer_exchange(Ctx *ctx) {
+  const Geom &g = ctx->geom;
+  const int S = ctx->cfg.n_species;
+  pic_status st = barrier(ctx);
+  if (st != PIC_OK) return st;
+  const Ctx::PeerLink &L = ctx->link[0];
+  if (L.mapped) {
+    PullArgs A;
+    for (int s = 0; s < S; ++s) {
+      A.mine[s] = ctx->sp[s].mom;
+      A.theirs[s] = L.mom[s];
+    }
+    A.face_yz = g.m_n[1] * g.m_n[2];
+    A.my_plane = g.m_plane;
+    A.my_nx = g.m_n[0];
+    A.my_x = g.G;
+    A.their_plane = L.m_plane;
+    A.their_nx = L.m_nx;
+    A.their_x = L.ghost_x;
+    ghost_pull_kernel<<<dim3(grid_for(A.face_yz * 10), S), 256, 0, ctx->stream>>>(A); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+  }
+  // periodic y / z folds over the owned x planes only
+  const int64_t nloc = g.slab_hi - g.slab_lo;
+  const bool last_open = !g.periodic[0] && g.slab_hi == g.ncell[0];
+  for (int s = 0; s < S; ++s) {
+    for (int axis = 1; axis <= 2; ++axis)
+      if (g.periodic[axis]) {
+        st = launch_fold_axis(ctx, s, axis, g.G, nloc + (last_open ? 1 : 0));
+        if (st != PIC_OK) return st;
+      }
+  }
+  return PIC_OK;
+}
+
+}  // namespace pic

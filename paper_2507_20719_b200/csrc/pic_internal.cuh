@@ -39,6 +39,26 @@ enum Stat {
   ST_NONFINITE = 5, ST_OVERFLOW = 6, ST_MULTIWRAP = 7, ST_N = 8
 };
 
+// Slab migration records: x y z u v w q and the id bits, 8 words per particle.
+constexpr int MIG_REC = 8;
+
+// Control words of the peer transport (peer.cu), in the workspace of every rank
+// and written by its neighbours over NVLink.
+struct PeerCtl {
+  unsigned long long flag[2];      // barrier epochs: [0] from the left neighbour, [1] from the right
+  unsigned long long err;          // barrier timeouts
+  unsigned long long pad;
+  unsigned long long cnt[2][PIC_MAX_SPECIES];   // arrivals reserved by [0] left / [1] right neighbour
+};
+
+// What a sender needs to write one species' leavers into its neighbours'
+// receive buffers (side 0: left neighbour, 1: right; null = no peer link).
+struct PeerOut {
+  double *buf[2];
+  unsigned long long *cnt[2];
+  int64_t cap[2];
+};
+
 // Geometry passed by value to kernels.
 struct Geom {
   int64_t ncell[3];       // global cells
@@ -107,7 +127,6 @@ struct SpeciesStore {
   int32_t n_iter = 3;
   bool moved = false, deposited = false, fused_deposit = false;
   bool order_valid = false;
-  bool mom_primed = false;         // mover zeroed the moments and deposited its slab leavers
   void swap_buffers() {
     for (int k = 0; k < 7; ++k) { double *t = a[k]; a[k] = b[k]; b[k] = t; }
     int64_t *t = id; id = id_b; id_b = t;
@@ -124,7 +143,7 @@ struct Ctx {
   bool fields_set = false;
   unsigned long long *stats = nullptr;  // ST_N device counters
   int64_t *dev_counts = nullptr;     // small device scratch for counts
-  int64_t *host_counts = nullptr;    // pinned? (plain host)
+  int64_t *host_counts = nullptr;    // pinned host [64] (migration counts)
   // exchange buffers
   double *ghost_send[2] = {};        // [0] to left, [1] to right
   double *ghost_recv[2] = {};
@@ -133,6 +152,20 @@ struct Ctx {
   double *mig_recv[2] = {};
   int64_t mig_cap = 0;
   double *pack = nullptr;            // moment copy-out staging
+  void *workspace = nullptr;         // caller's device workspace (pic_init)
+  // peer transport (peer.cu): own control block and the mapped neighbours
+  PeerCtl *peer_ctl = nullptr;
+  struct PeerLink {
+    char *mapped = nullptr;          // neighbour's workspace allocation (CUDA IPC)
+    bool owns_mapping = false;
+    unsigned long long *flag = nullptr, *cnt = nullptr;   // my slots in its PeerCtl
+    double *recv = nullptr;          // its receive records from me
+    int64_t mig_cap = 0;
+    double *mom[PIC_MAX_SPECIES] = {};
+    int64_t m_plane = 0, m_nx = 0, ghost_x = 0;
+  } link[2];                         // [0] left, [1] right
+  bool peer = false;
+  unsigned long long peer_epoch = 0;
   void *cub_temp = nullptr;
   size_t cub_bytes = 0;
   void *nccl = nullptr;              // ncclComm_t
@@ -143,10 +176,11 @@ struct Ctx {
   int64_t cycle = 0;
   int64_t cap_max = 0;
   std::string err;
-  // pic_profile: CUDA event pairs per phase (0 mover, 1 order, 2 deposit, 3 exchange)
+  // pic_profile: CUDA event pairs per phase (0 mover, 1 order, 2 deposit,
+  // 3 ghost exchange, 4 migration before the count sync, 5 after it)
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_pool;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[PIC_PROF_PHASES];
   cudaEvent_t prof_event() {
     if (!prof_pool.empty()) {
       cudaEvent_t e = prof_pool.back();
@@ -197,14 +231,20 @@ inline pic_status fail(Ctx *ctx, pic_status s, const std::string &m) {
 // -------------------------------------------------------------- launchers ----
 // (implemented in the .cu files; all enqueue on ctx->stream)
 pic_status launch_mover_basic(Ctx *ctx, int s);
-pic_status launch_moments_basic(Ctx *ctx, int s, bool leavers_only = false);
+pic_status launch_moments_basic(Ctx *ctx, int s);
 pic_status launch_tiled_deposit(Ctx *ctx, int s);
-pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit);
+pic_status launch_tiled_step(Ctx *ctx, int s);
 size_t order_temp_bytes(int64_t ncells);
 pic_status zero_cell_counts(Ctx *ctx, int s);
 pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to);
 pic_status build_order(Ctx *ctx, int s);
 pic_status exchange(Ctx *ctx);
+pic_status migrate(Ctx *ctx, int s0, int s1);
+pic_status peer_setup(Ctx *ctx);
+void peer_close(Ctx *ctx);
+PeerOut peer_out(const Ctx *ctx, int s);
+pic_status peer_migrate(Ctx *ctx, int s0, int s1);
+pic_status peer_exchange(Ctx *ctx);
 pic_status recompute_keys(Ctx *ctx, int s, int64_t from, int64_t to);
 pic_status zero_moments(Ctx *ctx, int s);
 pic_status pack_moments(Ctx *ctx, int s, double *out);
@@ -366,10 +406,46 @@ __device__ __forceinline__ uint32_t count_rank_finish(const RankTicket &t) {
   return (base + (uint32_t)__popc(t.peers & ((1u << lane) - 1u))) | (t.arrival ? RANK_ARRIVAL : 0u);
 }
 
+// Peer transport, warp-collective (all 32 lanes): lanes whose new key is
+// KEY_LEFT / KEY_RIGHT copy their record (read back from the output slot p the
+// mover just wrote) straight into the neighbour's receive buffer over NVLink.
+// One remote atomic per warp and side reserves the slots; a slot beyond the
+// neighbour's capacity is an overflow (pic_sync reports it).  Each writer
+// fences its stores at system scope before the barrier publishes them.
+__device__ __forceinline__ void send_leavers_peer(const PeerOut &po, uint32_t k, const double *const dst[7],
+                                                  const int64_t *dst_id, int64_t p,
+                                                  unsigned long long *stats) {
+  const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const bool mine = k == (side == 0 ? KEY_LEFT : KEY_RIGHT);
+    const unsigned mask = __ballot_sync(0xffffffffu, mine);
+    if (!mask) continue;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long slot0 = 0;
+    if ((int)lane == leader) {
+      slot0 = po.cnt[side] ? atomicAdd(po.cnt[side], (unsigned long long)__popc(mask)) : ~0ull >> 1;
+      atomicAdd(&stats[ST_SENT], (unsigned long long)__popc(mask));
+    }
+    slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+    if (mine) {
+      const int64_t slot = (int64_t)slot0 + __popc(mask & ((1u << lane) - 1u));
+      if (slot < po.cap[side]) {
+        double *rec = po.buf[side] + slot * MIG_REC;
+#pragma unroll
+        for (int c = 0; c < 7; ++c) rec[c] = dst[c][p];
+        rec[7] = __longlong_as_double(dst_id[p]);
+        __threadfence_system();
+      } else {
+        atomicAdd(&stats[ST_OVERFLOW], 1ull);
+      }
+    }
+  }
+}
+
 // Eq. 3 deposit of one particle with global fp64 atomics (80 RED), at a
-// cell-unit position relative to the ghosted moment arrays.  Used for the basic
-// family and for slab leavers, which the tiled mover deposits into the ghost
-// planes before they migrate (R15).  Returns false if the stencil is outside.
+// cell-unit position relative to the ghosted moment arrays (basic family).
+// Returns false if the stencil is outside.
 __device__ __forceinline__ bool deposit_global(const Geom &g, double *__restrict__ mom, const double xi[3], double q,
                                                const double v[3]) {
   int64_t idx[3];

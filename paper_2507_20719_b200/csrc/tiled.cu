@@ -65,10 +65,11 @@ struct MoverTArgs {
   uint32_t *key_new, *rank, *cell_count;
   int64_t *d_nraw;
   const double *field;        // global window (fallback sampling)
-  double *mom;                // ghosted moments (slab leavers, deposited by the mover)
   unsigned long long *stats;
   double ks, ks_c;
   int n_iter;
+  int peer;                   // slab leavers go straight into the neighbours' buffers (peer.cu)
+  PeerOut po;
 };
 
 struct DepositArgs {
@@ -307,14 +308,7 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
         xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
         vnew[d] = fma(2.0, vb[d], -vn[d]);
       }
-      const double x_pre = xnew[0];
       knew = finish_particle(g, xnew, vnew, clamped, A.stats);
-      if (g.multi_rank && (knew == KEY_LEFT || knew == KEY_RIGHT)) {
-        // slab leaver: deposit into the x ghost planes now, before it migrates
-        // (R15); x unwrapped, y and z wrapped (the moment arrays hold planes [0, N])
-        const double xdep[3] = {x_pre, xnew[1], xnew[2]};
-        if (!deposit_global(g, A.mom, xdep, qv, vnew)) atomicAdd(&A.stats[ST_FAR], 1ull);
-      }
       A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
       A.dst[3][p] = vnew[0]; A.dst[4][p] = vnew[1]; A.dst[5][p] = vnew[2];
       A.dst[6][p] = qv;
@@ -329,6 +323,8 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     }
     tk = count_rank_issue(A.cell_count, g.ncells, knew, act && knew < KEY_FIRST_RESERVED, knew != kold);
     pr_p = p;
+    if (A.peer && __any_sync(0xffffffffu, knew == KEY_LEFT || knew == KEY_RIGHT))
+      send_leavers_peer(A.po, knew, A.dst, A.dst_id, p, A.stats);
   }
   if (wbeg < wend) {
     const uint32_t r = count_rank_finish(tk);
@@ -572,9 +568,9 @@ static pic_status make_tmap(Ctx *ctx) {
 }
 
 // pic_mover, tiled family: move through the current order into buffer B, rank
-// the new keys, swap buffers and build the next order (order.cu).
-pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
-  *did_deposit = false;
+// the new keys and swap buffers; pic_mover then migrates slab leavers
+// (multi-rank) and builds the next order (order.cu).
+pic_status launch_tiled_step(Ctx *ctx, int s) {
   SpeciesStore &sp = ctx->sp[s];
   if (!ctx->tmap_ok) {
     pic_status st = make_tmap(ctx);
@@ -582,9 +578,6 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   }
   pic_status st = zero_cell_counts(ctx, s);
   if (st != PIC_OK) return st;
-  st = zero_moments(ctx, s);   // the mover deposits slab leavers (multi-rank)
-  if (st != PIC_OK) return st;
-  sp.mom_primed = true;
   MoverTArgs A;
   A.g = ctx->geom;
   for (int k = 0; k < 7; ++k) { A.src[k] = sp.a[k]; A.dst[k] = sp.b[k]; }
@@ -598,11 +591,12 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   A.cell_count = sp.cell_count;
   A.d_nraw = sp.d_nraw;
   A.field = ctx->field;
-  A.mom = sp.mom;
   A.stats = ctx->stats;
   A.ks = sp.qom * (ctx->geom.dt * 0.5);
   A.ks_c = A.ks / ctx->geom.c;
   A.n_iter = sp.n_iter;
+  A.peer = ctx->peer;
+  A.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
   const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap);
   const unsigned grid = (unsigned)ctx->geom.ntiles;
 #define PIC_LAUNCH(NIT) \
@@ -621,24 +615,20 @@ pic_status launch_tiled_step(Ctx *ctx, int s, bool *did_deposit) {
   ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   sp.swap_buffers();
-  PhaseTimer t(ctx, 1);
-  return build_order(ctx, s);
+  return PIC_OK;
 }
 
 // pic_moments, tiled family: deposit over the new order (requires the order
-// built by launch_tiled_step); slab leavers (not in the order) go through the
-// basic deposit restricted to them.
+// built by pic_mover after migration, so arrivals are included and leavers are
+// deposited by their new owner only).
 pic_status launch_tiled_deposit(Ctx *ctx, int s) {
   SpeciesStore &sp = ctx->sp[s];
   if (!ctx->tmap_ok) {
     pic_status st = make_tmap(ctx);
     if (st != PIC_OK) return st;
   }
-  if (!sp.mom_primed) {
-    pic_status st = zero_moments(ctx, s);
-    if (st != PIC_OK) return st;
-  }
-  sp.mom_primed = false;
+  pic_status st = zero_moments(ctx, s);
+  if (st != PIC_OK) return st;
   DepositArgs A;
   A.g = ctx->geom;
   for (int k = 0; k < 7; ++k) A.src[k] = sp.a[k];

@@ -38,6 +38,12 @@ class Species:
     vth: float                      # thermal speed per component
     drift: Tuple[float, float, float] = (0.0, 0.0, 0.0)
     ppc: int = 27
+    # optional non-uniform loading (C5): ppc_fn(Xc, Yc, Zc) -> int64 particles per
+    # cell at the cell centres, dens_fn(X, Y, Z) -> number density at positions;
+    # species of one `group` share positions (co-located pairs)
+    ppc_fn: Optional[Callable] = None
+    dens_fn: Optional[Callable] = None
+    group: int = 0
 
 
 @dataclass
@@ -219,46 +225,58 @@ def cell_range(w: Workload):
     return lo, hi
 
 
-def make_positions(w: Workload, ppc: int, gen: torch.Generator, device, planet_ok=True):
-    """ppc particles uniformly random in every cell of this rank's slab (id order:
-    cell-major over global cell index, then in-cell index)."""
+def _cell_centres(w: Workload, device):
     lo, hi = cell_range(w)
     nx, ny, nz = hi - lo, w.ncell[1], w.ncell[2]
-    ncells = nx * ny * nz
-    n = ncells * ppc
-    cell = torch.arange(ncells, device=device, dtype=torch.int64).repeat_interleave(ppc)
-    cx = cell % nx + lo
-    cy = (cell // nx) % ny
-    cz = cell // (nx * ny)
+    c = torch.arange(nx * ny * nz, device=device, dtype=torch.int64)
+    cx, cy, cz = c % nx + lo, (c // nx) % ny, c // (nx * ny)
+    dl = w.delta
+    return cx, cy, cz, ((cx.double() + 0.5) * dl[0], (cy.double() + 0.5) * dl[1], (cz.double() + 0.5) * dl[2])
+
+
+def make_positions(w: Workload, sp: Species, gen: torch.Generator, device, planet_ok=True):
+    """Particles uniformly random in every cell of this rank's slab: sp.ppc per
+    cell, or sp.ppc_fn(cell centre) for non-uniform loading.  ids = global cell
+    id * 1024 + in-cell index, independent of the slab split."""
+    cx, cy, cz, cen = _cell_centres(w, device)
+    if sp.ppc_fn is not None:
+        counts = sp.ppc_fn(*cen).to(torch.int64).clamp(0, 1023)
+    else:
+        counts = torch.full_like(cx, sp.ppc)
+    n = int(counts.sum().item())
+    cell = torch.repeat_interleave(torch.arange(cx.numel(), device=device), counts)
+    start = torch.cumsum(counts, 0) - counts
+    k = torch.arange(n, device=device, dtype=torch.int64) - start[cell]
+    cx, cy, cz = cx[cell], cy[cell], cz[cell]
     dl = w.delta
     r = torch.rand((3, n), generator=gen, device=device, dtype=torch.float64)
     x = (cx.to(torch.float64) + r[0]) * dl[0]
     y = (cy.to(torch.float64) + r[1]) * dl[1]
     z = (cz.to(torch.float64) + r[2]) * dl[2]
-    gid = ((cz * w.ncell[1] + cy) * w.ncell[0] + cx) * ppc + torch.arange(n, device=device) % ppc
+    gid = ((cz * w.ncell[1] + cy) * w.ncell[0] + cx) * 1024 + k
     keep = None
     if w.planet_radius > 0 and planet_ok:
         c = w.planet_center
         keep = ((x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2) >= w.planet_radius ** 2
-    return x, y, z, gid, keep
+    return x, y, z, gid, keep, counts[cell]
 
 
 def make_species(w: Workload, device="cpu") -> List[dict]:
     """Particles of every species of this rank: list of dicts of float64 tensors
-    x y z u v w q and int64 id (ids are global and independent of the slab split
-    when the generator runs per cell... here: global cell id * ppc + k)."""
+    x y z u v w q and int64 id (global: cell id * 1024 + in-cell index, plus
+    species * 2^40).  q_p = sign * n(x) V / ppc_cell (R14)."""
     gen = torch.Generator(device=device).manual_seed(w.seed * 7919 + w.slab_or_all()[0])
     out = []
-    base = None
+    groups = {}
+    V = w.delta[0] * w.delta[1] * w.delta[2]
     for si, sp in enumerate(w.species):
-        if base is None or not w.colocate or sp.ppc != base[4]:
-            x, y, z, gid, keep = make_positions(w, sp.ppc, gen, device)
-            base = (x, y, z, keep, sp.ppc, gid)
-        x, y, z, keep, ppc, gid = base
+        key = sp.group if w.colocate else si
+        if key not in groups:
+            groups[key] = make_positions(w, sp, gen, device)
+        x, y, z, gid, keep, ppc_cell = groups[key]
         n = x.numel()
-        V = w.delta[0] * w.delta[1] * w.delta[2]
-        dens = _density(w, y)
-        q = sp.sign * dens * V / ppc
+        dens = sp.dens_fn(x, y, z) if sp.dens_fn is not None else _density(w, y)
+        q = sp.sign * dens * V / ppc_cell.to(torch.float64)
         vel = torch.randn((3, n), generator=gen, device=device, dtype=torch.float64) * sp.vth
         u, v, ww = vel[0] + sp.drift[0], vel[1] + sp.drift[1], vel[2] + sp.drift[2]
         if w.density == "harris":
@@ -328,4 +346,44 @@ def c4(ncell=(512, 256, 256), ppc: int = 64, seed: int = 4) -> Workload:
         planet_center=center, planet_radius=R)
 
 
-CONFIGS = {"c1": c1, "c1r": lambda: c1(True), "c2": c2, "c3": c3, "c4": c4}
+def c5(ncell=(512, 256, 256), wind_ppc: int = 64, inner_ppc: int = 8, planet_ppc: int = 256, seed: int = 5) -> Workload:
+    """Ganymede-like magnetosphere: 4 species (solar-wind e-/p+ in a sub-Alfvenic
+    flow, planetary e-/p+ from the moon's surface), open boundaries, absorbing
+    moon, strongly non-uniform ppc: wind 64 ppc outside a magnetosphere
+    ellipsoid and 8 inside, planetary round(256 exp(-(r - R)/2)) (0..256).
+    Densities are smooth (weights carry n(x)), so ppc and weights vary, not n."""
+    d = 0.125
+    L = tuple(n * d for n in ncell)
+    sc = ncell[0] / 512
+    R = 2.0 * sc
+    center = (L[0] * 0.5, L[1] / 2, L[2] / 2)
+    vflow = 0.01
+    M = 0.005 * (4.0 * sc) ** 3 * 8
+    ax = (8.0 * sc, 6.0 * sc, 6.0 * sc)    # magnetosphere ellipsoid semi-axes
+
+    def r_of(X, Y, Z):
+        return torch.sqrt((X - center[0]) ** 2 + (Y - center[1]) ** 2 + (Z - center[2]) ** 2)
+
+    def wind_ppc_fn(X, Y, Z):
+        inside = ((X - center[0]) / ax[0]) ** 2 + ((Y - center[1]) / ax[1]) ** 2 + ((Z - center[2]) / ax[2]) ** 2 < 1
+        return torch.where(inside, inner_ppc, wind_ppc)
+
+    def planet_ppc_fn(X, Y, Z):
+        r = r_of(X, Y, Z)
+        return torch.where(r >= R, torch.round(planet_ppc * torch.exp(-(r - R) / (2.0 * sc))), 0.0)
+
+    def planet_dens(X, Y, Z):
+        return 2.0 * N0 * torch.exp(-(r_of(X, Y, Z) - R) / (2.0 * sc))
+
+    wind = lambda X, Y, Z: N0 + 0 * X
+    return Workload(
+        name="c5", ncell=ncell, length=L, bc=(OPEN,) * 3, dt=0.25, seed=seed,
+        species=[Species("sw e-", -256.0, -1.0, 0.05, (vflow, 0, 0), ppc_fn=wind_ppc_fn, dens_fn=wind, group=0),
+                 Species("sw p+", 1.0, 1.0, 0.0031, (vflow, 0, 0), ppc_fn=wind_ppc_fn, dens_fn=wind, group=0),
+                 Species("pl e-", -256.0, -1.0, 0.02, ppc_fn=planet_ppc_fn, dens_fn=planet_dens, group=1),
+                 Species("pl p+", 1.0, 1.0, 0.0015, ppc_fn=planet_ppc_fn, dens_fn=planet_dens, group=1)],
+        field_kind="dipole", field_params={"M": M, "Bimf": (0.0, 0.0, -0.005), "vsw": vflow},
+        planet_center=center, planet_radius=R)
+
+
+CONFIGS = {"c1": c1, "c1r": lambda: c1(True), "c2": c2, "c3": c3, "c4": c4, "c5": c5}

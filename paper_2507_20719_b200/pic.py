@@ -28,11 +28,12 @@ PIC_OK, PIC_EINVAL, PIC_ECUDA, PIC_ENCCL, PIC_ENOMEM, PIC_ESTATE, PIC_ERANGE, PI
 STATUS_NAMES = ["PIC_OK", "PIC_EINVAL", "PIC_ECUDA", "PIC_ENCCL", "PIC_ENOMEM", "PIC_ESTATE",
                 "PIC_ERANGE", "PIC_ENONFINITE"]
 KERNEL_AUTO, KERNEL_BASIC, KERNEL_TILED = 0, 1, 2
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_PEER = 0, 1, 2
 STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "overflow", "multiwrap"]
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -43,7 +44,7 @@ class pic_config(C.Structure):
         ("capacity", C.c_int64 * PIC_MAX_SPECIES),
         ("planet_center", C.c_double * 3), ("planet_radius", C.c_double),
         ("rank", C.c_int32), ("nranks", C.c_int32), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64),
-        ("ghost", C.c_int32), ("sort_every", C.c_int32), ("kernel", C.c_int32),
+        ("ghost", C.c_int32), ("transport", C.c_int32), ("kernel", C.c_int32),
     ]
 
 
@@ -82,6 +83,7 @@ def load_library(path: str = LIB_PATH):
         lib.pic_get_moments.argtypes = [vp, C.c_int32, vp]
         lib.pic_sync.argtypes = [vp, P(C.c_int64)]
         lib.pic_launch_count.argtypes = [vp, P(C.c_int64)]
+        lib.pic_get_transport.argtypes = [vp, P(C.c_int32)]
         lib.pic_profile.argtypes = [vp, C.c_int32]
         lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
@@ -119,7 +121,7 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
-def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, sort_every=0, kernel=KERNEL_AUTO,
+def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSPORT_AUTO, kernel=KERNEL_AUTO,
                 n_iter=None) -> pic_config:
     """pic_config from an inputs.Workload (marshalling only)."""
     cfg = pic_config()
@@ -136,7 +138,7 @@ def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, sort_every=0, ke
         cfg.n_iter[s] = n_iter if n_iter is not None else w.n_iter
         cfg.capacity[s] = capacity[s] if capacity is not None else 0
     cfg.rank, cfg.nranks, cfg.slab_lo, cfg.slab_hi = rank, nranks, lo, hi
-    cfg.ghost, cfg.sort_every, cfg.kernel = ghost, sort_every, kernel
+    cfg.ghost, cfg.transport, cfg.kernel = ghost, transport, kernel
     return cfg
 
 
@@ -228,15 +230,28 @@ class Context:
         _check(self.lib.pic_launch_count(self.h, C.byref(out)), self.h, "pic_launch_count")
         return out.value
 
+    @property
+    def transport(self) -> int:
+        """TRANSPORT_PEER / TRANSPORT_NCCL in use (nranks > 1), TRANSPORT_AUTO for one rank."""
+        out = C.c_int32()
+        _check(self.lib.pic_get_transport(self.h, C.byref(out)), self.h, "pic_get_transport")
+        return out.value
+
+    @property
+    def peer(self) -> bool:
+        return self.transport == TRANSPORT_PEER
+
     def profile(self, enable: bool = True):
         _check(self.lib.pic_profile(self.h, 1 if enable else 0), self.h, "pic_profile")
 
     def profile_read(self):
-        """{phase: (ms, launches)} for mover, order, deposit, exchange."""
-        ms = (C.c_double * 4)()
-        n = (C.c_int64 * 4)()
+        """{phase: (ms, launches)} for mover, order, deposit, exchange (ghost
+        sums + folds), migrate_pre / migrate_post (before / after the count sync)."""
+        names = ("mover", "order", "deposit", "exchange", "migrate_pre", "migrate_post")
+        ms = (C.c_double * len(names))()
+        n = (C.c_int64 * len(names))()
         _check(self.lib.pic_profile_read(self.h, ms, n), self.h, "pic_profile_read")
-        return {k: (ms[i], n[i]) for i, k in enumerate(("mover", "order", "deposit", "exchange"))}
+        return {k: (ms[i], n[i]) for i, k in enumerate(names)}
 
     def close(self):
         if getattr(self, "h", None):

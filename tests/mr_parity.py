@@ -4,7 +4,8 @@
         --master-port 29533 tests/mr_parity.py [--out report.json]
 
 Each rank owns an x-slab of the same global inputs, runs the full cycle through
-the C ABI (NCCL ghost-plane sums + migration), and rank 0 compares the union of
+the C ABI (both transports: peer memory over NVLink and NCCL messages, for
+ghost-plane sums + migration), and rank 0 compares the union of
 all slabs with the single-process CPU oracle (decomposition invariance, P14).
 """
 import argparse
@@ -24,7 +25,7 @@ import parity_util as PU  # noqa: E402
 from paper_2507_20719_b200 import decomp, inputs as I, pic  # noqa: E402
 
 
-def run_case(name, w, cycles, kernel, rank, world):
+def run_case(name, w, cycles, kernel, transport, rank, world):
     bounds = decomp.uniform_bounds(w.ncell[0], world)
     lo, hi = bounds[rank], bounds[rank + 1]
     parts_all = I.make_species(w.with_slab(0, w.ncell[0]), device="cpu")
@@ -36,8 +37,9 @@ def run_case(name, w, cycles, kernel, rank, world):
     wr = w.with_slab(lo, hi)
     cap = [int(p["x"].numel() * 1.5) + 4096 for p in parts_all]
     nid = decomp.broadcast_nccl_id(pic.pic_nccl_id)
-    cfg = pic.make_config(wr, rank=rank, nranks=world, capacity=cap, ghost=2, sort_every=1, kernel=kernel)
+    cfg = pic.make_config(wr, rank=rank, nranks=world, capacity=cap, ghost=2, kernel=kernel, transport=transport)
     ctx = pic.Context(cfg, nccl_id=nid)
+    assert ctx.transport == transport
     for s, p in enumerate(mine):
         ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
     _, EB = I.field_window(wr, 2, device="cpu")
@@ -61,7 +63,7 @@ def run_case(name, w, cycles, kernel, rank, world):
     for s, sp in enumerate(w.species):
         gp = {k: np.concatenate([gathered[r][0][s][0][k] for r in range(world)]) for k in gathered[0][0][s][0]}
         gm = np.concatenate([gathered[r][0][s][1] for r in range(world)], axis=3)
-        rep = {"case": name, "kernel": kernel, "species": sp.name, "world": world,
+        rep = {"case": name, "kernel": kernel, "transport": transport, "species": sp.name, "world": world,
                "sent": sum(g[1]["sent"] for g in gathered), "removed": sum(g[1]["removed"] for g in gathered)}
         okp = PU.compare_particles(w, sp, gp, orc[s][0], orc[s][1], rep)
         okm = PU.compare_moments(gm, orc[s][2], orc[s][3], rep)
@@ -81,15 +83,17 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     cases = [("c1r", I.c1(randomized=True), 4),
              ("c2s", I.c2(nx_per_rank=32, ppc=27), 3),
-             ("c4s", I.c4(ncell=(32, 16, 16), ppc=8), 4)]
+             ("c4s", I.c4(ncell=(32, 16, 16), ppc=8), 4),
+             ("c5s", I.c5(ncell=(64, 32, 32), wind_ppc=2, inner_ppc=1, planet_ppc=16), 3)]
     all_ok, reports = True, []
-    for kernel in (pic.KERNEL_TILED, pic.KERNEL_BASIC):
-        for name, w, cyc in cases:
-            res = run_case(name, w, cyc, kernel, rank, world)
-            if rank == 0:
-                ok, reps = res
-                all_ok &= ok
-                reports += reps
+    for transport in (pic.TRANSPORT_PEER, pic.TRANSPORT_NCCL):
+        for kernel in (pic.KERNEL_TILED, pic.KERNEL_BASIC):
+            for name, w, cyc in cases:
+                res = run_case(name, w, cyc, kernel, transport, rank, world)
+                if rank == 0:
+                    ok, reps = res
+                    all_ok &= ok
+                    reports += reps
     if rank == 0:
         txt = json.dumps({"ok": bool(all_ok), "reports": reports}, indent=1)
         print(txt)

@@ -16,9 +16,9 @@ import parity_util as PU
 pytestmark = pytest.mark.gpu
 
 
-def run_gpu(w, parts, cycles, kernel, ghost=2, sort_every=0, n_iter=None):
+def run_gpu(w, parts, cycles, kernel, ghost=2, n_iter=None):
     cap = [int(p["x"].numel() * 1.25) + 64 for p in parts]
-    cfg = pic.make_config(w, capacity=cap, ghost=ghost, sort_every=sort_every, kernel=kernel, n_iter=n_iter)
+    cfg = pic.make_config(w, capacity=cap, ghost=ghost, kernel=kernel, n_iter=n_iter)
     ctx = pic.Context(cfg)
     for s, p in enumerate(parts):
         ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
@@ -36,10 +36,10 @@ def run_gpu(w, parts, cycles, kernel, ghost=2, sort_every=0, n_iter=None):
     return out, stats
 
 
-def check(w, cycles, kernel, ghost=2, sort_every=0, n_iter=None):
+def check(w, cycles, kernel, ghost=2, n_iter=None):
     parts = I.make_species(w, device="cpu")
     orc = PU.run_oracle(w, parts, cycles, ghost=ghost, n_iter=n_iter)
-    gpu, stats = run_gpu(w, parts, cycles, kernel, ghost, sort_every, n_iter)
+    gpu, stats = run_gpu(w, parts, cycles, kernel, ghost, n_iter)
     reports = []
     for s, sp in enumerate(w.species):
         rep = {"species": sp.name}
@@ -55,26 +55,44 @@ KERNELS = [pic.KERNEL_BASIC, pic.KERNEL_TILED]
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_c1_uniform(kernel):
-    reps, stats = check(I.c1(), 5, kernel, sort_every=1)
+    reps, stats = check(I.c1(), 5, kernel)
     assert stats["removed"] == 0 and stats["far"] == 0
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_c1r_random_fields(kernel):
-    check(I.c1(randomized=True), 5, kernel, sort_every=2)
+    check(I.c1(randomized=True), 5, kernel)
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_c2_harris_scaled(kernel):
     # C2 structure at 1/8 size in x and reduced ppc (oracle in seconds)
     w = I.c2(nx_per_rank=16, ppc=27)
-    check(w, 3, kernel, sort_every=1)
+    check(w, 3, kernel)
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_c4_open_dipole_scaled(kernel):
     w = I.c4(ncell=(32, 16, 16), ppc=8)
-    reps, stats = check(w, 4, kernel, sort_every=1)
+    reps, stats = check(w, 4, kernel)
+    assert stats["removed"] > 0
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c3_fourier_scaled(kernel):
+    # C3 structure (B0 z + random Fourier modes, periodic cube) at 24^3, 8 ppc
+    w = I.c3(n_per_rank=24, ppc=8)
+    check(w, 3, kernel)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c5_four_species_nonuniform_ppc(kernel):
+    # C5 structure at 1/8 size: 4 species, wind ppc 4/1 in/out of the
+    # magnetosphere ellipsoid, planetary ppc round(32 exp(-(r-R)/2)), open BC
+    w = I.c5(ncell=(64, 32, 32), wind_ppc=4, inner_ppc=1, planet_ppc=32)
+    parts = I.make_species(w, device="cpu")
+    assert len(parts) == 4 and parts[2]["x"].numel() > 0
+    reps, stats = check(w, 3, kernel)
     assert stats["removed"] > 0
 
 
@@ -92,7 +110,7 @@ def test_ragged_and_empty_species():
     parts[0] = {k: v[keep].contiguous() for k, v in parts[0].items()}
     parts[1] = {k: v[:0].contiguous() for k, v in parts[1].items()}
     orc = PU.run_oracle(w, parts, 3)
-    gpu, _ = run_gpu(w, parts, 3, pic.KERNEL_TILED, sort_every=1)
+    gpu, _ = run_gpu(w, parts, 3, pic.KERNEL_TILED)
     rep = {}
     assert PU.compare_particles(w, w.species[0], gpu[0][0], orc[0][0], orc[0][1], rep), rep
     assert PU.compare_moments(gpu[0][1], orc[0][2], orc[0][3], rep), rep
@@ -105,7 +123,7 @@ def test_closed_form_gyration_on_gpu():
     w = I.c1()
     w.field_params = {"E": (0.0, 0.0, 0.0), "B": (0.0, 0.0, 0.01)}
     parts = I.make_species(w, device="cpu")
-    gpu, _ = run_gpu(w, parts, 1, pic.KERNEL_TILED, sort_every=1)
+    gpu, _ = run_gpu(w, parts, 1, pic.KERNEL_TILED)
     for s, sp in enumerate(w.species):
         gp = gpu[s][0]
         order = np.argsort(gp["id"])
