@@ -49,8 +49,16 @@ constexpr int SRC_STAGES = 3;    // mover: rounds of gathered sources in flight 
 constexpr int PK_SLOTS = 6;      // mover: perm/key ring slots
 constexpr int PK_AHEAD = 5;      // mover: perm/key fetched this many rounds ahead
 constexpr int MOVER_WARP_STAGE = SRC_STAGES * 8 * 32 + PK_SLOTS * 2 * 32 / 2;  // doubles per warp
-constexpr int SGRP = 36;                        // doubles per 4-particle group in the S buffer (32 + pad)
-constexpr int WBUF = 8 * SGRP + 32 * 10;        // doubles per warp: S[8][36] + V[32][10]
+// deposit staging per warp: S[32 particles][8 corners], V[32][moments 0..7]
+// and V2[32][moments 8, 9].  S and V rows are 8 doubles whose 16-byte pairs
+// are XOR-swizzled by row (stage_slot) so that both the row writes (STS.128,
+// 8 consecutive rows per quarter-warp) and the MMA fragment reads (lanes
+// (g, j) -> row 4t + j, column g) are free of bank conflicts.
+constexpr int WBUF = 32 * 8 * 2 + 32 * 2;
+#ifndef PIC_DEP_NACC
+#define PIC_DEP_NACC 2
+#endif
+constexpr int NACC = PIC_DEP_NACC;               // independent MMA accumulator sets
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (TILE3 * 80 + WARPS * WBUF);
 
 struct MoverTArgs {
@@ -333,6 +341,12 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
 }
 
 // --------------------------------------------------------------- deposit ----
+// word offset of column k (0..7) of row p in a swizzled 8-double staging row
+__device__ __forceinline__ int stage_slot(int p, int k) {
+  const int h = ((p >> 2) & 1) | (((p >> 1) & 1) << 1);
+  return p * 8 + ((((k >> 1) ^ h) << 1) | (k & 1));
+}
+
 __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const DepositArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *cacc = reinterpret_cast<double *>(smem_raw);  // [64 cells][8 corners][10]
@@ -369,26 +383,37 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   }
   const uint32_t wbeg = coff[cbeg];
   const uint32_t wend = coff[cend];
-  double *Sb = wbuf + warp * WBUF;       // [8 groups][36]: S[k][j] at grp*36 + k*4 + j
-  double *Vb = Sb + 8 * SGRP;            // [32][10]
-  const int kc = lane & 7, js = lane >> 3;
-  double accr[10];
+  double *Ss = wbuf + warp * WBUF;       // [32][8] swizzled
+  double *Vs = Ss + 32 * 8;              // [32][8] swizzled, moments 0..7
+  double *V2 = Vs + 32 * 8;              // [32][2], moments 8, 9
+  // Per cell, the corner sums are a matrix product over its particles:
+  //   M[corner][moment] = sum_p S[p][corner] V[p][moment]      (Eq. 3)
+  // done on the fp64 tensor cores with mma.m8n8k4 (M = 8 corners, K = 4
+  // particles per step, N = 8 + 8 moments, the second tile using 2 columns).
+  // Fragments: lane (g = lane / 4, j = lane % 4) supplies A[g][j] = S[4t+j][g],
+  // B[j][g] = V[4t+j][g] (and V2[4t+j][g]) and holds C[g][2j], C[g][2j+1].
+  // Step t accumulates into set t % NACC, so consecutive MMAs are independent.
+  const int g8 = lane >> 2, j4 = lane & 3;
+  double c0[NACC][2], c1[NACC][2];
 #pragma unroll
-  for (int m = 0; m < 10; ++m) accr[m] = 0.0;
-  int cur = -1;  // local cell (0..63) of the register accumulators, warp-uniform
+  for (int a = 0; a < NACC; ++a) c0[a][0] = c0[a][1] = c1[a][0] = c1[a][1] = 0.0;
+  int cur = -1;  // local cell (0..63) of the accumulators, warp-uniform
 
   auto flush = [&](int c) {
 #pragma unroll
-    for (int m = 0; m < 10; ++m) {
-      accr[m] += __shfl_xor_sync(0xffffffffu, accr[m], 8);
-      accr[m] += __shfl_xor_sync(0xffffffffu, accr[m], 16);
+    for (int a = 1; a < NACC; ++a) {
+      c0[0][0] += c0[a][0]; c0[0][1] += c0[a][1];
+      c1[0][0] += c1[a][0]; c1[0][1] += c1[a][1];
     }
-    double *dst = cacc + (c * 8 + kc) * 10;
+    double *dst = cacc + (c * 8 + g8) * 10;
+    *reinterpret_cast<double2 *>(dst + 2 * j4) = make_double2(c0[0][0], c0[0][1]);
+    if (j4 == 0) *reinterpret_cast<double2 *>(dst + 8) = make_double2(c1[0][0], c1[0][1]);
 #pragma unroll
-    for (int m = 0; m < 10; ++m) {
-      if ((m & 3) == js) dst[m] = accr[m];
-      accr[m] = 0.0;
-    }
+    for (int a = 0; a < NACC; ++a) c0[a][0] = c0[a][1] = c1[a][0] = c1[a][1] = 0.0;
+  };
+  auto mma = [](double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
   };
 
   // two-stage software pipeline: the sources of round r+1 and the perm/key of
@@ -449,18 +474,17 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
       Sk[0] = gx * w00; Sk[1] = fx * w00; Sk[2] = gx * w10; Sk[3] = fx * w10;
       Sk[4] = gx * w01; Sk[5] = fx * w01; Sk[6] = gx * w11; Sk[7] = fx * w11;
     }
-    {
-      const int grp = lane >> 2, j = lane & 3;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) Sb[grp * SGRP + k * 4 + j] = Sk[k];
-#pragma unroll
-      for (int m = 0; m < 10; m += 2)
-        *reinterpret_cast<double2 *>(Vb + lane * 10 + m) = make_double2(val[m], val[m + 1]);
+    for (int k = 0; k < 8; k += 2) {
+      const int o = stage_slot(lane, k);
+      *reinterpret_cast<double2 *>(Ss + o) = make_double2(Sk[k], Sk[k + 1]);
+      *reinterpret_cast<double2 *>(Vs + o) = make_double2(val[k], val[k + 1]);
     }
+    *reinterpret_cast<double2 *>(V2 + 2 * lane) = make_double2(val[8], val[9]);
     __syncwarp();
     // runs of equal cells in the round (the order is sorted, so a round holds
-    // a few contiguous runs); each run accumulates into the register sums of
-    // its cell, the sums being flushed when the cell changes
+    // a few contiguous runs); each run accumulates into the fragments of its
+    // cell, which are flushed when the cell changes
     const unsigned navail = min(32u, wend - r0);
     const int cprev = __shfl_up_sync(0xffffffffu, c, 1);
     unsigned starts = __ballot_sync(0xffffffffu, (unsigned)lane < navail && (lane == 0 || c != cprev));
@@ -474,30 +498,22 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
         cur = rc;
       }
       if (b == 0 && e == 32) {
-        // the whole round is one cell: straight-line, loads of all groups in flight
+        // the round is one cell: 8 steps, no masking
 #pragma unroll
-        for (int grp = 0; grp < 8; ++grp) {
-          const double s = Sb[grp * SGRP + kc * 4 + js];
-          const double *vv = Vb + (grp * 4 + js) * 10;
-#pragma unroll
-          for (int m = 0; m < 10; m += 2) {
-            const double2 t = *reinterpret_cast<const double2 *>(vv + m);
-            accr[m] = fma(s, t.x, accr[m]);
-            accr[m + 1] = fma(s, t.y, accr[m + 1]);
-          }
+        for (int t = 0; t < 8; ++t) {
+          const int pi = 4 * t + j4;
+          const int o = stage_slot(pi, g8);
+          mma(c0[t % NACC], Ss[o], Vs[o]);
+          mma(c1[t % NACC], Ss[o], V2[2 * pi + (g8 & 1)]);
         }
       } else {
-#pragma unroll 2
-        for (int grp = b >> 2; grp * 4 < e; ++grp) {
-          const int idx = grp * 4 + js;
-          const double s = (idx >= b && idx < e) ? Sb[grp * SGRP + kc * 4 + js] : 0.0;
-          const double *vv = Vb + idx * 10;
-#pragma unroll
-          for (int m = 0; m < 10; m += 2) {
-            const double2 t = *reinterpret_cast<const double2 *>(vv + m);
-            accr[m] = fma(s, t.x, accr[m]);
-            accr[m + 1] = fma(s, t.y, accr[m + 1]);
-          }
+        // steps overlapping the run [b, e), particles outside it masked
+        for (int t = b >> 2; 4 * t < e; ++t) {
+          const int pi = 4 * t + j4;
+          const int o = stage_slot(pi, g8);
+          const double a = (pi >= b && pi < e) ? Ss[o] : 0.0;
+          mma(c0[0], a, Vs[o]);
+          mma(c1[0], a, V2[2 * pi + (g8 & 1)]);
         }
       }
     }
@@ -507,32 +523,25 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   __syncthreads();
 
   // corner sums -> node sums of the tile (each node gathers its <= 8 cells)
-  // -> global moments (tile faces are shared with neighbour tiles: atomics)
-  for (int i = tid; i < MB3; i += THREADS) {
-    const int bx = i % MB, by = (i / MB) % MB, bz = i / (MB * MB);
-    double v[10];
-#pragma unroll
-    for (int m = 0; m < 10; ++m) v[m] = 0.0;
+  // -> global moments (tile faces are shared with neighbour tiles: atomics);
+  // one (node, moment) pair per thread
+  for (int i = tid; i < MB3 * 10; i += THREADS) {
+    const int n = i / 10, m = i - 10 * n;
+    const int bx = n % MB, by = (n / MB) % MB, bz = n / (MB * MB);
+    double v = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int cx = bx - (k & 1), cy = by - ((k >> 1) & 1), cz = bz - (k >> 2);
       if (cx < 0 || cx >= TILE || cy < 0 || cy >= TILE || cz < 0 || cz >= TILE) continue;
-      const double *src = cacc + ((cx + TILE * (cy + TILE * cz)) * 8 + k) * 10;
-#pragma unroll
-      for (int m = 0; m < 10; ++m) v[m] += src[m];
+      v += cacc[((cx + TILE * (cy + TILE * cz)) * 8 + k) * 10 + m];
     }
-    double vsum = 0.0;
-#pragma unroll
-    for (int m = 0; m < 10; ++m) vsum += fabs(v[m]);
-    if (vsum == 0.0) continue;
+    if (v == 0.0) continue;
     const int64_t node = moment_node(g, ox + bx, oy + by, oz + bz);
     if (node < 0) {
-      atomicAdd(&A.stats[ST_FAR], 1ull);
+      if (m == 0) atomicAdd(&A.stats[ST_FAR], 1ull);
       continue;
     }
-#pragma unroll
-    for (int m = 0; m < 10; ++m)
-      if (v[m] != 0.0) atomicAdd(A.mom + m * g.m_plane + node, v[m]);
+    atomicAdd(A.mom + m * g.m_plane + node, v);
   }
 }
 
