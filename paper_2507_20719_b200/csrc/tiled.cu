@@ -394,6 +394,13 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   // B[j][g] = V[4t+j][g] (and V2[4t+j][g]) and holds C[g][2j], C[g][2j+1].
   // Step t accumulates into set t % NACC, so consecutive MMAs are independent.
   const int g8 = lane >> 2, j4 = lane & 3;
+  // lane-constant staging offsets: row writes (column pairs 0..3 of row lane)
+  // and fragment reads (row 4t + j4, column g8: even / odd t)
+  int wslot[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) wslot[k] = stage_slot(lane, 2 * k);
+  const int rs0 = stage_slot(j4, g8), rs1 = stage_slot(4 + j4, g8) - 32;
+  const int v2off = 2 * j4 + (g8 & 1);
   double c0[NACC][2], c1[NACC][2];
 #pragma unroll
   for (int a = 0; a < NACC; ++a) c0[a][0] = c0[a][1] = c1[a][0] = c1[a][1] = 0.0;
@@ -449,14 +456,10 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
       k_n2 = A.key[p + 64];
       p_n2 = A.perm[p + 64];
     }
-    int c = 64;  // sentinel: no particle
+    // inactive lanes carry zeros (q = 0: every value is 0, the weights finite)
+    const int c = act ? (int)(k_cur & (TILE3 - 1)) : 64;   // 64: sentinel, no particle
     double Sk[8], val[10];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) Sk[k] = 0.0;
-#pragma unroll
-    for (int m = 0; m < 10; ++m) val[m] = 0.0;
-    if (act) {
-      c = (int)(k_cur & (TILE3 - 1));
+    {
       const double x = s_cur[0], y = s_cur[1], z = s_cur[2];
       const double u = s_cur[3], v = s_cur[4], w = s_cur[5], q = s_cur[6];
       // values q {1, v, vv} (Eq. 3, R16 order)
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
     }
 #pragma unroll
     for (int k = 0; k < 8; k += 2) {
-      const int o = stage_slot(lane, k);
+      const int o = wslot[k >> 1];
       *reinterpret_cast<double2 *>(Ss + o) = make_double2(Sk[k], Sk[k + 1]);
       *reinterpret_cast<double2 *>(Vs + o) = make_double2(val[k], val[k + 1]);
     }
@@ -501,19 +504,18 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
         // the round is one cell: 8 steps, no masking
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const int pi = 4 * t + j4;
-          const int o = stage_slot(pi, g8);
+          const int o = 32 * t + ((t & 1) ? rs1 : rs0);
           mma(c0[t % NACC], Ss[o], Vs[o]);
-          mma(c1[t % NACC], Ss[o], V2[2 * pi + (g8 & 1)]);
+          mma(c1[t % NACC], Ss[o], V2[8 * t + v2off]);
         }
       } else {
         // steps overlapping the run [b, e), particles outside it masked
         for (int t = b >> 2; 4 * t < e; ++t) {
           const int pi = 4 * t + j4;
-          const int o = stage_slot(pi, g8);
+          const int o = 32 * t + ((t & 1) ? rs1 : rs0);
           const double a = (pi >= b && pi < e) ? Ss[o] : 0.0;
           mma(c0[0], a, Vs[o]);
-          mma(c1[0], a, V2[2 * pi + (g8 & 1)]);
+          mma(c1[0], a, V2[8 * t + v2off]);
         }
       }
     }
