@@ -308,9 +308,29 @@ __device__ __forceinline__ uint32_t tile_key32(const Geom &g, uint32_t lx, uint3
 // Boundary conditions (R10, R11, R21) of a pushed particle and its destination
 // key.  xnew: in = pre-wrap position (cell units), out = post-wrap position.
 // Non-finite values fail the range tests, so the finiteness check only runs on
-// the rare flagged path.
+// the rare flagged path.  Fast path: the particle is still inside this rank's
+// slab and the domain (no wrap, no leaver, no open face) and outside the planet,
+// which is every particle but the few that cross a face this step.
 __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3], const double vnew[3],
                                                    bool clamped, unsigned long long *__restrict__ stats) {
+  if (xnew[0] >= (double)g.slab_lo && xnew[0] < (double)g.slab_hi && xnew[1] >= 0.0 &&
+      xnew[1] < (double)g.ncell[1] && xnew[2] >= 0.0 && xnew[2] < (double)g.ncell[2]) {
+    bool hit = false;
+    if (g.has_planet) {
+      double r2 = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double dx = (xnew[d] - g.planet_c[d]) * g.delta[d];
+        r2 += dx * dx;
+      }
+      hit = r2 < g.planet_r2;
+    }
+    if (!hit) {
+      if (clamped) atomicAdd(&stats[ST_CLAMPED], 1ull);
+      const int cx = (int)xnew[0], cy = (int)xnew[1], cz = (int)xnew[2];
+      return tile_key32(g, (uint32_t)(cx - (int)g.slab_lo), (uint32_t)cy, (uint32_t)cz);
+    }
+  }
   const double x_pre = xnew[0];
   bool bad = false, out = false;
 #pragma unroll

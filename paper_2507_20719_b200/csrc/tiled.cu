@@ -45,7 +45,10 @@ constexpr int MB = TILE + 1;            // deposit nodes per axis: 0 .. TILE
 constexpr int MB3 = MB * MB * MB;       // 125
 constexpr int WARPS = 8;
 constexpr int THREADS = 32 * WARPS;
-constexpr int SRC_STAGES = 3;    // mover: rounds of gathered sources in flight (ring)
+#ifndef PIC_SRC_STAGES
+#define PIC_SRC_STAGES 2
+#endif
+constexpr int SRC_STAGES = PIC_SRC_STAGES;   // mover: rounds of gathered sources in flight (ring)
 constexpr int PK_SLOTS = 6;      // mover: perm/key ring slots
 constexpr int PK_AHEAD = 5;      // mover: perm/key fetched this many rounds ahead
 constexpr int MOVER_WARP_STAGE = SRC_STAGES * 8 * 32 + PK_SLOTS * 2 * 32 / 2;  // doubles per warp
