@@ -62,7 +62,14 @@ constexpr int WBUF = 32 * 8 * 2 + 32 * 2;
 #define PIC_DEP_NACC 2
 #endif
 constexpr int NACC = PIC_DEP_NACC;               // independent MMA accumulator sets
-constexpr size_t DEPOSIT_SMEM = sizeof(double) * (TILE3 * 80 + WARPS * WBUF);
+#ifndef PIC_DEP_WARPS
+#define PIC_DEP_WARPS 8
+#endif
+#ifndef PIC_DEP_MINB
+#define PIC_DEP_MINB 3
+#endif
+constexpr int DWARPS = PIC_DEP_WARPS, DTHREADS = 32 * DWARPS;   // deposit CTA (one tile)
+constexpr size_t DEPOSIT_SMEM = sizeof(double) * (MB3 * 10 + DWARPS * WBUF);
 
 struct MoverTArgs {
   Geom g;
@@ -350,10 +357,10 @@ __device__ __forceinline__ int stage_slot(int p, int k) {
   return p * 8 + ((((k >> 1) ^ h) << 1) | (k & 1));
 }
 
-__global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const DepositArgs A) {
+__global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(const DepositArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double *cacc = reinterpret_cast<double *>(smem_raw);  // [64 cells][8 corners][10]
-  double *wbuf = cacc + TILE3 * 80;
+  double *nacc = reinterpret_cast<double *>(smem_raw);  // node sums of the tile box [MB^3][10]
+  double *wbuf = nacc + MB3 * 10;
   const Geom &g = A.g;
   const int tile = blockIdx.x;
   const uint32_t *coff = A.cell_off + (int64_t)tile * TILE3;   // 65 offsets of this tile's cells
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   const int tz = (int)(tile / (g.nt[0] * g.nt[1]));
   const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE, oz = (int64_t)tz * TILE;
   const int tid = threadIdx.x;
-  for (int i = tid; i < TILE3 * 80; i += THREADS) cacc[i] = 0.0;
+  for (int i = tid; i < MB3 * 10; i += DTHREADS) nacc[i] = 0.0;
   __syncthreads();
 
   // warp ranges are aligned to cell boundaries, so every cell belongs to one
@@ -373,15 +380,15 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   const uint32_t ntile = p1 - p0;
   int cbeg = 0, cend = 0;
   {
-    const uint32_t t0 = p0 + (uint32_t)(((uint64_t)ntile * warp) / WARPS);
-    const uint32_t t1 = p0 + (uint32_t)(((uint64_t)ntile * (warp + 1)) / WARPS);
+    const uint32_t t0 = p0 + (uint32_t)(((uint64_t)ntile * warp) / DWARPS);
+    const uint32_t t1 = p0 + (uint32_t)(((uint64_t)ntile * (warp + 1)) / DWARPS);
     // first cell starting at or after the target (lane-parallel search over 64 cells)
     const uint32_t o0 = coff[lane], o1 = coff[lane + 32];
     const unsigned b0a = __ballot_sync(0xffffffffu, o0 >= t0), b0b = __ballot_sync(0xffffffffu, o1 >= t0);
     const unsigned b1a = __ballot_sync(0xffffffffu, o0 >= t1), b1b = __ballot_sync(0xffffffffu, o1 >= t1);
     cbeg = b0a ? __ffs(b0a) - 1 : (b0b ? 32 + __ffs(b0b) - 1 : TILE3);
     cend = b1a ? __ffs(b1a) - 1 : (b1b ? 32 + __ffs(b1b) - 1 : TILE3);
-    if (warp == WARPS - 1) cend = TILE3;
+    if (warp == DWARPS - 1) cend = TILE3;
     if (warp == 0) cbeg = 0;
   }
   const uint32_t wbeg = coff[cbeg];
@@ -415,9 +422,17 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
       c0[0][0] += c0[a][0]; c0[0][1] += c0[a][1];
       c1[0][0] += c1[a][0]; c1[0][1] += c1[a][1];
     }
-    double *dst = cacc + (c * 8 + g8) * 10;
-    *reinterpret_cast<double2 *>(dst + 2 * j4) = make_double2(c0[0][0], c0[0][1]);
-    if (j4 == 0) *reinterpret_cast<double2 *>(dst + 8) = make_double2(c1[0][0], c1[0][1]);
+    // corner g8 of cell c is node (cx + gx, cy + gy, cz + gz) of the tile box;
+    // cells of different warps share nodes, hence shared-memory atomics (one
+    // flush per cell and warp: rare next to the per-particle work)
+    const int node = ((c & 3) + (g8 & 1)) + MB * ((((c >> 2) & 3) + ((g8 >> 1) & 1)) + MB * ((c >> 4) + (g8 >> 2)));
+    double *dst = nacc + node * 10;
+    atomicAdd(dst + 2 * j4, c0[0][0]);
+    atomicAdd(dst + 2 * j4 + 1, c0[0][1]);
+    if (j4 == 0) {
+      atomicAdd(dst + 8, c1[0][0]);
+      atomicAdd(dst + 9, c1[0][1]);
+    }
 #pragma unroll
     for (int a = 0; a < NACC; ++a) c0[a][0] = c0[a][1] = c1[a][0] = c1[a][1] = 0.0;
   };
@@ -427,7 +442,8 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   };
 
   // two-stage software pipeline: the sources of round r+1 and the perm/key of
-  // round r+2 are in flight while round r is reduced
+  // round r+2 are in flight while round r is reduced.  Lanes past the end load
+  // position 0 (always valid) and get q = 0 below, so the loads need no predicate.
   uint32_t k_nx = 0, p_nx = 0, k_n2 = 0, p_n2 = 0;
   double s_nx[7];
   {
@@ -441,7 +457,7 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
       p_n2 = A.perm[p + 32];
     }
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s_nx[k] = (p < wend) ? A.src[k][p_nx] : 0.0;
+    for (int k = 0; k < 7; ++k) s_nx[k] = A.src[k][p_nx];
   }
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
@@ -454,7 +470,8 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
     k_nx = k_n2;
     p_nx = p_n2;
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s_nx[k] = (p + 32 < wend) ? A.src[k][p_nx] : 0.0;
+    for (int k = 0; k < 7; ++k) s_nx[k] = A.src[k][p_nx];
+    p_n2 = 0;
     if (p + 64 < wend) {
       k_n2 = A.key[p + 64];
       p_n2 = A.perm[p + 64];
@@ -464,7 +481,7 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
     double Sk[8], val[10];
     {
       const double x = s_cur[0], y = s_cur[1], z = s_cur[2];
-      const double u = s_cur[3], v = s_cur[4], w = s_cur[5], q = s_cur[6];
+      const double u = s_cur[3], v = s_cur[4], w = s_cur[5], q = act ? s_cur[6] : 0.0;
       // values q {1, v, vv} (Eq. 3, R16 order)
       const double qu = q * u, qv = q * v, qw = q * w;
       val[0] = q; val[1] = qu; val[2] = qv; val[3] = qw;
@@ -527,19 +544,12 @@ __global__ void __launch_bounds__(THREADS, 2) deposit_tiled_kernel(const Deposit
   if (cur >= 0) flush(cur);
   __syncthreads();
 
-  // corner sums -> node sums of the tile (each node gathers its <= 8 cells)
-  // -> global moments (tile faces are shared with neighbour tiles: atomics);
-  // one (node, moment) pair per thread
-  for (int i = tid; i < MB3 * 10; i += THREADS) {
+  // node sums of the tile -> global moments (tile faces are shared with
+  // neighbour tiles: atomics); one (node, moment) pair per thread
+  for (int i = tid; i < MB3 * 10; i += DTHREADS) {
     const int n = i / 10, m = i - 10 * n;
     const int bx = n % MB, by = (n / MB) % MB, bz = n / (MB * MB);
-    double v = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int cx = bx - (k & 1), cy = by - ((k >> 1) & 1), cz = bz - (k >> 2);
-      if (cx < 0 || cx >= TILE || cy < 0 || cy >= TILE || cz < 0 || cz >= TILE) continue;
-      v += cacc[((cx + TILE * (cy + TILE * cz)) * 8 + k) * 10 + m];
-    }
+    const double v = nacc[i];
     if (v == 0.0) continue;
     const int64_t node = moment_node(g, ox + bx, oy + by, oz + bz);
     if (node < 0) {
@@ -651,7 +661,7 @@ pic_status launch_tiled_deposit(Ctx *ctx, int s) {
   A.cell_off = sp.cell_off;
   A.mom = sp.mom;
   A.stats = ctx->stats;
-  deposit_tiled_kernel<<<(unsigned)ctx->geom.ntiles, THREADS, DEPOSIT_SMEM, ctx->stream>>>(A); ++ctx->launches;
+  deposit_tiled_kernel<<<(unsigned)ctx->geom.ntiles, DTHREADS, DEPOSIT_SMEM, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }
