@@ -49,18 +49,31 @@ __global__ void total_kernel(const uint32_t *__restrict__ cell_count, uint32_t *
     tot[c] = cell_count[c] + cell_count[ncells + 1 + c];
 }
 
+constexpr int PERM_UNROLL = 4;
+
 __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t *__restrict__ rank,
                             const uint32_t *__restrict__ cell_off, const uint32_t *__restrict__ cell_count,
                             const int64_t *__restrict__ d_nraw, uint32_t *__restrict__ perm,
                             uint32_t *__restrict__ key) {
+  // PERM_UNROLL independent elements per thread and iteration (memory-level
+  // parallelism for the dependent cell_off gather)
   const int64_t n = *d_nraw;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = key_new[p];
-    if (k >= KEY_FIRST_RESERVED) continue;
-    const uint32_t r = rank[p];
-    const uint32_t q = cell_off[k] + ((r & RANK_ARRIVAL) ? cell_count[k] + (r & ~RANK_ARRIVAL) : r);
-    perm[q] = (uint32_t)p;
-    key[q] = k;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p0 < n; p0 += PERM_UNROLL * stride) {
+    uint32_t k[PERM_UNROLL], r[PERM_UNROLL];
+#pragma unroll
+    for (int u = 0; u < PERM_UNROLL; ++u) {
+      const int64_t p = p0 + u * stride;
+      k[u] = p < n ? key_new[p] : KEY_DEAD;
+      r[u] = p < n ? rank[p] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < PERM_UNROLL; ++u) {
+      if (k[u] >= KEY_FIRST_RESERVED) continue;
+      const uint32_t q = cell_off[k[u]] + ((r[u] & RANK_ARRIVAL) ? cell_count[k[u]] + (r[u] & ~RANK_ARRIVAL) : r[u]);
+      perm[q] = (uint32_t)(p0 + u * stride);
+      key[q] = k[u];
+    }
   }
 }
 

@@ -162,9 +162,9 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
   const double w00 = gy0 * gz0, w10 = f[1] * gz0, w01 = gy0 * f[2], w11 = f[1] * f[2];
   const double S[8] = {gx0 * w00, f[0] * w00, gx0 * w10, f[0] * w10,
                        gx0 * w01, f[0] * w01, gx0 * w11, f[0] * w11};
+  const int base = ((i[2] * NB + i[1]) * NB + i[0]) * 6;
 #pragma unroll
   for (int m = 0; m < 6; ++m) out[m] = 0.0;
-  const int base = ((i[2] * NB + i[1]) * NB + i[0]) * 6;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int off = base + 6 * ((c & 1) + NB * ((c >> 1) & 1) + NB * NB * (c >> 2));
@@ -187,7 +187,10 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
 #endif
 // NIT > 0: the iteration count is a compile-time constant (fully unrolled);
 // NIT == 0: runtime A.n_iter.
-constexpr int MOVER_WARPS = 8;
+#ifndef PIC_MOVER_WARPS
+#define PIC_MOVER_WARPS 8
+#endif
+constexpr int MOVER_WARPS = PIC_MOVER_WARPS;
 constexpr int MOVER_THREADS = 32 * MOVER_WARPS;
 constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + MOVER_WARPS * MOVER_WARP_STAGE) + 16;
 
