@@ -156,7 +156,11 @@ PIC_API pic_status pic_get_particles(pic_ctx *ctx, int32_t s, double *const xyzu
  *   x: [slab_lo - G, slab_hi + G],  y: [-G, ncell_y + G],  z: [-G, ncell_z + G]
  * i.e. (slab_hi - slab_lo + 1 + 2G) x (ncell_y + 1 + 2G) x (ncell_z + 1 + 2G)
  * nodes, periodic images replicated by the caller (R10, R11).  Copied into
- * the context (the caller's buffer may be reused after the next pic_sync).   */
+ * the context (the caller's buffer may be reused after the next pic_sync).
+ * Double-buffered: the copy goes to the buffer the NEXT pic_mover reads, on
+ * an internal copy stream, so a host-to-device copy of the next cycle's
+ * fields overlaps the current cycle (fields on the host for
+ * discrete GPUs); a device source is first ordered after the context stream. */
 PIC_API pic_status pic_set_fields(pic_ctx *ctx, const double *EB);
 
 /* Advance species s (-1 = all) one cycle with Eq. 2 (R1-R3, R7-R9), then
@@ -196,6 +200,17 @@ PIC_API pic_status pic_get_moments(pic_ctx *ctx, int32_t s, double *out);
  * [5] non-finite, [6] capacity overflow, [7] multi-wrap.  stats may be NULL.
  * Returns the first latched device error as a status.                        */
 PIC_API pic_status pic_sync(pic_ctx *ctx, int64_t stats[8]);
+
+/* Asynchronous pic_get_moments: the moments of species s are packed on the
+ * context stream into one of two staging slots of the species and copied to
+ * `out` (pinned host or device) on the internal copy stream, overlapping the
+ * next cycle.  `out` is complete after pic_join_copies followed by a
+ * synchronisation of the context stream, or after pic_sync.                  */
+PIC_API pic_status pic_get_moments_async(pic_ctx *ctx, int32_t s, double *out);
+
+/* Make the context stream wait (on the device, no host block) for every copy
+ * enqueued by pic_get_moments_async / pic_set_fields so far.                 */
+PIC_API pic_status pic_join_copies(pic_ctx *ctx);
 
 /* Transport in use: PIC_TRANSPORT_PEER or PIC_TRANSPORT_NCCL when nranks > 1
  * (AUTO resolved at pic_init), PIC_TRANSPORT_AUTO for a single rank.        */

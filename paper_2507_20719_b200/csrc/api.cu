@@ -136,7 +136,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
     }
   }
   int64_t field_elems = g.f_n[0] * g.f_n[1] * g.f_n[2] * 6;
-  int64_t ofield = L.take(8 * field_elems);
+  int64_t ofield[2] = {L.take(8 * field_elems), L.take(8 * field_elems)};
   int64_t ostats = L.take(8 * ST_N);
   int64_t ocounts = L.take(8 * 64);
   int64_t opeer = L.take(sizeof(PeerCtl));
@@ -149,9 +149,13 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   for (int k = 0; k < 4; ++k) om[k] = L.take(multi ? 8 * 8 * mig_cap * c->n_species : 8);
   const int64_t pack_elems = (g.k_n[0] + 1) * g.m_n[1] * g.m_n[2] * 10;
   int64_t opack = L.take(8 * pack_elems);
+  int64_t oslot[2 * PIC_MAX_SPECIES];
+  for (int k = 0; k < 2 * c->n_species; ++k) oslot[k] = L.take(8 * pack_elems);
   int64_t ocub = L.take((int64_t)cub_bytes);
   if (base) {
-    ctx->field = (double *)(base + ofield);
+    ctx->field_buf[0] = (double *)(base + ofield[0]);
+    ctx->field_buf[1] = (double *)(base + ofield[1]);
+    for (int k = 0; k < 2 * c->n_species; ++k) ctx->pack_slot[k] = (double *)(base + oslot[k]);
     ctx->field_elems = field_elems;
     ctx->stats = (unsigned long long *)(base + ostats);
     ctx->dev_counts = (int64_t *)(base + ocounts);
@@ -237,7 +241,20 @@ pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
   if (e != cudaSuccess) { delete ctx; return PIC_ECUDA; }
   e = cudaMemset(ctx->stats, 0, 8 * ST_N);
   if (e != cudaSuccess) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_ECUDA; }
-  e = cudaMemset(ctx->field, 0, 8 * ctx->field_elems);
+  e = cudaMemset(ctx->field_buf[0], 0, 8 * ctx->field_elems);
+  if (e == cudaSuccess) e = cudaMemset(ctx->field_buf[1], 0, 8 * ctx->field_elems);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&ctx->field_ready[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->field_free[k], cudaEventDisableTiming);
+  }
+  for (int k = 0; k < 2 * cfg->n_species && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&ctx->slot_packed[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->slot_free[k], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->copies_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fields_done, cudaEventDisableTiming);
   if (e != cudaSuccess) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_ECUDA; }
   if (cfg->nranks > 1) {
     if (!nccl_id) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_EINVAL; }
@@ -312,7 +329,22 @@ pic_status pic_get_particles(pic_ctx *p, int32_t s, double *const xyzuvwq[7], in
 pic_status pic_set_fields(pic_ctx *p, const double *EB) {
   if (!p || !EB) return PIC_EINVAL;
   Ctx *ctx = C(p);
-  PIC_CUDA(cudaMemcpyAsync(ctx->field, EB, 8 * ctx->field_elems, cudaMemcpyDefault, ctx->stream));
+  // into the buffer the next mover will read, on the copy stream, once the
+  // mover that last read that buffer is done (double buffering: the copy of
+  // the next cycle's fields overlaps the current cycle)
+  const int b = ctx->field_cur ^ 1;
+  PIC_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, ctx->field_free[b], 0));
+  // a device source may be produced by work on the caller's stream: order the
+  // copy after it (host sources need no ordering and overlap the cycle)
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, EB) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
+    PIC_CUDA(cudaEventRecord(ctx->field_ready[b], ctx->stream));
+    PIC_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, ctx->field_ready[b], 0));
+  }
+  cudaGetLastError();
+  PIC_CUDA(cudaMemcpyAsync(ctx->field_buf[b], EB, 8 * ctx->field_elems, cudaMemcpyDefault, ctx->h2d_stream));
+  PIC_CUDA(cudaEventRecord(ctx->field_ready[b], ctx->h2d_stream));
+  ctx->field_new = true;
   ctx->fields_set = true;
   return PIC_OK;
 }
@@ -327,12 +359,19 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
   for (int k = s0; k < s1; ++k)
     if (ctx->sp[k].moved || !ctx->sp[k].order_valid)
       return fail(ctx, PIC_ESTATE, "pic_mover called twice without pic_exchange");
+  if (ctx->field_new) {
+    ctx->field_cur ^= 1;
+    ctx->field_new = false;
+    PIC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->field_ready[ctx->field_cur], 0));
+  }
   for (int k = s0; k < s1; ++k) {
     st = use_tiled(ctx) ? launch_tiled_step(ctx, k) : launch_mover_basic(ctx, k);
     if (st != PIC_OK) return st;
     ctx->sp[k].moved = true;
     ctx->sp[k].deposited = false;
   }
+  // the field buffer may be refilled once these movers are done
+  PIC_CUDA(cudaEventRecord(ctx->field_free[ctx->field_cur], ctx->stream));
   // slab leavers go to their neighbour right after the mover (Alg. 1: the
   // particle communication follows the push), every species in one NCCL group
   // per message; the receiver deposits them like its own particles
@@ -420,6 +459,8 @@ pic_status pic_sync(pic_ctx *p, int64_t stats[8]) {
   if (!p) return PIC_EINVAL;
   Ctx *ctx = C(p);
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->h2d_stream));
   unsigned long long h[ST_N];
   PIC_CUDA(cudaMemcpy(h, ctx->stats, sizeof(h), cudaMemcpyDeviceToHost));
   int64_t all[ST_N];
@@ -435,6 +476,19 @@ pic_status pic_sync(pic_ctx *p, int64_t stats[8]) {
   if (all[ST_FAR] || all[ST_OVERFLOW] || all[ST_MULTIWRAP])
     return fail(ctx, PIC_ERANGE, "particle beyond ghost reach, capacity overflow or multiple wrap");
   return PIC_OK;
+}
+
+pic_status pic_get_moments_async(pic_ctx *p, int32_t s, double *out) {
+  if (!p || !out) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  return pack_moments_async(ctx, s, out);
+}
+
+pic_status pic_join_copies(pic_ctx *p) {
+  if (!p) return PIC_EINVAL;
+  return join_copies(C(p));
 }
 
 pic_status pic_get_transport(const pic_ctx *p, int32_t *out) {
@@ -489,6 +543,22 @@ const char *pic_last_error(const pic_ctx *p) {
 pic_status pic_destroy(pic_ctx *p) {
   if (!p) return PIC_EINVAL;
   Ctx *ctx = C(p);
+  cudaStreamSynchronize(ctx->stream);
+  for (cudaStream_t cs : {ctx->copy_stream, ctx->h2d_stream})
+    if (cs) {
+      cudaStreamSynchronize(cs);
+      cudaStreamDestroy(cs);
+    }
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->field_ready[k]) cudaEventDestroy(ctx->field_ready[k]);
+    if (ctx->field_free[k]) cudaEventDestroy(ctx->field_free[k]);
+  }
+  for (int k = 0; k < 2 * PIC_MAX_SPECIES; ++k) {
+    if (ctx->slot_packed[k]) cudaEventDestroy(ctx->slot_packed[k]);
+    if (ctx->slot_free[k]) cudaEventDestroy(ctx->slot_free[k]);
+  }
+  if (ctx->copies_done) cudaEventDestroy(ctx->copies_done);
+  if (ctx->fields_done) cudaEventDestroy(ctx->fields_done);
   peer_close(ctx);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
   for (auto &v : ctx->prof_ev)

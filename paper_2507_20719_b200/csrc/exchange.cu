@@ -382,6 +382,42 @@ __global__ void pack_moments_kernel(const double *__restrict__ mom, double *__re
   }
 }
 
+// Asynchronous copy-out: pack into one of the species' two staging slots on
+// the context stream, copy to `out` on the copy stream; the slot is reused
+// two calls later, after its copy completed.  `out` is valid after
+// pic_join_copies + a stream synchronisation, or pic_sync.
+pic_status pack_moments_async(Ctx *ctx, int s, double *out) {
+  const Geom &g = ctx->geom;
+  int64_t shape[3];
+  pic_moment_shape((const pic_ctx *)ctx, shape);
+  const double invV = 1.0 / (g.delta[0] * g.delta[1] * g.delta[2]);
+  const int64_t total = shape[0] * shape[1] * shape[2] * 10;
+  const int k = 2 * s + ctx->slot_next[s];
+  ctx->slot_next[s] ^= 1;
+  if (ctx->slot_used[k]) PIC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_free[k], 0));
+  pack_moments_kernel<<<grid_for(total), 256, 0, ctx->stream>>>(
+      ctx->sp[s].mom, ctx->pack_slot[k], g.G, shape[0], shape[1], shape[2], g.m_n[0], g.m_n[1], g.m_plane, invV); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  PIC_CUDA(cudaEventRecord(ctx->slot_packed[k], ctx->stream));
+  PIC_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->slot_packed[k], 0));
+  PIC_CUDA(cudaMemcpyAsync(out, ctx->pack_slot[k], sizeof(double) * total, cudaMemcpyDefault, ctx->copy_stream));
+  PIC_CUDA(cudaEventRecord(ctx->slot_free[k], ctx->copy_stream));
+  ctx->slot_used[k] = true;
+  ctx->copies_pending = true;
+  return PIC_OK;
+}
+
+// The context stream waits for every copy enqueued so far (no host block).
+pic_status join_copies(Ctx *ctx) {
+  PIC_CUDA(cudaEventRecord(ctx->fields_done, ctx->h2d_stream));
+  PIC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->fields_done, 0));
+  if (!ctx->copies_pending) return PIC_OK;
+  PIC_CUDA(cudaEventRecord(ctx->copies_done, ctx->copy_stream));
+  PIC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->copies_done, 0));
+  ctx->copies_pending = false;
+  return PIC_OK;
+}
+
 pic_status pack_moments(Ctx *ctx, int s, double *out) {
   const Geom &g = ctx->geom;
   int64_t shape[3];

@@ -119,7 +119,7 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   A.rank = S.rank;
   A.cell_count = S.cell_count;
   A.d_nraw = S.d_nraw;
-  A.F = ctx->field;
+  A.F = ctx->field();
   A.stats = ctx->stats;
   A.ks = S.qom * (ctx->geom.dt * 0.5);
   A.ks_c = A.ks / ctx->geom.c;

@@ -138,7 +138,22 @@ struct Ctx {
   Geom geom;
   cudaStream_t stream = nullptr;
   SpeciesStore sp[PIC_MAX_SPECIES];
-  double *field = nullptr;           // window
+  // field window, double-buffered: pic_set_fields copies into the buffer the
+  // next mover will use (on copy_stream) while the current one may still be read
+  double *field_buf[2] = {};
+  int field_cur = 0;                 // buffer of the last / next mover
+  bool field_new = false;            // pic_set_fields since the last mover: switch
+  cudaEvent_t field_ready[2] = {}, field_free[2] = {};
+  double *field() const { return field_buf[field_cur]; }
+  // asynchronous moment copy-out (pic_get_moments_async): 2 staging slots per species
+  cudaStream_t copy_stream = nullptr;   // device -> host moment copies
+  cudaStream_t h2d_stream = nullptr;    // field copies (separate: never queued behind a moment copy)
+  double *pack_slot[2 * PIC_MAX_SPECIES] = {};
+  cudaEvent_t slot_packed[2 * PIC_MAX_SPECIES] = {}, slot_free[2 * PIC_MAX_SPECIES] = {};
+  bool slot_used[2 * PIC_MAX_SPECIES] = {};
+  int slot_next[PIC_MAX_SPECIES] = {};
+  cudaEvent_t copies_done = nullptr, fields_done = nullptr;
+  bool copies_pending = false;
   int64_t field_elems = 0;
   bool fields_set = false;
   unsigned long long *stats = nullptr;  // ST_N device counters
@@ -171,7 +186,7 @@ struct Ctx {
   void *nccl = nullptr;              // ncclComm_t
   int64_t hstat[8] = {};             // host-side counters (sent / received)
   int64_t launches = 0;              // libpic kernel launches (pic_launch_count)
-  alignas(64) unsigned char tmap[128] = {};  // CUtensorMap of the field window (tiled.cu)
+  alignas(64) unsigned char tmap[2][128] = {};  // CUtensorMaps of the two field windows (tiled.cu)
   bool tmap_ok = false;
   int64_t cycle = 0;
   int64_t cap_max = 0;
@@ -248,6 +263,8 @@ pic_status peer_exchange(Ctx *ctx);
 pic_status recompute_keys(Ctx *ctx, int s, int64_t from, int64_t to);
 pic_status zero_moments(Ctx *ctx, int s);
 pic_status pack_moments(Ctx *ctx, int s, double *out);
+pic_status pack_moments_async(Ctx *ctx, int s, double *out);
+pic_status join_copies(Ctx *ctx);
 pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
 pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id);
 pic_status live_count(Ctx *ctx, int s, int64_t *n);

@@ -575,15 +575,17 @@ static pic_status make_tmap(Ctx *ctx) {
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const Geom &g = ctx->geom;
-  CUtensorMap *map = reinterpret_cast<CUtensorMap *>(ctx->tmap);
   cuuint64_t dims[4] = {6, (cuuint64_t)g.f_n[0], (cuuint64_t)g.f_n[1], (cuuint64_t)g.f_n[2]};
   cuuint64_t strides[3] = {48, (cuuint64_t)(48 * g.f_n[0]), (cuuint64_t)(48 * g.f_n[0] * g.f_n[1])};
   cuuint32_t box[4] = {6, NB, NB, NB};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)ctx->field, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
+  for (int b = 0; b < 2; ++b) {   // one map per field buffer
+    CUtensorMap *map = reinterpret_cast<CUtensorMap *>(ctx->tmap[b]);
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)ctx->field_buf[b], dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
+  }
 #define PIC_SET_SMEM(NIT) \
   PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM))
   PIC_SET_SMEM(0); PIC_SET_SMEM(1); PIC_SET_SMEM(2); PIC_SET_SMEM(3); PIC_SET_SMEM(4);
@@ -617,14 +619,14 @@ pic_status launch_tiled_step(Ctx *ctx, int s) {
   A.rank = sp.rank;
   A.cell_count = sp.cell_count;
   A.d_nraw = sp.d_nraw;
-  A.field = ctx->field;
+  A.field = ctx->field();
   A.stats = ctx->stats;
   A.ks = sp.qom * (ctx->geom.dt * 0.5);
   A.ks_c = A.ks / ctx->geom.c;
   A.n_iter = sp.n_iter;
   A.peer = ctx->peer;
   A.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
-  const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap);
+  const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap[ctx->field_cur]);
   const unsigned grid = (unsigned)ctx->geom.ntiles;
 #define PIC_LAUNCH(NIT) \
   mover_tiled_kernel<NIT><<<grid, MOVER_THREADS, MOVER_SMEM, ctx->stream>>>(tm, A)

@@ -33,7 +33,7 @@ STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "ove
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH):
         lib.pic_sync.argtypes = [vp, P(C.c_int64)]
         lib.pic_launch_count.argtypes = [vp, P(C.c_int64)]
         lib.pic_get_transport.argtypes = [vp, P(C.c_int32)]
+        lib.pic_get_moments_async.argtypes = [vp, C.c_int32, vp]
+        lib.pic_join_copies.argtypes = [vp]
         lib.pic_profile.argtypes = [vp, C.c_int32]
         lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
@@ -216,6 +218,18 @@ class Context:
             out = torch.empty((10, nz, ny, nx), dtype=torch.float64, device=device)
         _check(self.lib.pic_get_moments(self.h, s, _ptr(out)), self.h, "pic_get_moments")
         return out
+
+    def get_moments_async(self, s: int, out: torch.Tensor) -> torch.Tensor:
+        """Enqueue the copy-out of species s into `out` (pinned host or device);
+        complete after join_copies() + a stream synchronisation, or sync()."""
+        nx, ny, nz = self.moment_shape()
+        assert out.dtype == torch.float64 and out.numel() == 10 * nx * ny * nz and out.is_contiguous()
+        _check(self.lib.pic_get_moments_async(self.h, s, _ptr(out)), self.h, "pic_get_moments_async")
+        return out
+
+    def join_copies(self):
+        """The context stream waits (on the device) for all enqueued copies."""
+        _check(self.lib.pic_join_copies(self.h), self.h, "pic_join_copies")
 
     def sync(self, raise_on_error: bool = True) -> Dict[str, int]:
         st_arr = (C.c_int64 * 8)()

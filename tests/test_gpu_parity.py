@@ -177,3 +177,54 @@ def test_nonfinite_flag():
         ctx.sync()
     assert e.value.status == pic.PIC_ENONFINITE
     ctx.close()
+
+
+def test_field_sequence_and_async_moments():
+    """Fields change every cycle (double-buffered pic_set_fields from pinned host
+    and device sources) and moments come back through pic_get_moments_async;
+    the oracle runs the same field sequence."""
+    import copy
+    import oracle as O
+    wa = I.c1(randomized=True)
+    wb = copy.deepcopy(wa)
+    wb.field_params["B"] = tuple(2.0 * b for b in wa.field_params["B"])
+    wb.field_params["E"] = tuple(-3.0 * e for e in wa.field_params["E"])
+    seq = [wa, wb, wa, wb]
+    parts = I.make_species(wa, device="cpu")
+    # oracle
+    g = PU.oracle_grid(wa)
+    Fs = {id(w): PU.oracle_field(w, 2) for w in (wa, wb)}
+    orc = []
+    for s, sp in enumerate(wa.species):
+        P = PU.to_numpy_parts(parts[s])
+        st = np.zeros(len(P["x"]), dtype=np.int8)
+        for w in seq:
+            st, bad = O.mover(g, Fs[id(w)], sp.qom, wa.n_iter, P, st)
+            assert bad == 0
+        mom, am = O.moments(g, P, st)
+        orc.append((P, st, mom, am))
+    # GPU
+    cap = [int(p["x"].numel() * 1.25) + 64 for p in parts]
+    ctx = pic.Context(pic.make_config(wa, capacity=cap, kernel=pic.KERNEL_TILED))
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+    EB = {id(w): I.field_window(w, 2, device="cpu")[1] for w in (wa, wb)}
+    EB_pinned = {k: v.pin_memory() for k, v in EB.items()}
+    shape = ctx.moment_shape()
+    outs = [torch.empty((10, shape[2], shape[1], shape[0]), dtype=torch.float64).pin_memory()
+            for _ in wa.species]
+    for i, w in enumerate(seq):
+        ctx.set_fields(EB_pinned[id(w)] if i % 2 == 0 else EB[id(w)].cuda())
+        ctx.cycle()
+        for s in range(len(wa.species)):
+            ctx.get_moments_async(s, outs[s])
+    ctx.join_copies()
+    ctx.sync()
+    for s, sp in enumerate(wa.species):
+        gp = {k: v.cpu().numpy() for k, v in ctx.get_particles(s).items()}
+        rep = {"species": sp.name}
+        assert PU.compare_particles(wa, sp, gp, orc[s][0], orc[s][1], rep), rep
+        assert PU.compare_moments(outs[s].numpy(), orc[s][2], orc[s][3], rep), rep
+        # the synchronous copy-out agrees bit for bit
+        assert torch.equal(ctx.get_moments(s).cpu(), outs[s])
+    ctx.close()
