@@ -96,9 +96,11 @@ def test_c5_four_species_nonuniform_ppc(kernel):
     assert stats["removed"] > 0
 
 
-@pytest.mark.parametrize("n_iter", [1, 2, 5])
-def test_n_iter_variants(n_iter):
-    check(I.c1(randomized=True), 2, pic.KERNEL_TILED, n_iter=n_iter)
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("n_iter", [1, 2, 4, 5])
+def test_n_iter_variants(n_iter, kernel):
+    # 1, 2, 4: compile-time iteration counts of the tiled mover; 5: runtime count
+    check(I.c1(randomized=True), 2, kernel, n_iter=n_iter)
 
 
 def test_ragged_and_empty_species():
@@ -227,4 +229,65 @@ def test_field_sequence_and_async_moments():
         assert PU.compare_moments(outs[s].numpy(), orc[s][2], orc[s][3], rep), rep
         # the synchronous copy-out agrees bit for bit
         assert torch.equal(ctx.get_moments(s).cpu(), outs[s])
+    ctx.close()
+
+
+def _ctx_for(w, parts, kernel=pic.KERNEL_TILED, extra=64):
+    ctx = pic.Context(pic.make_config(w, capacity=[p["x"].numel() + extra for p in parts], kernel=kernel))
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+    ctx.set_fields(I.field_window(w, 2)[1].cuda())
+    return ctx
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_single_particle_and_sparse_tiles(kernel):
+    """One particle per species in a 16^3 box (63 of 64 tiles empty): parity."""
+    w = I.c1(randomized=True)
+    parts = I.make_species(w, device="cpu")
+    parts = [{k: v[1234:1235].contiguous() for k, v in p.items()} for p in parts]
+    orc = PU.run_oracle(w, parts, 3)
+    gpu, _ = run_gpu(w, parts, 3, kernel)
+    for s, sp in enumerate(w.species):
+        rep = {}
+        assert PU.compare_particles(w, sp, gpu[s][0], orc[s][0], orc[s][1], rep), rep
+        assert PU.compare_moments(gpu[s][1], orc[s][2], orc[s][3], rep), rep
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_multiple_wrap_is_an_error(kernel):
+    """R10: a particle that would wrap more than once in one step -> PIC_ERANGE."""
+    w = I.c1()
+    parts = I.make_species(w, device="cpu")
+    parts[0]["u"][7] = 3.0 * w.length[0] / w.dt     # three box lengths per step
+    ctx = _ctx_for(w, parts, kernel)
+    ctx.cycle()
+    with pytest.raises(pic.PicError) as e:
+        ctx.sync()
+    assert e.value.status == pic.PIC_ERANGE
+    ctx.close()
+
+
+def test_capacity_is_enforced():
+    w = I.c1()
+    parts = I.make_species(w, device="cpu")
+    ctx = pic.Context(pic.make_config(w, capacity=[10, 10]))
+    with pytest.raises(pic.PicError) as e:
+        ctx.set_particles(0, {k: v.cuda() for k, v in parts[0].items()})
+    assert e.value.status == pic.PIC_ERANGE
+    ctx.close()
+
+
+def test_open_boundary_removal_counts():
+    """C4 clone: particles leaving through open faces or into the planet are
+    removed; the live count plus the removed count is conserved."""
+    w = I.c4(ncell=(32, 16, 16), ppc=8)
+    parts = I.make_species(w, device="cpu")
+    n0 = sum(p["x"].numel() for p in parts)
+    ctx = _ctx_for(w, parts)
+    for _ in range(6):
+        ctx.cycle()
+    stats = ctx.sync()
+    n1 = sum(ctx.count(s) for s in range(len(parts)))
+    assert stats["removed"] > 0 and n1 + stats["removed"] == n0
     ctx.close()
