@@ -60,6 +60,9 @@ def _load():
         lib.oracle_mover.argtypes = [P(Grid), P(Field), C.c_double, C.c_int, C.c_int64,
                                      d, d, d, d, d, d, P(C.c_int8)]
         lib.oracle_mover.restype = C.c_int64
+        lib.oracle_mover_ex.argtypes = [P(Grid), P(Field), C.c_double, C.c_int, C.c_int, C.c_int64,
+                                        d, d, d, d, d, d, P(C.c_int8)]
+        lib.oracle_mover_ex.restype = C.c_int64
         lib.oracle_moments.argtypes = [P(Grid), C.c_int64, d, d, d, d, d, d, d, P(C.c_int8), d, d]
         lib.oracle_moments.restype = C.c_int64
         lib.oracle_node_counts.argtypes = [P(Grid), P(C.c_int64)]
@@ -114,16 +117,18 @@ def sample(g: Grid, F: FieldWindow, pos) -> np.ndarray:
     return out
 
 
-def mover(g: Grid, F: FieldWindow, qom: float, n_iter: int, parts: dict, status=None):
-    """Push one species in place.  parts: dict of float64 arrays x y z u v w."""
+def mover(g: Grid, F: FieldWindow, qom: float, n_iter: int, parts: dict, status=None,
+          relativistic: bool = False):
+    """Push one species in place.  parts: dict of float64 arrays x y z u v w.
+    relativistic: Eq. 2 with gamma (NEXT-1, readings R4/R5), else gamma == 1 (R3)."""
     n = len(parts["x"])
     if status is None:
         status = np.zeros(n, dtype=np.int8)
     for k in "xyzuvw":
         assert parts[k].dtype == np.float64 and parts[k].flags.c_contiguous
-    bad = _load().oracle_mover(C.byref(g), C.byref(F.c), float(qom), int(n_iter), n,
-                               *[_dptr(parts[k]) for k in "xyzuvw"],
-                               status.ctypes.data_as(C.POINTER(C.c_int8)))
+    bad = _load().oracle_mover_ex(C.byref(g), C.byref(F.c), float(qom), int(n_iter), int(bool(relativistic)), n,
+                                  *[_dptr(parts[k]) for k in "xyzuvw"],
+                                  status.ctypes.data_as(C.POINTER(C.c_int8)))
     return status, int(bad)
 
 

@@ -168,24 +168,85 @@ static int push_one(const oracle_grid *g, const oracle_field *F, double qom,
   return status;
 }
 
+/* Eq. 2, relativistic form (NEXT-1), one particle.
+ * Velocities v are stored; gamma = 1 / sqrt(1 - |v|^2 / c^2).
+ *   gn  <- gamma(vn) ; un <- gn vn ; gt <- gn   (R5: gamma-tilde starts at gamma^n)
+ *   xb  <- xn                                    (R1)
+ *   repeat n_iter times                          (R2)
+ *     (E,B) <- W(xb)                             (R12)
+ *     vt    <- gn vn + (q/m)(dt/2) E             (Eq. 2 line 3)
+ *     a     <- (dt/(2 gt)) Omega, Omega = (q/(m c)) B          (R8)
+ *     D     <- gt (1 + a.a)                      (R6)
+ *     vb    <- (vt + vt x a + (vt.a) a) / D      (Eq. 2 line 4; the GC term
+ *              with (dt/(2 gt))^2 (vt.Omega) Omega, R4's derived factor)
+ *     u1    <- 2 gt vb - gn vn ; g1 <- sqrt(1 + u1.u1 / c^2)   (R5)
+ *     gt    <- (gn + g1) / 2
+ *     xb    <- xn + vb dt/2
+ *   x^{n+1} <- xn + vb dt ; v^{n+1} <- u1 / g1   (Eq. 2 lines 1-2, R5)
+ *   boundary conditions.  |vn| >= c makes gn non-finite: ORACLE_BAD (R23). */
+static int push_one_rel(const oracle_grid *g, const oracle_field *F, double qom,
+                        int n_iter, double xn[3], double vn[3]) {
+  double c = g->c;
+  double v2 = vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2];
+  double gn = 1.0 / sqrt(1.0 - v2 / (c * c));
+  double gt = gn;
+  double xb[3] = {xn[0], xn[1], xn[2]};
+  double vb[3] = {vn[0], vn[1], vn[2]};
+  double u1[3] = {gn * vn[0], gn * vn[1], gn * vn[2]};
+  double g1 = gn;
+  for (int it = 0; it < n_iter; ++it) {
+    double EB[6];
+    oracle_sample(g, F, xb, EB);
+    double vt[3], a[3];
+    for (int d = 0; d < 3; ++d) vt[d] = gn * vn[d] + qom * (g->dt / 2.0) * EB[d];
+    for (int d = 0; d < 3; ++d) a[d] = (g->dt / (2.0 * gt)) * ((qom / c) * EB[3 + d]);
+    double cross[3];
+    cross[0] = vt[1] * a[2] - vt[2] * a[1];
+    cross[1] = vt[2] * a[0] - vt[0] * a[2];
+    cross[2] = vt[0] * a[1] - vt[1] * a[0];
+    double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
+    double D = gt * (1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2]));
+    for (int d = 0; d < 3; ++d) vb[d] = (vt[d] + cross[d] + dot * a[d]) / D;
+    for (int d = 0; d < 3; ++d) u1[d] = 2.0 * gt * vb[d] - gn * vn[d];
+    g1 = sqrt(1.0 + (u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2]) / (c * c));
+    gt = (gn + g1) / 2.0;
+    for (int d = 0; d < 3; ++d) xb[d] = xn[d] + vb[d] * (g->dt / 2.0);
+  }
+  for (int d = 0; d < 3; ++d) {
+    xn[d] = xn[d] + vb[d] * g->dt;
+    vn[d] = u1[d] / g1;
+  }
+  int status = apply_bc(g, xn);
+  for (int d = 0; d < 3; ++d)
+    if (!(vn[d] == vn[d]) || isinf(vn[d]) || !(xn[d] == xn[d])) status = ORACLE_BAD;
+  return status;
+}
+
 /* Mover over np particles of one species (SoA, updated in place).  status[p]
  * on entry: ORACLE_ALIVE particles are pushed, others are skipped.  Returns
  * the number of particles whose status became ORACLE_BAD.                   */
-int64_t oracle_mover(const oracle_grid *g, const oracle_field *F, double qom,
-                     int n_iter, int64_t np, double *x, double *y, double *z,
-                     double *u, double *v, double *w, int8_t *status) {
+int64_t oracle_mover_ex(const oracle_grid *g, const oracle_field *F, double qom,
+                        int n_iter, int relativistic, int64_t np, double *x, double *y,
+                        double *z, double *u, double *v, double *w, int8_t *status) {
   int64_t bad = 0;
   for (int64_t p = 0; p < np; ++p) {
     if (status[p] != ORACLE_ALIVE) continue;
     double xn[3] = {x[p], y[p], z[p]};
     double vn[3] = {u[p], v[p], w[p]};
-    int s = push_one(g, F, qom, n_iter, xn, vn);
+    int s = relativistic ? push_one_rel(g, F, qom, n_iter, xn, vn)
+                         : push_one(g, F, qom, n_iter, xn, vn);
     x[p] = xn[0]; y[p] = xn[1]; z[p] = xn[2];
     u[p] = vn[0]; v[p] = vn[1]; w[p] = vn[2];
     status[p] = (int8_t)s;
     if (s == ORACLE_BAD) ++bad;
   }
   return bad;
+}
+
+int64_t oracle_mover(const oracle_grid *g, const oracle_field *F, double qom,
+                     int n_iter, int64_t np, double *x, double *y, double *z,
+                     double *u, double *v, double *w, int8_t *status) {
+  return oracle_mover_ex(g, F, qom, n_iter, 0, np, x, y, z, u, v, w, status);
 }
 
 /* ----------------------------------------------------------- the moments -- */
