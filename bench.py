@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
     ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
+    ap.add_argument("--relativistic", action="store_true", help="relativistic Eq. 2 (NEXT-1) on the same workload")
     ap.add_argument("--ghost", type=int, default=2)
     ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
@@ -64,6 +65,9 @@ def workload(args, nranks, rank):
         w = I.c1()
         per = 16 // nranks
         desc = "C1 16^3 periodic uniform Maxwellian, 2 species, 27 ppc (L2-resident; not a roofline config)"
+    if args.relativistic:
+        w.relativistic = True
+        desc += "; relativistic Eq. 2 (NEXT-1)"
     return w.with_slab(rank * per, (rank + 1) * per), desc
 
 
@@ -146,7 +150,7 @@ def oracle_rate(w, parts_cpu, target_s, n_iter=3):
         for s, sp in enumerate(w.species):
             P = {k: parts_cpu[s][k][:n_per_species].numpy().copy() for k in "xyzuvwq"}
             st = np.zeros(len(P["x"]), dtype=np.int8)
-            O.mover(g, F, sp.qom, n_iter, P, st)
+            O.mover(g, F, sp.qom, n_iter, P, st, relativistic=w.relativistic)
             O.moments(g, P, st, with_abs=False)
             tot += len(P["x"])
         return tot, time.perf_counter() - t0

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define PIC_ABI_VERSION 2
+#define PIC_ABI_VERSION 3
 #define PIC_MAX_SPECIES 8
 #define PIC_NCCL_ID_BYTES 128
 #define PIC_N_MOMENTS 10  /* rho, Jx, Jy, Jz, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz (R16) */
@@ -105,6 +105,9 @@ typedef struct {
                                     moment ghost node planes per x-side (R22)     */
   int32_t transport;             /* pic_transport (nranks > 1)                    */
   int32_t kernel;                /* pic_kernel                                    */
+  int32_t relativistic;          /* 0: gamma == 1 limit of Eq. 2 (R3, the hot path);
+                                    1: relativistic Eq. 2 with gamma (NEXT-1, R4-R6);
+                                    |v| >= c is then a non-finite update (R23)    */
 } pic_config;
 
 /* ABI version (PIC_ABI_VERSION).                                             */

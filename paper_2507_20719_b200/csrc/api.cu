@@ -56,6 +56,7 @@ pic_status validate(const pic_config *c, std::string *why) {
   if (c->planet_radius < 0) { *why = "planet_radius < 0"; return PIC_EINVAL; }
   if (c->transport < PIC_TRANSPORT_AUTO || c->transport > PIC_TRANSPORT_PEER) { *why = "bad transport"; return PIC_EINVAL; }
   if (c->kernel < 0 || c->kernel > 2) { *why = "bad kernel"; return PIC_EINVAL; }
+  if (c->relativistic != 0 && c->relativistic != 1) { *why = "relativistic must be 0 or 1"; return PIC_EINVAL; }
   return PIC_OK;
 }
 

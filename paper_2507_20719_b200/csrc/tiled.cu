@@ -194,7 +194,9 @@ constexpr int MOVER_WARPS = PIC_MOVER_WARPS;
 constexpr int MOVER_THREADS = 32 * MOVER_WARPS;
 constexpr size_t MOVER_SMEM = sizeof(double) * (NB3 * 6 + MOVER_WARPS * MOVER_WARP_STAGE) + 16;
 
-template <int NIT>
+// REL = 1: relativistic Eq. 2 (NEXT-1, readings R4, R5), a separate
+// instantiation so the gamma == 1 hot path keeps its registers.
+template <int NIT, int REL>
 __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap, const MoverTArgs A) {
   constexpr int MW = MOVER_WARPS;
@@ -302,32 +304,70 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       double vb[3];
       bool clamped = false;
       const int n_iter = NIT > 0 ? NIT : A.n_iter;
-#pragma unroll
-      for (int it = 0; it < n_iter; ++it) {
-        double EB[6];
-        const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
-        if (!gather_smem(fld, u, EB)) {
-          clamped |= sample_window(g, A.field, xb, EB);
-#pragma unroll
-          for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
-        }
-        // Eq. 2: vt = vn + k E ; a = k B / c ; vb = (vt + vt x a + (vt.a) a) / (1 + a.a)
-        const double vt0 = vn[0] + EB[0], vt1 = vn[1] + EB[1], vt2 = vn[2] + EB[2];
-        const double a0 = EB[3], a1 = EB[4], a2 = EB[5];
-        const double dot = fma(vt0, a0, fma(vt1, a1, vt2 * a2));
-        const double D = fma(a0, a0, fma(a1, a1, fma(a2, a2, 1.0)));
-        const double invD = rcp_ge1(D);
-        vb[0] = fma(dot, a0, fma(vt1, a2, fma(-vt2, a1, vt0))) * invD;
-        vb[1] = fma(dot, a1, fma(vt2, a0, fma(-vt0, a2, vt1))) * invD;
-        vb[2] = fma(dot, a2, fma(vt0, a1, fma(-vt1, a0, vt2))) * invD;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
-      }
       double xnew[3], vnew[3];
+      if constexpr (REL == 0) {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
-        vnew[d] = fma(2.0, vb[d], -vn[d]);
+        for (int it = 0; it < n_iter; ++it) {
+          double EB[6];
+          const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
+          if (!gather_smem(fld, u, EB)) {
+            clamped |= sample_window(g, A.field, xb, EB);
+#pragma unroll
+            for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
+          }
+          // Eq. 2: vt = vn + k E ; a = k B / c ; vb = (vt + vt x a + (vt.a) a) / (1 + a.a)
+          const double vt0 = vn[0] + EB[0], vt1 = vn[1] + EB[1], vt2 = vn[2] + EB[2];
+          const double a0 = EB[3], a1 = EB[4], a2 = EB[5];
+          const double dot = fma(vt0, a0, fma(vt1, a1, vt2 * a2));
+          const double D = fma(a0, a0, fma(a1, a1, fma(a2, a2, 1.0)));
+          const double invD = rcp_ge1(D);
+          vb[0] = fma(dot, a0, fma(vt1, a2, fma(-vt2, a1, vt0))) * invD;
+          vb[1] = fma(dot, a1, fma(vt2, a0, fma(-vt0, a2, vt1))) * invD;
+          vb[2] = fma(dot, a2, fma(vt0, a1, fma(-vt1, a0, vt2))) * invD;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
+          vnew[d] = fma(2.0, vb[d], -vn[d]);
+        }
+      } else {
+        // relativistic Eq. 2 (R4, R5): vt = gn vn + k E,
+        // a = k B / (c gt), D = gt (1 + a.a), u1 = 2 gt vb - gn vn,
+        // g1 = sqrt(1 + u1.u1 / c^2), gt = (gn + g1) / 2; v^{n+1} = u1 / g1
+        const double ic2 = 1.0 / (g.c * g.c);
+        const double gn = 1.0 / sqrt(1.0 - (vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2]) * ic2);
+        double gt = gn, g1 = gn, u1[3] = {gn * vn[0], gn * vn[1], gn * vn[2]};
+#pragma unroll
+        for (int it = 0; it < n_iter; ++it) {
+          double EB[6];
+          const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
+          if (!gather_smem(fld, u, EB)) {
+            clamped |= sample_window(g, A.field, xb, EB);
+#pragma unroll
+            for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
+          }
+          const double igt = 1.0 / gt;
+          const double vt0 = fma(gn, vn[0], EB[0]), vt1 = fma(gn, vn[1], EB[1]), vt2 = fma(gn, vn[2], EB[2]);
+          const double a0 = EB[3] * igt, a1 = EB[4] * igt, a2 = EB[5] * igt;
+          const double dot = fma(vt0, a0, fma(vt1, a1, vt2 * a2));
+          const double invD = rcp_ge1(fma(a0, a0, fma(a1, a1, fma(a2, a2, 1.0)))) * igt;
+          vb[0] = fma(dot, a0, fma(vt1, a2, fma(-vt2, a1, vt0))) * invD;
+          vb[1] = fma(dot, a1, fma(vt2, a0, fma(-vt0, a2, vt1))) * invD;
+          vb[2] = fma(dot, a2, fma(vt0, a1, fma(-vt1, a0, vt2))) * invD;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) u1[d] = fma(2.0 * gt, vb[d], -gn * vn[d]);
+          g1 = sqrt(fma(u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2], ic2, 1.0));
+          gt = 0.5 * (gn + g1);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
+          vnew[d] = u1[d] / g1;
+        }
       }
       knew = finish_particle(g, xnew, vnew, clamped, A.stats);
       A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
@@ -587,7 +627,8 @@ static pic_status make_tmap(Ctx *ctx) {
     if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
   }
 #define PIC_SET_SMEM(NIT) \
-  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM))
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM)); \
+  PIC_CUDA(cudaFuncSetAttribute(mover_tiled_kernel<NIT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVER_SMEM))
   PIC_SET_SMEM(0); PIC_SET_SMEM(1); PIC_SET_SMEM(2); PIC_SET_SMEM(3); PIC_SET_SMEM(4);
 #undef PIC_SET_SMEM
   PIC_CUDA(cudaFuncSetAttribute(deposit_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -628,8 +669,13 @@ pic_status launch_tiled_step(Ctx *ctx, int s) {
   A.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
   const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap[ctx->field_cur]);
   const unsigned grid = (unsigned)ctx->geom.ntiles;
-#define PIC_LAUNCH(NIT) \
-  mover_tiled_kernel<NIT><<<grid, MOVER_THREADS, MOVER_SMEM, ctx->stream>>>(tm, A)
+#define PIC_LAUNCH(NIT)                                                                            \
+  do {                                                                                             \
+    if (ctx->cfg.relativistic)                                                                     \
+      mover_tiled_kernel<NIT, 1><<<grid, MOVER_THREADS, MOVER_SMEM, ctx->stream>>>(tm, A);         \
+    else                                                                                           \
+      mover_tiled_kernel<NIT, 0><<<grid, MOVER_THREADS, MOVER_SMEM, ctx->stream>>>(tm, A);         \
+  } while (0)
   {
     PhaseTimer t(ctx, 0);
     switch (sp.n_iter) {

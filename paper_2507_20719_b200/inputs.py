@@ -67,6 +67,7 @@ class Workload:
     colocate: bool = True           # e-/p+ pairs at the same positions
     density: str = "uniform"        # or "harris"
     slab: Tuple[int, int] = (0, 0)  # x-cells [lo, hi) of this rank (set by with_slab)
+    relativistic: bool = False      # Eq. 2 with gamma (NEXT-1)
 
     @property
     def delta(self):
@@ -278,6 +279,9 @@ def make_species(w: Workload, device="cpu") -> List[dict]:
         dens = sp.dens_fn(x, y, z) if sp.dens_fn is not None else _density(w, y)
         q = sp.sign * dens * V / ppc_cell.to(torch.float64)
         vel = torch.randn((3, n), generator=gen, device=device, dtype=torch.float64) * sp.vth
+        if w.relativistic:
+            # draw the momentum per unit mass u = gamma v, so |v| = |u| / sqrt(1 + u^2/c^2) < c
+            vel = vel / torch.sqrt(1.0 + (vel * vel).sum(0, keepdim=True) / (w.c * w.c))
         u, v, ww = vel[0] + sp.drift[0], vel[1] + sp.drift[1], vel[2] + sp.drift[2]
         if w.density == "harris":
             # sheet populations drift along +-z (GEM); background is at rest
@@ -303,6 +307,17 @@ def c1(randomized: bool = False, seed: int = 1) -> Workload:
         bc=(PERIODIC,) * 3, dt=0.5, seed=seed,
         species=[Species("e-", -256.0, -1.0, 0.05, ppc=27), Species("p+", 1.0, 1.0, 0.0070, ppc=27)],
         field_kind="uniform", field_params=fp)
+
+
+def c1rel(seed: int = 6) -> Workload:
+    """NEXT-1 check: C1 with relativistic thermal speeds (electron v_th = 0.3 c, so
+    gamma up to ~2 in the tail; v drawn below c) and the relativistic mover."""
+    w = c1(randomized=True, seed=seed)
+    w.relativistic = True
+    w.species[0].vth = 0.3
+    w.species[1].vth = 0.05
+    w.field_params = dict(w.field_params, B=(0.0, 0.0, 0.05))
+    return w
 
 
 def c2(scale_x: int = 1, nx_per_rank: int = 128, seed: int = 2, ppc: int = 125) -> Workload:
@@ -386,4 +401,4 @@ def c5(ncell=(512, 256, 256), wind_ppc: int = 64, inner_ppc: int = 8, planet_ppc
         planet_center=center, planet_radius=R)
 
 
-CONFIGS = {"c1": c1, "c1r": lambda: c1(True), "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+CONFIGS = {"c1": c1, "c1r": lambda: c1(True), "c1rel": c1rel, "c2": c2, "c3": c3, "c4": c4, "c5": c5}

@@ -44,7 +44,7 @@ class pic_config(C.Structure):
         ("capacity", C.c_int64 * PIC_MAX_SPECIES),
         ("planet_center", C.c_double * 3), ("planet_radius", C.c_double),
         ("rank", C.c_int32), ("nranks", C.c_int32), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64),
-        ("ghost", C.c_int32), ("transport", C.c_int32), ("kernel", C.c_int32),
+        ("ghost", C.c_int32), ("transport", C.c_int32), ("kernel", C.c_int32), ("relativistic", C.c_int32),
     ]
 
 
@@ -124,7 +124,7 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSPORT_AUTO, kernel=KERNEL_AUTO,
-                n_iter=None) -> pic_config:
+                n_iter=None, relativistic=None) -> pic_config:
     """pic_config from an inputs.Workload (marshalling only)."""
     cfg = pic_config()
     lo, hi = w.slab_or_all()
@@ -141,6 +141,7 @@ def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSP
         cfg.capacity[s] = capacity[s] if capacity is not None else 0
     cfg.rank, cfg.nranks, cfg.slab_lo, cfg.slab_hi = rank, nranks, lo, hi
     cfg.ghost, cfg.transport, cfg.kernel = ghost, transport, kernel
+    cfg.relativistic = int(bool(getattr(w, "relativistic", False) if relativistic is None else relativistic))
     return cfg
 
 

@@ -46,7 +46,7 @@ def run_oracle(w: I.Workload, species_parts, cycles: int, ghost: int = 2, n_iter
         P = to_numpy_parts(species_parts[s])
         st = np.zeros(len(P["x"]), dtype=np.int8)
         for _ in range(cycles):
-            st, bad = O.mover(g, F, sp.qom, n_iter or w.n_iter, P, st)
+            st, bad = O.mover(g, F, sp.qom, n_iter or w.n_iter, P, st, relativistic=w.relativistic)
             assert bad == 0, "oracle flagged a bad particle"
         mom, am = O.moments(g, P, st)
         out.append((P, st, mom, am))

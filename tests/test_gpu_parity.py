@@ -79,6 +79,16 @@ def test_c4_open_dipole_scaled(kernel):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
+def test_c1_relativistic(kernel):
+    # NEXT-1: relativistic Eq. 2 (gamma up to ~2 for the electrons)
+    w = I.c1rel()
+    parts = I.make_species(w, device="cpu")
+    g = 1.0 / torch.sqrt(1.0 - (parts[0]["u"] ** 2 + parts[0]["v"] ** 2 + parts[0]["w"] ** 2))
+    assert float(g.max()) > 1.5
+    check(w, 4, kernel)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 def test_c3_fourier_scaled(kernel):
     # C3 structure (B0 z + random Fourier modes, periodic cube) at 24^3, 8 ppc
     w = I.c3(n_per_rank=24, ppc=8)
