@@ -66,6 +66,8 @@ def _load():
         lib.oracle_moments.argtypes = [P(Grid), C.c_int64, d, d, d, d, d, d, d, P(C.c_int8), d, d]
         lib.oracle_moments.restype = C.c_int64
         lib.oracle_node_counts.argtypes = [P(Grid), P(C.c_int64)]
+        lib.oracle_implicit_sources.argtypes = [P(Grid), C.c_int, d, P(d), d, d, d, d]
+        lib.oracle_implicit_sources.restype = None
         _lib = lib
     return _lib
 
@@ -144,3 +146,22 @@ def moments(g: Grid, parts: dict, status=None, with_abs: bool = True):
     if out:
         raise ValueError(f"{out} particles outside the grid in oracle.moments")
     return mom, am
+
+
+def implicit_sources(g: Grid, qoms, moms, B: np.ndarray):
+    """Eq. 5-6 (NEXT-2): chi[9][nz][ny][nx], rho_hat[nz][ny][nx], J_hat[3][nz][ny][nx]
+    from per-species moments (oracle.moments layout) and node B[nz][ny][nx][3]."""
+    nx, ny, nz = node_counts(g)
+    S = len(moms)
+    ms = [np.ascontiguousarray(m, dtype=np.float64) for m in moms]
+    for m in ms:
+        assert m.shape == (10, nz, ny, nx)
+    Bc = np.ascontiguousarray(B, dtype=np.float64)
+    assert Bc.shape == (nz, ny, nx, 3)
+    q = np.ascontiguousarray(qoms, dtype=np.float64)
+    arr = (C.POINTER(C.c_double) * S)(*[_dptr(m) for m in ms])
+    chi = np.zeros((9, nz, ny, nx))
+    rh = np.zeros((nz, ny, nx))
+    jh = np.zeros((3, nz, ny, nx))
+    _load().oracle_implicit_sources(C.byref(g), S, _dptr(q), arr, _dptr(Bc), _dptr(chi), _dptr(rh), _dptr(jh))
+    return chi, rh, jh

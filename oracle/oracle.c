@@ -18,6 +18,8 @@
  *   Eq. 3   PAPER.md:184-187  moments {rho, J, Pi}_g = sum_p q {1, v, vv} W
  *   Alg. 1  PAPER.md:291-334  phase order: mover, then interpolation
  *   §III-B  PAPER.md:235-236  open boundaries: particles leaving are removed
+ *   Eq. 5-6 PAPER.md:199-213  susceptibility chi and corrected rho-hat, J-hat
+ *                             (NEXT-2, the first consumer of the moments)
  * Readings where the paper is silent or garbled are R1..R23 in DESIGN.md §3
  * (taken from SURVEY.md §8(c)); each use below names its reading.
  *
@@ -322,4 +324,110 @@ int64_t oracle_moments(const oracle_grid *g, int64_t np, const double *x,
 /* Convenience for tests: unique node counts per axis.                      */
 void oracle_node_counts(const oracle_grid *g, int64_t out[3]) {
   for (int d = 0; d < 3; ++d) out[d] = nodes_axis(g, d);
+}
+
+/* ------------------------------------------- NEXT-2: chi, rho-hat, J-hat -- */
+
+/* d f / d x_axis at node (i,j,k) of a unique-node array f[nz][ny][nx]:
+ * second-order central difference, periodic wrap on periodic axes; one-sided
+ * first-order difference at the two boundary nodes of an open axis (R27).   */
+static double node_diff(const oracle_grid *g, const double *f, const int64_t nn[3], int64_t i,
+                        int64_t j, int64_t k, int axis) {
+  int64_t c[3] = {i, j, k};
+  int64_t n = nn[axis];
+  double delta = g->len[axis] / (double)g->ncell[axis];
+  int64_t lo[3] = {c[0], c[1], c[2]}, hi[3] = {c[0], c[1], c[2]};
+  double h = 2.0 * delta;
+  if (g->bc[axis] == 0) {
+    lo[axis] = (c[axis] - 1 + n) % n;
+    hi[axis] = (c[axis] + 1) % n;
+  } else if (c[axis] == 0) {
+    hi[axis] = 1;
+    h = delta;
+  } else if (c[axis] == n - 1) {
+    lo[axis] = n - 2;
+    h = delta;
+  } else {
+    lo[axis] = c[axis] - 1;
+    hi[axis] = c[axis] + 1;
+  }
+  double fh = f[(hi[2] * nn[1] + hi[1]) * nn[0] + hi[0]];
+  double fl = f[(lo[2] * nn[1] + lo[1]) * nn[0] + lo[0]];
+  return (fh - fl) / h;
+}
+
+/* R_s(Omega_s dt/2) applied to x: with a = Omega_s dt/2,
+ * R x = (x - a x x + (a.x) a) / (1 + a.a).  The printed R omits the scalar
+ * 1/(1 + a.a); it is included (R25) so that R is exactly the linear response
+ * of the mover's average velocity to E (Eq. 2: vb = R vt), which the pins
+ * check against push_one.                                                  */
+static void apply_R(const double a[3], const double x[3], double out[3]) {
+  double cr[3];
+  cr[0] = a[1] * x[2] - a[2] * x[1];
+  cr[1] = a[2] * x[0] - a[0] * x[2];
+  cr[2] = a[0] * x[1] - a[1] * x[0];
+  double dot = a[0] * x[0] + a[1] * x[1] + a[2] * x[2];
+  double den = 1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+  for (int d = 0; d < 3; ++d) out[d] = (x[d] - cr[d] + dot * a[d]) / den;
+}
+
+/* Eq. 5 and Eq. 6 from the moments of S species (NEXT-2).
+ *   mom[s]: species s moments [10][nz][ny][nx] over the unique nodes (after
+ *           1/V, the output of oracle_moments); B: node field [nz][ny][nx][3]
+ *   chi[9][nz][ny][nx] = sum_s (1/2)(omega_ps dt)^2 R_s        (Eq. 5)
+ *       omega_ps^2 = 4 pi rho_s q_s/m_s (rho_s and q_s share their sign, R24)
+ *   J_hat[3][...] = sum_s R_s (J_s - (dt/2) div Pi_s)         (Eq. 6, R26: per
+ *       species with its own R_s, then summed)
+ *   rho_hat[...] = sum_s rho_s - dt div J_hat                 (Eq. 6)
+ * Derivatives: node_diff (R27).  Gaussian units, 4 pi explicit.             */
+void oracle_implicit_sources(const oracle_grid *g, int n_species, const double *qom,
+                             const double *const *mom, const double *B, double *chi,
+                             double *rho_hat, double *J_hat) {
+  int64_t nn[3] = {nodes_axis(g, 0), nodes_axis(g, 1), nodes_axis(g, 2)};
+  int64_t plane = nn[0] * nn[1] * nn[2];
+  const double four_pi = 4.0 * 3.14159265358979323846;
+  double dt = g->dt;
+  for (int64_t m = 0; m < 9 * plane; ++m) chi[m] = 0.0;
+  for (int64_t m = 0; m < 3 * plane; ++m) J_hat[m] = 0.0;
+  for (int64_t k = 0; k < nn[2]; ++k)
+    for (int64_t j = 0; j < nn[1]; ++j)
+      for (int64_t i = 0; i < nn[0]; ++i) {
+        int64_t node = (k * nn[1] + j) * nn[0] + i;
+        for (int s = 0; s < n_species; ++s) {
+          const double *ms = mom[s];
+          double a[3];
+          for (int d = 0; d < 3; ++d) a[d] = (qom[s] * B[3 * node + d] / g->c) * (dt / 2.0);
+          double w2 = four_pi * ms[node] * qom[s];
+          /* chi_s columns: R_s applied to the unit vectors */
+          for (int col = 0; col < 3; ++col) {
+            double e[3] = {0.0, 0.0, 0.0}, r[3];
+            e[col] = 1.0;
+            apply_R(a, e, r);
+            for (int row = 0; row < 3; ++row)
+              chi[(row * 3 + col) * plane + node] += 0.5 * w2 * dt * dt * r[row];
+          }
+          /* div Pi_s: (div Pi)_a = sum_b d Pi_ab / d x_b; Pi order xx xy xz yy yz zz */
+          static const int pidx[3][3] = {{4, 5, 6}, {5, 7, 8}, {6, 8, 9}};
+          double divPi[3];
+          for (int ra = 0; ra < 3; ++ra) {
+            divPi[ra] = 0.0;
+            for (int b = 0; b < 3; ++b)
+              divPi[ra] += node_diff(g, ms + pidx[ra][b] * plane, nn, i, j, k, b);
+          }
+          double x[3], r[3];
+          for (int d = 0; d < 3; ++d) x[d] = ms[(1 + d) * plane + node] - (dt / 2.0) * divPi[d];
+          apply_R(a, x, r);
+          for (int d = 0; d < 3; ++d) J_hat[d * plane + node] += r[d];
+        }
+      }
+  for (int64_t k = 0; k < nn[2]; ++k)
+    for (int64_t j = 0; j < nn[1]; ++j)
+      for (int64_t i = 0; i < nn[0]; ++i) {
+        int64_t node = (k * nn[1] + j) * nn[0] + i;
+        double rho = 0.0;
+        for (int s = 0; s < n_species; ++s) rho += mom[s][node];
+        double divJ = 0.0;
+        for (int b = 0; b < 3; ++b) divJ += node_diff(g, J_hat + b * plane, nn, i, j, k, b);
+        rho_hat[node] = rho - dt * divJ;
+      }
 }
