@@ -363,6 +363,28 @@ def main():
                "d2h_bytes_per_step": sum(m.numel() * 8 for m in mom_h)}
         ctx.sync()
 
+    # ---- NEXT-2: the field solver's sources (Eq. 5-6) from this step's moments
+    next2 = None
+    if world == 1:
+        ctx.implicit_sources()                      # warm-up (allocates the outputs)
+        nx_, ny_, nz_ = ctx.moment_shape()
+        a2 = torch.cuda.Event(enable_timing=True)
+        b2 = torch.cuda.Event(enable_timing=True)
+        reps = 5
+        a2.record(stream)
+        for _ in range(reps):
+            ctx.implicit_sources()
+        b2.record(stream)
+        torch.cuda.synchronize()
+        ms2 = a2.elapsed_time(b2) / reps
+        nodes = nx_ * ny_ * nz_
+        # algorithmic bytes per node: 10 moments x S in, B in, chi 9 + J-hat 3 +
+        # rho-hat 1 out, J-hat read back for the divergence
+        b_node = 80 * n_sp + 24 + 104 + 24
+        next2 = {"what": "chi, rho-hat, J-hat (Eq. 5-6) over the owned nodes, incl. output allocation and sync",
+                 "ms_per_call": ms2, "nodes": nodes, "bytes_per_node": b_node,
+                 "achieved_gbs": nodes * b_node / (ms2 / 1e3) / 1e9}
+
     cpu = None
     if parts_cpu_sample is not None:
         threads = torch.get_num_threads()
@@ -384,6 +406,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "next2_sources": next2,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "phase_ms": {"mover+order": mover_avg, "moments+exchange": sum(rest_ms) / len(rest_ms),

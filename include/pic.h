@@ -211,6 +211,20 @@ PIC_API pic_status pic_sync(pic_ctx *ctx, int64_t stats[8]);
  * synchronisation of the context stream, or after pic_sync.                  */
 PIC_API pic_status pic_get_moments_async(pic_ctx *ctx, int32_t s, double *out);
 
+/* NEXT-2 (Eq. 5-6; readings R24-R27): the implicit field
+ * solver's particle sources from the moments of every species (after
+ * pic_exchange) and B of the most recent pic_set_fields, over the owned nodes
+ * (pic_moment_shape, layout [..][z][y][x]; host or device buffers, any may be
+ * NULL):
+ *   chi[9]      sum_s (1/2)(omega_ps dt)^2 R_s, row-major 3x3 per node,
+ *               omega_ps^2 = 4 pi rho_s q_s/m_s, R_s = (I - [a]x + a a^T)/(1+a.a),
+ *               a = q_s B dt / (2 m_s c)  (Gaussian units)
+ *   J_hat[3]    sum_s R_s (J_s - (dt/2) div Pi_s)
+ *   rho_hat[1]  sum_s rho_s - dt div J_hat
+ * Central differences (periodic wrap; one-sided at open-axis boundary nodes).
+ * Single rank in this build (PIC_EINVAL otherwise).  Synchronises.          */
+PIC_API pic_status pic_implicit_sources(pic_ctx *ctx, double *chi, double *rho_hat, double *J_hat);
+
 /* Make the context stream wait (on the device, no host block) for every copy
  * enqueued by pic_get_moments_async / pic_set_fields so far.                 */
 PIC_API pic_status pic_join_copies(pic_ctx *ctx);

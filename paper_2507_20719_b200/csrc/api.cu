@@ -150,6 +150,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   for (int k = 0; k < 4; ++k) om[k] = L.take(multi ? 8 * 8 * mig_cap * c->n_species : 8);
   const int64_t pack_elems = (g.k_n[0] + 1) * g.m_n[1] * g.m_n[2] * 10;
   int64_t opack = L.take(8 * pack_elems);
+  int64_t osrc = L.take(8 * 13 * (pack_elems / 10));
   int64_t oslot[2 * PIC_MAX_SPECIES];
   for (int k = 0; k < 2 * c->n_species; ++k) oslot[k] = L.take(8 * pack_elems);
   int64_t ocub = L.take((int64_t)cub_bytes);
@@ -172,6 +173,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
     ctx->mig_recv[1] = (double *)(base + om[3]);
     ctx->mig_cap = mig_cap;
     ctx->pack = (double *)(base + opack);
+    ctx->src_buf = (double *)(base + osrc);
     ctx->cub_temp = base + ocub;
     ctx->cub_bytes = cub_bytes;
     ctx->cap_max = cap_max;
@@ -485,6 +487,16 @@ pic_status pic_get_moments_async(pic_ctx *p, int32_t s, double *out) {
   pic_status st = check_species(ctx, s, false);
   if (st != PIC_OK) return st;
   return pack_moments_async(ctx, s, out);
+}
+
+pic_status pic_implicit_sources(pic_ctx *p, double *chi, double *rho_hat, double *J_hat) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  for (int k = 0; k < ctx->cfg.n_species; ++k)
+    if (ctx->sp[k].moved || ctx->sp[k].deposited)
+      return fail(ctx, PIC_ESTATE, "pic_implicit_sources needs the moments after pic_exchange");
+  if (!ctx->fields_set) return fail(ctx, PIC_ESTATE, "pic_implicit_sources needs pic_set_fields (B)");
+  return implicit_sources(ctx, chi, rho_hat, J_hat);
 }
 
 pic_status pic_join_copies(pic_ctx *p) {

@@ -167,6 +167,7 @@ struct Ctx {
   double *mig_recv[2] = {};
   int64_t mig_cap = 0;
   double *pack = nullptr;            // moment copy-out staging
+  double *src_buf = nullptr;         // NEXT-2 sources: chi [9], J-hat [3], rho-hat [1] per owned node
   void *workspace = nullptr;         // caller's device workspace (pic_init)
   // peer transport (peer.cu): own control block and the mapped neighbours
   PeerCtl *peer_ctl = nullptr;
@@ -265,6 +266,7 @@ pic_status zero_moments(Ctx *ctx, int s);
 pic_status pack_moments(Ctx *ctx, int s, double *out);
 pic_status pack_moments_async(Ctx *ctx, int s, double *out);
 pic_status join_copies(Ctx *ctx);
+pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_hat);
 pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
 pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id);
 pic_status live_count(Ctx *ctx, int s, int64_t *n);

@@ -33,7 +33,7 @@ STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "ove
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -86,6 +86,7 @@ def load_library(path: str = LIB_PATH):
         lib.pic_get_transport.argtypes = [vp, P(C.c_int32)]
         lib.pic_get_moments_async.argtypes = [vp, C.c_int32, vp]
         lib.pic_join_copies.argtypes = [vp]
+        lib.pic_implicit_sources.argtypes = [vp, vp, vp, vp]
         lib.pic_profile.argtypes = [vp, C.c_int32]
         lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
@@ -227,6 +228,15 @@ class Context:
         assert out.dtype == torch.float64 and out.numel() == 10 * nx * ny * nz and out.is_contiguous()
         _check(self.lib.pic_get_moments_async(self.h, s, _ptr(out)), self.h, "pic_get_moments_async")
         return out
+
+    def implicit_sources(self, device="cuda"):
+        """NEXT-2 (Eq. 5-6): (chi[9][nz][ny][nx], rho_hat[nz][ny][nx], J_hat[3][nz][ny][nx])."""
+        nx, ny, nz = self.moment_shape()
+        chi = torch.empty((9, nz, ny, nx), dtype=torch.float64, device=device)
+        rh = torch.empty((nz, ny, nx), dtype=torch.float64, device=device)
+        jh = torch.empty((3, nz, ny, nx), dtype=torch.float64, device=device)
+        _check(self.lib.pic_implicit_sources(self.h, _ptr(chi), _ptr(rh), _ptr(jh)), self.h, "pic_implicit_sources")
+        return chi, rh, jh
 
     def join_copies(self):
         """The context stream waits (on the device) for all enqueued copies."""

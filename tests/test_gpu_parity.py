@@ -301,3 +301,30 @@ def test_open_boundary_removal_counts():
     n1 = sum(ctx.count(s) for s in range(len(parts)))
     assert stats["removed"] > 0 and n1 + stats["removed"] == n0
     ctx.close()
+
+
+@pytest.mark.parametrize("cfg", ["c1r", "c4s"])
+def test_implicit_sources_two_level(cfg):
+    """NEXT-2 (Eq. 5-6): GPU chi, rho-hat, J-hat against the oracle fed with the
+    GPU's own moments (two-level parity, P13: isolates the sources stencil; the
+    moments themselves are pinned by the parity tests above)."""
+    import oracle as O
+    w = I.c1(randomized=True) if cfg == "c1r" else I.c4(ncell=(32, 16, 16), ppc=8)
+    parts = I.make_species(w, device="cpu")
+    ctx = _ctx_for(w, parts)
+    for _ in range(2):
+        ctx.cycle()
+    ctx.sync()
+    gm = [ctx.get_moments(s).cpu().numpy() for s in range(len(parts))]
+    chi, rh, jh = (t.cpu().numpy() for t in ctx.implicit_sources())
+    ctx.close()
+    G = 2
+    lo, EB = I.field_window(w, G)
+    nz, ny, nx = gm[0].shape[1:]
+    Bn = EB[G:G + nz, G:G + ny, G:G + nx, 3:6].numpy()
+    g = PU.oracle_grid(w)
+    ochi, orh, ojh = O.implicit_sources(g, [sp.qom for sp in w.species], gm, Bn)
+    for got, want in ((chi, ochi), (rh, orh), (jh, ojh)):
+        scale = np.abs(want).max()
+        assert scale > 0
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-12 * scale)
