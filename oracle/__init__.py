@@ -68,6 +68,12 @@ def _load():
         lib.oracle_node_counts.argtypes = [P(Grid), P(C.c_int64)]
         lib.oracle_implicit_sources.argtypes = [P(Grid), C.c_int, d, P(d), d, d, d, d]
         lib.oracle_implicit_sources.restype = None
+        lib.oracle_philox4x32_10.argtypes = [P(C.c_uint32), P(C.c_uint32)]
+        lib.oracle_philox4x32_10.restype = None
+        lib.oracle_inject.argtypes = [P(Grid), P(Field), C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint32,
+                                      C.c_uint32, C.c_int64, C.c_int, C.c_double, d, C.c_double, C.c_int64,
+                                      d, d, d, d, d, d, d, P(C.c_int64)]
+        lib.oracle_inject.restype = C.c_int64
         _lib = lib
     return _lib
 
@@ -165,3 +171,30 @@ def implicit_sources(g: Grid, qoms, moms, B: np.ndarray):
     jh = np.zeros((3, nz, ny, nx))
     _load().oracle_implicit_sources(C.byref(g), S, _dptr(q), arr, _dptr(Bc), _dptr(chi), _dptr(rh), _dptr(jh))
     return chi, rh, jh
+
+
+def philox(counter, key):
+    """Philox4x32-10 of one counter (4 x uint32) under key (2 x uint32)."""
+    c = (C.c_uint32 * 4)(*[int(v) & 0xffffffff for v in counter])
+    k = (C.c_uint32 * 2)(*[int(v) & 0xffffffff for v in key])
+    _load().oracle_philox4x32_10(c, k)
+    return [int(v) for v in c]
+
+
+def inject(g: Grid, F: FieldWindow, species: int, qom: float, n_iter: int, seed: int, cycle: int, ppc: int,
+           vth: float, drift, q: float, relativistic: bool = False) -> dict:
+    """NEXT-3 inflow injection (reading R28): the particles that enter through the
+    x = 0 face this cycle, after their first push (dict of arrays incl. int64 id)."""
+    cap = int(g.ncell[1] * g.ncell[2] * ppc)
+    out = {k: np.zeros(cap) for k in "xyzuvwq"}
+    ids = np.zeros(cap, dtype=np.int64)
+    dr = np.ascontiguousarray(drift, dtype=np.float64)
+    n = _load().oracle_inject(C.byref(g), C.byref(F.c), int(species), float(qom), int(n_iter), int(bool(relativistic)),
+                              seed & 0xffffffff, (seed >> 32) & 0xffffffff, int(cycle), int(ppc), float(vth), _dptr(dr),
+                              float(q), cap, *[_dptr(out[k]) for k in "xyzuvwq"],
+                              ids.ctypes.data_as(C.POINTER(C.c_int64)))
+    if n < 0:
+        raise ValueError("injection needs an open x axis")
+    res = {k: a[:n].copy() for k, a in out.items()}
+    res["id"] = ids[:n].copy()
+    return res

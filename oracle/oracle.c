@@ -20,6 +20,8 @@
  *   §III-B  PAPER.md:235-236  open boundaries: particles leaving are removed
  *   Eq. 5-6 PAPER.md:199-213  susceptibility chi and corrected rho-hat, J-hat
  *                             (NEXT-2, the first consumer of the moments)
+ *   §III-B  PAPER.md:232-233  inflow injection of wind particles with a
+ *                             prescribed bulk velocity (NEXT-3, reading R28)
  * Readings where the paper is silent or garbled are R1..R23 in DESIGN.md §3
  * (taken from SURVEY.md §8(c)); each use below names its reading.
  *
@@ -430,4 +432,89 @@ void oracle_implicit_sources(const oracle_grid *g, int n_species, const double *
         for (int b = 0; b < 3; ++b) divJ += node_diff(g, J_hat + b * plane, nn, i, j, k, b);
         rho_hat[node] = rho - dt * divJ;
       }
+}
+
+/* --------------------------------------------- NEXT-3: inflow injection -- */
+
+/* Philox4x32-10 (Salmon et al., SC'11), the counter-based generator both the
+ * oracle and the CUDA path implement (their shared random numbers; pinned by
+ * the published known-answer vectors).  c: counter (in/out), k: key.       */
+void oracle_philox4x32_10(uint32_t c[4], const uint32_t k_in[2]) {
+  uint32_t k0 = k_in[0], k1 = k_in[1];
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k0, n1 = lo1, n2 = hi0 ^ c[3] ^ k1, n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+/* 53-bit uniform in [0, 1) from two words. */
+static double u53(uint32_t a, uint32_t b) {
+  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
+}
+
+/* Draw call `call` of particle k of ghost cell gc: two uniforms. */
+static void draw2(uint32_t gc, uint32_t k, uint32_t cycle, uint32_t species, uint32_t call,
+                  const uint32_t key[2], double *ua, double *ub) {
+  uint32_t c[4] = {gc, k, cycle, (species << 8) | call};
+  oracle_philox4x32_10(c, key);
+  *ua = u53(c[0], c[1]);
+  *ub = u53(c[2], c[3]);
+}
+
+/* Inflow injection at the x = 0 face of an open x axis (PAPER.md:232-233,
+ * reading R28): in every ghost cell (-1, cy, cz) of the face, ppc particles
+ * with uniform positions in the cell and velocities drift + vth * N(0,1)^3
+ * (Box-Muller), charge q, id 2^62 | cycle << 40 | species << 37 | (gc ppc + k),
+ * gc = cz Ny + cy, are pushed one step with Eq. 2 (push_one / push_one_rel)
+ * and kept when they end inside the domain (apply_bc ALIVE); kept particles
+ * are appended to the output arrays (at most cap).  Draws: call 0 -> (u0,u1),
+ * 1 -> (u2,u3), 2 -> (u4,u5), 3 -> (u6,u7) of Philox(counter {gc, k, cycle,
+ * species << 8 | call}, key {seed_lo, seed_hi});
+ *   x = (-1 + u0) dx, y = (cy + u1) dy, z = (cz + u2) dz,
+ *   (n0, n1) = sqrt(-2 ln(1 - u3)) (cos, sin)(2 pi u4),
+ *   n2 = sqrt(-2 ln(1 - u5)) cos(2 pi u6)   (u7 unused).
+ * Returns the number appended; -1 if the x axis is not open.                */
+int64_t oracle_inject(const oracle_grid *g, const oracle_field *F, int species, double qom, int n_iter,
+                      int relativistic, uint32_t seed_lo, uint32_t seed_hi, int64_t cycle, int ppc,
+                      double vth, const double drift[3], double q, int64_t cap, double *x, double *y,
+                      double *z, double *u, double *v, double *w, double *qo, int64_t *id) {
+  if (g->bc[0] != 1) return -1;
+  const uint32_t key[2] = {seed_lo, seed_hi};
+  double dl[3];
+  for (int d = 0; d < 3; ++d) dl[d] = g->len[d] / (double)g->ncell[d];
+  const double two_pi = 2.0 * 3.14159265358979323846;
+  int64_t n = 0;
+  for (int64_t cz = 0; cz < g->ncell[2]; ++cz)
+    for (int64_t cy = 0; cy < g->ncell[1]; ++cy) {
+      uint32_t gc = (uint32_t)(cz * g->ncell[1] + cy);
+      for (int k = 0; k < ppc; ++k) {
+        double r[8];
+        for (int call = 0; call < 4; ++call)
+          draw2(gc, (uint32_t)k, (uint32_t)cycle, (uint32_t)species, (uint32_t)call, key, &r[2 * call],
+                &r[2 * call + 1]);
+        double xn[3] = {(-1.0 + r[0]) * dl[0], ((double)cy + r[1]) * dl[1], ((double)cz + r[2]) * dl[2]};
+        double rad1 = sqrt(-2.0 * log(1.0 - r[3]));
+        double rad2 = sqrt(-2.0 * log(1.0 - r[5]));
+        double vn[3] = {drift[0] + vth * (rad1 * cos(two_pi * r[4])),
+                        drift[1] + vth * (rad1 * sin(two_pi * r[4])),
+                        drift[2] + vth * (rad2 * cos(two_pi * r[6]))};
+        int st = relativistic ? push_one_rel(g, F, qom, n_iter, xn, vn) : push_one(g, F, qom, n_iter, xn, vn);
+        if (st != ORACLE_ALIVE) continue;
+        if (n < cap) {
+          x[n] = xn[0]; y[n] = xn[1]; z[n] = xn[2];
+          u[n] = vn[0]; v[n] = vn[1]; w[n] = vn[2];
+          qo[n] = q;
+          id[n] = (int64_t)((1ull << 62) | ((uint64_t)cycle << 40) | ((uint64_t)species << 37) |
+                            ((uint64_t)gc * (uint64_t)ppc + (uint64_t)k));
+        }
+        ++n;
+      }
+    }
+  return n;
 }
