@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4s"])
     ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
     ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
@@ -61,6 +61,11 @@ def workload(args, nranks, rank):
         w = I.c3(nranks=nranks, ppc=args.ppc or 64)
         per = 192
         desc = "C3 weak-scaling cube 192^3 cells per GPU, 2 species, 64 ppc, 3 PC iterations"
+    elif args.config == "c4s":
+        w = I.c4(ncell=(128 * nranks, 128, 128), ppc=args.ppc or 64)
+        per = 128
+        desc = ("C4 structure at 128^3 cells per GPU: open boundaries, absorbing planet, dipole + IMF, wind e-/p+ "
+                "64 ppc, inflow injection of both species at x = 0 (NEXT-3), 3 PC iterations")
     else:
         w = I.c1()
         per = 16 // nranks
@@ -218,7 +223,8 @@ def main():
     w, desc = workload(args, world, rank)
     parts = I.make_species(w, device="cuda")
     n_local = [p["x"].numel() for p in parts]
-    cap = [int(n * 1.08) + 65536 for n in n_local]
+    face = w.ncell[1] * w.ncell[2]
+    cap = [int(n * 1.08) + 65536 + (4 * face * 64 if args.config == "c4s" else 0) for n in n_local]
     nccl_id = decomp.broadcast_nccl_id(pic.pic_nccl_id) if world > 1 else None
     cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
                           transport=args.transport, kernel=args.kernel)
@@ -226,6 +232,10 @@ def main():
     ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
     for s, p in enumerate(parts):
         ctx.set_particles(s, p)
+        if args.config == "c4s":
+            # NEXT-3: wind injection at the x = 0 face with the bulk wind's parameters
+            sp = w.species[s]
+            ctx.set_injection(s, 64, sp.vth, sp.drift, float(p["q"][0].item()), 4242 + s)
     lo, EB = I.field_window(w, args.ghost, device="cuda")
     ctx.set_fields(EB)
     parts_cpu_sample = None

@@ -225,6 +225,18 @@ PIC_API pic_status pic_get_moments_async(pic_ctx *ctx, int32_t s, double *out);
  * Single rank in this build (PIC_EINVAL otherwise).  Synchronises.          */
 PIC_API pic_status pic_implicit_sources(pic_ctx *ctx, double *chi, double *rho_hat, double *J_hat);
 
+/* NEXT-3: inflow injection at the x = 0 face of an open x axis (PAPER.md:
+ * 232-233, "wind electrons and protons are injected with a prescribed bulk
+ * velocity"; reading R28).  From the next pic_mover on, every cycle places ppc
+ * particles of species s uniformly in each ghost cell (-1, cy, cz) of the face,
+ * velocities drift + vth * N(0,1)^3 (Box-Muller on Philox4x32-10 draws keyed by
+ * seed, counter {face cell, index, cycle, species << 8 | draw}), charge q per
+ * particle, id 2^62 | cycle << 40 | s << 37 | (face cell * ppc + index); each is
+ * pushed one step with Eq. 2 and joins the store iff it ends inside the domain.
+ * Applied on the rank whose slab starts at x = 0.  ppc = 0 switches it off.   */
+PIC_API pic_status pic_set_injection(pic_ctx *ctx, int32_t s, int32_t ppc, double vth, const double drift[3],
+                                     double q, uint64_t seed);
+
 /* Make the context stream wait (on the device, no host block) for every copy
  * enqueued by pic_get_moments_async / pic_set_fields so far.                 */
 PIC_API pic_status pic_join_copies(pic_ctx *ctx);
@@ -245,9 +257,10 @@ PIC_API pic_status pic_launch_count(const pic_ctx *ctx, int64_t *n);
  *   ms[2] deposit kernels (Eq. 3), ms[3] pic_exchange (folds, ghost sums),
  *   ms[4] migration up to the count message (pack + NCCL counts),
  *   ms[5] migration after the host learnt the counts (payload + append);
- *   the host wait between ms[4] and ms[5] is in neither.
+ *   the host wait between ms[4] and ms[5] is in neither;
+ *   ms[6] inflow injection (NEXT-3).
  *   launches[k] the number of timed intervals of each phase.                 */
-#define PIC_PROF_PHASES 6
+#define PIC_PROF_PHASES 7
 PIC_API pic_status pic_profile(pic_ctx *ctx, int32_t enable);
 PIC_API pic_status pic_profile_read(pic_ctx *ctx, double ms[PIC_PROF_PHASES], int64_t launches[PIC_PROF_PHASES]);
 

@@ -373,6 +373,12 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
     ctx->sp[k].moved = true;
     ctx->sp[k].deposited = false;
   }
+  // inflow injection (NEXT-3) appends the wind particles that entered this cycle
+  for (int k = s0; k < s1; ++k) {
+    PhaseTimer t(ctx, 6);
+    st = inject(ctx, k);
+    if (st != PIC_OK) return st;
+  }
   // the field buffer may be refilled once these movers are done
   PIC_CUDA(cudaEventRecord(ctx->field_free[ctx->field_cur], ctx->stream));
   // slab leavers go to their neighbour right after the mover (Alg. 1: the
@@ -497,6 +503,23 @@ pic_status pic_implicit_sources(pic_ctx *p, double *chi, double *rho_hat, double
       return fail(ctx, PIC_ESTATE, "pic_implicit_sources needs the moments after pic_exchange");
   if (!ctx->fields_set) return fail(ctx, PIC_ESTATE, "pic_implicit_sources needs pic_set_fields (B)");
   return implicit_sources(ctx, chi, rho_hat, J_hat);
+}
+
+pic_status pic_set_injection(pic_ctx *p, int32_t s, int32_t ppc, double vth, const double drift[3], double q,
+                             uint64_t seed) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  if (ppc < 0 || !(vth >= 0.0) || !drift) return fail(ctx, PIC_EINVAL, "bad injection parameters");
+  if (ppc > 0 && ctx->cfg.bc[0] != PIC_BC_OPEN) return fail(ctx, PIC_EINVAL, "injection needs an open x axis");
+  InjectParams &ip = ctx->inj[s];
+  ip.ppc = ppc;
+  ip.vth = vth;
+  for (int d = 0; d < 3; ++d) ip.drift[d] = drift[d];
+  ip.q = q;
+  ip.seed = seed;
+  return PIC_OK;
 }
 
 pic_status pic_join_copies(pic_ctx *p) {

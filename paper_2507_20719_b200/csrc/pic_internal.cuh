@@ -133,6 +133,13 @@ struct SpeciesStore {
   }
 };
 
+// NEXT-3 inflow injection of one species (pic_set_injection).
+struct InjectParams {
+  int ppc = 0;             // ghost particles per face cell per cycle (0: off)
+  double vth = 0.0, drift[3] = {0.0, 0.0, 0.0}, q = 0.0;
+  uint64_t seed = 0;
+};
+
 struct Ctx {
   pic_config cfg;
   Geom geom;
@@ -182,6 +189,7 @@ struct Ctx {
   } link[2];                         // [0] left, [1] right
   bool peer = false;
   unsigned long long peer_epoch = 0;
+  InjectParams inj[PIC_MAX_SPECIES];
   void *cub_temp = nullptr;
   size_t cub_bytes = 0;
   void *nccl = nullptr;              // ncclComm_t
@@ -193,7 +201,7 @@ struct Ctx {
   int64_t cap_max = 0;
   std::string err;
   // pic_profile: CUDA event pairs per phase (0 mover, 1 order, 2 deposit,
-  // 3 ghost exchange, 4 migration before the count sync, 5 after it)
+  // 3 ghost exchange, 4 migration before the count sync, 5 after it, 6 injection)
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[PIC_PROF_PHASES];
@@ -267,6 +275,7 @@ pic_status pack_moments(Ctx *ctx, int s, double *out);
 pic_status pack_moments_async(Ctx *ctx, int s, double *out);
 pic_status join_copies(Ctx *ctx);
 pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_hat);
+pic_status inject(Ctx *ctx, int s);
 pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
 pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id);
 pic_status live_count(Ctx *ctx, int s, int64_t *n);

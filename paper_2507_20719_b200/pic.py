@@ -33,7 +33,7 @@ STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "ove
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -87,6 +87,8 @@ def load_library(path: str = LIB_PATH):
         lib.pic_get_moments_async.argtypes = [vp, C.c_int32, vp]
         lib.pic_join_copies.argtypes = [vp]
         lib.pic_implicit_sources.argtypes = [vp, vp, vp, vp]
+        lib.pic_set_injection.argtypes = [vp, C.c_int32, C.c_int32, C.c_double, P(C.c_double), C.c_double,
+                                          C.c_uint64]
         lib.pic_profile.argtypes = [vp, C.c_int32]
         lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
@@ -238,6 +240,12 @@ class Context:
         _check(self.lib.pic_implicit_sources(self.h, _ptr(chi), _ptr(rh), _ptr(jh)), self.h, "pic_implicit_sources")
         return chi, rh, jh
 
+    def set_injection(self, s: int, ppc: int, vth: float, drift, q: float, seed: int):
+        """NEXT-3 inflow injection of species s at the open x = 0 face."""
+        dr = (C.c_double * 3)(*[float(v) for v in drift])
+        _check(self.lib.pic_set_injection(self.h, s, int(ppc), float(vth), dr, float(q), int(seed)), self.h,
+               "pic_set_injection")
+
     def join_copies(self):
         """The context stream waits (on the device) for all enqueued copies."""
         _check(self.lib.pic_join_copies(self.h), self.h, "pic_join_copies")
@@ -272,7 +280,7 @@ class Context:
     def profile_read(self):
         """{phase: (ms, launches)} for mover, order, deposit, exchange (ghost
         sums + folds), migrate_pre / migrate_post (before / after the count sync)."""
-        names = ("mover", "order", "deposit", "exchange", "migrate_pre", "migrate_post")
+        names = ("mover", "order", "deposit", "exchange", "migrate_pre", "migrate_post", "inject")
         ms = (C.c_double * len(names))()
         n = (C.c_int64 * len(names))()
         _check(self.lib.pic_profile_read(self.h, ms, n), self.h, "pic_profile_read")

@@ -328,3 +328,52 @@ def test_implicit_sources_two_level(cfg):
         scale = np.abs(want).max()
         assert scale > 0
         np.testing.assert_allclose(got, want, rtol=0, atol=1e-12 * scale)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_inflow_injection(kernel):
+    """NEXT-3: inflow injection at the open x = 0 face (both species, drifting
+    Maxwellian, Philox draws on both sides) over several cycles of a C4 clone;
+    particles (incl. the injected ones, by id) and moments match the oracle."""
+    import oracle as O
+    w = I.c4(ncell=(32, 16, 16), ppc=8)
+    parts = I.make_species(w, device="cpu")
+    cycles, ppc, drift = 4, 8, (0.15, 0.01, -0.02)
+    inj = [dict(ppc=ppc, vth=sp.vth, drift=drift, q=float(parts[s]["q"][0]), seed=1000 + 17 * s)
+           for s, sp in enumerate(w.species)]
+    g = PU.oracle_grid(w)
+    F = PU.oracle_field(w, 2)
+    orc = []
+    for s, sp in enumerate(w.species):
+        P = PU.to_numpy_parts(parts[s])
+        st = np.zeros(len(P["x"]), dtype=np.int8)
+        n_inj = 0
+        for c in range(cycles):
+            st, bad = O.mover(g, F, sp.qom, w.n_iter, P, st)
+            assert bad == 0
+            a = inj[s]
+            new = O.inject(g, F, s, sp.qom, w.n_iter, a["seed"], c, a["ppc"], a["vth"], a["drift"], a["q"])
+            n_inj += len(new["x"])
+            P = {k: np.concatenate([P[k], new[k]]) for k in P}
+            st = np.concatenate([st, np.zeros(len(new["x"]), dtype=np.int8)])
+        assert n_inj > 100
+        mom, am = O.moments(g, P, st)
+        orc.append((P, st, mom, am))
+    cap = [int(p["x"].numel() * 1.25) + cycles * 16 * 16 * ppc + 64 for p in parts]
+    ctx = pic.Context(pic.make_config(w, capacity=cap, kernel=kernel))
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+        a = inj[s]
+        ctx.set_injection(s, a["ppc"], a["vth"], a["drift"], a["q"], a["seed"])
+    ctx.set_fields(I.field_window(w, 2)[1].cuda())
+    for _ in range(cycles):
+        ctx.cycle()
+    ctx.sync()
+    for s, sp in enumerate(w.species):
+        gp = {k: v.cpu().numpy() for k, v in ctx.get_particles(s).items()}
+        gm = ctx.get_moments(s).cpu().numpy()
+        rep = {"species": sp.name}
+        assert PU.compare_particles(w, sp, gp, orc[s][0], orc[s][1], rep), rep
+        assert PU.compare_moments(gm, orc[s][2], orc[s][3], rep), rep
+        assert (gp["id"] >> 62 == 1).sum() > 100
+    ctx.close()
