@@ -23,7 +23,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 PERIODIC, OPEN = 0, 1
-ALIVE, REMOVED, BAD = 0, 1, 2
+ALIVE, REMOVED, BAD, MERGED = 0, 1, 2, 3
 
 
 def build(force: bool = False) -> str:
@@ -74,6 +74,15 @@ def _load():
                                       C.c_uint32, C.c_int64, C.c_int, C.c_double, d, C.c_double, C.c_int64,
                                       d, d, d, d, d, d, d, P(C.c_int64)]
         lib.oracle_inject.restype = C.c_int64
+        lib.oracle_split.argtypes = [P(Grid), C.c_int, C.c_int64, C.c_int64, d, d, d, d, d, d, d,
+                                     P(C.c_int64), P(C.c_int8), C.c_double, C.c_double, C.c_uint32, C.c_uint32,
+                                     C.c_int64]
+        lib.oracle_split.restype = C.c_int64
+        lib.oracle_coalesce.argtypes = [P(Grid), C.c_int64, d, d, d, d, d, d, d, P(C.c_int64), P(C.c_int8),
+                                        C.c_double, C.c_double]
+        lib.oracle_coalesce.restype = C.c_int64
+        lib.oracle_child_id.argtypes = [C.c_int64, C.c_int64]
+        lib.oracle_child_id.restype = C.c_int64
         _lib = lib
     return _lib
 
@@ -198,3 +207,36 @@ def inject(g: Grid, F: FieldWindow, species: int, qom: float, n_iter: int, seed:
     res = {k: a[:n].copy() for k, a in out.items()}
     res["id"] = ids[:n].copy()
     return res
+
+
+def split(g: Grid, species: int, parts: dict, status, p_split: float, eps: float, seed: int, cycle: int):
+    """NEXT-3 splitting (reading R30): returns (parts, status) with the children appended."""
+    n = len(parts["x"])
+    cap = 2 * n + 1
+    P = {k: np.zeros(cap) for k in "xyzuvwq"}
+    ids = np.zeros(cap, dtype=np.int64)
+    st = np.zeros(cap, dtype=np.int8)
+    for k in "xyzuvwq":
+        P[k][:n] = parts[k]
+    ids[:n] = parts["id"]
+    st[:n] = status
+    m = _load().oracle_split(C.byref(g), int(species), n, cap, *[_dptr(P[k]) for k in "xyzuvwq"],
+                             ids.ctypes.data_as(C.POINTER(C.c_int64)), st.ctypes.data_as(C.POINTER(C.c_int8)),
+                             float(p_split), float(eps), seed & 0xffffffff, (seed >> 32) & 0xffffffff, int(cycle))
+    out = {k: P[k][:m].copy() for k in "xyzuvwq"}
+    out["id"] = ids[:m].copy()
+    return out, st[:m].copy()
+
+
+def coalesce(g: Grid, parts: dict, status, dv: float, frac: float) -> int:
+    """NEXT-3 coalescence (reading R31), in place; merged particles get status MERGED."""
+    n = len(parts["x"])
+    for k in "xyzuvwq":
+        assert parts[k].dtype == np.float64 and parts[k].flags.c_contiguous
+    return int(_load().oracle_coalesce(C.byref(g), n, *[_dptr(parts[k]) for k in "xyzuvwq"],
+                                       parts["id"].ctypes.data_as(C.POINTER(C.c_int64)),
+                                       status.ctypes.data_as(C.POINTER(C.c_int8)), float(dv), float(frac)))
+
+
+def child_id(parent: int, cycle: int) -> int:
+    return int(_load().oracle_child_id(int(parent), int(cycle)))

@@ -22,6 +22,8 @@
  *                             (NEXT-2, the first consumer of the moments)
  *   §III-B  PAPER.md:232-233  inflow injection of wind particles with a
  *                             prescribed bulk velocity (NEXT-3, reading R28)
+ *   §III-B  PAPER.md:238-245  particle control: splitting and pair-wise
+ *                             coalescence (NEXT-3, readings R29-R31)
  * Readings where the paper is silent or garbled are R1..R23 in DESIGN.md §3
  * (taken from SURVEY.md §8(c)); each use below names its reading.
  *
@@ -36,6 +38,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <stdio.h>
 
 /* ---------------------------------------------------------------- types -- */
 
@@ -517,4 +520,150 @@ int64_t oracle_inject(const oracle_grid *g, const oracle_field *F, int species, 
       }
     }
   return n;
+}
+
+/* ------------------------------------------- NEXT-3: particle control -- */
+
+uint64_t oracle_splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* Id of the second child of a split (R30): tagged with bit 61, otherwise a
+ * hash of the parent id and the cycle (unique with overwhelming probability). */
+int64_t oracle_child_id(int64_t parent, int64_t cycle) {
+  uint64_t h = oracle_splitmix64((uint64_t)parent ^ ((uint64_t)cycle << 48) ^ 0x5BD1E995ull);
+  return (int64_t)((h & ((1ull << 61) - 1)) | (1ull << 61));
+}
+
+/* Splitting ("randomly select particles and split each into
+ * multiple particles, adjusting their statistical weights"; reading R30):
+ * particle i (ALIVE, i < np) splits iff u0 < p_split, u0 from Philox(counter
+ * {id lo, id hi, cycle, species << 8 | 0x80}, key {seed}).  Direction e = n/|n|
+ * with n = three Box-Muller normals from the draws 0x80 (u1), 0x81 (u2, u3),
+ * 0x82 (u4): n0,n1 = sqrt(-2 ln(1-u1)) (cos, sin)(2 pi u2), n2 = sqrt(-2 ln(1-u3))
+ * cos(2 pi u4).  Children at x -/+ eps Delta_d e_d (per axis), each with q/2
+ * and the parent's velocity (charge, momentum, energy and charge centroid
+ * conserved); the split is skipped if a child would leave the parent's cell.
+ * Child 1 keeps the parent's slot and id, child 2 is appended with
+ * oracle_child_id.  Returns the new particle count (<= cap).               */
+int64_t oracle_split(const oracle_grid *g, int species, int64_t np, int64_t cap, double *x, double *y,
+                     double *z, double *u, double *v, double *w, double *q, int64_t *id, int8_t *status,
+                     double p_split, double eps, uint32_t seed_lo, uint32_t seed_hi, int64_t cycle) {
+  const uint32_t key[2] = {seed_lo, seed_hi};
+  const double two_pi = 2.0 * 3.14159265358979323846;
+  double dl[3];
+  for (int d = 0; d < 3; ++d) dl[d] = g->len[d] / (double)g->ncell[d];
+  int64_t n = np;
+  for (int64_t i = 0; i < np; ++i) {
+    if (status[i] != ORACLE_ALIVE) continue;
+    uint64_t uid = (uint64_t)id[i];
+    double r[6];
+    for (int call = 0; call < 3; ++call) {
+      uint32_t c[4] = {(uint32_t)uid, (uint32_t)(uid >> 32), (uint32_t)cycle, ((uint32_t)species << 8) | (0x80u + call)};
+      oracle_philox4x32_10(c, key);
+      r[2 * call] = u53(c[0], c[1]);
+      r[2 * call + 1] = u53(c[2], c[3]);
+    }
+    if (!(r[0] < p_split)) continue;
+    double rad1 = sqrt(-2.0 * log(1.0 - r[1]));
+    double rad2 = sqrt(-2.0 * log(1.0 - r[3]));
+    double nv[3] = {rad1 * cos(two_pi * r[2]), rad1 * sin(two_pi * r[2]), rad2 * cos(two_pi * r[4])};
+    double nrm = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+    if (!(nrm > 0.0)) continue;
+    double pos[3] = {x[i], y[i], z[i]}, a[3], b[3];
+    int ok = 1;
+    for (int d = 0; d < 3; ++d) {
+      double dd = eps * dl[d] * (nv[d] / nrm);
+      a[d] = pos[d] - dd;
+      b[d] = pos[d] + dd;
+      double c0 = floor(pos[d] / dl[d]);
+      if (floor(a[d] / dl[d]) != c0 || floor(b[d] / dl[d]) != c0) ok = 0;
+    }
+    if (!ok || n >= cap) continue;
+    double qh = q[i] / 2.0;
+    x[n] = b[0]; y[n] = b[1]; z[n] = b[2];
+    u[n] = u[i]; v[n] = v[i]; w[n] = w[i];
+    q[n] = qh;
+    id[n] = oracle_child_id(id[i], cycle);
+    status[n] = ORACLE_ALIVE;
+    ++n;
+    x[i] = a[0]; y[i] = a[1]; z[i] = a[2];
+    q[i] = qh;
+  }
+  return n;
+}
+
+/* Coalescence ("pair-wise merging between particles that are
+ * close in the phase space by combining their statistical weights"; reading
+ * R31).  Per cell with 2 <= n_c <= 512 ALIVE particles: sort them by
+ * (floor(u/dv), floor(v/dv), floor(w/dv), id); scan the sorted list and merge
+ * neighbours i, i+1 whose three velocity bins are equal (then continue at i+2)
+ * until m_c = floor(frac n_c) merges.  Merge: q = q1 + q2, x = (q1 x1 + q2 x2)/q,
+ * v = (q1 v1 + q2 v2)/q per component (charge, momentum and the charge
+ * centroid conserved); the particle with the smaller id keeps the result, the
+ * other becomes ORACLE_MERGED.  Returns the number of merges.               */
+enum { ORACLE_MERGED = 3 };
+typedef struct { int64_t cell, bx, by, bz, id, idx; } coal_key;
+static int coal_cmp(const void *pa, const void *pb) {
+  const coal_key *a = (const coal_key *)pa, *b = (const coal_key *)pb;
+  if (a->cell != b->cell) return a->cell < b->cell ? -1 : 1;
+  if (a->bx != b->bx) return a->bx < b->bx ? -1 : 1;
+  if (a->by != b->by) return a->by < b->by ? -1 : 1;
+  if (a->bz != b->bz) return a->bz < b->bz ? -1 : 1;
+  if (a->id != b->id) return a->id < b->id ? -1 : 1;
+  return 0;
+}
+int64_t oracle_coalesce(const oracle_grid *g, int64_t np, double *x, double *y, double *z, double *u,
+                        double *v, double *w, double *q, int64_t *id, int8_t *status, double dv, double frac) {
+  double dl[3];
+  for (int d = 0; d < 3; ++d) dl[d] = g->len[d] / (double)g->ncell[d];
+  coal_key *k = (coal_key *)malloc(sizeof(coal_key) * (size_t)(np > 0 ? np : 1));
+  int64_t m = 0;
+  for (int64_t i = 0; i < np; ++i) {
+    if (status[i] != ORACLE_ALIVE) continue;
+    int64_t cx = (int64_t)floor(x[i] / dl[0]), cy = (int64_t)floor(y[i] / dl[1]), cz = (int64_t)floor(z[i] / dl[2]);
+    k[m].cell = (cz * g->ncell[1] + cy) * g->ncell[0] + cx;
+    k[m].bx = (int64_t)floor(u[i] / dv);
+    k[m].by = (int64_t)floor(v[i] / dv);
+    k[m].bz = (int64_t)floor(w[i] / dv);
+    k[m].id = id[i];
+    k[m].idx = i;
+    ++m;
+  }
+  qsort(k, (size_t)m, sizeof(coal_key), coal_cmp);
+  int64_t merges = 0;
+  for (int64_t s0 = 0; s0 < m;) {
+    int64_t s1 = s0;
+    while (s1 < m && k[s1].cell == k[s0].cell) ++s1;
+    int64_t nc = s1 - s0;
+    if (nc >= 2 && nc <= 512) {
+      int64_t mc = (int64_t)floor(frac * (double)nc), done = 0;
+      for (int64_t t = s0; t + 1 < s1 && done < mc;) {
+        const coal_key *a = &k[t], *b = &k[t + 1];
+        if (a->bx == b->bx && a->by == b->by && a->bz == b->bz) {
+          int64_t i1 = a->idx, i2 = b->idx;        /* a has the smaller id */
+          double qs = q[i1] + q[i2];
+          double nx = (q[i1] * x[i1] + q[i2] * x[i2]) / qs;
+          double ny = (q[i1] * y[i1] + q[i2] * y[i2]) / qs;
+          double nz = (q[i1] * z[i1] + q[i2] * z[i2]) / qs;
+          double nu = (q[i1] * u[i1] + q[i2] * u[i2]) / qs;
+          double nv = (q[i1] * v[i1] + q[i2] * v[i2]) / qs;
+          double nw = (q[i1] * w[i1] + q[i2] * w[i2]) / qs;
+          x[i1] = nx; y[i1] = ny; z[i1] = nz; u[i1] = nu; v[i1] = nv; w[i1] = nw; q[i1] = qs;
+          status[i2] = ORACLE_MERGED;
+          ++done;
+          t += 2;
+        } else {
+          t += 1;
+        }
+      }
+      merges += done;
+    }
+    s0 = s1;
+  }
+  free(k);
+  return merges;
 }
