@@ -237,6 +237,19 @@ PIC_API pic_status pic_implicit_sources(pic_ctx *ctx, double *chi, double *rho_h
 PIC_API pic_status pic_set_injection(pic_ctx *ctx, int32_t s, int32_t ppc, double vth, const double drift[3],
                                      double q, uint64_t seed);
 
+/* NEXT-3 particle control of species s on this rank (
+ * readings R29-R31), between cycles.  Monitor: n = live count (synchronises);
+ * n < target (1 - theta): splitting — each particle splits with probability
+ * p = min(1, (target - n)/n) (Philox draw keyed by its id, seed and the cycle)
+ * into two of half charge at x -/+ eps Delta e, e a random unit vector, unless
+ * a child would leave the cell; n > target (1 + theta): coalescence — in each
+ * cell with 2..512 particles sorted by (floor(v/dv) per component, id),
+ * neighbours with equal velocity bins merge pair-wise (charge-weighted x and
+ * v; the smaller id survives) until floor(frac n_c) merges, frac = (n -
+ * target)/n.  *action: 0 none, 1 split, 2 coalesced.                       */
+PIC_API pic_status pic_control(pic_ctx *ctx, int32_t s, int64_t target, double theta, double eps, double dv,
+                               uint64_t seed, int32_t *action);
+
 /* Make the context stream wait (on the device, no host block) for every copy
  * enqueued by pic_get_moments_async / pic_set_fields so far.                 */
 PIC_API pic_status pic_join_copies(pic_ctx *ctx);

@@ -522,6 +522,19 @@ pic_status pic_set_injection(pic_ctx *p, int32_t s, int32_t ppc, double vth, con
   return PIC_OK;
 }
 
+pic_status pic_control(pic_ctx *p, int32_t s, int64_t target, double theta, double eps, double dv, uint64_t seed,
+                       int32_t *action) {
+  if (!p || !action) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  if (ctx->sp[s].moved || !ctx->sp[s].order_valid)
+    return fail(ctx, PIC_ESTATE, "pic_control runs between cycles (after pic_exchange)");
+  if (!(theta >= 0.0) || !(eps > 0.0 && eps < 0.5) || !(dv > 0.0))
+    return fail(ctx, PIC_EINVAL, "pic_control: theta >= 0, 0 < eps < 0.5, dv > 0");
+  return control(ctx, s, target, theta, eps, dv, seed, action);
+}
+
 pic_status pic_join_copies(pic_ctx *p) {
   if (!p) return PIC_EINVAL;
   return join_copies(C(p));

@@ -1,0 +1,293 @@
+// control.cu — NEXT-3 particle control (readings R29-R31,
+// DESIGN.md §3): the per-domain monitor, splitting and pair-wise coalescence.
+//
+// Splitting: one thread per live particle (cell order); Philox draws keyed by
+// the particle id decide and orient the split; the second child is appended
+// and ranked as an arrival (the order is rebuilt afterwards).  Coalescence:
+// one CTA per tile, one warp per cell at a time; the cell's particles are
+// bitonic-sorted in shared memory by (velocity bins, id), lane 0 picks the
+// pairs, the lanes merge them (the keeper is written in place, the partner's
+// key becomes KEY_DEAD) and the order is recounted.
+#include "pic_internal.cuh"
+
+namespace pic {
+
+__device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n1 = lo1, n2 = hi0 ^ c[3] ^ k1, n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+__device__ __forceinline__ double unif53(uint32_t a, uint32_t b) {
+  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
+}
+__device__ __forceinline__ int64_t child_id(int64_t parent, int64_t cycle) {
+  uint64_t z = (uint64_t)parent ^ ((uint64_t)cycle << 48) ^ 0x5BD1E995ull;
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (int64_t)((z & ((1ull << 61) - 1)) | (1ull << 61));
+}
+
+struct SplitArgs {
+  Geom g;
+  double *a[7];
+  int64_t *id;
+  const uint32_t *perm, *key, *nlive;
+  uint32_t *key_new, *rank, *cell_count;
+  int64_t *d_nraw;
+  int64_t cap;
+  unsigned long long *stats;
+  double p_split, eps;
+  uint32_t seed_lo, seed_hi, cycle, species;
+};
+
+__global__ void __launch_bounds__(256) split_kernel(const SplitArgs A) {
+  const int64_t n = *A.nlive;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int64_t)blockIdx.x * blockDim.x >= n) return;   // whole warps leave together
+  int64_t slot = -1;
+  uint32_t k = KEY_DEAD;
+  if (q < n) {
+    const uint32_t p = A.perm[q];
+    const uint64_t uid = (uint64_t)A.id[p];
+    double r[6];
+#pragma unroll
+    for (int call = 0; call < 3; ++call) {
+      uint32_t c[4] = {(uint32_t)uid, (uint32_t)(uid >> 32), A.cycle, (A.species << 8) | (0x80u + call)};
+      philox10(c, A.seed_lo, A.seed_hi);
+      r[2 * call] = unif53(c[0], c[1]);
+      r[2 * call + 1] = unif53(c[2], c[3]);
+    }
+    if (r[0] < A.p_split) {
+      const double two_pi = 2.0 * 3.14159265358979323846;
+      const double rad1 = sqrt(-2.0 * log(1.0 - r[1])), rad2 = sqrt(-2.0 * log(1.0 - r[3]));
+      const double nv[3] = {rad1 * cos(two_pi * r[2]), rad1 * sin(two_pi * r[2]), rad2 * cos(two_pi * r[4])};
+      const double nrm = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+      if (nrm > 0.0) {
+        // positions are in cell units: the displacement eps Delta_d e_d is eps e_d
+        double lo[3], hi[3];
+        bool ok = true;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double x = A.a[d][p], dd = A.eps * (nv[d] / nrm);
+          lo[d] = x - dd;
+          hi[d] = x + dd;
+          const double c0 = floor(x);
+          ok &= floor(lo[d]) == c0 && floor(hi[d]) == c0;
+        }
+        if (ok) {
+          slot = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(A.d_nraw), 1ull);
+          if (slot >= A.cap) {
+            atomicAdd(&A.stats[ST_OVERFLOW], 1ull);
+            slot = -1;
+          } else {
+            const double qh = A.a[6][p] * 0.5;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              A.a[d][slot] = hi[d];
+              A.a[3 + d][slot] = A.a[3 + d][p];
+              A.a[d][p] = lo[d];
+            }
+            A.a[6][slot] = qh;
+            A.a[6][p] = qh;
+            A.id[slot] = child_id((int64_t)uid, A.cycle);
+            k = A.key[q];
+            A.key_new[slot] = k;
+          }
+        }
+      }
+    }
+  }
+  const bool counted = slot >= 0;
+  const uint32_t rk = count_rank(A.cell_count, A.g.ncells, k, counted, true);
+  if (counted) A.rank[slot] = rk;
+}
+
+// ---------------------------------------------------------- coalescence ----
+constexpr int COAL_MAX = 512;        // cells with more particles are left alone (R31)
+constexpr int COAL_WARPS = 4;
+struct CoalItem { int64_t bx, by, bz, id; int32_t q; int32_t pad; };
+constexpr size_t COAL_SMEM = sizeof(CoalItem) * COAL_MAX * COAL_WARPS + sizeof(int32_t) * COAL_MAX * COAL_WARPS;
+
+struct CoalArgs {
+  Geom g;
+  double *a[7];
+  const int64_t *id;
+  const uint32_t *perm, *cell_off;
+  uint32_t *key_new;
+  double dv, frac;
+  unsigned long long *merges;
+};
+
+__device__ __forceinline__ bool coal_less(const CoalItem &x, const CoalItem &y) {
+  if (x.bx != y.bx) return x.bx < y.bx;
+  if (x.by != y.by) return x.by < y.by;
+  if (x.bz != y.bz) return x.bz < y.bz;
+  return x.id < y.id;
+}
+
+__global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  CoalItem *it = reinterpret_cast<CoalItem *>(smem_raw) + warp * COAL_MAX;
+  int32_t *pairs = reinterpret_cast<int32_t *>(reinterpret_cast<CoalItem *>(smem_raw) + COAL_WARPS * COAL_MAX) +
+                   warp * COAL_MAX;
+  const int64_t tile = blockIdx.x;
+  for (int cl = warp; cl < TILE3; cl += COAL_WARPS) {
+    const int64_t c = tile * TILE3 + cl;
+    const uint32_t q0 = A.cell_off[c], q1 = A.cell_off[c + 1];
+    const int nc = (int)(q1 - q0);
+    if (nc < 2 || nc > COAL_MAX) continue;
+    int N = 1;
+    while (N < nc) N <<= 1;
+    for (int i = lane; i < N; i += 32) {
+      CoalItem e;
+      if (i < nc) {
+        const uint32_t p = A.perm[q0 + i];
+        e.bx = (int64_t)floor(A.a[3][p] / A.dv);
+        e.by = (int64_t)floor(A.a[4][p] / A.dv);
+        e.bz = (int64_t)floor(A.a[5][p] / A.dv);
+        e.id = A.id[p];
+        e.q = (int32_t)i;
+      } else {
+        e.bx = e.by = e.bz = e.id = INT64_MAX;
+        e.q = -1;
+      }
+      it[i] = e;
+    }
+    __syncwarp();
+    // bitonic sort of N items by (bins, id)
+    for (int kk = 2; kk <= N; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < N; i += 32) {
+          const int l = i ^ j;
+          if (l > i) {
+            const bool up = (i & kk) == 0;
+            CoalItem x = it[i], y = it[l];
+            if (coal_less(y, x) == up) { it[i] = y; it[l] = x; }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    // pairs in sorted order (lane 0, sequential like the definition)
+    int np = 0;
+    if (lane == 0) {
+      const int mc = (int)floor(A.frac * (double)nc);
+      for (int t = 0; t + 1 < nc && np < mc;) {
+        const CoalItem &x = it[t], &y = it[t + 1];
+        if (x.bx == y.bx && x.by == y.by && x.bz == y.bz) {
+          pairs[np++] = t;
+          t += 2;
+        } else {
+          t += 1;
+        }
+      }
+    }
+    np = __shfl_sync(0xffffffffu, np, 0);
+    __syncwarp();
+    for (int m = lane; m < np; m += 32) {
+      const int t = pairs[m];
+      const uint32_t p1 = A.perm[q0 + it[t].q], p2 = A.perm[q0 + it[t + 1].q];   // p1 has the smaller id
+      const double qa = A.a[6][p1], qb = A.a[6][p2], qs = qa + qb;
+#pragma unroll
+      for (int d = 0; d < 6; ++d) A.a[d][p1] = (qa * A.a[d][p1] + qb * A.a[d][p2]) / qs;
+      A.a[6][p1] = qs;
+      A.key_new[p2] = KEY_DEAD;
+    }
+    if (lane == 0 && np) atomicAdd(A.merges, (unsigned long long)np);
+    __syncwarp();
+  }
+}
+
+// Rank every position [0, *d_nraw) anew (after coalescence killed some).
+__global__ void recount_kernel(const uint32_t *__restrict__ key_new, uint32_t *__restrict__ rank,
+                               uint32_t *__restrict__ cell_count, int64_t ncells, const int64_t *__restrict__ d_nraw) {
+  const int64_t n = *d_nraw;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t p = base + threadIdx.x;
+    const bool act = p < n;
+    const uint32_t k = act ? key_new[p] : KEY_DEAD;
+    const bool counted = act && k < KEY_FIRST_RESERVED;
+    const uint32_t r = count_rank(cell_count, ncells, k, counted, true);
+    if (counted) rank[p] = r;
+  }
+}
+
+pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, double dv, uint64_t seed,
+                   int32_t *action) {
+  SpeciesStore &sp = ctx->sp[s];
+  int64_t n = 0;
+  pic_status st = live_count(ctx, s, &n);
+  if (st != PIC_OK) return st;
+  *action = 0;
+  if (n == 0 || target <= 0) return PIC_OK;
+  const Geom &g = ctx->geom;
+  const uint32_t *nlive = sp.cell_off + g.ncells;
+  if ((double)n < (double)target * (1.0 - theta)) {
+    // splitting (R30): every live particle splits with probability p
+    SplitArgs A;
+    A.g = g;
+    for (int k = 0; k < 7; ++k) A.a[k] = sp.a[k];
+    A.id = sp.id;
+    A.perm = sp.perm;
+    A.key = sp.key;
+    A.nlive = nlive;
+    A.key_new = sp.key_new;
+    A.rank = sp.rank;
+    A.cell_count = sp.cell_count;
+    A.d_nraw = sp.d_nraw;
+    A.cap = sp.cap;
+    A.stats = ctx->stats;
+    A.p_split = std::min(1.0, (double)(target - n) / (double)n);
+    A.eps = eps;
+    A.seed_lo = (uint32_t)seed;
+    A.seed_hi = (uint32_t)(seed >> 32);
+    A.cycle = (uint32_t)ctx->cycle;
+    A.species = (uint32_t)s;
+    split_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(A); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+    sp.n_raw = std::min<int64_t>(sp.cap, sp.n_raw + n);
+    *action = 1;
+    return build_order(ctx, s);
+  }
+  if ((double)n > (double)target * (1.0 + theta)) {
+    // coalescence (R31): pairs in each cell, then a full recount of the order
+    CoalArgs A;
+    A.g = g;
+    for (int k = 0; k < 7; ++k) A.a[k] = sp.a[k];
+    A.id = sp.id;
+    A.perm = sp.perm;
+    A.cell_off = sp.cell_off;
+    A.key_new = sp.key_new;
+    A.dv = dv;
+    A.frac = (double)(n - target) / (double)n;
+    A.merges = reinterpret_cast<unsigned long long *>(ctx->dev_counts + 60);
+    PIC_CUDA(cudaMemsetAsync(A.merges, 0, sizeof(unsigned long long), ctx->stream));
+    PIC_CUDA(cudaFuncSetAttribute(coalesce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COAL_SMEM));
+    coalesce_kernel<<<(unsigned)g.ntiles, 32 * COAL_WARPS, COAL_SMEM, ctx->stream>>>(A); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+    *action = 2;
+    st = zero_cell_counts(ctx, s);
+    if (st != PIC_OK) return st;
+    // key_new holds the cell of every position below d_nraw (mover outputs and
+    // appends); the merged partners now carry KEY_DEAD
+    int64_t blocks = (sp.n_raw + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    recount_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_count,
+                                                                                  g.ncells, sp.d_nraw); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
+    return build_order(ctx, s);
+  }
+  return PIC_OK;
+}
+
+}  // namespace pic

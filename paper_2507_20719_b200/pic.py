@@ -33,7 +33,7 @@ STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "ove
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH):
         lib.pic_implicit_sources.argtypes = [vp, vp, vp, vp]
         lib.pic_set_injection.argtypes = [vp, C.c_int32, C.c_int32, C.c_double, P(C.c_double), C.c_double,
                                           C.c_uint64]
+        lib.pic_control.argtypes = [vp, C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                    P(C.c_int32)]
         lib.pic_profile.argtypes = [vp, C.c_int32]
         lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
@@ -245,6 +247,13 @@ class Context:
         dr = (C.c_double * 3)(*[float(v) for v in drift])
         _check(self.lib.pic_set_injection(self.h, s, int(ppc), float(vth), dr, float(q), int(seed)), self.h,
                "pic_set_injection")
+
+    def control(self, s: int, target: int, theta: float, eps: float, dv: float, seed: int) -> int:
+        """NEXT-3 particle control of species s; returns 0 (none), 1 (split), 2 (coalesced)."""
+        act = C.c_int32()
+        _check(self.lib.pic_control(self.h, s, int(target), float(theta), float(eps), float(dv), int(seed),
+                                    C.byref(act)), self.h, "pic_control")
+        return act.value
 
     def join_copies(self):
         """The context stream waits (on the device) for all enqueued copies."""

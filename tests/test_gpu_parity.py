@@ -377,3 +377,63 @@ def test_inflow_injection(kernel):
         assert PU.compare_moments(gm, orc[s][2], orc[s][3], rep), rep
         assert (gp["id"] >> 62 == 1).sum() > 100
     ctx.close()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_particle_control(kernel):
+    """NEXT-3 particle control between cycles: a split pass (target above the
+    count) and a coalescence pass (target below), then more cycles; particles
+    (children by their hashed ids, merged ones gone) and moments match the oracle
+    running the same sequence."""
+    import oracle as O
+    w = I.c1(randomized=True)
+    parts = I.make_species(w, device="cpu")
+    eps, seed = 0.1, 99
+    dvs = [sp.vth / 2 for sp in w.species]
+    # plan: (cycles, then control with target factor)
+    plan = [(1, 1.3), (1, 0.8), (1, None)]
+    g = PU.oracle_grid(w)
+    F = PU.oracle_field(w, 2)
+    orc = []
+    for s, sp in enumerate(w.species):
+        P = PU.to_numpy_parts(parts[s])
+        st = np.zeros(len(P["x"]), dtype=np.int8)
+        cyc = 0
+        n0 = len(P["x"])
+        for ncyc, fac in plan:
+            for _ in range(ncyc):
+                st, bad = O.mover(g, F, sp.qom, w.n_iter, P, st)
+                assert bad == 0
+                cyc += 1
+            if fac is None:
+                continue
+            n = int((st == O.ALIVE).sum())
+            target = int(fac * n0)
+            if n < target * (1 - 0.05):
+                P, st = O.split(g, s, P, st, min(1.0, (target - n) / n), eps, seed, cyc)
+            elif n > target * (1 + 0.05):
+                assert O.coalesce(g, P, st, dvs[s], (n - target) / n) > 0
+        mom, am = O.moments(g, P, st)
+        orc.append((P, st, mom, am))
+    cap = [int(p["x"].numel() * 2.2) + 64 for p in parts]
+    ctx = pic.Context(pic.make_config(w, capacity=cap, kernel=kernel))
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+    ctx.set_fields(I.field_window(w, 2)[1].cuda())
+    n0s = [p["x"].numel() for p in parts]
+    acts = []
+    for ncyc, fac in plan:
+        for _ in range(ncyc):
+            ctx.cycle()
+        if fac is not None:
+            acts.append([ctx.control(s, int(fac * n0s[s]), 0.05, eps, dvs[s], seed) for s in range(len(parts))])
+    # the last cycle's moments are of the state after the last control pass + cycle
+    ctx.sync()
+    assert acts == [[1, 1], [2, 2]]
+    for s, sp in enumerate(w.species):
+        gp = {k: v.cpu().numpy() for k, v in ctx.get_particles(s).items()}
+        gm = ctx.get_moments(s).cpu().numpy()
+        rep = {"species": sp.name}
+        assert PU.compare_particles(w, sp, gp, orc[s][0], orc[s][1], rep), rep
+        assert PU.compare_moments(gm, orc[s][2], orc[s][3], rep), rep
+    ctx.close()
