@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
     ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
     ap.add_argument("--relativistic", action="store_true", help="relativistic Eq. 2 (NEXT-1) on the same workload")
+    ap.add_argument("--control", action="store_true", help="also time one particle-control split and coalescence pass (NEXT-3)")
     ap.add_argument("--ghost", type=int, default=2)
     ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
@@ -224,7 +225,8 @@ def main():
     parts = I.make_species(w, device="cuda")
     n_local = [p["x"].numel() for p in parts]
     face = w.ncell[1] * w.ncell[2]
-    cap = [int(n * 1.08) + 65536 + (4 * face * 64 if args.config == "c4s" else 0) for n in n_local]
+    cap = [int(n * (1.35 if args.control else 1.08)) + 65536 + (4 * face * 64 if args.config == "c4s" else 0)
+           for n in n_local]
     nccl_id = decomp.broadcast_nccl_id(pic.pic_nccl_id) if world > 1 else None
     cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
                           transport=args.transport, kernel=args.kernel)
@@ -395,6 +397,25 @@ def main():
                  "ms_per_call": ms2, "nodes": nodes, "bytes_per_node": b_node,
                  "achieved_gbs": nodes * b_node / (ms2 / 1e3) / 1e9}
 
+    # ---- NEXT-3 particle control: one split pass (+20 % target) and one
+    # coalescence pass (back to the initial count), timed on the device
+    next3 = None
+    if args.control and world == 1:
+        res = {}
+        for name, fac in (("split", 1.2), ("coalesce", 0.9)):
+            n0 = [ctx.count(s) for s in range(n_sp)]
+            a3 = torch.cuda.Event(enable_timing=True)
+            b3 = torch.cuda.Event(enable_timing=True)
+            a3.record(stream)
+            acts = [ctx.control(s, int(fac * n0[s]) if name == "split" else int(n_alive / n_sp * fac), 0.05, 0.1,
+                                w.species[s].vth / 2, 7) for s in range(n_sp)]
+            b3.record(stream)
+            torch.cuda.synchronize()
+            n1 = [ctx.count(s) for s in range(n_sp)]
+            res[name] = {"ms": a3.elapsed_time(b3), "actions": acts, "particles_before": sum(n0),
+                         "particles_after": sum(n1)}
+        next3 = {"what": "pic_control on every species (count sync, pass, order rebuild)", **res}
+
     cpu = None
     if parts_cpu_sample is not None:
         threads = torch.get_num_threads()
@@ -417,6 +438,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "next2_sources": next2,
+            "next3_control": next3,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "phase_ms": {"mover+order": mover_avg, "moments+exchange": sum(rest_ms) / len(rest_ms),

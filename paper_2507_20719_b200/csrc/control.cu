@@ -255,6 +255,8 @@ pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, do
     A.species = (uint32_t)s;
     split_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(A); ++ctx->launches;
     PIC_CUDA(cudaGetLastError());
+    st = clamp_nraw(ctx, s);
+    if (st != PIC_OK) return st;
     sp.n_raw = std::min<int64_t>(sp.cap, sp.n_raw + n);
     *action = 1;
     return build_order(ctx, s);

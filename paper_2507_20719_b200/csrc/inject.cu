@@ -154,6 +154,16 @@ __global__ void __launch_bounds__(256) inject_kernel(const InjectArgs A) {
   if (counted) A.rank[slot] = r;
 }
 
+__global__ void clamp_nraw_kernel(int64_t *d_nraw, int64_t cap) {
+  if (*d_nraw > cap) *d_nraw = cap;
+}
+
+pic_status clamp_nraw(Ctx *ctx, int s) {
+  clamp_nraw_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sp[s].d_nraw, ctx->sp[s].cap); ++ctx->launches;
+  PIC_CUDA(cudaGetLastError());
+  return PIC_OK;
+}
+
 pic_status inject(Ctx *ctx, int s) {
   SpeciesStore &sp = ctx->sp[s];
   const InjectParams &ip = ctx->inj[s];
@@ -185,6 +195,8 @@ pic_status inject(Ctx *ctx, int s) {
   const int64_t total = g.ncell[1] * g.ncell[2] * (int64_t)ip.ppc;
   inject_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
+  pic_status st = clamp_nraw(ctx, s);
+  if (st != PIC_OK) return st;
   sp.n_raw = std::min<int64_t>(sp.cap, sp.n_raw + total);
   return PIC_OK;
 }

@@ -276,6 +276,9 @@ pic_status pack_moments_async(Ctx *ctx, int s, double *out);
 pic_status join_copies(Ctx *ctx);
 pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_hat);
 pic_status inject(Ctx *ctx, int s);
+// After an append kernel whose slot counter may have run past the capacity
+// (those appends were dropped and counted as overflow): d_nraw = min(d_nraw, cap).
+pic_status clamp_nraw(Ctx *ctx, int s);
 pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, double dv, uint64_t seed,
                    int32_t *action);
 pic_status live_count(Ctx *ctx, int s, int64_t *n);
