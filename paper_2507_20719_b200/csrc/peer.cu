@@ -55,6 +55,8 @@ struct PeerDesc {
   int64_t mig_cap;             // records per side and species
   int64_t m_plane, m_nx;       // moment array plane stride and x extent
   int64_t ghost_x;             // array x index of node slab_hi (the plane the right neighbour pulls)
+  int64_t src_off;             // NEXT-2 sources buffer (J-hat at 9 x owned nodes)
+  int64_t owned_nx;            // owned x node planes (pic_moment_shape x)
 };
 
 static unsigned grid_for(int64_t total) {
@@ -103,6 +105,12 @@ pic_status peer_setup(Ctx *ctx) {
   mine.m_plane = g.m_plane;
   mine.m_nx = g.m_n[0];
   mine.ghost_x = g.G + (g.slab_hi - g.slab_lo);
+  mine.src_off = reinterpret_cast<char *>(ctx->src_buf) - b;
+  {
+    int64_t shape[3];
+    pic_moment_shape((const pic_ctx *)ctx, shape);
+    mine.owned_nx = shape[0];
+  }
 
   // neighbours' descriptors: NCCL point-to-point through a device staging area
   char *stage = reinterpret_cast<char *>(ctx->pack);
@@ -167,6 +175,8 @@ pic_status peer_setup(Ctx *ctx) {
     L.m_plane = nb[side].m_plane;
     L.m_nx = nb[side].m_nx;
     L.ghost_x = nb[side].ghost_x;
+    L.src = reinterpret_cast<double *>(mapped[side] + nb[side].src_off);
+    L.owned_nx = nb[side].owned_nx;
   }
   PIC_CUDA(cudaMemset(ctx->peer_ctl, 0, sizeof(PeerCtl)));
   PIC_CUDA(cudaDeviceSynchronize());
@@ -222,7 +232,7 @@ __global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long 
   }
 }
 
-static pic_status barrier(Ctx *ctx) {
+pic_status peer_barrier(Ctx *ctx) {
   ++ctx->peer_epoch;
   peer_barrier_kernel<<<1, 1, 0, ctx->stream>>>(ctx->peer_ctl->flag, ctx->link[0].flag, ctx->link[1].flag,
                                                 ctx->peer_epoch, &ctx->peer_ctl->err); ++ctx->launches;
@@ -302,7 +312,7 @@ __global__ void arrive_finish_kernel(const ArriveArgs A, int S) {
 pic_status peer_migrate(Ctx *ctx, int s0, int s1) {
   {
     PhaseTimer t(ctx, 4);
-    pic_status st = barrier(ctx);
+    pic_status st = peer_barrier(ctx);
     if (st != PIC_OK) return st;
   }
   PhaseTimer t(ctx, 5);
@@ -355,7 +365,7 @@ pic_status launch_fold_axis(Ctx *ctx, int s, int axis, int64_t x0, int64_t nxr);
 pic_status peer_exchange(Ctx *ctx) {
   const Geom &g = ctx->geom;
   const int S = ctx->cfg.n_species;
-  pic_status st = barrier(ctx);
+  pic_status st = peer_barrier(ctx);
   if (st != PIC_OK) return st;
   const Ctx::PeerLink &L = ctx->link[0];
   if (L.mapped) {

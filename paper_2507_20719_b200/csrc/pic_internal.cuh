@@ -186,6 +186,8 @@ struct Ctx {
     int64_t mig_cap = 0;
     double *mom[PIC_MAX_SPECIES] = {};
     int64_t m_plane = 0, m_nx = 0, ghost_x = 0;
+    double *src = nullptr;           // its NEXT-2 sources buffer
+    int64_t owned_nx = 0;
   } link[2];                         // [0] left, [1] right
   bool peer = false;
   unsigned long long peer_epoch = 0;
@@ -269,6 +271,7 @@ void peer_close(Ctx *ctx);
 PeerOut peer_out(const Ctx *ctx, int s);
 pic_status peer_migrate(Ctx *ctx, int s0, int s1);
 pic_status peer_exchange(Ctx *ctx);
+pic_status peer_barrier(Ctx *ctx);
 pic_status recompute_keys(Ctx *ctx, int s, int64_t from, int64_t to);
 pic_status zero_moments(Ctx *ctx, int s);
 pic_status pack_moments(Ctx *ctx, int s, double *out);

@@ -8,7 +8,7 @@
 // rho-hat = sum_s rho_s - dt div J-hat.  Derivatives: second-order central
 // differences over the owned nodes, periodic wrap, one-sided first order at
 // the boundary nodes of an open axis (R27).  Two HBM-bound stencil passes over
-// the owned nodes (one thread per node); single rank in this build.
+// the owned nodes (one thread per node).
 #include "pic_internal.cuh"
 
 namespace pic {
@@ -22,6 +22,12 @@ struct SourcesArgs {
   int64_t n[3];                         // owned nodes
   double invV;
   double *chi, *rho_hat, *J_hat;        // [9][n], [n], [3][n] (owned-node layout)
+  // x neighbours (multi-rank, peer transport): their moment arrays and J-hat
+  int has_nb[2];                        // [0] left, [1] right
+  const double *nb_mom[2][PIC_MAX_SPECIES];
+  int64_t nb_plane[2], nb_nx[2], nb_xm[2];   // moment plane stride, x extent, x index of the adjacent plane
+  const double *nb_jh[2];               // J-hat [3][nb_total]
+  int64_t nb_total[2], nb_xj[2];        // their owned node count, x index of the adjacent owned plane
 };
 
 // owned node (i, j, k) -> element of the ghosted moment arrays
@@ -29,14 +35,28 @@ __device__ __forceinline__ int64_t src_node(const SourcesArgs &A, int64_t i, int
   return (k * A.g.m_n[1] + j) * A.g.m_n[0] + (A.g.G + i);
 }
 
-// d f / d x_axis at owned node c of a field given by a functor over owned nodes
+// d f / d x_axis at owned node c of a field given by a functor over owned nodes;
+// along x a functor index of -1 / n[0] means the left / right neighbour's
+// adjacent plane (multi-rank)
 template <class F>
 __device__ __forceinline__ double node_diff(const SourcesArgs &A, const int64_t c[3], int axis, F f) {
   const int64_t n = A.n[axis];
   const double delta = A.g.delta[axis];
   int64_t lo[3] = {c[0], c[1], c[2]}, hi[3] = {c[0], c[1], c[2]};
   double h = 2.0 * delta;
-  if (A.g.periodic[axis]) {
+  if (axis == 0 && A.g.multi_rank) {
+    const bool L = c[0] == 0, R = c[0] == n - 1;
+    if ((!L || A.has_nb[0]) && (!R || A.has_nb[1])) {
+      lo[0] = c[0] - 1;   // -1: left neighbour
+      hi[0] = c[0] + 1;   // n: right neighbour
+    } else if (L) {       // global open face: one-sided (R27)
+      hi[0] = 1;          // (== n with one owned plane: the right neighbour)
+      h = delta;
+    } else {
+      lo[0] = n - 2;
+      h = delta;
+    }
+  } else if (A.g.periodic[axis]) {
     lo[axis] = c[axis] == 0 ? n - 1 : c[axis] - 1;
     hi[axis] = c[axis] == n - 1 ? 0 : c[axis] + 1;
   } else if (c[axis] == 0) {
@@ -99,8 +119,16 @@ __global__ void chi_jhat_kernel(const SourcesArgs A) {
         double div = 0.0;
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
-          const double *comp = m + pidx[ra][b] * P;
-          div += node_diff(A, c, b, [&](const int64_t q[3]) { return comp[src_node(A, q[0], q[1], q[2])] * A.invV; });
+          const int cm = pidx[ra][b];
+          const double *comp = m + cm * P;
+          div += node_diff(A, c, b, [&](const int64_t q[3]) {
+            if (q[0] < 0 || q[0] >= A.n[0]) {   // neighbour's adjacent owned plane
+              const int sd = q[0] < 0 ? 0 : 1;
+              return A.nb_mom[sd][s][cm * A.nb_plane[sd] + (q[2] * A.g.m_n[1] + q[1]) * A.nb_nx[sd] + A.nb_xm[sd]] *
+                     A.invV;
+            }
+            return comp[src_node(A, q[0], q[1], q[2])] * A.invV;
+          });
         }
         x[ra] = m[(1 + ra) * P + me] * A.invV - (dt / 2.0) * div;
       }
@@ -127,15 +155,22 @@ __global__ void rho_hat_kernel(const SourcesArgs A) {
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       const double *comp = A.J_hat + b * total;
-      div += node_diff(A, c, b, [&](const int64_t q[3]) { return comp[(q[2] * A.n[1] + q[1]) * A.n[0] + q[0]]; });
+      div += node_diff(A, c, b, [&](const int64_t q[3]) {
+        if (q[0] < 0 || q[0] >= A.n[0]) {
+          const int sd = q[0] < 0 ? 0 : 1;
+          return A.nb_jh[sd][b * A.nb_total[sd] + (q[2] * A.n[1] + q[1]) * (A.nb_total[sd] / (A.n[1] * A.n[2])) +
+                             A.nb_xj[sd]];
+        }
+        return comp[(q[2] * A.n[1] + q[1]) * A.n[0] + q[0]];
+      });
     }
     A.rho_hat[t] = rho - A.g.dt * div;
   }
 }
 
 pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_hat) {
-  if (ctx->cfg.nranks != 1)
-    return fail(ctx, PIC_EINVAL, "pic_implicit_sources: single rank in this build (slab halos are NEXT)");
+  if (ctx->cfg.nranks > 1 && !ctx->peer)
+    return fail(ctx, PIC_EINVAL, "pic_implicit_sources with several ranks needs the peer transport");
   const Geom &g = ctx->geom;
   int64_t shape[3];
   pic_moment_shape((const pic_ctx *)ctx, shape);
@@ -156,9 +191,30 @@ pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_ha
   A.chi = ctx->src_buf;
   A.J_hat = ctx->src_buf + 9 * total;
   A.rho_hat = ctx->src_buf + 12 * total;
+  for (int sd = 0; sd < 2; ++sd) {
+    const Ctx::PeerLink &L = ctx->link[sd];
+    A.has_nb[sd] = (g.multi_rank && L.mapped) ? 1 : 0;
+    for (int s = 0; s < A.n_species; ++s) A.nb_mom[sd][s] = L.mom[s];
+    A.nb_plane[sd] = L.m_plane;
+    A.nb_nx[sd] = L.m_nx;
+    // left: its last owned plane (array x index ghost_x - 1); right: its first (G)
+    A.nb_xm[sd] = sd == 0 ? L.ghost_x - 1 : g.G;
+    A.nb_total[sd] = L.owned_nx * shape[1] * shape[2];
+    A.nb_jh[sd] = L.src ? L.src + 9 * A.nb_total[sd] : nullptr;
+    A.nb_xj[sd] = sd == 0 ? L.owned_nx - 1 : 0;
+  }
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  pic_status st;
+  if (g.multi_rank) {   // the neighbours' moments are final (their pic_exchange)
+    st = peer_barrier(ctx);
+    if (st != PIC_OK) return st;
+  }
   chi_jhat_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(A); ++ctx->launches;
+  if (g.multi_rank) {   // the neighbours' J-hat is complete
+    st = peer_barrier(ctx);
+    if (st != PIC_OK) return st;
+  }
   rho_hat_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   if (chi) PIC_CUDA(cudaMemcpyAsync(chi, A.chi, 9 * sizeof(double) * total, cudaMemcpyDefault, ctx->stream));

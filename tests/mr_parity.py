@@ -52,9 +52,13 @@ def run_case(name, w, cycles, kernel, transport, rank, world):
         gp = {k: v.cpu().numpy() for k, v in ctx.get_particles(s).items()}
         gm = ctx.get_moments(s).cpu().numpy()
         local.append((gp, gm))
+    # NEXT-2 sources (collective with the peer transport)
+    src = None
+    if transport == pic.TRANSPORT_PEER:
+        src = tuple(t.cpu().numpy() for t in ctx.implicit_sources())
     ctx.close()
     gathered = [None] * world
-    dist.all_gather_object(gathered, (local, stats))
+    dist.all_gather_object(gathered, (local, stats, src))
     if rank != 0:
         return None
     orc = PU.run_oracle(w.with_slab(0, w.ncell[0]), parts_all, cycles)
@@ -70,6 +74,21 @@ def run_case(name, w, cycles, kernel, transport, rank, world):
         rep["ok"] = bool(okp and okm)
         ok &= rep["ok"]
         reps.append(rep)
+    if transport == pic.TRANSPORT_PEER:
+        # two-level: sources over the union of slabs vs the oracle fed with the
+        # union of the GPU moments
+        import oracle as O
+        gms = [np.concatenate([gathered[r][0][s][1] for r in range(world)], axis=3) for s in range(len(w.species))]
+        got = [np.concatenate([gathered[r][2][i] for r in range(world)], axis=-1) for i in range(3)]
+        G = 2
+        _, EB = I.field_window(w.with_slab(0, w.ncell[0]), G)
+        nz, ny, nx = gms[0].shape[1:]
+        Bn = EB[G:G + nz, G:G + ny, G:G + nx, 3:6].numpy()
+        want = O.implicit_sources(PU.oracle_grid(w), [sp.qom for sp in w.species], gms, Bn)
+        okS = all(np.allclose(a, b, rtol=0, atol=1e-12 * np.abs(b).max()) for a, b in zip(got, want))
+        reps.append({"case": name, "kernel": kernel, "transport": transport, "sources_ok": bool(okS),
+                     "sources_err": [float(np.abs(a - b).max() / np.abs(b).max()) for a, b in zip(got, want)]})
+        ok &= okS
     return ok, reps
 
 
