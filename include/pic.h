@@ -70,7 +70,8 @@ typedef enum {
   PIC_KERNEL_AUTO = 0,     /* best available (tiled where the config allows)  */
   PIC_KERNEL_BASIC = 1,    /* one thread per particle, global field reads,
                               global fp64 atomics for the deposit              */
-  PIC_KERNEL_TILED = 2     /* cell-sorted, tile-staged fused mover + deposit   */
+  PIC_KERNEL_TILED = 2     /* cell-ordered: TMA-staged tile mover, tensor-core
+                              per-cell deposit                                 */
 } pic_kernel;
 
 /* Multi-rank transport (pic_config.transport).                              */

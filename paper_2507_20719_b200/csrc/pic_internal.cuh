@@ -125,7 +125,7 @@ struct SpeciesStore {
   int64_t cap = 0;
   double qom = 0;
   int32_t n_iter = 3;
-  bool moved = false, deposited = false, fused_deposit = false;
+  bool moved = false, deposited = false;
   bool order_valid = false;
   void swap_buffers() {
     for (int k = 0; k < 7; ++k) { double *t = a[k]; a[k] = b[k]; b[k] = t; }

@@ -10,25 +10,29 @@
 //     memory; the CTA pre-scales them by k_s = (q/m) dt/2 and k_s / c so the
 //     iteration reads E' = k_s E and a = k_s B / c directly (R7, R8).
 //  2. Warps split the tile's particles evenly; lane = particle, rounds of 32.
-//     Sources are gathered through perm (mostly contiguous runs: every cell
-//     lists its stayers first) with the next round prefetched into L1.
-//     n_iter predictor-corrector iterations (R1, R2) with trilinear gathers
-//     from shared memory (R12); x^{n+1}, v^{n+1}, boundary conditions (R10,
-//     R11, R21); the result goes to buffer B at q (sequential), and the new
-//     cell key is ranked for the counting sort of the next order.
+//     perm/key run PK_AHEAD rounds ahead and the sources SRC_STAGES - 1 rounds
+//     ahead through cp.async (LDGSTS) rings in shared memory (mostly
+//     contiguous runs: every cell lists its stayers first).  n_iter predictor-
+//     corrector iterations (R1, R2) with trilinear gathers from shared memory
+//     (R12); x^{n+1}, v^{n+1}, boundary conditions (R10, R11, R21; fast path
+//     for particles that stay inside the slab); the result goes to buffer B at
+//     q and the new cell key is ranked for the counting sort of the next order
+//     (the rank atomic of a round completes during the next one).  With the
+//     peer transport, slab leavers are written straight into the neighbour's
+//     receive buffer (send_leavers_peer).  REL = 1 instantiates the
+//     relativistic Eq. 2 (NEXT-1).
 //
 // deposit_tiled_kernel  (pic_moments; Eq. 3)
 //  Runs over the NEW order, so every particle of a cell segment really is in
-//  that cell: each lane of a warp takes one of the 8 corner nodes of the
-//  current cell for one of 4 particle slots, and accumulates the 10 moments
-//  q{1, v, vv} S_c in registers across the cell's particles (no atomics inside
-//  a cell).  When the cell changes, the 4 slots are reduced with shuffles and
-//  added to the tile's shared node accumulators (5^3 nodes x 10; shared CAS
-//  only at cell changes, where warps may meet).  Finally the tile's
-//  accumulators are added to the global ghosted moment arrays (tile faces are
-//  shared with neighbour tiles, so with fp64 atomics).  The paper's
-//  "GPU-shared memory ... and atomic operations", privatised
-//  per tile and reduced in registers.
+//  that cell.  Warp ranges are cell-aligned; per round each lane computes its
+//  particle's 8 corner weights S and 10 values q{1, v, vv} and stages them in
+//  shared memory (XOR-swizzled, conflict-free); for each run of equal cells
+//  the corner sums M = S^T V are accumulated on the fp64 tensor cores
+//  (mma.m8n8k4: 8 corners x 4 particles x 8 + 8 moments), flushed into the
+//  tile's shared node sums (5^3 x 10, shared atomics only at cell changes)
+//  and finally added to the global ghosted moment arrays with fp64 atomics
+//  (tile faces are shared).  The paper's "GPU-shared memory ... and atomic
+//  operations", privatised per tile, reduced on tensor cores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
