@@ -1,15 +1,20 @@
 /*
  * pic.h — C ABI of the B200-native particle hot path of the implicit-moment
  * PIC cycle (arXiv 2507.20719, iPIC3D): the implicit predictor-corrector
- * mover (Eq. 2) and the moment gatherer (Eq. 3), with slab decomposition and
- * NCCL exchange of ghost-node moments and migrating particles.
+ * mover (Eq. 2) and the moment gatherer (Eq. 3), with slab decomposition,
+ * ghost-node moment sums and particle migration over NVLink peer memory (or
+ * NCCL), plus the NEXT rows built on it: the relativistic mover (NEXT-1), the
+ * field solver's sources chi, rho-hat, J-hat (Eq. 5-6, NEXT-2), inflow
+ * injection and particle control (NEXT-3).
  *
  *   PAPER.md:141-145  Eq. 1  equations of motion; q_s, m_s, x_p, v_p, E_p, B_p
  *   PAPER.md:149-165  Eq. 2  predictor-corrector mover, fixed-point on v-bar
  *   PAPER.md:184-187  Eq. 3  {rho, J, Pi}_g = sum_p q {1, v, vv} W(x - x_p)
  *   PAPER.md:235-236  §III-B open boundaries (outflow particles are removed)
  *   PAPER.md:256-261, 291-334  Alg. 1: mover -> interpolation -> MPI exchange
- * Readings of the paper (R1..R23) are listed in DESIGN.md §3.
+ *   PAPER.md:199-213  Eq. 5-6 susceptibility and corrected sources (NEXT-2)
+ *   PAPER.md:232-249  §III-B injection and particle control (NEXT-3)
+ * Readings of the paper (R1..R31) are listed in DESIGN.md §3.
  *
  * Conventions (all calls):
  *  - Every entry point returns pic_status; none throws, exits or prints.
@@ -171,7 +176,8 @@ PIC_API pic_status pic_set_fields(pic_ctx *ctx, const double *EB);
  * apply the boundary conditions (R10, R11, R21).  With nranks > 1 this call
  * is COLLECTIVE: particles that left the slab migrate to their new owner rank
  * ("exiting particles are transferred using MPI"),
- * which blocks the host once for the message counts.  Ends by building the
+ * (with the NCCL transport this blocks the host once for the message counts;
+ * the peer transport does not block).  Ends by building the
  * cell order of the new state that pic_moments deposits over.                */
 PIC_API pic_status pic_mover(pic_ctx *ctx, int32_t s);
 
