@@ -83,6 +83,10 @@ def _load():
         lib.oracle_coalesce.restype = C.c_int64
         lib.oracle_child_id.argtypes = [C.c_int64, C.c_int64]
         lib.oracle_child_id.restype = C.c_int64
+        lib.oracle_bin_velocities.argtypes = [C.c_int64, d, d, d, d, P(C.c_int8), C.c_int, C.c_double, d]
+        lib.oracle_bin_velocities.restype = C.c_int64
+        lib.oracle_fit_gmm.argtypes = [C.c_int, C.c_double, d, C.c_int, C.c_int, d, d, d]
+        lib.oracle_fit_gmm.restype = C.c_int
         _lib = lib
     return _lib
 
@@ -240,3 +244,24 @@ def coalesce(g: Grid, parts: dict, status, dv: float, frac: float) -> int:
 
 def child_id(parent: int, cycle: int) -> int:
     return int(_load().oracle_child_id(int(parent), int(cycle)))
+
+
+def bin_velocities(parts: dict, status, B: int, vmax: float):
+    """NEXT-4 velocity histogram (reading R32): (hist[B][B][B] as [bz][by][bx], clipped)."""
+    n = len(parts["u"])
+    h = np.zeros((B, B, B))
+    st = status.ctypes.data_as(C.POINTER(C.c_int8)) if status is not None else None
+    c = _load().oracle_bin_velocities(n, *[_dptr(np.ascontiguousarray(parts[k], dtype=np.float64)) for k in "uvwq"],
+                                      st, int(B), float(vmax), _dptr(h))
+    return h, int(c)
+
+
+def fit_gmm(hist: np.ndarray, vmax: float, M: int, n_em: int):
+    """NEXT-4 EM fit (reading R33): (alpha[M], mu[M][3], sigma[M][6] as xx xy xz yy yz zz)."""
+    B = hist.shape[0]
+    h = np.ascontiguousarray(hist, dtype=np.float64)
+    a, mu, sg = np.zeros(M), np.zeros((M, 3)), np.zeros((M, 6))
+    rc = _load().oracle_fit_gmm(int(B), float(vmax), _dptr(h), int(M), int(n_em), _dptr(a), _dptr(mu), _dptr(sg))
+    if rc != 0:
+        raise ValueError("fewer occupied bins than components")
+    return a, mu, sg

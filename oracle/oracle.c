@@ -24,6 +24,8 @@
  *                             prescribed bulk velocity (NEXT-3, reading R28)
  *   §III-B  PAPER.md:238-245  particle control: splitting and pair-wise
  *                             coalescence (NEXT-3, readings R29-R31)
+ *   §III-D  PAPER.md:368-372  velocity binning and the Gaussian-mixture fit by
+ *                             EM (NEXT-4, readings R32-R33)
  * Readings where the paper is silent or garbled are R1..R23 in DESIGN.md §3
  * (taken from SURVEY.md §8(c)); each use below names its reading.
  *
@@ -666,4 +668,154 @@ int64_t oracle_coalesce(const oracle_grid *g, int64_t np, double *x, double *y, 
   }
   free(k);
   return merges;
+}
+
+/* --------------------------------------------------- NEXT-4: GMM fit -- */
+
+/* Velocity binning ("a three-dimensional binning operation in
+ * velocity space"; reading R32): B bins per axis over [-vmax, vmax); bin of
+ * a component = floor((v + vmax) / (2 vmax) * B) clipped to [0, B-1] (clipped
+ * particles counted); weight |q| (the statistical weight).  hist[(bz*B + by)*B
+ * + bx] += |q|.  Returns the number of clipped particles.                   */
+int64_t oracle_bin_velocities(int64_t np, const double *u, const double *v, const double *w,
+                              const double *q, const int8_t *status, int B, double vmax, double *hist) {
+  int64_t clipped = 0;
+  for (int64_t p = 0; p < np; ++p) {
+    if (status && status[p] != ORACLE_ALIVE) continue;
+    const double vel[3] = {u[p], v[p], w[p]};
+    int64_t b[3];
+    int clip = 0;
+    for (int d = 0; d < 3; ++d) {
+      double t = floor((vel[d] + vmax) / (2.0 * vmax) * (double)B);
+      if (t < 0.0) { t = 0.0; clip = 1; }
+      if (t > (double)(B - 1)) { t = (double)(B - 1); clip = 1; }
+      b[d] = (int64_t)t;
+    }
+    clipped += clip;
+    hist[(b[2] * B + b[1]) * B + b[0]] += fabs(q[p]);
+  }
+  return clipped;
+}
+
+static void inv3(const double S[6], double out[6], double *det) {
+  /* symmetric xx xy xz yy yz zz */
+  double a = S[0], b = S[1], c = S[2], d = S[3], e = S[4], f = S[5];
+  double A = d * f - e * e, Bc = -(b * f - c * e), C = b * e - c * d;
+  double D = a * f - c * c, E = -(a * e - b * c), Fz = a * d - b * b;
+  double dt = a * A + b * Bc + c * C;
+  *det = dt;
+  out[0] = A / dt; out[1] = Bc / dt; out[2] = C / dt; out[3] = D / dt; out[4] = E / dt; out[5] = Fz / dt;
+}
+
+/* Gaussian-mixture fit by EM on the histogram (reading
+ * R33): data = bin centres c_b = -vmax + (b + 1/2) 2 vmax / B with weights
+ * hist_b > 0.  Initialisation: mu_1 = centre of the heaviest bin (lowest index
+ * on ties), then farthest-point seeding (the occupied bin maximising the
+ * squared distance to the nearest chosen centre, lowest index on ties);
+ * Sigma_i = the histogram's weighted covariance + eps I; alpha_i = 1/M.
+ * Exactly n_em iterations of
+ *   E: r_bi = alpha_i N(c_b | mu_i, Sigma_i) / sum_j alpha_j N(c_b | mu_j, Sigma_j)
+ *   M: W_i = sum_b h_b r_bi; alpha_i = W_i / W; mu_i = sum_b h_b r_bi c_b / W_i;
+ *      Sigma_i = sum_b h_b r_bi (c_b - mu_i)(c_b - mu_i)^T / W_i + eps I,
+ * eps = 1e-6 (2 vmax / B)^2.  Covariances as xx xy xz yy yz zz.  Returns 0,
+ * or -1 if fewer than M bins are occupied.                                  */
+int oracle_fit_gmm(int B, double vmax, const double *hist, int M, int n_em, double *alpha, double *mu,
+                   double *sigma) {
+  const int64_t nb = (int64_t)B * B * B;
+  const double bw = 2.0 * vmax / (double)B;
+  const double eps = 1e-6 * bw * bw;
+  const double two_pi3 = pow(2.0 * 3.14159265358979323846, 1.5);
+  int64_t nocc = 0;
+  for (int64_t b = 0; b < nb; ++b) nocc += hist[b] > 0.0;
+  if (nocc < M || M < 1) return -1;
+  double *cen = (double *)malloc(sizeof(double) * 3 * (size_t)nb);
+  double W = 0.0, m1[3] = {0, 0, 0};
+  for (int64_t b = 0; b < nb; ++b) {
+    int64_t bx = b % B, by = (b / B) % B, bz = b / ((int64_t)B * B);
+    cen[3 * b] = -vmax + ((double)bx + 0.5) * bw;
+    cen[3 * b + 1] = -vmax + ((double)by + 0.5) * bw;
+    cen[3 * b + 2] = -vmax + ((double)bz + 0.5) * bw;
+    if (hist[b] > 0.0) {
+      W += hist[b];
+      for (int d = 0; d < 3; ++d) m1[d] += hist[b] * cen[3 * b + d];
+    }
+  }
+  for (int d = 0; d < 3; ++d) m1[d] /= W;
+  double cov[6] = {0, 0, 0, 0, 0, 0};
+  static const int ia[6] = {0, 0, 0, 1, 1, 2}, ib[6] = {0, 1, 2, 1, 2, 2};
+  for (int64_t b = 0; b < nb; ++b)
+    if (hist[b] > 0.0)
+      for (int k = 0; k < 6; ++k)
+        cov[k] += hist[b] * (cen[3 * b + ia[k]] - m1[ia[k]]) * (cen[3 * b + ib[k]] - m1[ib[k]]);
+  for (int k = 0; k < 6; ++k) cov[k] /= W;
+  cov[0] += eps; cov[3] += eps; cov[5] += eps;
+  /* farthest-point seeding */
+  int64_t first = -1;
+  for (int64_t b = 0; b < nb; ++b)
+    if (hist[b] > 0.0 && (first < 0 || hist[b] > hist[first])) first = b;
+  for (int d = 0; d < 3; ++d) mu[d] = cen[3 * first + d];
+  for (int i = 1; i < M; ++i) {
+    int64_t best = -1;
+    double bestd = -1.0;
+    for (int64_t b = 0; b < nb; ++b) {
+      if (!(hist[b] > 0.0)) continue;
+      double dmin = INFINITY;
+      for (int j = 0; j < i; ++j) {
+        double dd = 0.0;
+        for (int d = 0; d < 3; ++d) {
+          double t = cen[3 * b + d] - mu[3 * j + d];
+          dd += t * t;
+        }
+        if (dd < dmin) dmin = dd;
+      }
+      if (dmin > bestd) { bestd = dmin; best = b; }
+    }
+    for (int d = 0; d < 3; ++d) mu[3 * i + d] = cen[3 * best + d];
+  }
+  for (int i = 0; i < M; ++i) {
+    alpha[i] = 1.0 / (double)M;
+    for (int k = 0; k < 6; ++k) sigma[6 * i + k] = cov[k];
+  }
+  double *r = (double *)malloc(sizeof(double) * (size_t)M);
+  double *acc = (double *)malloc(sizeof(double) * (size_t)M * 10);
+  for (int it = 0; it < n_em; ++it) {
+    double inv[16][6], nrm[16];
+    for (int i = 0; i < M; ++i) {
+      double det;
+      inv3(sigma + 6 * i, inv[i], &det);
+      nrm[i] = alpha[i] / (two_pi3 * sqrt(det));
+    }
+    for (int64_t k = 0; k < (int64_t)M * 10; ++k) acc[k] = 0.0;
+    for (int64_t b = 0; b < nb; ++b) {
+      if (!(hist[b] > 0.0)) continue;
+      double tot = 0.0;
+      for (int i = 0; i < M; ++i) {
+        double x = cen[3 * b] - mu[3 * i], y = cen[3 * b + 1] - mu[3 * i + 1], z = cen[3 * b + 2] - mu[3 * i + 2];
+        const double *A = inv[i];
+        double q2 = A[0] * x * x + A[3] * y * y + A[5] * z * z + 2.0 * (A[1] * x * y + A[2] * x * z + A[4] * y * z);
+        r[i] = nrm[i] * exp(-0.5 * q2);
+        tot += r[i];
+      }
+      if (!(tot > 0.0)) continue;
+      for (int i = 0; i < M; ++i) {
+        double wr = hist[b] * (r[i] / tot);
+        double *a = acc + 10 * i;
+        a[0] += wr;
+        for (int d = 0; d < 3; ++d) a[1 + d] += wr * cen[3 * b + d];
+        for (int k = 0; k < 6; ++k) a[4 + k] += wr * cen[3 * b + ia[k]] * cen[3 * b + ib[k]];
+      }
+    }
+    for (int i = 0; i < M; ++i) {
+      const double *a = acc + 10 * i;
+      if (!(a[0] > 0.0)) continue;   /* an empty component keeps its parameters */
+      alpha[i] = a[0] / W;
+      for (int d = 0; d < 3; ++d) mu[3 * i + d] = a[1 + d] / a[0];
+      for (int k = 0; k < 6; ++k)
+        sigma[6 * i + k] = a[4 + k] / a[0] - mu[3 * i + ia[k]] * mu[3 * i + ib[k]] + ((ia[k] == ib[k]) ? eps : 0.0);
+    }
+  }
+  free(r);
+  free(acc);
+  free(cen);
+  return 0;
 }
