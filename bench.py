@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
     ap.add_argument("--relativistic", action="store_true", help="relativistic Eq. 2 (NEXT-1) on the same workload")
     ap.add_argument("--control", action="store_true", help="also time one particle-control split and coalescence pass (NEXT-3)")
+    ap.add_argument("--gmm", action="store_true", help="also time the velocity binning + GMM fit of every species (NEXT-4)")
     ap.add_argument("--ghost", type=int, default=2)
     ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
@@ -416,6 +417,20 @@ def main():
                          "particles_after": sum(n1)}
         next3 = {"what": "pic_control on every species (count sync, pass, order rebuild)", **res}
 
+    # ---- NEXT-4: velocity histogram + Gaussian-mixture fit per species
+    next4 = None
+    if args.gmm and world == 1:
+        import time as _t
+        res = []
+        for s in range(n_sp):
+            vmax = 5.0 * w.species[s].vth
+            t0 = _t.perf_counter()
+            a, mu, sg, h, clipped = ctx.gmm(s, 24, vmax, 4, 50)
+            res.append({"species": w.species[s].name, "ms": (_t.perf_counter() - t0) * 1e3, "bins": 24, "M": 4,
+                        "n_em": 50, "alpha": a.tolist(), "clipped": clipped})
+        next4 = {"what": "pic_gmm per species: 24^3 velocity bins, 4 components, 50 EM iterations (host-timed, synchronous)",
+                 "fits": res}
+
     cpu = None
     if parts_cpu_sample is not None:
         threads = torch.get_num_threads()
@@ -439,6 +454,7 @@ def main():
             "e2e": e2e,
             "next2_sources": next2,
             "next3_control": next3,
+            "next4_gmm": next4,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "phase_ms": {"mover+order": mover_avg, "moments+exchange": sum(rest_ms) / len(rest_ms),

@@ -257,6 +257,18 @@ PIC_API pic_status pic_set_injection(pic_ctx *ctx, int32_t s, int32_t ppc, doubl
 PIC_API pic_status pic_control(pic_ctx *ctx, int32_t s, int64_t target, double theta, double eps, double dv,
                                uint64_t seed, int32_t *action);
 
+/* NEXT-4 physics-aware compression (readings R32, R33) of
+ * species s on this rank, between cycles: the velocity histogram with B bins
+ * per axis over [-vmax, vmax) (weights |q|, out-of-range particles clipped to
+ * the edge bins and counted in *clipped), then a Gaussian-mixture fit with M
+ * components by n_em EM iterations on the bin centres (heaviest-bin +
+ * farthest-point seeding, covariance floor 1e-6 (2 vmax / B)^2).  Outputs
+ * (host or device, any may be NULL): alpha[M], mu[M][3], sigma[M][6] (xx xy xz
+ * yy yz zz), hist[B][B][B] ([bz][by][bx]).  1 <= B <= 64, 1 <= M <= 8.
+ * Synchronises.                                                              */
+PIC_API pic_status pic_gmm(pic_ctx *ctx, int32_t s, int32_t B, double vmax, int32_t M, int32_t n_em, double *alpha,
+                           double *mu, double *sigma, double *hist, int64_t *clipped);
+
 /* Make the context stream wait (on the device, no host block) for every copy
  * enqueued by pic_get_moments_async / pic_set_fields so far.                 */
 PIC_API pic_status pic_join_copies(pic_ctx *ctx);

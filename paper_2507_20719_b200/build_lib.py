@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpic.so")
-SOURCES = ["api.cu", "control.cu", "kernels_basic.cu", "exchange.cu", "inject.cu", "order.cu", "peer.cu", "sources.cu", "tiled.cu"]
+SOURCES = ["api.cu", "control.cu", "kernels_basic.cu", "exchange.cu", "gmm.cu", "inject.cu", "order.cu", "peer.cu", "sources.cu", "tiled.cu"]
 
 
 def _nccl_dirs():

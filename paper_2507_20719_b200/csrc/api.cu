@@ -151,6 +151,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
   const int64_t pack_elems = (g.k_n[0] + 1) * g.m_n[1] * g.m_n[2] * 10;
   int64_t opack = L.take(8 * pack_elems);
   int64_t osrc = L.take(8 * 13 * (pack_elems / 10));
+  int64_t ogmm = L.take(8 * (64 * 64 * 64 + 128));
   int64_t oslot[2 * PIC_MAX_SPECIES];
   for (int k = 0; k < 2 * c->n_species; ++k) oslot[k] = L.take(8 * pack_elems);
   int64_t ocub = L.take((int64_t)cub_bytes);
@@ -174,6 +175,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
     ctx->mig_cap = mig_cap;
     ctx->pack = (double *)(base + opack);
     ctx->src_buf = (double *)(base + osrc);
+    ctx->gmm_buf = (double *)(base + ogmm);
     ctx->cub_temp = base + ocub;
     ctx->cub_bytes = cub_bytes;
     ctx->cap_max = cap_max;
@@ -533,6 +535,17 @@ pic_status pic_control(pic_ctx *p, int32_t s, int64_t target, double theta, doub
   if (!(theta >= 0.0) || !(eps > 0.0 && eps < 0.5) || !(dv > 0.0))
     return fail(ctx, PIC_EINVAL, "pic_control: theta >= 0, 0 < eps < 0.5, dv > 0");
   return control(ctx, s, target, theta, eps, dv, seed, action);
+}
+
+pic_status pic_gmm(pic_ctx *p, int32_t s, int32_t B, double vmax, int32_t M, int32_t n_em, double *alpha, double *mu,
+                   double *sigma, double *hist, int64_t *clipped) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  if (ctx->sp[s].moved || !ctx->sp[s].order_valid)
+    return fail(ctx, PIC_ESTATE, "pic_gmm runs between cycles (after pic_exchange)");
+  return gmm_fit(ctx, s, B, vmax, M, n_em, alpha, mu, sigma, hist, clipped);
 }
 
 pic_status pic_join_copies(pic_ctx *p) {

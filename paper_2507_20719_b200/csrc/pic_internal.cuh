@@ -175,6 +175,7 @@ struct Ctx {
   int64_t mig_cap = 0;
   double *pack = nullptr;            // moment copy-out staging
   double *src_buf = nullptr;         // NEXT-2 sources: chi [9], J-hat [3], rho-hat [1] per owned node
+  double *gmm_buf = nullptr;         // NEXT-4: velocity histogram [64^3] + mixture parameters
   void *workspace = nullptr;         // caller's device workspace (pic_init)
   // peer transport (peer.cu): own control block and the mapped neighbours
   PeerCtl *peer_ctl = nullptr;
@@ -287,7 +288,8 @@ pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, do
 pic_status live_count(Ctx *ctx, int s, int64_t *n);
 pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
 pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id);
-pic_status live_count(Ctx *ctx, int s, int64_t *n);
+pic_status gmm_fit(Ctx *ctx, int s, int B, double vmax, int M, int n_em, double *alpha, double *mu, double *sigma,
+                   double *hist_out, int64_t *clipped);
 
 // ---------------------------------------------------------- device helpers ---
 // Periodic wrap of a cell-unit coordinate (R10): one wrap, then test.

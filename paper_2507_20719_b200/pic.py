@@ -33,7 +33,7 @@ STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "ove
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_gmm", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH):
                                           C.c_uint64]
         lib.pic_control.argtypes = [vp, C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                     P(C.c_int32)]
+        lib.pic_gmm.argtypes = [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, vp, vp, vp, vp,
+                                P(C.c_int64)]
         lib.pic_profile.argtypes = [vp, C.c_int32]
         lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
@@ -254,6 +256,16 @@ class Context:
         _check(self.lib.pic_control(self.h, s, int(target), float(theta), float(eps), float(dv), int(seed),
                                     C.byref(act)), self.h, "pic_control")
         return act.value
+
+    def gmm(self, s: int, B: int, vmax: float, M: int, n_em: int):
+        """NEXT-4: (alpha[M], mu[M][3], sigma[M][6], hist[B][B][B], clipped) as numpy arrays."""
+        import numpy as np
+        a, mu, sg = np.zeros(M), np.zeros((M, 3)), np.zeros((M, 6))
+        h = np.zeros((B, B, B))
+        clipped = C.c_int64()
+        _check(self.lib.pic_gmm(self.h, s, int(B), float(vmax), int(M), int(n_em), a.ctypes.data, mu.ctypes.data,
+                                sg.ctypes.data, h.ctypes.data, C.byref(clipped)), self.h, "pic_gmm")
+        return a, mu, sg, h, clipped.value
 
     def join_copies(self):
         """The context stream waits (on the device) for all enqueued copies."""

@@ -437,3 +437,29 @@ def test_particle_control(kernel):
         assert PU.compare_particles(w, sp, gp, orc[s][0], orc[s][1], rep), rep
         assert PU.compare_moments(gm, orc[s][2], orc[s][3], rep), rep
     ctx.close()
+
+
+@pytest.mark.parametrize("M", [1, 3])
+def test_gmm_histogram_and_em(M):
+    """NEXT-4: the GPU velocity histogram against the oracle's (same particles
+    after two cycles) and the GPU EM fit against the oracle fed with the GPU's
+    histogram (two-level)."""
+    import oracle as O
+    w = I.c1(randomized=True)
+    parts = I.make_species(w, device="cpu")
+    orc = PU.run_oracle(w, parts, 2)
+    ctx = _ctx_for(w, parts)
+    for _ in range(2):
+        ctx.cycle()
+    ctx.sync()
+    for s, sp in enumerate(w.species):
+        B, vmax = 16, 4.0 * sp.vth
+        a, mu, sg, h, clipped = ctx.gmm(s, B, vmax, M, 25)
+        oh, oc = O.bin_velocities(orc[s][0], orc[s][1], B, vmax)
+        assert clipped == oc
+        np.testing.assert_allclose(h, oh, rtol=1e-12, atol=0)
+        oa, omu, osg = O.fit_gmm(h, vmax, M, 25)
+        np.testing.assert_allclose(a, oa, rtol=1e-9, atol=1e-14)
+        np.testing.assert_allclose(mu, omu, rtol=1e-9, atol=1e-9 * vmax)
+        np.testing.assert_allclose(sg, osg, rtol=1e-8, atol=1e-9 * vmax * vmax)
+    ctx.close()
