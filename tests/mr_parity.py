@@ -25,7 +25,7 @@ import parity_util as PU  # noqa: E402
 from paper_2507_20719_b200 import decomp, inputs as I, pic  # noqa: E402
 
 
-def run_case(name, w, cycles, kernel, transport, rank, world):
+def run_case(name, w, cycles, kernel, transport, rank, world, inject=None):
     bounds = decomp.uniform_bounds(w.ncell[0], world)
     lo, hi = bounds[rank], bounds[rank + 1]
     parts_all = I.make_species(w.with_slab(0, w.ncell[0]), device="cpu")
@@ -42,6 +42,9 @@ def run_case(name, w, cycles, kernel, transport, rank, world):
     assert ctx.transport == transport
     for s, p in enumerate(mine):
         ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+        if inject:
+            ctx.set_injection(s, inject["ppc"], w.species[s].vth, inject["drift"], float(parts_all[s]["q"][0]),
+                              500 + s)
     _, EB = I.field_window(wr, 2, device="cpu")
     ctx.set_fields(EB.cuda())
     for _ in range(cycles):
@@ -61,7 +64,24 @@ def run_case(name, w, cycles, kernel, transport, rank, world):
     dist.all_gather_object(gathered, (local, stats, src))
     if rank != 0:
         return None
-    orc = PU.run_oracle(w.with_slab(0, w.ncell[0]), parts_all, cycles)
+    if inject:
+        import oracle as O
+        wf = w.with_slab(0, w.ncell[0])
+        g, F = PU.oracle_grid(wf), PU.oracle_field(wf, 2)
+        orc = []
+        for s, sp in enumerate(w.species):
+            P = PU.to_numpy_parts(parts_all[s])
+            st = np.zeros(len(P["x"]), dtype=np.int8)
+            for c in range(cycles):
+                st, _ = O.mover(g, F, sp.qom, w.n_iter, P, st)
+                new = O.inject(g, F, s, sp.qom, w.n_iter, 500 + s, c, inject["ppc"], sp.vth, inject["drift"],
+                               float(parts_all[s]["q"][0]))
+                P = {k: np.concatenate([P[k], new[k]]) for k in P}
+                st = np.concatenate([st, np.zeros(len(new["x"]), dtype=np.int8)])
+            mom, am = O.moments(g, P, st)
+            orc.append((P, st, mom, am))
+    else:
+        orc = PU.run_oracle(w.with_slab(0, w.ncell[0]), parts_all, cycles)
     reps = []
     ok = True
     for s, sp in enumerate(w.species):
@@ -105,10 +125,11 @@ def main():
              ("c4s", I.c4(ncell=(32, 16, 16), ppc=8), 4),
              ("c5s", I.c5(ncell=(64, 32, 32), wind_ppc=2, inner_ppc=1, planet_ppc=16), 3)]
     all_ok, reports = True, []
+    inj_case = ("c4inj", I.c4(ncell=(32, 16, 16), ppc=8), 3, {"ppc": 8, "drift": (0.15, 0.0, 0.0)})
     for transport in (pic.TRANSPORT_PEER, pic.TRANSPORT_NCCL):
         for kernel in (pic.KERNEL_TILED, pic.KERNEL_BASIC):
-            for name, w, cyc in cases:
-                res = run_case(name, w, cyc, kernel, transport, rank, world)
+            for name, w, cyc, *inj in cases + [inj_case]:
+                res = run_case(name, w, cyc, kernel, transport, rank, world, inject=inj[0] if inj else None)
                 if rank == 0:
                     ok, reps = res
                     all_ok &= ok
