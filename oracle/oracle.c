@@ -600,7 +600,8 @@ int64_t oracle_split(const oracle_grid *g, int species, int64_t np, int64_t cap,
 
 /* Coalescence ("pair-wise merging between particles that are
  * close in the phase space by combining their statistical weights"; reading
- * R31).  Per cell with 2 <= n_c <= 512 ALIVE particles: sort them by
+ * R31).  Per cell with 2 <= n_c <= 512 ALIVE particles, all with velocity bins
+ * inside (-2^20, 2^20) (other cells are left alone): sort them by
  * (floor(u/dv), floor(v/dv), floor(w/dv), id); scan the sorted list and merge
  * neighbours i, i+1 whose three velocity bins are equal (then continue at i+2)
  * until m_c = floor(frac n_c) merges.  Merge: q = q1 + q2, x = (q1 x1 + q2 x2)/q,
@@ -641,7 +642,13 @@ int64_t oracle_coalesce(const oracle_grid *g, int64_t np, double *x, double *y, 
     int64_t s1 = s0;
     while (s1 < m && k[s1].cell == k[s0].cell) ++s1;
     int64_t nc = s1 - s0;
-    if (nc >= 2 && nc <= 512) {
+    int wide = 0;
+    for (int64_t t = s0; t < s1; ++t) {
+      const int64_t lim = 1 << 20;
+      if (k[t].bx <= -lim || k[t].bx >= lim || k[t].by <= -lim || k[t].by >= lim || k[t].bz <= -lim || k[t].bz >= lim)
+        wide = 1;
+    }
+    if (nc >= 2 && nc <= 512 && !wide) {
       int64_t mc = (int64_t)floor(frac * (double)nc), done = 0;
       for (int64_t t = s0; t + 1 < s1 && done < mc;) {
         const coal_key *a = &k[t], *b = &k[t + 1];

@@ -112,9 +112,11 @@ __global__ void __launch_bounds__(256) split_kernel(const SplitArgs A) {
 
 // ---------------------------------------------------------- coalescence ----
 constexpr int COAL_MAX = 512;        // cells with more particles are left alone (R31)
-constexpr int COAL_WARPS = 4;
-struct CoalItem { int64_t bx, by, bz, id; int32_t q; int32_t pad; };
-constexpr size_t COAL_SMEM = sizeof(CoalItem) * COAL_MAX * COAL_WARPS + sizeof(int32_t) * COAL_MAX * COAL_WARPS;
+constexpr int COAL_WARPS = 8;
+constexpr int64_t COAL_BIN_LIM = 1 << 20;   // |velocity bin| bound of the packed key (R31)
+// per warp: packed bin key, id, particle index in the cell, pair list
+constexpr size_t COAL_WARP_BYTES = COAL_MAX * (8 + 8 + 4) + (COAL_MAX / 2) * 4;
+constexpr size_t COAL_SMEM = COAL_WARP_BYTES * COAL_WARPS;
 
 struct CoalArgs {
   Geom g;
@@ -126,19 +128,19 @@ struct CoalArgs {
   unsigned long long *merges;
 };
 
-__device__ __forceinline__ bool coal_less(const CoalItem &x, const CoalItem &y) {
-  if (x.bx != y.bx) return x.bx < y.bx;
-  if (x.by != y.by) return x.by < y.by;
-  if (x.bz != y.bz) return x.bz < y.bz;
-  return x.id < y.id;
+// (bx, by, bz) packed into 63 bits, bx most significant (lexicographic order)
+__device__ __forceinline__ uint64_t pack_bins(int64_t bx, int64_t by, int64_t bz) {
+  return ((uint64_t)(bx + COAL_BIN_LIM) << 42) | ((uint64_t)(by + COAL_BIN_LIM) << 21) | (uint64_t)(bz + COAL_BIN_LIM);
 }
 
 __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  CoalItem *it = reinterpret_cast<CoalItem *>(smem_raw) + warp * COAL_MAX;
-  int32_t *pairs = reinterpret_cast<int32_t *>(reinterpret_cast<CoalItem *>(smem_raw) + COAL_WARPS * COAL_MAX) +
-                   warp * COAL_MAX;
+  unsigned char *base = smem_raw + warp * COAL_WARP_BYTES;
+  uint64_t *key = reinterpret_cast<uint64_t *>(base);
+  int64_t *ids = reinterpret_cast<int64_t *>(base + COAL_MAX * 8);
+  int32_t *ix = reinterpret_cast<int32_t *>(base + COAL_MAX * 16);
+  int32_t *pairs = reinterpret_cast<int32_t *>(base + COAL_MAX * 20);
   const int64_t tile = blockIdx.x;
   for (int cl = warp; cl < TILE3; cl += COAL_WARPS) {
     const int64_t c = tile * TILE3 + cl;
@@ -147,31 +149,40 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
     if (nc < 2 || nc > COAL_MAX) continue;
     int N = 1;
     while (N < nc) N <<= 1;
+    bool wide = false;
     for (int i = lane; i < N; i += 32) {
-      CoalItem e;
       if (i < nc) {
         const uint32_t p = A.perm[q0 + i];
-        e.bx = (int64_t)floor(A.a[3][p] / A.dv);
-        e.by = (int64_t)floor(A.a[4][p] / A.dv);
-        e.bz = (int64_t)floor(A.a[5][p] / A.dv);
-        e.id = A.id[p];
-        e.q = (int32_t)i;
+        const int64_t bx = (int64_t)floor(A.a[3][p] / A.dv), by = (int64_t)floor(A.a[4][p] / A.dv),
+                      bz = (int64_t)floor(A.a[5][p] / A.dv);
+        wide |= bx <= -COAL_BIN_LIM || bx >= COAL_BIN_LIM || by <= -COAL_BIN_LIM || by >= COAL_BIN_LIM ||
+                bz <= -COAL_BIN_LIM || bz >= COAL_BIN_LIM;
+        key[i] = pack_bins(bx, by, bz);
+        ids[i] = A.id[p];
+        ix[i] = i;
       } else {
-        e.bx = e.by = e.bz = e.id = INT64_MAX;
-        e.q = -1;
+        key[i] = ~0ull;
+        ids[i] = INT64_MAX;
+        ix[i] = -1;
       }
-      it[i] = e;
     }
+    if (__any_sync(0xffffffffu, wide)) continue;   // a bin beyond the packed range: cell left alone
     __syncwarp();
-    // bitonic sort of N items by (bins, id)
+    // bitonic sort by (key, id)
     for (int kk = 2; kk <= N; kk <<= 1) {
       for (int j = kk >> 1; j > 0; j >>= 1) {
         for (int i = lane; i < N; i += 32) {
           const int l = i ^ j;
           if (l > i) {
             const bool up = (i & kk) == 0;
-            CoalItem x = it[i], y = it[l];
-            if (coal_less(y, x) == up) { it[i] = y; it[l] = x; }
+            const uint64_t ka = key[i], kb = key[l];
+            const int64_t ia = ids[i], ib = ids[l];
+            const bool b_less = kb < ka || (kb == ka && ib < ia);
+            if (b_less == up) {
+              key[i] = kb; key[l] = ka;
+              ids[i] = ib; ids[l] = ia;
+              const int32_t t = ix[i]; ix[i] = ix[l]; ix[l] = t;
+            }
           }
         }
         __syncwarp();
@@ -182,8 +193,7 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
     if (lane == 0) {
       const int mc = (int)floor(A.frac * (double)nc);
       for (int t = 0; t + 1 < nc && np < mc;) {
-        const CoalItem &x = it[t], &y = it[t + 1];
-        if (x.bx == y.bx && x.by == y.by && x.bz == y.bz) {
+        if (key[t] == key[t + 1]) {
           pairs[np++] = t;
           t += 2;
         } else {
@@ -195,7 +205,7 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
     __syncwarp();
     for (int m = lane; m < np; m += 32) {
       const int t = pairs[m];
-      const uint32_t p1 = A.perm[q0 + it[t].q], p2 = A.perm[q0 + it[t + 1].q];   // p1 has the smaller id
+      const uint32_t p1 = A.perm[q0 + ix[t]], p2 = A.perm[q0 + ix[t + 1]];   // p1 has the smaller id
       const double qa = A.a[6][p1], qb = A.a[6][p2], qs = qa + qb;
 #pragma unroll
       for (int d = 0; d < 6; ++d) A.a[d][p1] = (qa * A.a[d][p1] + qb * A.a[d][p2]) / qs;
