@@ -269,6 +269,15 @@ PIC_API pic_status pic_control(pic_ctx *ctx, int32_t s, int64_t target, double t
 PIC_API pic_status pic_gmm(pic_ctx *ctx, int32_t s, int32_t B, double vmax, int32_t M, int32_t n_em, double *alpha,
                            double *mu, double *sigma, double *hist, int64_t *clipped);
 
+/* Zero-copy access to the ghosted moment arrays of species s (device memory,
+ * valid after pic_exchange until the next pic_moments): *ptr points at owned
+ * node (0, 0, 0) of component comp (0..9: rho, Jx, Jy, Jz, Pxx, Pxy, Pxz,
+ * Pyy, Pyz, Pzz), element (i, j, k) at ptr[i strides[0] + j strides[1] +
+ * k strides[2]] for i, j, k < pic_moment_shape, global node origin + (i, j,
+ * k).  Values are the raw sums sum q S {1, v, vv}; multiply by *scale = 1/V. */
+PIC_API pic_status pic_moment_ptr(const pic_ctx *ctx, int32_t s, int32_t comp, const double **ptr,
+                                  int64_t strides[3], int64_t origin[3], double *scale);
+
 /* Make the context stream wait (on the device, no host block) for every copy
  * enqueued by pic_get_moments_async / pic_set_fields so far.                 */
 PIC_API pic_status pic_join_copies(pic_ctx *ctx);

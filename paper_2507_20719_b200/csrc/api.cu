@@ -548,6 +548,23 @@ pic_status pic_gmm(pic_ctx *p, int32_t s, int32_t B, double vmax, int32_t M, int
   return gmm_fit(ctx, s, B, vmax, M, n_em, alpha, mu, sigma, hist, clipped);
 }
 
+pic_status pic_moment_ptr(const pic_ctx *p, int32_t s, int32_t comp, const double **ptr, int64_t strides[3],
+                          int64_t origin[3], double *scale) {
+  if (!p || !ptr || !strides || !origin || !scale) return PIC_EINVAL;
+  const Ctx *ctx = C(p);
+  if (s < 0 || s >= ctx->cfg.n_species || comp < 0 || comp >= 10) return PIC_EINVAL;
+  const Geom &g = ctx->geom;
+  *ptr = ctx->sp[s].mom + comp * g.m_plane + g.G;
+  strides[0] = 1;
+  strides[1] = g.m_n[0];
+  strides[2] = g.m_n[0] * g.m_n[1];
+  origin[0] = g.slab_lo;
+  origin[1] = 0;
+  origin[2] = 0;
+  *scale = 1.0 / (g.delta[0] * g.delta[1] * g.delta[2]);
+  return PIC_OK;
+}
+
 pic_status pic_join_copies(pic_ctx *p) {
   if (!p) return PIC_EINVAL;
   return join_copies(C(p));

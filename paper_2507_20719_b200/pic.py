@@ -33,7 +33,7 @@ STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "ove
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
-           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_gmm", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
+           "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_gmm", "pic_moment_ptr", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
 class pic_config(C.Structure):
@@ -93,6 +93,8 @@ def load_library(path: str = LIB_PATH):
                                     P(C.c_int32)]
         lib.pic_gmm.argtypes = [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, vp, vp, vp, vp,
                                 P(C.c_int64)]
+        lib.pic_moment_ptr.argtypes = [vp, C.c_int32, C.c_int32, P(vp), P(C.c_int64), P(C.c_int64),
+                                       P(C.c_double)]
         lib.pic_profile.argtypes = [vp, C.c_int32]
         lib.pic_profile_read.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         lib.pic_last_error.argtypes = [vp]
@@ -266,6 +268,22 @@ class Context:
         _check(self.lib.pic_gmm(self.h, s, int(B), float(vmax), int(M), int(n_em), a.ctypes.data, mu.ctypes.data,
                                 sg.ctypes.data, h.ctypes.data, C.byref(clipped)), self.h, "pic_gmm")
         return a, mu, sg, h, clipped.value
+
+    def moment_view(self, s: int, comp: int) -> torch.Tensor:
+        """Zero-copy [nz][ny][nx] view (raw sums x 1/V applied by the caller) of
+        moment component comp of species s, valid until the next moments call."""
+        ptr = C.c_void_p()
+        st = (C.c_int64 * 3)()
+        org = (C.c_int64 * 3)()
+        scale = C.c_double()
+        _check(self.lib.pic_moment_ptr(self.h, s, comp, C.byref(ptr), st, org, C.byref(scale)), self.h,
+               "pic_moment_ptr")
+        nx, ny, nz = self.moment_shape()
+        base = self.workspace
+        off = (ptr.value - base.data_ptr()) // 8
+        flat = base[: (base.numel() // 8) * 8].view(torch.float64)
+        view = torch.as_strided(flat, (nz, ny, nx), (st[2], st[1], st[0]), off)
+        return view * scale.value
 
     def join_copies(self):
         """The context stream waits (on the device) for all enqueued copies."""

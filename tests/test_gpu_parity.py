@@ -41,12 +41,21 @@ def check(w, cycles, kernel, ghost=2, n_iter=None):
     orc = PU.run_oracle(w, parts, cycles, ghost=ghost, n_iter=n_iter)
     gpu, stats = run_gpu(w, parts, cycles, kernel, ghost, n_iter)
     reports = []
+    import oracle as O
+    g = PU.oracle_grid(w)
     for s, sp in enumerate(w.species):
         rep = {"species": sp.name}
         ok_p = PU.compare_particles(w, sp, gpu[s][0], orc[s][0], orc[s][1], rep)
         ok_m = PU.compare_moments(gpu[s][1], orc[s][2], orc[s][3], rep)
+        # P13 two-level: the oracle's deposit of the GPU's own particles against
+        # the GPU moments (isolates Eq. 3 from the mover)
+        gp = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in gpu[s][0].items() if k != "id"}
+        m2, a2 = O.moments(g, gp, None)
+        rep2 = {}
+        ok_d = PU.compare_moments(gpu[s][1], m2, a2, rep2)
+        rep["deposit_only_ratio"] = rep2.get("mom_ratio")
         reports.append(rep)
-        assert ok_p and ok_m, rep
+        assert ok_p and ok_m and ok_d, rep
     return reports, stats
 
 
@@ -462,4 +471,17 @@ def test_gmm_histogram_and_em(M):
         np.testing.assert_allclose(a, oa, rtol=1e-9, atol=1e-14)
         np.testing.assert_allclose(mu, omu, rtol=1e-9, atol=1e-9 * vmax)
         np.testing.assert_allclose(sg, osg, rtol=1e-8, atol=1e-9 * vmax * vmax)
+    ctx.close()
+
+
+def test_moment_ptr_matches_copy_out():
+    w = I.c1(randomized=True)
+    parts = I.make_species(w, device="cpu")
+    ctx = _ctx_for(w, parts)
+    ctx.cycle()
+    ctx.sync()
+    for s in range(len(parts)):
+        full = ctx.get_moments(s)
+        for comp in (0, 3, 9):
+            assert torch.equal(ctx.moment_view(s, comp), full[comp])
     ctx.close()
