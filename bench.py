@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4s"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4s", "c5s"])
     ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
     ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
@@ -68,6 +68,11 @@ def workload(args, nranks, rank):
         per = 128
         desc = ("C4 structure at 128^3 cells per GPU: open boundaries, absorbing planet, dipole + IMF, wind e-/p+ "
                 "64 ppc, inflow injection of both species at x = 0 (NEXT-3), 3 PC iterations")
+    elif args.config == "c5s":
+        w = I.c5(ncell=(128 * nranks, 128, 128))
+        per = 128
+        desc = ("C5 structure at 128^3 cells per GPU: 4 species (wind e-/p+ 64 ppc outside the magnetosphere "
+                "ellipsoid, 8 inside; planetary e-/p+ round(256 exp(-(r-R)/2)) ppc), open boundaries, absorbing moon")
     else:
         w = I.c1()
         per = 16 // nranks
