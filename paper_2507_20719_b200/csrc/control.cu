@@ -293,7 +293,7 @@ pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, do
     // key_new holds the cell of every position below d_nraw (mover outputs and
     // appends); the merged partners now carry KEY_DEAD
     int64_t blocks = (sp.n_raw + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > kSMs * 16) blocks = kSMs * 16;
     recount_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_count,
                                                                                   g.ncells, sp.d_nraw); ++ctx->launches;
     PIC_CUDA(cudaGetLastError());

@@ -90,7 +90,7 @@ __global__ void fold_x_local_kernel(double *mom, int64_t N, int G, int64_t nx, i
 
 static unsigned grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
-  if (b > 148 * 16) b = 148 * 16;
+  if (b > kSMs * 16) b = kSMs * 16;
   if (b < 1) b = 1;
   return (unsigned)b;
 }

@@ -283,7 +283,7 @@ pic_status gmm_fit(Ctx *ctx, int s, int B, double vmax, int M, int n_em, double 
   const size_t smem = B <= GMM_BMAX_SMEM ? sizeof(double) * nb : 0;
   PIC_CUDA(cudaFuncSetAttribute(bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(double) * GMM_BMAX_SMEM * GMM_BMAX_SMEM * GMM_BMAX_SMEM)));
-  bin_kernel<<<148 * 2, 256, smem, ctx->stream>>>(Bn); ++ctx->launches;
+  bin_kernel<<<kSMs * 2, 256, smem, ctx->stream>>>(Bn); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   EmArgs E;
   E.hist = hist;

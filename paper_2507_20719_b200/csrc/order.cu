@@ -19,7 +19,7 @@ namespace pic {
 
 static unsigned grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
-  if (b > 148 * 32) b = 148 * 32;
+  if (b > kSMs * 32) b = kSMs * 32;
   return (unsigned)(b < 1 ? 1 : b);
 }
 

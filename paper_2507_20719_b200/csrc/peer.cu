@@ -61,7 +61,7 @@ struct PeerDesc {
 
 static unsigned grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
-  if (b > 148 * 16) b = 148 * 16;
+  if (b > kSMs * 16) b = kSMs * 16;
   if (b < 1) b = 1;
   return (unsigned)b;
 }
@@ -336,7 +336,7 @@ pic_status peer_migrate(Ctx *ctx, int s0, int s1) {
   A.ctl = ctx->peer_ctl;
   A.stats = ctx->stats;
   A.s0 = s0;
-  dim3 grid(148, s1 - s0);
+  dim3 grid(kSMs, s1 - s0);
   arrive_kernel<<<grid, 256, 0, ctx->stream>>>(A); ++ctx->launches;
   arrive_finish_kernel<<<1, 32, 0, ctx->stream>>>(A, s1 - s0); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());

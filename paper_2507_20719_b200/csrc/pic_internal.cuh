@@ -39,6 +39,10 @@ enum Stat {
   ST_NONFINITE = 5, ST_OVERFLOW = 6, ST_MULTIWRAP = 7, ST_N = 8
 };
 
+// Grid sizing of the grid-stride kernels: multiples of the B200's 148 SMs
+// (the loops stay correct on any SM count).
+constexpr int kSMs = 148;
+
 // Slab migration records: x y z u v w q and the id bits, 8 words per particle.
 constexpr int MIG_REC = 8;
 

@@ -204,7 +204,7 @@ pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_ha
     A.nb_xj[sd] = sd == 0 ? L.owned_nx - 1 : 0;
   }
   int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > kSMs * 16) blocks = kSMs * 16;
   pic_status st;
   if (g.multi_rank) {   // the neighbours' moments are final (their pic_exchange)
     st = peer_barrier(ctx);
