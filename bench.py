@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--relativistic", action="store_true", help="relativistic Eq. 2 (NEXT-1) on the same workload")
     ap.add_argument("--control", action="store_true", help="also time one particle-control split and coalescence pass (NEXT-3)")
     ap.add_argument("--gmm", action="store_true", help="also time the velocity binning + GMM fit of every species (NEXT-4)")
+    ap.add_argument("--balance", type=int, default=1, help="c4s/c5s with N>1: count-balanced slabs (1) or uniform (0)")
     ap.add_argument("--ghost", type=int, default=2)
     ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
@@ -80,6 +81,12 @@ def workload(args, nranks, rank):
     if args.relativistic:
         w.relativistic = True
         desc += "; relativistic Eq. 2 (NEXT-1)"
+    if args.config in ("c4s", "c5s") and nranks > 1 and args.balance:
+        # magnetosphere configs: slabs cut by the particle count per x-plane (H10)
+        from paper_2507_20719_b200 import decomp
+        b = decomp.balanced_bounds(I.plane_counts(w).tolist(), nranks, min_width=8)
+        desc += "; count-balanced x-slabs"
+        return w.with_slab(b[rank], b[rank + 1]), desc
     return w.with_slab(rank * per, (rank + 1) * per), desc
 
 

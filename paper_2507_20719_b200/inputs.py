@@ -262,6 +262,23 @@ def make_positions(w: Workload, sp: Species, gen: torch.Generator, device, plane
     return x, y, z, gid, keep, counts[cell]
 
 
+def plane_counts(w: Workload, device="cpu") -> torch.Tensor:
+    """Expected particles per global x-plane of cells (all species; the planet
+    volume counted as empty): the histogram that count-balanced slabs cut
+    (SURVEY.md H10).  Uses the species' ppc at the cell centres."""
+    full = w.with_slab(0, w.ncell[0])
+    cx, cy, cz, cen = _cell_centres(full, device)
+    tot = torch.zeros(w.ncell[0], dtype=torch.float64, device=device)
+    keep = torch.ones_like(cx, dtype=torch.bool)
+    if w.planet_radius > 0:
+        c = w.planet_center
+        keep = ((cen[0] - c[0]) ** 2 + (cen[1] - c[1]) ** 2 + (cen[2] - c[2]) ** 2) >= w.planet_radius ** 2
+    for sp in w.species:
+        n = sp.ppc_fn(*cen).to(torch.float64) if sp.ppc_fn is not None else torch.full_like(cx, sp.ppc, dtype=torch.float64)
+        tot.index_add_(0, cx, n * keep)
+    return tot
+
+
 def make_species(w: Workload, device="cpu") -> List[dict]:
     """Particles of every species of this rank: list of dicts of float64 tensors
     x y z u v w q and int64 id (global: cell id * 1024 + in-cell index, plus
