@@ -54,3 +54,18 @@ def test_ids_independent_of_slab_split():
     a = I.make_species(w.with_slab(0, 8))[0]["id"]
     b = I.make_species(w.with_slab(8, 16))[0]["id"]
     assert torch.equal(torch.sort(full).values, torch.sort(torch.cat([a, b])).values)
+
+
+def test_plane_counts_match_generated_particles():
+    """The per-x-plane histogram that count-balanced slabs cut (H10) agrees with
+    the particles the generator draws (exactly away from the planet)."""
+    w = I.c5(ncell=(64, 32, 32), wind_ppc=4, inner_ppc=1, planet_ppc=32)
+    counts = I.plane_counts(w)
+    parts = I.make_species(w)
+    got = torch.zeros(w.ncell[0], dtype=torch.float64)
+    for p in parts:
+        cx = torch.floor(p["x"] / w.delta[0]).to(torch.int64)
+        got.index_add_(0, cx, torch.ones_like(p["x"]))
+    assert abs(float(got.sum()) - float(counts.sum())) < 0.02 * float(counts.sum())
+    far = torch.arange(w.ncell[0]) < 20           # planes away from the moon
+    assert torch.equal(got[far], counts[far])
