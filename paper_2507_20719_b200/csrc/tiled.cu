@@ -53,8 +53,11 @@ constexpr int THREADS = 32 * WARPS;
 #define PIC_SRC_STAGES 2
 #endif
 constexpr int SRC_STAGES = PIC_SRC_STAGES;   // mover: rounds of gathered sources in flight (ring)
-constexpr int PK_SLOTS = 6;      // mover: perm/key ring slots
-constexpr int PK_AHEAD = 5;      // mover: perm/key fetched this many rounds ahead
+#ifndef PIC_PK_AHEAD
+#define PIC_PK_AHEAD 3
+#endif
+constexpr int PK_AHEAD = PIC_PK_AHEAD;   // mover: perm/key fetched this many rounds ahead
+constexpr int PK_SLOTS = PK_AHEAD + 1;   // mover: perm/key ring slots
 constexpr int MOVER_WARP_STAGE = SRC_STAGES * 8 * 32 + PK_SLOTS * 2 * 32 / 2;  // doubles per warp
 // deposit staging per warp: S[32 particles][8 corners], V[32][moments 0..7]
 // and V2[32][moments 8, 9].  S and V rows are 8 doubles whose 16-byte pairs
