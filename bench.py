@@ -329,20 +329,24 @@ def main():
     mover_launch_ms = prof["mover"][0] / max(1, prof["mover"][1])
     achieved = n_alive * b_mover / (mover_ms_step / 1e3) / 1e9
     traffic = None
+    ncu_pct = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
             if tj.get("config") == args.config:
                 # ncu --set full capture of one mover launch (one species): DRAM bytes per
-                # particle update, scaled to this launch's particles
+                # particle update, scaled to this launch's particles; pipe utilisations
                 traffic = tj["mover_bytes_per_update"] * n_alive / n_sp
+                ncu_pct = {k: tj[k] for k in ("mover_fp64_pipe_pct", "mover_issue_active_pct", "mover_dram_pct",
+                                              "deposit_dram_pct") if k in tj}
         except Exception:
             traffic = None
     kname = "mover_tiled_kernel" if args.kernel in (0, 2) else "mover_basic_kernel"
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
+            "ncu_utilisation_pct": ncu_pct,
             "bytes_per_update": b_mover, "launch_ms": mover_launch_ms,
             "launches_per_step": prof["mover"][1] / args.steps,
             "step_frac": (value / world) * (B_ALG_PARTICLE + grid_share) / (peak * 1e9),
