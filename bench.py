@@ -108,27 +108,43 @@ class ClockSampler:
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
-        self.rows = []
+        self.rows = []          # (wall time, fields)
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        """Start nvidia-smi BEFORE the timed region and wait for its first row, so
+        that even a sub-second timed region is sampled (its start-up takes ~1 s)."""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 8.0
+            while not self.rows and time.time() < deadline and self.proc.poll() is None:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
+
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+        if self.proc:           # one more row after the region closes
+            n = len(self.rows)
+            deadline = time.time() + 0.5
+            while len(self.rows) == n and time.time() < deadline:
+                time.sleep(0.02)
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -138,16 +154,22 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        t0 = self.t0 if self.t0 is not None else self.rows[0][0]
+        t1 = self.t1 if self.t1 is not None else self.rows[-1][0]
+        inside = [r for ts, r in self.rows if t0 <= ts <= t1 + 0.15]
+        if not inside:          # region shorter than the sampling period: nearest row
+            inside = [min(self.rows, key=lambda tr: abs(tr[0] - 0.5 * (t0 + t1)))[1]]
+        rows = inside
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for k, nm in enumerate(names):
                 if len(r) > 5 + k and r[5 + k].lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(rows)}
 
 
 # ----------------------------------------------------------- oracle (CPU) --
@@ -235,30 +257,53 @@ def main():
     from paper_2507_20719_b200 import decomp, inputs as I, pic
 
     w, desc = workload(args, world, rank)
-    parts = I.make_species(w, device="cuda")
-    n_local = [p["x"].numel() for p in parts]
-    face = w.ncell[1] * w.ncell[2]
-    cap = [int(n * (1.35 if args.control else 1.08)) + 65536 + (4 * face * 64 if args.config == "c4s" else 0)
-           for n in n_local]
     nccl_id = decomp.broadcast_nccl_id(pic.pic_nccl_id) if world > 1 else None
-    cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
-                          transport=args.transport, kernel=args.kernel)
     stream = torch.cuda.current_stream()
-    ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
-    for s, p in enumerate(parts):
-        ctx.set_particles(s, p)
-        if args.config == "c4s":
-            # NEXT-3: wind injection at the x = 0 face with the bulk wind's parameters
-            sp = w.species[s]
-            ctx.set_injection(s, 64, sp.vth, sp.drift, float(p["q"][0].item()), 4242 + s)
+    parts_cpu_sample = None
+    want_sample = rank == 0 and world == 1 and not args.no_cpu_baseline
+    if args.config == "c3":
+        # C3 holds 0.9 G particles per GPU (the store alone is 136 GB): allocate
+        # it first (exact capacity: uniform ppc, periodic; +2 % migration headroom
+        # with several ranks) and generate each species in host memory
+        import copy as _copy
+        ncell_loc = (w.slab_or_all()[1] - w.slab_or_all()[0]) * w.ncell[1] * w.ncell[2]
+        cap = [int(ncell_loc * sp.ppc * (1.02 if world > 1 else 1.0)) + 65536 for sp in w.species]
+        cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
+                              transport=args.transport, kernel=args.kernel)
+        ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
+        parts_cpu_sample = [] if want_sample else None
+        for s, sp in enumerate(w.species):
+            w1 = _copy.copy(w)
+            w1.species = [sp]
+            w1.seed = w.seed * 16 + s
+            p = I.make_species(w1, device="cpu")[0]
+            ctx.set_particles(s, p)
+            if want_sample:
+                parts_cpu_sample.append({k: v[:2_000_000].cpu() for k, v in p.items()})
+            del p
+            torch.cuda.empty_cache()
+    else:
+        parts = I.make_species(w, device="cuda")
+        n_local = [p["x"].numel() for p in parts]
+        face = w.ncell[1] * w.ncell[2]
+        cap = [int(n * (1.35 if args.control else 1.08)) + 65536 + (4 * face * 64 if args.config == "c4s" else 0)
+               for n in n_local]
+        cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
+                              transport=args.transport, kernel=args.kernel)
+        ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
+        for s, p in enumerate(parts):
+            ctx.set_particles(s, p)
+            if args.config == "c4s":
+                # NEXT-3: wind injection at the x = 0 face with the bulk wind's parameters
+                sp = w.species[s]
+                ctx.set_injection(s, 64, sp.vth, sp.drift, float(p["q"][0].item()), 4242 + s)
+        if want_sample:
+            # bounded oracle sample: first particles of the store in id order (x-planes 0..)
+            parts_cpu_sample = [{k: v[: min(v.numel(), 2_000_000)].cpu() for k, v in p.items()} for p in parts]
+        del parts
+    torch.cuda.empty_cache()
     lo, EB = I.field_window(w, args.ghost, device="cuda")
     ctx.set_fields(EB)
-    parts_cpu_sample = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # bounded oracle sample: first particles of the store in id order (x-planes 0..)
-        parts_cpu_sample = [{k: v[: min(v.numel(), 2_000_000)].cpu() for k, v in p.items()} for p in parts]
-    del parts
-    torch.cuda.empty_cache()
 
     def barrier():
         torch.cuda.synchronize()
@@ -276,8 +321,9 @@ def main():
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = ctx.launch_count()
     ctx.profile(True)        # CUDA events around each phase, on the libpic stream
-    barrier()
     with ClockSampler(local) as clk:
+        barrier()
+        clk.begin()
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
@@ -291,6 +337,7 @@ def main():
             e2.record(stream)
         end.record(stream)
         barrier()
+        clk.end()
     launches = ctx.launch_count() - launches0
     prof = ctx.profile_read()
     ctx.profile(False)
