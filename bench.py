@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4s", "c5s"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c4s", "c5s"])
     ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
     ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
@@ -64,6 +64,16 @@ def workload(args, nranks, rank):
         w = I.c3(nranks=nranks, ppc=args.ppc or 64)
         per = 192
         desc = "C3 weak-scaling cube 192^3 cells per GPU, 2 species, 64 ppc, 3 PC iterations"
+    elif args.config == "c4":
+        w = I.c4(ppc=args.ppc or 64)
+        per = w.ncell[0] // nranks
+        desc = ("C4 at full size: 512x256x256 cells (4.29e9 particles), open boundaries, absorbing planet, "
+                "dipole + IMF, wind e-/p+ 64 ppc, removal only, 3 PC iterations (needs >= 4 GPUs)")
+    elif args.config == "c5":
+        w = I.c5()
+        per = w.ncell[0] // nranks
+        desc = ("C5 at full size: 512x256x256 cells, 4 species (wind e-/p+ 64/8 ppc, planetary e-/p+ "
+                "round(256 exp(-(r-R)/2)) ppc), open boundaries, absorbing moon, 3 PC iterations (needs >= 4 GPUs)")
     elif args.config == "c4s":
         w = I.c4(ncell=(128 * nranks, 128, 128), ppc=args.ppc or 64)
         per = 128
@@ -81,7 +91,7 @@ def workload(args, nranks, rank):
     if args.relativistic:
         w.relativistic = True
         desc += "; relativistic Eq. 2 (NEXT-1)"
-    if args.config in ("c4s", "c5s") and nranks > 1 and args.balance:
+    if args.config in ("c4", "c5", "c4s", "c5s") and nranks > 1 and args.balance:
         # magnetosphere configs: slabs cut by the particle count per x-plane (H10)
         from paper_2507_20719_b200 import decomp
         b = decomp.balanced_bounds(I.plane_counts(w).tolist(), nranks, min_width=8)
@@ -261,27 +271,28 @@ def main():
     stream = torch.cuda.current_stream()
     parts_cpu_sample = None
     want_sample = rank == 0 and world == 1 and not args.no_cpu_baseline
-    if args.config == "c3":
-        # C3 holds 0.9 G particles per GPU (the store alone is 136 GB): allocate
-        # it first (exact capacity: uniform ppc, periodic; +2 % migration headroom
-        # with several ranks) and generate each species in host memory
-        import copy as _copy
-        ncell_loc = (w.slab_or_all()[1] - w.slab_or_all()[0]) * w.ncell[1] * w.ncell[2]
-        cap = [int(ncell_loc * sp.ppc * (1.02 if world > 1 else 1.0)) + 65536 for sp in w.species]
+    if args.config in ("c3", "c4", "c5"):
+        # full-size weak-scaling / magnetosphere slabs hold ~0.9-1.1 G particles
+        # per GPU (the store alone is 136-165 GB): allocate it first (capacity =
+        # particles before the planet cut, +2 % migration headroom with several
+        # ranks) and draw the particles in host memory, sub-slab by sub-slab
+        ub = I.species_upper_counts(w)
+        cap = [int(n * (1.02 if world > 1 else 1.0)) + 65536 for n in ub]
         cfg = pic.make_config(w, rank=rank, nranks=world, capacity=cap, ghost=args.ghost,
                               transport=args.transport, kernel=args.kernel)
+        need = pic.pic_workspace_bytes(cfg)
+        free_b = torch.cuda.mem_get_info()[0]
+        if need > free_b:
+            raise SystemExit(f"{args.config}: store needs {need / 1e9:.1f} GB on rank {rank}, "
+                             f"{free_b / 1e9:.1f} GB free: run it on more GPUs")
         ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
-        parts_cpu_sample = [] if want_sample else None
-        for s, sp in enumerate(w.species):
-            w1 = _copy.copy(w)
-            w1.species = [sp]
-            w1.seed = w.seed * 16 + s
-            p = I.make_species(w1, device="cpu")[0]
+        parts = I.make_species_chunked(w)
+        for s, p in enumerate(parts):
             ctx.set_particles(s, p)
-            if want_sample:
-                parts_cpu_sample.append({k: v[:2_000_000].cpu() for k, v in p.items()})
-            del p
-            torch.cuda.empty_cache()
+        ctx.sync()
+        if want_sample:
+            parts_cpu_sample = [{k: v[:2_000_000].clone() for k, v in p.items()} for p in parts]
+        del parts
     else:
         parts = I.make_species(w, device="cuda")
         n_local = [p["x"].numel() for p in parts]
@@ -508,7 +519,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": desc, "particles_per_gpu": n_alive, "cells_per_gpu": list(w.ncell[1:]),
+            "config": {"workload": desc, "particles_per_gpu": n_alive, "cells_per_gpu": [w.slab_or_all()[1] - w.slab_or_all()[0]] + list(w.ncell[1:]),
                        "kernel": ["auto", "basic", "tiled"][args.kernel], "transport": (["nccl", "peer"][int(ctx.peer)] if world > 1 else None),
                        "l2": "inputs (%.2f GB per GPU) exceed the 126 MB L2; no flush" % (n_alive * 64 / 1e9),
                        "parallelism": f"x-slabs{world}"},

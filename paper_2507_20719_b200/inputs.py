@@ -314,6 +314,44 @@ def make_species(w: Workload, device="cpu") -> List[dict]:
     return out
 
 
+def species_upper_counts(w: Workload) -> List[int]:
+    """Particles per species of this rank's slab before the planet cut (an upper
+    bound of `make_species`' counts): the capacity of a store allocated before
+    the particles are drawn."""
+    cx, cy, cz, cen = _cell_centres(w, "cpu")
+    out = []
+    for sp in w.species:
+        if sp.ppc_fn is not None:
+            out.append(int(sp.ppc_fn(*cen).to(torch.int64).clamp(0, 1023).sum().item()))
+        else:
+            out.append(int(cx.numel()) * sp.ppc)
+    return out
+
+
+def make_species_chunked(w: Workload, chunk_particles: int = 32_000_000) -> List[dict]:
+    """`make_species` for slabs too large to draw in one piece (C3-C5 at full
+    size): the slab is drawn in sub-slabs of whole x-planes (each seeded by its
+    first plane, as `make_species` seeds a slab) and assembled in host memory,
+    so the transient memory is one sub-slab's.  Same recipe and co-location;
+    a different random stream from a one-piece draw of the same slab."""
+    lo, hi = w.slab_or_all()
+    ub = species_upper_counts(w)
+    step = max(1, int(chunk_particles * (hi - lo) // max(1, sum(ub))))
+    keys = ("x", "y", "z", "u", "v", "w", "q", "id")
+    out = [{k: torch.empty(ub[s], dtype=torch.int64 if k == "id" else torch.float64) for k in keys}
+           for s in range(len(w.species))]
+    fill = [0] * len(w.species)
+    for a in range(lo, hi, step):
+        parts = make_species(w.with_slab(a, min(hi, a + step)), device="cpu")
+        for s, p in enumerate(parts):
+            n = p["x"].numel()
+            for k in keys:
+                out[s][k][fill[s]:fill[s] + n].copy_(p[k])
+            fill[s] += n
+        del parts
+    return [{k: t[:fill[s]] for k, t in out[s].items()} for s in range(len(w.species))]
+
+
 # ----------------------------------------------------------------- configs --
 def c1(randomized: bool = False, seed: int = 1) -> Workload:
     fp = {"E": (0.0, 1e-4, 0.0), "B": (0.0, 0.0, 0.01)}

@@ -69,3 +69,23 @@ def test_plane_counts_match_generated_particles():
     assert abs(float(got.sum()) - float(counts.sum())) < 0.02 * float(counts.sum())
     far = torch.arange(w.ncell[0]) < 20           # planes away from the moon
     assert torch.equal(got[far], counts[far])
+
+
+def test_chunked_generation_matches_recipe():
+    """The sub-slab generator of the full-size bench (C3-C5) draws the same
+    particle set shape as one-piece generation: identical ids per cell, the
+    slab, co-located e-/p+ pairs, the upper bound of `species_upper_counts`."""
+    w = I.c5(ncell=(64, 32, 32), wind_ppc=4, inner_ppc=1, planet_ppc=32).with_slab(20, 44)
+    ub = I.species_upper_counts(w)
+    a = I.make_species_chunked(w, chunk_particles=20000)
+    b = I.make_species(w)
+    for s in range(len(w.species)):
+        assert a[s]["x"].numel() <= ub[s]
+        # ids encode (cell, in-cell index): per-cell counts agree except in cells the
+        # moon cuts (positions are redrawn, so the cut differs)
+        ca = torch.bincount((a[s]["id"] % (1 << 40)) // 1024, minlength=64 * 32 * 32)
+        cb = torch.bincount((b[s]["id"] % (1 << 40)) // 1024, minlength=64 * 32 * 32)
+        assert int((ca != cb).sum()) < 0.02 * int((cb > 0).sum())
+        assert a[s]["id"].unique().numel() == a[s]["id"].numel()
+        assert float(a[s]["x"].min()) >= 20 * w.delta[0] and float(a[s]["x"].max()) < 44 * w.delta[0]
+    assert torch.equal(a[0]["x"], a[1]["x"]) and torch.equal(a[2]["z"], a[3]["z"])
