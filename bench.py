@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--relativistic", action="store_true", help="relativistic Eq. 2 (NEXT-1) on the same workload")
     ap.add_argument("--control", action="store_true", help="also time one particle-control split and coalescence pass (NEXT-3)")
     ap.add_argument("--gmm", action="store_true", help="also time the velocity binning + GMM fit of every species (NEXT-4)")
+    ap.add_argument("--strong", action="store_true", help="c2/c3: fixed total problem (one GPU's) split over the N ranks")
     ap.add_argument("--balance", type=int, default=1, help="c4s/c5s with N>1: count-balanced slabs (1) or uniform (0)")
     ap.add_argument("--ghost", type=int, default=2)
     ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
@@ -56,14 +57,18 @@ def parse():
 
 def workload(args, nranks, rank):
     from paper_2507_20719_b200 import inputs as I
+    strong = getattr(args, "strong", False)
     if args.config == "c2":
-        w = I.c2(scale_x=nranks, ppc=args.ppc or 125)
-        per = 128
-        desc = "C2 GEM double Harris sheet, 128x64x32 cells per GPU (x-slab weak scaling), 2 species, 125 ppc, mass ratio 256, 3 PC iterations"
+        w = I.c2(scale_x=1 if strong else nranks, ppc=args.ppc or 125)
+        per = 128 // nranks if strong else 128
+        desc = ("C2 GEM double Harris sheet, 128x64x32 cells in total split into N x-slabs (strong scaling)" if strong else
+                "C2 GEM double Harris sheet, 128x64x32 cells per GPU (x-slab weak scaling)") + \
+            ", 2 species, 125 ppc, mass ratio 256, 3 PC iterations"
     elif args.config == "c3":
-        w = I.c3(nranks=nranks, ppc=args.ppc or 64)
-        per = 192
-        desc = "C3 weak-scaling cube 192^3 cells per GPU, 2 species, 64 ppc, 3 PC iterations"
+        w = I.c3(nranks=1 if strong else nranks, ppc=args.ppc or 64)
+        per = 192 // nranks if strong else 192
+        desc = ("C3 cube 192^3 cells in total split into N x-slabs (strong scaling)" if strong else
+                "C3 weak-scaling cube 192^3 cells per GPU") + ", 2 species, 64 ppc, 3 PC iterations"
     elif args.config == "c4":
         w = I.c4(ppc=args.ppc or 64)
         per = w.ncell[0] // nranks
@@ -517,7 +522,7 @@ def main():
         line = {
             "metric": "particle updates/s (mover+moments)", "value": value, "unit": "particle updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": desc, "particles_per_gpu": n_alive, "cells_per_gpu": [w.slab_or_all()[1] - w.slab_or_all()[0]] + list(w.ncell[1:]),
                        "kernel": ["auto", "basic", "tiled"][args.kernel], "transport": (["nccl", "peer"][int(ctx.peer)] if world > 1 else None),
