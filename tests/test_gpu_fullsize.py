@@ -1,0 +1,103 @@
+"""Parity at BASELINE.json's full size, in bench.py's launch configuration.
+
+C2 (128 x 64 x 32 cells, 2 species x 32.8 M particles, ghost 2, tiled kernels,
+capacity 1.08 n + 65536), two cycles on one GPU.  The oracle cannot move 65.5 M
+particles in seconds, so (task ③) it checks sampled outputs one by one:
+
+- particles: a seeded sample of ids is moved by the oracle from the same inputs
+  and compared by id with the GPU's particles (north_star tolerances);
+- moments: at sampled nodes, the oracle moves every input particle that starts
+  within 2 cells of the node (the particles move < 0.2 cells per cycle here, so
+  these are all the node's contributors after two cycles) and deposits them;
+  the node's 10 moments are compared with the GPU's (R19 bound);
+- properties over everything: sum_g rho_g V = sum_p q_p and the sums of J and
+  Pi against the GPU's own output particles (P8).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2507_20719_b200 import inputs as I
+from paper_2507_20719_b200 import pic
+import parity_util as PU
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CYCLES = 2
+N_SAMPLE = 3000
+N_NODES = 12
+
+
+def _box_mask(parts, node, w, half):
+    """Input particles whose cell lies within `half` cells of `node` (min-image)."""
+    m = torch.ones(parts["x"].numel(), dtype=torch.bool)
+    for d, k in enumerate("xyz"):
+        n = w.ncell[d]
+        c = torch.floor(parts[k] / w.delta[d])
+        diff = c - float(node[d])
+        diff = diff - n * torch.round(diff / n)
+        m &= (diff >= -half) & (diff <= half - 1)
+    return m
+
+
+def test_c2_full_size_sampled():
+    w = I.c2()
+    parts = I.make_species(w, device="cpu")
+    cap = [int(p["x"].numel() * 1.08) + 65536 for p in parts]
+    cfg = pic.make_config(w, capacity=cap, ghost=2)
+    ctx = pic.Context(cfg)
+    for s, p in enumerate(parts):
+        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+    lo, EB = I.field_window(w, 2, device="cuda")
+    ctx.set_fields(EB)
+    for _ in range(CYCLES):
+        ctx.cycle()
+    stats = ctx.sync()
+    assert stats["far"] == 0 and stats["nonfinite"] == 0
+    g = PU.oracle_grid(w)
+    F = PU.oracle_field(w, 2)
+    rng = np.random.default_rng(20719)
+    V = w.delta[0] * w.delta[1] * w.delta[2]
+    nz, ny, nx = w.ncell[2], w.ncell[1], w.ncell[0]
+    nodes = [(int(rng.integers(nx)), int(rng.integers(ny)), int(rng.integers(nz))) for _ in range(N_NODES)]
+    for s, sp in enumerate(w.species):
+        gp_dev = ctx.get_particles(s)
+        gm = ctx.get_moments(s).cpu().numpy()
+        n = parts[s]["x"].numel()
+        assert gp_dev["x"].numel() == n          # periodic: nothing removed
+        # -- sampled particles, one by one against the oracle
+        pick = torch.from_numpy(rng.choice(n, N_SAMPLE, replace=False))
+        sub = {k: v[pick] for k, v in parts[s].items()}
+        P = PU.to_numpy_parts(sub)
+        st = np.zeros(N_SAMPLE, dtype=np.int8)
+        for _ in range(CYCLES):
+            st, bad = O.mover(g, F, sp.qom, w.n_iter, P, st)
+            assert bad == 0
+        sel = torch.isin(gp_dev["id"], sub["id"].cuda())
+        gsub = {k: v[sel].cpu().numpy() for k, v in gp_dev.items()}
+        rep = {}
+        assert PU.compare_particles(w, sp, gsub, P, st, rep), rep
+        # -- sampled nodes: every contributor moved and deposited by the oracle
+        for node in nodes:
+            m = _box_mask(parts[s], node, w, 2)
+            P = PU.to_numpy_parts({k: v[m] for k, v in parts[s].items()})
+            st = np.zeros(len(P["x"]), dtype=np.int8)
+            for _ in range(CYCLES):
+                st, bad = O.mover(g, F, sp.qom, w.n_iter, P, st)
+            mom, am = O.moments(g, P, st)
+            ix, iy, iz = node
+            o, a, gv = mom[:, iz, iy, ix], am[:, iz, iy, ix], gm[:, iz, iy, ix]
+            assert np.all(a > 0)
+            ratio = np.abs(gv - o) / (PU.MOM_TOL * a)
+            assert ratio.max() <= 1.0, (s, node, ratio.max())
+        # -- P8 over all particles: the GPU moments carry the GPU particles' sums
+        q = gp_dev["q"].cpu().numpy()
+        u, v, ww = (gp_dev[k].cpu().numpy() for k in "uvw")
+        terms = [q, q * u, q * v, q * ww, q * u * u, q * u * v, q * u * ww, q * v * v, q * v * ww, q * ww * ww]
+        for comp, t in enumerate(terms):
+            got = float(gm[comp].sum()) * V
+            assert abs(got - float(t.sum())) <= 1e-11 * float(np.abs(t).sum()), (s, comp, got, float(t.sum()))
+        del gp_dev
+        torch.cuda.empty_cache()
+    ctx.close()
