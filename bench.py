@@ -116,49 +116,94 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons DURING the timed region.
+
+    NVML is polled every ~2 ms from a thread (the GPU is matched by its PCI bus
+    id, not by index), so even a 20 ms timed region gets a dozen samples;
+    `nvidia-smi -lms 100` is the fallback when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
-        self.rows = []          # (wall time, fields)
+        self.rows = []          # (wall time, sm MHz, max sm MHz, set of reason names)
         self.proc = None
+        self.nvml = None
         self.t0 = self.t1 = None
+        self.stop = False
+
+    def _open_nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = None
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.idx)
+            h = N.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        except Exception:
+            h = N.nvmlDeviceGetHandleByIndex(self.idx)
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        return N, h, bits, mx
+
+    def _poll_nvml(self):
+        N, h, bits, mx = self.nvml
+        while not self.stop:
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((time.time(), float(sm), float(mx), {k for k, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
-        """Start nvidia-smi BEFORE the timed region and wait for its first row, so
-        that even a sub-second timed region is sampled (its start-up takes ~1 s)."""
+        try:
+            self.nvml = self._open_nvml()
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t = threading.Thread(target=self._read_smi, daemon=True)
             self.t.start()
-            deadline = time.time() + 8.0
+            deadline = time.time() + 8.0       # nvidia-smi takes ~1 s to start sampling
             while not self.rows and time.time() < deadline and self.proc.poll() is None:
                 time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
+            r = [c.strip() for c in line.split(",")]
+            try:
+                reasons = {nm for k, nm in enumerate(self.NAMES) if len(r) > 5 + k and r[5 + k].lower() == "active"}
+                self.rows.append((time.time(), float(r[1]), float(r[2]), reasons))
+            except (ValueError, IndexError):
+                pass
 
     def begin(self):
         self.t0 = time.time()
 
     def end(self):
         self.t1 = time.time()
-        if self.proc:           # one more row after the region closes
-            n = len(self.rows)
-            deadline = time.time() + 0.5
-            while len(self.rows) == n and time.time() < deadline:
-                time.sleep(0.02)
+        n = len(self.rows)
+        deadline = time.time() + (0.5 if self.proc else 0.05)   # one more sample after the region
+        while len(self.rows) == n and time.time() < deadline:
+            time.sleep(0.005)
 
     def __exit__(self, *a):
+        self.stop = True
         if self.proc:
             self.proc.terminate()
             try:
@@ -168,23 +213,16 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         t0 = self.t0 if self.t0 is not None else self.rows[0][0]
         t1 = self.t1 if self.t1 is not None else self.rows[-1][0]
-        inside = [r for ts, r in self.rows if t0 <= ts <= t1 + 0.15]
-        if not inside:          # region shorter than the sampling period: nearest row
-            inside = [min(self.rows, key=lambda tr: abs(tr[0] - 0.5 * (t0 + t1)))[1]]
-        rows = inside
-        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in rows:
-            for k, nm in enumerate(names):
-                if len(r) > 5 + k and r[5 + k].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+        slack = 0.15 if self.proc else 0.005
+        rows = [r for r in self.rows if t0 <= r[0] <= t1 + slack]
+        if not rows:            # region shorter than the sampling period: nearest sample
+            rows = [min(self.rows, key=lambda r: abs(r[0] - 0.5 * (t0 + t1)))]
+        reasons = set().union(*[r[3] for r in rows])
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ----------------------------------------------------------- oracle (CPU) --
