@@ -189,6 +189,9 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
 }
 
 // ----------------------------------------------------------------- mover ----
+#ifndef PIC_MOVER_KOLD_FROM_X
+#define PIC_MOVER_KOLD_FROM_X 1
+#endif
 #ifndef PIC_MOVER_MINB
 #define PIC_MOVER_MINB 2
 #endif
@@ -264,7 +267,9 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     if (q < wend) {
       uint32_t *slot = pk + (ri % PK_SLOTS) * 64 + lane;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(A.perm + q) : "memory");
+#if !PIC_MOVER_KOLD_FROM_X
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 32)), "l"(A.key + q) : "memory");
+#endif
     }
   };
   auto fetch_src = [&](int ri) {       // sources of round ri (its perm is already in the ring)
@@ -295,7 +300,11 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32, ++ri) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
+#if PIC_MOVER_KOLD_FROM_X
+    uint32_t kold = 0u;          // set from x^n below
+#else
     const uint32_t kold = act ? pk[(ri % PK_SLOTS) * 64 + 32 + lane] : 0u;
+#endif
     fetch_src(ri + SRC_STAGES - 1);
     fetch_pk(ri + PK_AHEAD);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -307,6 +316,12 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       const int64_t idv = __double_as_longlong(sv[7 * 32]);
       const double xn[3] = {sv[0], sv[32], sv[64]};
       const double vn[3] = {sv[96], sv[128], sv[160]};
+#if PIC_MOVER_KOLD_FROM_X
+      // the cell of x^n (the key the order was built from: keys are always
+      // taken from the stored position, so no key array needs to be read; a
+      // mismatch would only reclassify a stayer as an arrival or back)
+      kold = tile_key32(g, (uint32_t)((int)xn[0] - (int)g.slab_lo), (uint32_t)(int)xn[1], (uint32_t)(int)xn[2]);
+#endif
       double xb[3] = {xn[0], xn[1], xn[2]};
       double vb[3];
       bool clamped = false;
