@@ -1,5 +1,5 @@
 """Multi-GPU parity (P14, decomposition invariance): launches tests/mr_parity.py
-under torchrun on 2 (and 4 when available) GPUs of this box."""
+under torchrun on 2, 3 and 4 GPUs of this box (when available; 3 = an odd ring)."""
 import json
 import os
 import subprocess
@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("nproc", [2, 3, 4])
 def test_multirank_parity(nproc):
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
