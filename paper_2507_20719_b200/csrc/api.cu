@@ -110,7 +110,7 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
     for (int k = 0; k < 7; ++k) oa[k] = L.take(8 * cap);
     for (int k = 0; k < 7; ++k) ob[k] = L.take(8 * cap);
     int64_t oid = L.take(8 * cap), oidb = L.take(8 * cap);
-    int64_t okn = L.take(4 * cap), ork = L.take(4 * cap), opm = L.take(4 * cap), okey = L.take(4 * cap);
+    int64_t okn = L.take(4 * cap), ork = L.take(4 * cap), opm = L.take(4 * cap);
     int64_t occ = L.take(8 * (g.ncells + 1)), oco = L.take(4 * (g.ncells + 1)), oct = L.take(4 * (g.ncells + 1));
     int64_t onraw = L.take(8);
     int64_t omom = L.take(8 * 10 * g.m_plane);
@@ -125,7 +125,6 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
       sp.key_new = (uint32_t *)(base + okn);
       sp.rank = (uint32_t *)(base + ork);
       sp.perm = (uint32_t *)(base + opm);
-      sp.key = (uint32_t *)(base + okey);
       sp.cell_count = (uint32_t *)(base + occ);
       sp.cell_off = (uint32_t *)(base + oco);
       sp.cell_tot = (uint32_t *)(base + oct);

@@ -39,7 +39,7 @@ struct SplitArgs {
   Geom g;
   double *a[7];
   int64_t *id;
-  const uint32_t *perm, *key, *nlive;
+  const uint32_t *perm, *nlive;
   uint32_t *key_new, *rank, *cell_count;
   int64_t *d_nraw;
   int64_t cap;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) split_kernel(const SplitArgs A) {
             A.a[6][slot] = qh;
             A.a[6][p] = qh;
             A.id[slot] = child_id((int64_t)uid, A.cycle);
-            k = A.key[q];
+            k = A.key_new[p];   // the parent's cell (key of its store position)
             A.key_new[slot] = k;
           }
         }
@@ -249,7 +249,6 @@ pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, do
     for (int k = 0; k < 7; ++k) A.a[k] = sp.a[k];
     A.id = sp.id;
     A.perm = sp.perm;
-    A.key = sp.key;
     A.nlive = nlive;
     A.key_new = sp.key_new;
     A.rank = sp.rank;

@@ -24,7 +24,6 @@ struct MoverArgs {
   double *dst[7];
   int64_t *dst_id;
   const uint32_t *perm;
-  const uint32_t *key;        // key[q]: cell of x^n (stayer test)
   const uint32_t *cell_off;   // cell_off[ncells] = number of particles to move
   uint32_t *key_new, *rank, *cell_count;
   int64_t *d_nraw;
@@ -44,10 +43,12 @@ __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
   if (q == 0) *A.d_nraw = n;
   if ((int64_t)blockIdx.x * blockDim.x >= n) return;   // whole warps leave together
   const bool act = q < n;
-  uint32_t k = KEY_DEAD;
+  uint32_t k = KEY_DEAD, kold = KEY_DEAD;
   if (act) {
     const uint32_t p = A.perm[q];
     const double xn[3] = {A.src[0][p], A.src[1][p], A.src[2][p]};
+    // the cell of x^n (keys are always taken from the stored position)
+    kold = tile_key32(g, (uint32_t)((int)xn[0] - (int)g.slab_lo), (uint32_t)(int)xn[1], (uint32_t)(int)xn[2]);
     const double vn[3] = {A.src[3][p], A.src[4][p], A.src[5][p]};
     const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
     double xb[3] = {xn[0], xn[1], xn[2]};
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
     A.key_new[q] = k;
   }
   const bool counted = act && k < KEY_FIRST_RESERVED;
-  const uint32_t r = count_rank(A.cell_count, g.ncells, k, counted, !act || k != A.key[q]);
+  const uint32_t r = count_rank(A.cell_count, g.ncells, k, counted, !act || k != kold);
   if (counted) A.rank[q] = r;
   if (A.peer && __any_sync(0xffffffffu, k == KEY_LEFT || k == KEY_RIGHT))
     send_leavers_peer(A.po, k, A.dst, A.dst_id, q, A.stats);
@@ -148,7 +149,6 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   A.src_id = S.id;
   A.dst_id = S.id_b;
   A.perm = S.perm;
-  A.key = S.key;
   A.cell_off = S.cell_off;
   A.key_new = S.key_new;
   A.rank = S.rank;

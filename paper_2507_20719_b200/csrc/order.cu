@@ -6,10 +6,11 @@
 // (count_rank, warp-aggregated atomics on cell_count) while it moves; the
 // exchange ranks received particles the same way.  build_order then turns the
 // counts into cell offsets (exclusive scan) and scatters perm[cell_off[k] +
-// rank] = position, key[...] = k.  The next mover gathers its inputs through
-// perm and writes them in that order, so no separate permutation pass over the
-// particle data is ever needed (≈ 16 B / particle of order metadata instead of
-// a radix sort + gather of all arrays).  Removed particles and slab leavers are
+// rank] = position.  The next mover gathers its inputs through perm and writes
+// them in that order, so no separate permutation pass over the particle data
+// is ever needed (≈ 12 B / particle of order metadata instead of a radix sort
+// + gather of all arrays).  No key array is kept: a particle's cell always
+// follows from its stored position.  Removed particles and slab leavers are
 // not counted and so drop out of the next order.
 #include <cub/device/device_scan.cuh>
 
@@ -53,8 +54,7 @@ constexpr int PERM_UNROLL = 4;
 
 __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t *__restrict__ rank,
                             const uint32_t *__restrict__ cell_off, const uint32_t *__restrict__ cell_count,
-                            const int64_t *__restrict__ d_nraw, uint32_t *__restrict__ perm,
-                            uint32_t *__restrict__ key) {
+                            const int64_t *__restrict__ d_nraw, uint32_t *__restrict__ perm) {
   // PERM_UNROLL independent elements per thread and iteration (memory-level
   // parallelism for the dependent cell_off gather)
   const int64_t n = *d_nraw;
@@ -72,7 +72,6 @@ __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t
       if (k[u] >= KEY_FIRST_RESERVED) continue;
       const uint32_t q = cell_off[k[u]] + ((r[u] & RANK_ARRIVAL) ? cell_count[k[u]] + (r[u] & ~RANK_ARRIVAL) : r[u]);
       perm[q] = (uint32_t)(p0 + u * stride);
-      key[q] = k[u];
     }
   }
 }
@@ -91,7 +90,7 @@ pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to) {
   return PIC_OK;
 }
 
-// Exclusive scan of the counts and the perm / key scatter (positions [0, d_nraw)).
+// Exclusive scan of the counts and the perm scatter (positions [0, d_nraw)).
 pic_status build_order(Ctx *ctx, int s) {
   SpeciesStore &sp = ctx->sp[s];
   const int64_t nc = ctx->geom.ncells;
@@ -102,7 +101,7 @@ pic_status build_order(Ctx *ctx, int s) {
   if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("scan: ") + cudaGetErrorString(e));
   if (sp.n_raw > 0) {
     perm_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_off, sp.cell_count,
-                                                             sp.d_nraw, sp.perm, sp.key); ++ctx->launches;
+                                                             sp.d_nraw, sp.perm); ++ctx->launches;
   }
   PIC_CUDA(cudaGetLastError());
   sp.order_valid = true;

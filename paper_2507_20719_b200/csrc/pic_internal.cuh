@@ -118,7 +118,6 @@ struct SpeciesStore {
   uint32_t *key_new = nullptr;    // [cap] key of the particle at A-position p
   uint32_t *rank = nullptr;       // [cap] rank of A-position p within its cell
   uint32_t *perm = nullptr;       // [cap] q -> A-position (cell order)
-  uint32_t *key = nullptr;        // [cap] key[q] = key_new[perm[q]]
   uint32_t *cell_count = nullptr; // [2][ncells + 1]: stayers (kept their cell), arrivals
   uint32_t *cell_tot = nullptr;   // [ncells + 1] stayers + arrivals (scan input)
   uint32_t *cell_off = nullptr;   // [ncells + 1]; cell_off[ncells] = live count

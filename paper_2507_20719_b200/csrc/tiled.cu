@@ -85,7 +85,6 @@ struct MoverTArgs {
   double *dst[7];             // buffer B (written in cell order)
   int64_t *dst_id;
   const uint32_t *perm;       // q -> A-position
-  const uint32_t *key;        // key[q]: cell of x^n
   const uint32_t *cell_off;   // tile t covers q in [cell_off[64 t], cell_off[64 (t+1)])
   uint32_t *key_new, *rank, *cell_count;
   int64_t *d_nraw;
@@ -101,7 +100,6 @@ struct DepositArgs {
   Geom g;
   const double *src[7];       // particle state (buffer A after the mover)
   const uint32_t *perm;       // new order
-  const uint32_t *key;
   const uint32_t *cell_off;
   double *mom;                // ghosted moment arrays [10][m_plane]
   unsigned long long *stats;
@@ -189,9 +187,6 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
 }
 
 // ----------------------------------------------------------------- mover ----
-#ifndef PIC_MOVER_KOLD_FROM_X
-#define PIC_MOVER_KOLD_FROM_X 1
-#endif
 #ifndef PIC_MOVER_MINB
 #define PIC_MOVER_MINB 2
 #endif
@@ -267,9 +262,6 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     if (q < wend) {
       uint32_t *slot = pk + (ri % PK_SLOTS) * 64 + lane;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(A.perm + q) : "memory");
-#if !PIC_MOVER_KOLD_FROM_X
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 32)), "l"(A.key + q) : "memory");
-#endif
     }
   };
   auto fetch_src = [&](int ri) {       // sources of round ri (its perm is already in the ring)
@@ -300,11 +292,7 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32, ++ri) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-#if PIC_MOVER_KOLD_FROM_X
-    uint32_t kold = 0u;          // set from x^n below
-#else
-    const uint32_t kold = act ? pk[(ri % PK_SLOTS) * 64 + 32 + lane] : 0u;
-#endif
+    uint32_t kold = 0u;          // the cell of x^n, set below
     fetch_src(ri + SRC_STAGES - 1);
     fetch_pk(ri + PK_AHEAD);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -316,12 +304,10 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       const int64_t idv = __double_as_longlong(sv[7 * 32]);
       const double xn[3] = {sv[0], sv[32], sv[64]};
       const double vn[3] = {sv[96], sv[128], sv[160]};
-#if PIC_MOVER_KOLD_FROM_X
       // the cell of x^n (the key the order was built from: keys are always
-      // taken from the stored position, so no key array needs to be read; a
-      // mismatch would only reclassify a stayer as an arrival or back)
+      // taken from the stored position, so no key array is kept; a mismatch
+      // would only reclassify a stayer as an arrival or back)
       kold = tile_key32(g, (uint32_t)((int)xn[0] - (int)g.slab_lo), (uint32_t)(int)xn[1], (uint32_t)(int)xn[2]);
-#endif
       double xb[3] = {xn[0], xn[1], xn[2]};
       double vb[3];
       bool clamped = false;
@@ -509,40 +495,37 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
   // two-stage software pipeline: the sources of round r+1 and the perm/key of
   // round r+2 are in flight while round r is reduced.  Lanes past the end load
   // position 0 (always valid) and get q = 0 below, so the loads need no predicate.
-  uint32_t k_nx = 0, p_nx = 0, k_n2 = 0, p_n2 = 0;
+  uint32_t p_nx = 0, p_n2 = 0;
   double s_nx[7];
   {
     const uint32_t p = wbeg + lane;
-    if (p < wend) {
-      k_nx = A.key[p];
-      p_nx = A.perm[p];
-    }
-    if (p + 32 < wend) {
-      k_n2 = A.key[p + 32];
-      p_n2 = A.perm[p + 32];
-    }
+    if (p < wend) p_nx = A.perm[p];
+    if (p + 32 < wend) p_n2 = A.perm[p + 32];
 #pragma unroll
     for (int k = 0; k < 7; ++k) s_nx[k] = A.src[k][p_nx];
   }
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
     const bool act = p < wend;
-    const uint32_t k_cur = k_nx;
     double s_cur[7];
 #pragma unroll
     for (int k = 0; k < 7; ++k) s_cur[k] = s_nx[k];
     // advance the pipeline
-    k_nx = k_n2;
     p_nx = p_n2;
 #pragma unroll
     for (int k = 0; k < 7; ++k) s_nx[k] = A.src[k][p_nx];
-    p_n2 = 0;
-    if (p + 64 < wend) {
-      k_n2 = A.key[p + 64];
-      p_n2 = A.perm[p + 64];
-    }
+    p_n2 = (p + 64 < wend) ? A.perm[p + 64] : 0u;
     // inactive lanes carry zeros (q = 0: every value is 0, the weights finite)
-    const int c = act ? (int)(k_cur & (TILE3 - 1)) : 64;   // 64: sentinel, no particle
+    // the particle's cell in the tile, from its position (the order's cell:
+    // keys are taken from positions; clamped to the tile, where a cell one off
+    // still gives the same weights, f = 0 or 1)
+    int c = 64;   // 64: sentinel, no particle
+    if (act) {
+      const int lx = min(max((int)s_cur[0] - (int)ox, 0), TILE - 1);
+      const int ly = min(max((int)s_cur[1] - (int)oy, 0), TILE - 1);
+      const int lz = min(max((int)s_cur[2] - (int)oz, 0), TILE - 1);
+      c = lx + TILE * (ly + TILE * lz);
+    }
     double Sk[8], val[10];
     {
       const double x = s_cur[0], y = s_cur[1], z = s_cur[2];
@@ -676,7 +659,6 @@ pic_status launch_tiled_step(Ctx *ctx, int s) {
   A.src_id = sp.id;
   A.dst_id = sp.id_b;
   A.perm = sp.perm;
-  A.key = sp.key;
   A.cell_off = sp.cell_off;
   A.key_new = sp.key_new;
   A.rank = sp.rank;
@@ -730,7 +712,6 @@ pic_status launch_tiled_deposit(Ctx *ctx, int s) {
   A.g = ctx->geom;
   for (int k = 0; k < 7; ++k) A.src[k] = sp.a[k];
   A.perm = sp.perm;
-  A.key = sp.key;
   A.cell_off = sp.cell_off;
   A.mom = sp.mom;
   A.stats = ctx->stats;
