@@ -10,7 +10,7 @@
 //     memory; the CTA pre-scales them by k_s = (q/m) dt/2 and k_s / c so the
 //     iteration reads E' = k_s E and a = k_s B / c directly (R7, R8).
 //  2. Warps split the tile's particles evenly; lane = particle, rounds of 32.
-//     perm/key run PK_AHEAD rounds ahead and the sources SRC_STAGES - 1 rounds
+//     perm runs PK_AHEAD rounds ahead and the sources SRC_STAGES - 1 rounds
 //     ahead through cp.async (LDGSTS) rings in shared memory (mostly
 //     contiguous runs: every cell lists its stayers first).  n_iter predictor-
 //     corrector iterations (R1, R2) with trilinear gathers from shared memory
@@ -56,8 +56,8 @@ constexpr int SRC_STAGES = PIC_SRC_STAGES;   // mover: rounds of gathered source
 #ifndef PIC_PK_AHEAD
 #define PIC_PK_AHEAD 3
 #endif
-constexpr int PK_AHEAD = PIC_PK_AHEAD;   // mover: perm/key fetched this many rounds ahead
-constexpr int PK_SLOTS = PK_AHEAD + 1;   // mover: perm/key ring slots
+constexpr int PK_AHEAD = PIC_PK_AHEAD;   // mover: perm fetched this many rounds ahead
+constexpr int PK_SLOTS = PK_AHEAD + 1;   // mover: perm ring slots
 constexpr int MOVER_WARP_STAGE = SRC_STAGES * 8 * 32 + PK_SLOTS * 2 * 32 / 2;  // doubles per warp
 // deposit staging per warp: S[32 particles][8 corners], V[32][moments 0..7]
 // and V2[32][moments 8, 9].  S and V rows are 8 doubles whose 16-byte pairs
@@ -250,14 +250,15 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
   const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
 
   // Software pipeline through shared memory (cp.async / LDGSTS, no register
-  // dependencies): in round r the warp gathers the sources of round r+2 into a
-  // 3-deep buffer ring and fetches perm/key of round r+5 into a 6-slot ring, one
-  // commit group per round; "wait_group 2" then guarantees round r's sources.
-  // The counting-sort rank of a round completes during the next one, so the
-  // global atomic's latency overlaps compute.
-  double *stg = stage_base + (size_t)warp * MOVER_WARP_STAGE;          // [3][8][32] doubles
-  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + SRC_STAGES * 8 * 32);  // [6][2][32] (perm, key)
-  auto fetch_pk = [&](int ri) {        // perm/key of round ri
+  // dependencies): in round r the warp gathers the sources of round
+  // r+SRC_STAGES-1 into an SRC_STAGES-deep ring and fetches perm of round
+  // r+PK_AHEAD into the perm ring, one commit group per round; "wait_group
+  // SRC_STAGES-1" then guarantees round r's sources.  The counting-sort rank of
+  // a round completes during the next one, so the global atomic's latency
+  // overlaps compute.
+  double *stg = stage_base + (size_t)warp * MOVER_WARP_STAGE;          // [SRC_STAGES][8][32] doubles
+  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + SRC_STAGES * 8 * 32);  // [PK_SLOTS][64]: perm in [0, 32)
+  auto fetch_pk = [&](int ri) {        // perm of round ri
     const uint32_t q = wbeg + 32u * ri + lane;
     if (q < wend) {
       uint32_t *slot = pk + (ri % PK_SLOTS) * 64 + lane;
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
                  : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
   };
 
-  // two-stage software pipeline: the sources of round r+1 and the perm/key of
+  // two-stage software pipeline: the sources of round r+1 and the perm of
   // round r+2 are in flight while round r is reduced.  Lanes past the end load
   // position 0 (always valid) and get q = 0 below, so the loads need no predicate.
   uint32_t p_nx = 0, p_n2 = 0;
