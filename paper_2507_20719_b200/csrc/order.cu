@@ -50,7 +50,10 @@ __global__ void total_kernel(const uint32_t *__restrict__ cell_count, uint32_t *
     tot[c] = cell_count[c] + cell_count[ncells + 1 + c];
 }
 
-constexpr int PERM_UNROLL = 4;
+#ifndef PIC_PERM_UNROLL
+#define PIC_PERM_UNROLL 8
+#endif
+constexpr int PERM_UNROLL = PIC_PERM_UNROLL;
 
 __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t *__restrict__ rank,
                             const uint32_t *__restrict__ cell_off, const uint32_t *__restrict__ cell_count,
