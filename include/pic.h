@@ -5,7 +5,8 @@
  * ghost-node moment sums and particle migration over NVLink peer memory (or
  * NCCL), plus the NEXT rows built on it: the relativistic mover (NEXT-1), the
  * field solver's sources chi, rho-hat, J-hat (Eq. 5-6, NEXT-2), inflow
- * injection and particle control (NEXT-3).
+ * injection and particle control (NEXT-3), and the velocity-histogram
+ * Gaussian-mixture fit of the GMM compression (NEXT-4).
  *
  *   PAPER.md:141-145  Eq. 1  equations of motion; q_s, m_s, x_p, v_p, E_p, B_p
  *   PAPER.md:149-165  Eq. 2  predictor-corrector mover, fixed-point on v-bar
@@ -14,7 +15,8 @@
  *   PAPER.md:256-261, 291-334  Alg. 1: mover -> interpolation -> MPI exchange
  *   PAPER.md:199-213  Eq. 5-6 susceptibility and corrected sources (NEXT-2)
  *   PAPER.md:232-249  §III-B injection and particle control (NEXT-3)
- * Readings of the paper (R1..R31) are listed in DESIGN.md §3.
+ *   PAPER.md:366-379  §IV GMM velocity binning and EM fit (NEXT-4)
+ * Readings of the paper (R1..R33) are listed in DESIGN.md §3.
  *
  * Conventions (all calls):
  *  - Every entry point returns pic_status; none throws, exits or prints.
