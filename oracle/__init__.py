@@ -132,10 +132,15 @@ def node_counts(g: Grid):
 
 
 def sample(g: Grid, F: FieldWindow, pos) -> np.ndarray:
+    return sample_ex(g, F, pos)[0]
+
+
+def sample_ex(g: Grid, F: FieldWindow, pos):
+    """(E,B at pos, 1 if the R11 clamp to the window was applied else 0)."""
     p = np.ascontiguousarray(pos, dtype=np.float64)
     out = np.zeros(6)
-    _load().oracle_sample(C.byref(g), C.byref(F.c), _dptr(p), _dptr(out))
-    return out
+    clamped = _load().oracle_sample(C.byref(g), C.byref(F.c), _dptr(p), _dptr(out))
+    return out, int(clamped)
 
 
 def mover(g: Grid, F: FieldWindow, qom: float, n_iter: int, parts: dict, status=None,

@@ -32,9 +32,9 @@
  * Pins (tests/test_oracle_pins.py) tie every function here to closed forms:
  * free streaming, gyration angle/radius, ExB drift, uniform-E kick, the
  * linear-field worked example, node/cell-centre stencils, global sums,
- * gather/scatter adjointness, lattice loading and exact-rational brute force.
- * oracle_mover with open boundaries near the ghost clamp (R11) is
- * "parity unpinned" for the clamp branch itself.
+ * gather/scatter adjointness, lattice loading and exact-rational brute force;
+ * the R11 clamp branch of oracle_sample by the closed form of a linear field
+ * at the clamped point (test_sample_clamp_branch_linear_field_closed_form).
  */
 #include <math.h>
 #include <stdint.h>
@@ -600,16 +600,17 @@ int64_t oracle_split(const oracle_grid *g, int species, int64_t np, int64_t cap,
 
 /* Coalescence ("pair-wise merging between particles that are
  * close in the phase space by combining their statistical weights"; reading
- * R31).  Per cell with 2 <= n_c <= 512 ALIVE particles, all with velocity bins
- * inside (-2^20, 2^20) (other cells are left alone): sort them by
- * (floor(u/dv), floor(v/dv), floor(w/dv), id); scan the sorted list and merge
- * neighbours i, i+1 whose three velocity bins are equal (then continue at i+2)
- * until m_c = floor(frac n_c) merges.  Merge: q = q1 + q2, x = (q1 x1 + q2 x2)/q,
- * v = (q1 v1 + q2 v2)/q per component (charge, momentum and the charge
- * centroid conserved); the particle with the smaller id keeps the result, the
- * other becomes ORACLE_MERGED.  Returns the number of merges.               */
+ * R31).  In every cell with n_c >= 2 ALIVE particles ("in cells
+ * with an excessive number of particles"; no size or velocity limit): sort them
+ * by the velocity bins (floor(u/dv), floor(v/dv), floor(w/dv)) -- compared as
+ * fp64 values, so any finite velocity has a bin -- then by id; scan the sorted
+ * list and merge neighbours i, i+1 whose three bins are equal (then continue
+ * at i+2) until m_c = floor(frac n_c) merges.  Merge: q = q1 + q2,
+ * x = (q1 x1 + q2 x2)/q, v = (q1 v1 + q2 v2)/q per component (charge, momentum
+ * and the charge centroid conserved); the particle with the smaller id keeps
+ * the result, the other becomes ORACLE_MERGED.  Returns the number of merges. */
 enum { ORACLE_MERGED = 3 };
-typedef struct { int64_t cell, bx, by, bz, id, idx; } coal_key;
+typedef struct { int64_t cell; double bx, by, bz; int64_t id, idx; } coal_key;
 static int coal_cmp(const void *pa, const void *pb) {
   const coal_key *a = (const coal_key *)pa, *b = (const coal_key *)pb;
   if (a->cell != b->cell) return a->cell < b->cell ? -1 : 1;
@@ -629,9 +630,9 @@ int64_t oracle_coalesce(const oracle_grid *g, int64_t np, double *x, double *y, 
     if (status[i] != ORACLE_ALIVE) continue;
     int64_t cx = (int64_t)floor(x[i] / dl[0]), cy = (int64_t)floor(y[i] / dl[1]), cz = (int64_t)floor(z[i] / dl[2]);
     k[m].cell = (cz * g->ncell[1] + cy) * g->ncell[0] + cx;
-    k[m].bx = (int64_t)floor(u[i] / dv);
-    k[m].by = (int64_t)floor(v[i] / dv);
-    k[m].bz = (int64_t)floor(w[i] / dv);
+    k[m].bx = floor(u[i] / dv);
+    k[m].by = floor(v[i] / dv);
+    k[m].bz = floor(w[i] / dv);
     k[m].id = id[i];
     k[m].idx = i;
     ++m;
@@ -642,13 +643,7 @@ int64_t oracle_coalesce(const oracle_grid *g, int64_t np, double *x, double *y, 
     int64_t s1 = s0;
     while (s1 < m && k[s1].cell == k[s0].cell) ++s1;
     int64_t nc = s1 - s0;
-    int wide = 0;
-    for (int64_t t = s0; t < s1; ++t) {
-      const int64_t lim = 1 << 20;
-      if (k[t].bx <= -lim || k[t].bx >= lim || k[t].by <= -lim || k[t].by >= lim || k[t].bz <= -lim || k[t].bz >= lim)
-        wide = 1;
-    }
-    if (nc >= 2 && nc <= 512 && !wide) {
+    if (nc >= 2) {
       int64_t mc = (int64_t)floor(frac * (double)nc), done = 0;
       for (int64_t t = s0; t + 1 < s1 && done < mc;) {
         const coal_key *a = &k[t], *b = &k[t + 1];

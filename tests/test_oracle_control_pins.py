@@ -122,3 +122,35 @@ def test_coalesce_hand_worked_cell():
     assert p["q"][0] == 4.0
     np.testing.assert_allclose([p["x"][0], p["u"][0], p["w"][0]],
                                [(0.1 + 3 * 0.7) / 4, (0.25 + 3 * 0.5) / 4, (0.0 + 3 * 0.25) / 4], rtol=1e-15)
+
+
+def test_coalesce_overfull_cell_and_wide_bins_hand_worked():
+    """R31 / PAPER.md:243 ("in cells with an excessive number of particles"): no
+    cell-size or velocity-range limit.  One cell with 2000 particles, ids 0..1999,
+    u = (id % 2) + 1/2 (dv = 1: even ids in bin 0, odd ids in bin 1), frac = 1/2
+    -> m = 1000 merges: the sorted list is [0, 2, ..., 1998 | 1, 3, ..., 1999], so
+    the pairs are (0,2), (4,6), ..., (1996,1998) then (1,3), ..., (1997,1999) --
+    every id = 2 mod 4 or 3 mod 4 is merged into id - 2.  A second cell holds
+    two particles at u = 3e12 and 3e12 + 0.5 (same bin, floor = 3e12, far beyond
+    any packed-key range) and one at -7e15 (own bin): frac 0.5 of 3 -> 1 merge."""
+    g = O.make_grid((2, 1, 1), (2.0, 1.0, 1.0), bc=(1, 1, 1), dt=0.5)
+    n = 2000
+    ids = np.arange(n, dtype=np.int64)
+    rng = np.random.default_rng(4)
+    p = {"x": rng.uniform(0.01, 0.99, n), "y": rng.uniform(0.01, 0.99, n), "z": rng.uniform(0.01, 0.99, n),
+         "u": (ids % 2) + 0.5, "v": np.full(n, 0.25), "w": np.full(n, 0.75), "q": np.full(n, 1.0), "id": ids}
+    wide = {"x": np.array([1.5, 1.25, 1.75]), "y": np.array([0.5, 0.5, 0.5]), "z": np.array([0.5, 0.5, 0.5]),
+            "u": np.array([3e12, 3e12 + 0.5, -7e15]), "v": np.zeros(3), "w": np.zeros(3), "q": np.array([1.0, 3.0, 1.0]),
+            "id": np.array([5000, 5001, 5002], dtype=np.int64)}
+    P = {k: np.ascontiguousarray(np.concatenate([p[k], wide[k]])) for k in p}
+    st = np.zeros(n + 3, dtype=np.int8)
+    m = O.coalesce(g, P, st, 1.0, 0.5)
+    assert m == 1000 + 1
+    merged = set(np.nonzero(st == O.MERGED)[0].tolist())
+    want = {i for i in range(n) if i % 4 in (2, 3)} | {n + 1}
+    assert merged == want
+    for i in range(0, n, 4):
+        for k in (i, i + 1):
+            assert P["q"][k] == 2.0 and P["u"][k] == p["u"][k]
+            assert P["x"][k] == (p["x"][k] + p["x"][k + 2]) / 2
+    assert P["q"][n] == 4.0 and P["u"][n] == (3e12 + 3 * (3e12 + 0.5)) / 4

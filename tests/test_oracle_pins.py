@@ -448,3 +448,47 @@ def test_removed_particles_excluded():
     st = np.array([O.REMOVED], dtype=np.int8)
     mom, _ = O.moments(g, p, status=st)
     assert not mom.any()
+
+
+# ------------------------------------------ R11: the clamp to the window ----
+def test_sample_clamp_branch_linear_field_closed_form():
+    """R11: a position outside the field window is clamped to
+    the window box (constant extension along the outward normal).  For a linear
+    field the trilinear sample at the clamped point is the field there, so the
+    expected value is the linear function evaluated at clip(p, box) -- a closed
+    form that does not use the oracle.  Positions beyond every face, edge and
+    corner of the box, and NaN (clamped to the low face), are covered; the
+    clamp flag is set exactly when a coordinate is outside."""
+    G = 2
+    g = O.make_grid(NC, LEN, bc=(O.OPEN,) * 3)
+    fn = lambda X, Y, Z: [X, 2 * Y - 1, 0.5 * Z + X, -Y + 3, Z - X, 0.25 * X + Y + Z]
+    F = window(NC, G, fn, LEN)
+    d = LEN[0] / NC[0]
+    lo, hi = -G * d, (NC[0] + G) * d          # window box per axis (cubic here)
+    rng = np.random.default_rng(11)
+    checked = 0
+    for sx in (-1, 0, 1):
+        for sy in (-1, 0, 1):
+            for sz in (-1, 0, 1):
+                for _ in range(6):
+                    p = rng.uniform(lo + 0.01, hi - 0.01, 3)
+                    for ax, sgn in enumerate((sx, sy, sz)):
+                        if sgn < 0:
+                            p[ax] = lo - rng.uniform(1e-9, 5.0)
+                        elif sgn > 0:
+                            p[ax] = hi + rng.uniform(1e-9, 5.0)
+                    c = np.clip(p, lo, hi)
+                    got, flag = O.sample_ex(g, F, p)
+                    np.testing.assert_allclose(got, fn(*c), rtol=0, atol=1e-12)
+                    assert flag == int((sx, sy, sz) != (0, 0, 0))
+                    checked += 1
+    assert checked == 27 * 6
+    # exactly on the top face: inside (no clamp), value of the face
+    p = np.array([hi, 1.0, 1.0])
+    got, flag = O.sample_ex(g, F, p)
+    assert flag == 0
+    np.testing.assert_allclose(got, fn(*p), rtol=0, atol=1e-12)
+    # NaN coordinate: clamped to the low face, flagged
+    got, flag = O.sample_ex(g, F, np.array([np.nan, 1.0, 1.0]))
+    assert flag == 1
+    np.testing.assert_allclose(got, fn(lo, 1.0, 1.0), rtol=0, atol=1e-12)
