@@ -368,6 +368,7 @@ def main():
             dist.barrier()
             torch.cuda.synchronize()
 
+    barrier()    # every rank has its context, particles and fields before the first (collective) cycle
     for _ in range(args.warmup):
         ctx.cycle()
     ctx.sync()

@@ -30,7 +30,7 @@
  *  - All GPU work is enqueued on the context stream (pic_set_stream) and is
  *    asynchronous unless stated; device-side errors (non-finite values,
  *    particles beyond ghost reach, capacity overflow) are latched in device
- *    flags and surfaced by the next pic_sync / pic_exchange.
+ *    flags and surfaced by the next pic_sync.
  *  - Per cycle the call order is pic_mover -> pic_moments -> pic_exchange
  *    (for each species, mover before moments); other orders return
  *    PIC_ESTATE.  With nranks > 1, pic_mover and pic_exchange are COLLECTIVE
@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define PIC_ABI_VERSION 3
+#define PIC_ABI_VERSION 4
 #define PIC_MAX_SPECIES 8
 #define PIC_NCCL_ID_BYTES 128
 #define PIC_N_MOMENTS 10  /* rho, Jx, Jy, Jz, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz (R16) */
@@ -87,10 +87,21 @@ typedef enum {
                               neighbours' workspaces (CUDA IPC), else NCCL     */
   PIC_TRANSPORT_NCCL = 1,  /* NCCL point-to-point messages, host sync for the
                               migration counts                                 */
-  PIC_TRANSPORT_PEER = 2   /* the mover writes slab leavers into the
+  PIC_TRANSPORT_PEER = 2,  /* the mover writes slab leavers into the
                               neighbour's buffer over NVLink and ghost planes
                               are read from peer memory; pic_init fails if the
                               neighbours cannot be mapped                      */
+  PIC_TRANSPORT_LOOPBACK = 3  /* the nranks slab contexts live in ONE process
+                              on ONE device (no NCCL, nccl_id ignored) and are
+                              joined by pic_loopback_link; the peer transport's
+                              data-path kernels then run unchanged (migration
+                              stores from the mover, arrivals, ghost-plane
+                              reads); its barriers become event handshakes
+                              between the contexts' streams.  Each context
+                              needs its own non-default stream and its own
+                              host thread (a barrier blocks that thread until
+                              the neighbours reach it, 20 s at most).  For
+                              testing the multi-rank path on one GPU.         */
 } pic_transport;
 
 typedef struct {
@@ -137,6 +148,16 @@ PIC_API pic_status pic_workspace_bytes(const pic_config *cfg, int64_t *bytes);
  * may be NULL when nranks == 1).  The config is copied.                      */
 PIC_API pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
                     int64_t bytes, pic_ctx **out);
+
+/* Join the n contexts of a loopback decomposition (PIC_TRANSPORT_LOOPBACK):
+ * ctxs[r] must be rank r of n, all on one device, their slabs tiling the x
+ * axis in rank order.  Afterwards each context addresses its slab neighbours'
+ * receive buffers, control words and moment planes directly, exactly as the
+ * peer transport does over CUDA IPC (the particle
+ * communication of Alg. 1 phase 2, here within one device).  Call once, after
+ * pic_init of all n and before the first pic_mover.  Synchronises the device.
+ * Errors: PIC_EINVAL (mismatched configs / devices), PIC_ESTATE (linked twice). */
+PIC_API pic_status pic_loopback_link(pic_ctx *const *ctxs, int32_t n);
 
 /* Stream for all subsequent work (a cudaStream_t, e.g. torch's current
  * stream).  NULL = the legacy default stream.                                */
@@ -188,9 +209,16 @@ PIC_API pic_status pic_mover(pic_ctx *ctx, int32_t s);
  * final after pic_exchange).                                                 */
 PIC_API pic_status pic_moments(pic_ctx *ctx, int32_t s);
 
-/* COLLECTIVE when nranks > 1.  Sum ghost-node moment planes into their owners
- * (periodic folds along y, z, and along x when nranks == 1).  Surfaces
- * latched device errors.                                                     */
+/* Alg. 1 phase 2, PAPER.md:256-261, 317-320 (the nodes a slab shares with its
+ * neighbour; the paper's "particle communication" exchange point) and R18
+ * (periodic node N == node 0).  COLLECTIVE when nranks > 1: adds the ghost
+ * node planes deposited next to the slab face into their owner's planes
+ * (peer transport: the owner reads its left neighbour's plane x = slab_lo
+ * over NVLink; NCCL transport: one send/recv group), then folds the periodic
+ * images along y, z (and along x when nranks == 1).  Requires pic_moments of
+ * every species since the last pic_mover (PIC_ESTATE otherwise).  Afterwards
+ * the owned node values are final (pic_get_moments / pic_moment_ptr).
+ * Asynchronous; latched device errors are returned by pic_sync.              */
 PIC_API pic_status pic_exchange(pic_ctx *ctx);
 
 /* Shorthand for one full cycle: pic_mover(-1), pic_moments(-1),
@@ -231,7 +259,10 @@ PIC_API pic_status pic_get_moments_async(pic_ctx *ctx, int32_t s, double *out);
  *   J_hat[3]    sum_s R_s (J_s - (dt/2) div Pi_s)
  *   rho_hat[1]  sum_s rho_s - dt div J_hat
  * Central differences (periodic wrap; one-sided at open-axis boundary nodes).
- * Single rank in this build (PIC_EINVAL otherwise).  Synchronises.          */
+ * nranks > 1: COLLECTIVE with the peer transport (the x derivatives at a slab
+ * face read the neighbour's adjacent owned plane from its mapped workspace,
+ * behind a flag barrier); the NCCL transport returns PIC_EINVAL.
+ * Synchronises.                                                              */
 PIC_API pic_status pic_implicit_sources(pic_ctx *ctx, double *chi, double *rho_hat, double *J_hat);
 
 /* NEXT-3: inflow injection at the x = 0 face of an open x axis (PAPER.md:
@@ -252,10 +283,12 @@ PIC_API pic_status pic_set_injection(pic_ctx *ctx, int32_t s, int32_t ppc, doubl
  * p = min(1, (target - n)/n) (Philox draw keyed by its id, seed and the cycle)
  * into two of half charge at x -/+ eps Delta e, e a random unit vector, unless
  * a child would leave the cell; n > target (1 + theta): coalescence — in each
- * cell with 2..512 particles sorted by (floor(v/dv) per component, id),
- * neighbours with equal velocity bins merge pair-wise (charge-weighted x and
- * v; the smaller id survives) until floor(frac n_c) merges, frac = (n -
- * target)/n.  *action: 0 none, 1 split, 2 coalesced.                       */
+ * cell with >= 2 particles (any number: cells of more than 512 particles or
+ * with a velocity bin beyond +-2^20 take an unpacked global-memory sort)
+ * sorted by (floor(v/dv) per component, id), neighbours with equal velocity
+ * bins merge pair-wise (charge-weighted x and v; the smaller id survives)
+ * until floor(frac n_c) merges, frac = (n - target)/n.  Uses the store's
+ * second buffer as scratch.  *action: 0 none, 1 split, 2 coalesced.         */
 PIC_API pic_status pic_control(pic_ctx *ctx, int32_t s, int64_t target, double theta, double eps, double dv,
                                uint64_t seed, int32_t *action);
 
@@ -284,7 +317,7 @@ PIC_API pic_status pic_moment_ptr(const pic_ctx *ctx, int32_t s, int32_t comp, c
  * enqueued by pic_get_moments_async / pic_set_fields so far.                 */
 PIC_API pic_status pic_join_copies(pic_ctx *ctx);
 
-/* Transport in use: PIC_TRANSPORT_PEER or PIC_TRANSPORT_NCCL when nranks > 1
+/* Transport in use: PIC_TRANSPORT_PEER, _NCCL or _LOOPBACK when nranks > 1
  * (AUTO resolved at pic_init), PIC_TRANSPORT_AUTO for a single rank.        */
 PIC_API pic_status pic_get_transport(const pic_ctx *ctx, int32_t *out);
 

@@ -54,7 +54,7 @@ pic_status validate(const pic_config *c, std::string *why) {
                          ((c->ncell[2] + TILE - 1) / TILE) * TILE3;
   if (tcells >= (int64_t)KEY_FIRST_RESERVED) { *why = "too many local cells for 32-bit keys"; return PIC_EINVAL; }
   if (c->planet_radius < 0) { *why = "planet_radius < 0"; return PIC_EINVAL; }
-  if (c->transport < PIC_TRANSPORT_AUTO || c->transport > PIC_TRANSPORT_PEER) { *why = "bad transport"; return PIC_EINVAL; }
+  if (c->transport < PIC_TRANSPORT_AUTO || c->transport > PIC_TRANSPORT_LOOPBACK) { *why = "bad transport"; return PIC_EINVAL; }
   if (c->kernel < 0 || c->kernel > 2) { *why = "bad kernel"; return PIC_EINVAL; }
   if (c->relativistic != 0 && c->relativistic != 1) { *why = "relativistic must be 0 or 1"; return PIC_EINVAL; }
   return PIC_OK;
@@ -260,7 +260,11 @@ pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->copies_done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fields_done, cudaEventDisableTiming);
   if (e != cudaSuccess) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_ECUDA; }
-  if (cfg->nranks > 1) {
+  if (cfg->nranks > 1 && cfg->transport == PIC_TRANSPORT_LOOPBACK) {
+    // no communicator: pic_loopback_link joins the contexts of this process
+    e = cudaMemset(ctx->peer_ctl, 0, sizeof(PeerCtl));
+    if (e != cudaSuccess) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_ECUDA; }
+  } else if (cfg->nranks > 1) {
     if (!nccl_id) { cudaFreeHost(ctx->host_counts); delete ctx; return PIC_EINVAL; }
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof(id));
@@ -283,6 +287,37 @@ pic_status pic_init(const pic_config *cfg, const void *nccl_id, void *workspace,
   }
   *out = reinterpret_cast<pic_ctx *>(ctx);
   return PIC_OK;
+}
+
+pic_status pic_loopback_link(pic_ctx *const *ctxs, int32_t n) {
+  if (!ctxs || n < 2 || n > 64) return PIC_EINVAL;
+  int dev0 = -1;
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r]) return PIC_EINVAL;
+    Ctx *ctx = C(ctxs[r]);
+    const pic_config &c = ctx->cfg;
+    if (c.transport != PIC_TRANSPORT_LOOPBACK || c.nranks != n || c.rank != r)
+      return fail(ctx, PIC_EINVAL, "pic_loopback_link: ctxs[r] must be rank r of a loopback config with nranks == n");
+    if (ctx->peer) return fail(ctx, PIC_ESTATE, "pic_loopback_link: already linked");
+    if (r > 0) {
+      const pic_config &c0 = C(ctxs[0])->cfg;
+      bool same = c.n_species == c0.n_species && c.ghost == c0.ghost && c.slab_lo == C(ctxs[r - 1])->cfg.slab_hi;
+      for (int d = 0; d < 3; ++d) same = same && c.ncell[d] == c0.ncell[d] && c.bc[d] == c0.bc[d];
+      if (!same) return fail(ctx, PIC_EINVAL, "pic_loopback_link: slabs must tile one grid in rank order");
+    }
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ctx->workspace) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, PIC_ECUDA, "pic_loopback_link: workspace is not device memory");
+    }
+    if (dev0 < 0) dev0 = at.device;
+    if (at.device != dev0) return fail(ctx, PIC_EINVAL, "pic_loopback_link: contexts on different devices");
+  }
+  if (C(ctxs[0])->cfg.slab_lo != 0 || C(ctxs[n - 1])->cfg.slab_hi != C(ctxs[0])->cfg.ncell[0])
+    return fail(C(ctxs[0]), PIC_EINVAL, "pic_loopback_link: slabs must cover the x axis");
+  std::vector<Ctx *> v(n);
+  for (int r = 0; r < n; ++r) v[r] = C(ctxs[r]);
+  return loopback_link(v.data(), n);
 }
 
 pic_status pic_set_stream(pic_ctx *p, void *stream) {
@@ -359,6 +394,13 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
   pic_status st = check_species(ctx, s, true);
   if (st != PIC_OK) return st;
   if (!ctx->fields_set) return fail(ctx, PIC_ESTATE, "pic_set_fields must precede pic_mover");
+  if (ctx->cfg.nranks > 1 && ctx->cfg.transport == PIC_TRANSPORT_LOOPBACK) {
+    if (!ctx->peer) return fail(ctx, PIC_ESTATE, "loopback contexts need pic_loopback_link before pic_mover");
+    // the flag barriers spin on the device: every context needs its own stream
+    for (Ctx *nb : ctx->loop_nb)
+      if (!ctx->stream || (nb && nb->stream == ctx->stream))
+        return fail(ctx, PIC_EINVAL, "loopback contexts need distinct non-default streams (pic_set_stream)");
+  }
   const int s0 = s < 0 ? 0 : s, s1 = s < 0 ? ctx->cfg.n_species : s + 1;
   for (int k = s0; k < s1; ++k)
     if (ctx->sp[k].moved || !ctx->sp[k].order_valid)
@@ -572,7 +614,9 @@ pic_status pic_join_copies(pic_ctx *p) {
 pic_status pic_get_transport(const pic_ctx *p, int32_t *out) {
   if (!p || !out) return PIC_EINVAL;
   const Ctx *ctx = C(p);
-  *out = ctx->cfg.nranks < 2 ? PIC_TRANSPORT_AUTO : (ctx->peer ? PIC_TRANSPORT_PEER : PIC_TRANSPORT_NCCL);
+  *out = ctx->cfg.nranks < 2 ? PIC_TRANSPORT_AUTO
+        : ctx->cfg.transport == PIC_TRANSPORT_LOOPBACK ? PIC_TRANSPORT_LOOPBACK
+        : (ctx->peer ? PIC_TRANSPORT_PEER : PIC_TRANSPORT_NCCL);
   return PIC_OK;
 }
 

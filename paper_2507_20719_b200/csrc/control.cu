@@ -111,9 +111,19 @@ __global__ void __launch_bounds__(256) split_kernel(const SplitArgs A) {
 }
 
 // ---------------------------------------------------------- coalescence ----
-constexpr int COAL_MAX = 512;        // cells with more particles are left alone (R31)
+// Every cell with >= 2 particles is coalesced (R31: "in cells
+// with an excessive number of particles, we perform pair-wise merging").  Two
+// paths reach the same sorted order (velocity bins, then id) and the same pairs:
+//  * coalesce_kernel: a warp per cell, for cells of 2..COAL_MAX particles whose
+//    bins fit the packed 63-bit key (|bin| < 2^20): bitonic sort in shared memory;
+//  * coalesce_big_kernel: every other cell (overfull, or a bin beyond the
+//    packed range), listed by the first kernel: a CTA per cell sorts the
+//    unpacked keys (bins as fp64, id) in global scratch (the free B buffers of
+//    the store) with a bitonic network of ascending compare-exchanges, which
+//    handles any cell size.
+constexpr int COAL_MAX = 512;        // shared-memory path: particles per cell
 constexpr int COAL_WARPS = 8;
-constexpr int64_t COAL_BIN_LIM = 1 << 20;   // |velocity bin| bound of the packed key (R31)
+constexpr int64_t COAL_BIN_LIM = 1 << 20;   // |velocity bin| bound of the packed key
 // per warp: packed bin key, id, particle index in the cell, pair list
 constexpr size_t COAL_WARP_BYTES = COAL_MAX * (8 + 8 + 4) + (COAL_MAX / 2) * 4;
 constexpr size_t COAL_SMEM = COAL_WARP_BYTES * COAL_WARPS;
@@ -126,6 +136,18 @@ struct CoalArgs {
   uint32_t *key_new;
   double dv, frac;
   unsigned long long *merges;
+  // cells for coalesce_big_kernel: list[2 e] = cell, list[2 e + 1] = scratch offset
+  unsigned long long *n_big, *big_used;
+  int64_t *big_list;
+};
+
+// Global scratch of coalesce_big_kernel, one record per particle of a listed
+// cell at [offset, offset + n_c): the sort keys and the particle position.
+struct CoalBig {
+  double *bx, *by, *bz;
+  int64_t *id;
+  uint32_t *idx;
+  int32_t *pairs;
 };
 
 // (bx, by, bz) packed into 63 bits, bx most significant (lexicographic order)
@@ -145,8 +167,20 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
   for (int cl = warp; cl < TILE3; cl += COAL_WARPS) {
     const int64_t c = tile * TILE3 + cl;
     const uint32_t q0 = A.cell_off[c], q1 = A.cell_off[c + 1];
-    const int nc = (int)(q1 - q0);
-    if (nc < 2 || nc > COAL_MAX) continue;
+    const int64_t nc64 = (int64_t)q1 - (int64_t)q0;
+    if (nc64 < 2) continue;
+    auto list_big = [&]() {
+      if (lane == 0) {
+        const unsigned long long e = atomicAdd(A.n_big, 1ull);
+        A.big_list[2 * e] = c;
+        A.big_list[2 * e + 1] = (int64_t)atomicAdd(A.big_used, (unsigned long long)nc64);
+      }
+    };
+    if (nc64 > COAL_MAX) {
+      list_big();
+      continue;
+    }
+    const int nc = (int)nc64;
     int N = 1;
     while (N < nc) N <<= 1;
     bool wide = false;
@@ -166,7 +200,11 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
         ix[i] = -1;
       }
     }
-    if (__any_sync(0xffffffffu, wide)) continue;   // a bin beyond the packed range: cell left alone
+    if (__any_sync(0xffffffffu, wide)) {   // a bin beyond the packed key: the unpacked path
+      list_big();
+      __syncwarp();
+      continue;
+    }
     __syncwarp();
     // bitonic sort by (key, id)
     for (int kk = 2; kk <= N; kk <<= 1) {
@@ -214,6 +252,87 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
     }
     if (lane == 0 && np) atomicAdd(A.merges, (unsigned long long)np);
     __syncwarp();
+  }
+}
+
+// (bins, id) of record a < that of record b (the oracle's order, R31)
+__device__ __forceinline__ bool big_less(const CoalBig &B, int64_t a, int64_t b) {
+  if (B.bx[a] != B.bx[b]) return B.bx[a] < B.bx[b];
+  if (B.by[a] != B.by[b]) return B.by[a] < B.by[b];
+  if (B.bz[a] != B.bz[b]) return B.bz[a] < B.bz[b];
+  return B.id[a] < B.id[b];
+}
+__device__ __forceinline__ void big_swap(const CoalBig &B, int64_t a, int64_t b) {
+  double t;
+  t = B.bx[a]; B.bx[a] = B.bx[b]; B.bx[b] = t;
+  t = B.by[a]; B.by[a] = B.by[b]; B.by[b] = t;
+  t = B.bz[a]; B.bz[a] = B.bz[b]; B.bz[b] = t;
+  const int64_t i = B.id[a]; B.id[a] = B.id[b]; B.id[b] = i;
+  const uint32_t x = B.idx[a]; B.idx[a] = B.idx[b]; B.idx[b] = x;
+}
+
+// One CTA per listed cell (grid-stride over the list).  Records are sorted
+// ascending by a bitonic network whose every compare-exchange puts the smaller
+// record at the lower index (first step of each merge compares i with its
+// mirror in the block), so the virtual +infinity records that pad n_c to a
+// power of two never move and are simply skipped.
+__global__ void __launch_bounds__(256) coalesce_big_kernel(const CoalArgs A, const CoalBig B) {
+  const unsigned long long nbig = *A.n_big;
+  __shared__ int s_np;
+  for (unsigned long long e = blockIdx.x; e < nbig; e += gridDim.x) {
+    const int64_t c = A.big_list[2 * e], off = A.big_list[2 * e + 1];
+    const uint32_t q0 = A.cell_off[c];
+    const int64_t nc = (int64_t)A.cell_off[c + 1] - (int64_t)q0;
+    for (int64_t i = threadIdx.x; i < nc; i += blockDim.x) {
+      const uint32_t p = A.perm[q0 + i];
+      // + 0.0 maps a -0 bin to +0 (equal bins compare equal, as in the oracle)
+      B.bx[off + i] = floor(A.a[3][p] / A.dv) + 0.0;
+      B.by[off + i] = floor(A.a[4][p] / A.dv) + 0.0;
+      B.bz[off + i] = floor(A.a[5][p] / A.dv) + 0.0;
+      B.id[off + i] = A.id[p];
+      B.idx[off + i] = p;
+    }
+    __syncthreads();
+    int64_t N = 1;
+    while (N < nc) N <<= 1;
+    for (int64_t k = 2; k <= N; k <<= 1) {
+      for (int64_t j = k >> 1; j > 0; j >>= 1) {
+        for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+          // first step of the merge: mirror partner; later steps: i ^ j
+          const int64_t l = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);
+          if (l > i && l < nc && big_less(B, off + l, off + i)) big_swap(B, off + i, off + l);
+        }
+        __syncthreads();
+      }
+    }
+    // pairs in sorted order (one thread, sequential like the definition)
+    if (threadIdx.x == 0) {
+      const int64_t mc = (int64_t)floor(A.frac * (double)nc);
+      int np = 0;
+      for (int64_t t = 0; t + 1 < nc && np < mc;) {
+        const int64_t a = off + t, b = a + 1;
+        if (B.bx[a] == B.bx[b] && B.by[a] == B.by[b] && B.bz[a] == B.bz[b]) {
+          B.pairs[off / 2 + np++] = (int32_t)t;
+          t += 2;
+        } else {
+          t += 1;
+        }
+      }
+      s_np = np;
+      if (np) atomicAdd(A.merges, (unsigned long long)np);
+    }
+    __syncthreads();
+    const int np = s_np;
+    for (int m = threadIdx.x; m < np; m += blockDim.x) {
+      const int64_t t = off + B.pairs[off / 2 + m];
+      const uint32_t p1 = B.idx[t], p2 = B.idx[t + 1];   // p1 has the smaller id
+      const double qa = A.a[6][p1], qb = A.a[6][p2], qs = qa + qb;
+#pragma unroll
+      for (int d = 0; d < 6; ++d) A.a[d][p1] = (qa * A.a[d][p1] + qb * A.a[d][p2]) / qs;
+      A.a[6][p1] = qs;
+      A.key_new[p2] = KEY_DEAD;
+    }
+    __syncthreads();
   }
 }
 
@@ -282,9 +401,23 @@ pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, do
     A.dv = dv;
     A.frac = (double)(n - target) / (double)n;
     A.merges = reinterpret_cast<unsigned long long *>(ctx->dev_counts + 60);
-    PIC_CUDA(cudaMemsetAsync(A.merges, 0, sizeof(unsigned long long), ctx->stream));
+    A.n_big = reinterpret_cast<unsigned long long *>(ctx->dev_counts + 61);
+    A.big_used = reinterpret_cast<unsigned long long *>(ctx->dev_counts + 62);
+    // scratch of the unpacked path: the B buffers of the store are free between
+    // cycles (cap records each; the cell list needs <= cap / 2 entries of 2 words,
+    // the pair list <= cap / 2 ints at offset / 2)
+    A.big_list = reinterpret_cast<int64_t *>(sp.b[4]);
+    CoalBig B;
+    B.bx = sp.b[0];
+    B.by = sp.b[1];
+    B.bz = sp.b[2];
+    B.id = sp.id_b;
+    B.idx = reinterpret_cast<uint32_t *>(sp.b[3]);
+    B.pairs = reinterpret_cast<int32_t *>(sp.b[5]);
+    PIC_CUDA(cudaMemsetAsync(A.merges, 0, 3 * sizeof(unsigned long long), ctx->stream));
     PIC_CUDA(cudaFuncSetAttribute(coalesce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COAL_SMEM));
     coalesce_kernel<<<(unsigned)g.ntiles, 32 * COAL_WARPS, COAL_SMEM, ctx->stream>>>(A); ++ctx->launches;
+    coalesce_big_kernel<<<kSMs * 2, 256, 0, ctx->stream>>>(A, B); ++ctx->launches;
     PIC_CUDA(cudaGetLastError());
     *action = 2;
     st = zero_cell_counts(ctx, s);

@@ -291,19 +291,27 @@ pic_status migrate(Ctx *ctx, int s0, int s1) {
   }
   // the one host synchronisation of the cycle
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  // Capacity limits are applied identically on both sides of every message
+  // (no early return: a rank that stopped here would leave its neighbour's
+  // matching ncclSend / ncclRecv blocked forever).  A side sends and receives
+  // min(count, mig_cap) records (the pack kernel stored no more); what does
+  // not fit is dropped, counted as overflow and reported by pic_sync
+  // (PIC_ERANGE), like the peer transport does.
   int64_t nl[PIC_MAX_SPECIES], nr[PIC_MAX_SPECIES], nraw[PIC_MAX_SPECIES];
-  int64_t recvL[PIC_MAX_SPECIES], recvR[PIC_MAX_SPECIES];
+  int64_t recvL[PIC_MAX_SPECIES], recvR[PIC_MAX_SPECIES], keepL[PIC_MAX_SPECIES], keepR[PIC_MAX_SPECIES];
   for (int s = s0; s < s1; ++s) {
-    nl[s] = hc[2 * s];
-    nr[s] = hc[2 * s + 1];
+    const int64_t wl = hc[2 * s], wr = hc[2 * s + 1];
     nraw[s] = hc[2 * S + s];
-    recvR[s] = (right >= 0) ? hc[3 * S + 2 * s + 0] : 0;
-    recvL[s] = (left >= 0) ? hc[3 * S + 2 * s + 1] : 0;
-    if (nl[s] > mc || nr[s] > mc) return fail(ctx, PIC_ERANGE, "migration buffer capacity exceeded");
-    if ((nl[s] && left < 0) || (nr[s] && right < 0)) return fail(ctx, PIC_ERANGE, "slab leaver with no neighbour");
-    if (recvL[s] > mc || recvR[s] > mc) return fail(ctx, PIC_ERANGE, "migration receive capacity exceeded");
-    if (nraw[s] + recvL[s] + recvR[s] > ctx->sp[s].cap)
-      return fail(ctx, PIC_ERANGE, "particle capacity exceeded after migration");
+    nl[s] = left >= 0 ? std::min(wl, mc) : 0;     // no neighbour: cannot happen (open faces remove first)
+    nr[s] = right >= 0 ? std::min(wr, mc) : 0;
+    ctx->hstat[ST_OVERFLOW] += (wl - nl[s]) + (wr - nr[s]);
+    recvR[s] = (right >= 0) ? std::min(hc[3 * S + 2 * s + 0], mc) : 0;
+    recvL[s] = (left >= 0) ? std::min(hc[3 * S + 2 * s + 1], mc) : 0;
+    // appended arrivals that fit the store (the rest were received but are dropped)
+    const int64_t room = std::max<int64_t>(0, ctx->sp[s].cap - nraw[s]);
+    keepL[s] = std::min(recvL[s], room);
+    keepR[s] = std::min(recvR[s], room - keepL[s]);
+    ctx->hstat[ST_OVERFLOW] += (recvL[s] - keepL[s]) + (recvR[s] - keepR[s]);
   }
   PhaseTimer t(ctx, 5);
   // payloads of every species in one NCCL group, one message per neighbour
@@ -320,20 +328,20 @@ pic_status migrate(Ctx *ctx, int s0, int s1) {
     SpeciesStore &sp = ctx->sp[s];
     Arr7 arrs;
     for (int k = 0; k < 7; ++k) arrs.a[k] = sp.a[k];
-    if (recvL[s])
-      append_kernel<<<grid_for(recvL[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0] + s * ms,
-                                                                  recvL[s], nraw[s], ctx->stats); ++ctx->launches;
-    if (recvR[s])
-      append_kernel<<<grid_for(recvR[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1] + s * ms,
-                                                                  recvR[s], nraw[s] + recvL[s], ctx->stats); ++ctx->launches;
+    if (keepL[s])
+      append_kernel<<<grid_for(keepL[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[0] + s * ms,
+                                                                  keepL[s], nraw[s], ctx->stats); ++ctx->launches;
+    if (keepR[s])
+      append_kernel<<<grid_for(keepR[s]), 256, 0, ctx->stream>>>(g, arrs, sp.id, sp.key_new, ctx->mig_recv[1] + s * ms,
+                                                                  keepR[s], nraw[s] + keepL[s], ctx->stats); ++ctx->launches;
     PIC_CUDA(cudaGetLastError());
-    const int64_t nnew = nraw[s] + recvL[s] + recvR[s];
+    const int64_t nnew = nraw[s] + keepL[s] + keepR[s];
     set_scalar_kernel<<<1, 1, 0, ctx->stream>>>(sp.d_nraw, nnew); ++ctx->launches;
     pic_status st = count_positions(ctx, s, nraw[s], nnew);
     if (st != PIC_OK) return st;
     sp.n_raw = std::max(sp.n_raw, nnew);
     ctx->hstat[ST_SENT] += nl[s] + nr[s];
-    ctx->hstat[ST_RECEIVED] += recvL[s] + recvR[s];
+    ctx->hstat[ST_RECEIVED] += keepL[s] + keepR[s];
   }
   return PIC_OK;
 }

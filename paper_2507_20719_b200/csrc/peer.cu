@@ -31,7 +31,11 @@
 #include <nccl.h>
 
 #include <cuda.h>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
+#include <new>
 
 #include "pic_internal.cuh"
 
@@ -67,6 +71,50 @@ static unsigned grid_for(int64_t total) {
 }
 
 // ----------------------------------------------------------------- setup ----
+// Descriptor of this rank's workspace relative to `base` (the start of the
+// allocation that holds it: the CUDA-IPC mapping for the peer transport, the
+// workspace itself for the loopback transport).
+static PeerDesc describe(Ctx *ctx, char *b) {
+  const pic_config &c = ctx->cfg;
+  const Geom &g = ctx->geom;
+  PeerDesc d;
+  memset(&d, 0, sizeof(d));
+  d.ctl_off = reinterpret_cast<char *>(ctx->peer_ctl) - b;
+  d.recv_off[0] = reinterpret_cast<char *>(ctx->mig_recv[0]) - b;
+  d.recv_off[1] = reinterpret_cast<char *>(ctx->mig_recv[1]) - b;
+  for (int s = 0; s < c.n_species; ++s) d.mom_off[s] = reinterpret_cast<char *>(ctx->sp[s].mom) - b;
+  d.mig_cap = ctx->mig_cap;
+  d.m_plane = g.m_plane;
+  d.m_nx = g.m_n[0];
+  d.ghost_x = g.G + (g.slab_hi - g.slab_lo);
+  d.src_off = reinterpret_cast<char *>(ctx->src_buf) - b;
+  int64_t shape[3];
+  pic_moment_shape((const pic_ctx *)ctx, shape);
+  d.owned_nx = shape[0];
+  return d;
+}
+
+// My link to the neighbour on `side` (0 left, 1 right) whose workspace
+// allocation is visible at `mapped` and described by `d`.
+static void fill_link(Ctx *ctx, int side, char *mapped, const PeerDesc &d, bool owns) {
+  Ctx::PeerLink &L = ctx->link[side];
+  L.mapped = mapped;
+  L.owns_mapping = owns;
+  // I am the neighbour's right (side 0) or left (side 1) neighbour
+  const int from = side == 0 ? 1 : 0;
+  PeerCtl *pc = reinterpret_cast<PeerCtl *>(mapped + d.ctl_off);
+  L.flag = &pc->flag[from];
+  L.cnt = &pc->cnt[from][0];
+  L.recv = reinterpret_cast<double *>(mapped + d.recv_off[from]);
+  L.mig_cap = d.mig_cap;
+  for (int s = 0; s < ctx->cfg.n_species; ++s) L.mom[s] = reinterpret_cast<double *>(mapped + d.mom_off[s]);
+  L.m_plane = d.m_plane;
+  L.m_nx = d.m_nx;
+  L.ghost_x = d.ghost_x;
+  L.src = reinterpret_cast<double *>(mapped + d.src_off);
+  L.owned_nx = d.owned_nx;
+}
+
 pic_status peer_setup(Ctx *ctx) {
   const pic_config &c = ctx->cfg;
   const Geom &g = ctx->geom;
@@ -76,6 +124,12 @@ pic_status peer_setup(Ctx *ctx) {
   const int left = (r > 0) ? r - 1 : (per ? P - 1 : -1);
   const int right = (r < P - 1) ? r + 1 : (per ? 0 : -1);
 
+  // Clear the own control block BEFORE any neighbour can learn where it is:
+  // a neighbour writes into it (arrival counts, barrier epochs) only after it
+  // has received this rank's descriptor below, so the clear cannot erase a
+  // remote write (a late clear could drop a count or a barrier epoch).
+  PIC_CUDA(cudaMemset(ctx->peer_ctl, 0, sizeof(PeerCtl)));
+  PIC_CUDA(cudaDeviceSynchronize());
   PeerDesc mine;
   memset(&mine, 0, sizeof(mine));
   // base of the allocation holding the workspace (driver API through the runtime)
@@ -96,20 +150,12 @@ pic_status peer_setup(Ctx *ctx) {
     mine.ok = 1;
   }
   cudaGetLastError();
-  char *b = reinterpret_cast<char *>(base);
-  mine.ctl_off = reinterpret_cast<char *>(ctx->peer_ctl) - b;
-  mine.recv_off[0] = reinterpret_cast<char *>(ctx->mig_recv[0]) - b;
-  mine.recv_off[1] = reinterpret_cast<char *>(ctx->mig_recv[1]) - b;
-  for (int s = 0; s < c.n_species; ++s) mine.mom_off[s] = reinterpret_cast<char *>(ctx->sp[s].mom) - b;
-  mine.mig_cap = ctx->mig_cap;
-  mine.m_plane = g.m_plane;
-  mine.m_nx = g.m_n[0];
-  mine.ghost_x = g.G + (g.slab_hi - g.slab_lo);
-  mine.src_off = reinterpret_cast<char *>(ctx->src_buf) - b;
   {
-    int64_t shape[3];
-    pic_moment_shape((const pic_ctx *)ctx, shape);
-    mine.owned_nx = shape[0];
+    const cudaIpcMemHandle_t h = mine.handle;
+    const int64_t ok = mine.ok;
+    mine = describe(ctx, reinterpret_cast<char *>(base));
+    mine.handle = h;
+    mine.ok = ok;
   }
 
   // neighbours' descriptors: NCCL point-to-point through a device staging area
@@ -159,32 +205,113 @@ pic_status peer_setup(Ctx *ctx) {
       return fail(ctx, PIC_ECUDA, "peer transport requested but a neighbour workspace cannot be mapped");
     return PIC_OK;   // AUTO: NCCL transport
   }
-  for (int side = 0; side < 2; ++side) {
-    Ctx::PeerLink &L = ctx->link[side];
-    L.mapped = mapped[side];
-    if (!mapped[side]) continue;
-    L.owns_mapping = !(side == 1 && mapped[1] == mapped[0]);
-    // I am the neighbour's right (side 0) or left (side 1) neighbour
-    const int from = side == 0 ? 1 : 0;
-    PeerCtl *pc = reinterpret_cast<PeerCtl *>(mapped[side] + nb[side].ctl_off);
-    L.flag = &pc->flag[from];
-    L.cnt = &pc->cnt[from][0];
-    L.recv = reinterpret_cast<double *>(mapped[side] + nb[side].recv_off[from]);
-    L.mig_cap = nb[side].mig_cap;
-    for (int s = 0; s < c.n_species; ++s) L.mom[s] = reinterpret_cast<double *>(mapped[side] + nb[side].mom_off[s]);
-    L.m_plane = nb[side].m_plane;
-    L.m_nx = nb[side].m_nx;
-    L.ghost_x = nb[side].ghost_x;
-    L.src = reinterpret_cast<double *>(mapped[side] + nb[side].src_off);
-    L.owned_nx = nb[side].owned_nx;
-  }
-  PIC_CUDA(cudaMemset(ctx->peer_ctl, 0, sizeof(PeerCtl)));
-  PIC_CUDA(cudaDeviceSynchronize());
+  for (int side = 0; side < 2; ++side)
+    if (mapped[side]) fill_link(ctx, side, mapped[side], nb[side], !(side == 1 && mapped[1] == mapped[0]));
   ctx->peer = true;
   return PIC_OK;
 }
 
+// Loopback transport: the P slab contexts of one process on one device link
+// to each other directly (the neighbour's workspace needs no mapping).  Every
+// data-path kernel of the peer transport runs unchanged (send_leavers_peer in
+// the movers, arrive_kernel, ghost_pull_kernel, the sources' neighbour reads);
+// only the barrier differs.  A spinning device barrier between streams of ONE
+// device can deadlock when two contexts' streams share a hardware queue (the
+// spinner blocks the work it waits for), so a loopback barrier is an event
+// handshake instead: each context records an event on its stream, its host
+// thread waits until both neighbours have recorded theirs for the same epoch,
+// and its stream waits on those events.  Each context is driven by its own
+// host thread, as a rank would be.
+struct LoopGroup {
+  std::mutex mu;
+  std::condition_variable cv;
+  int n = 0, refs = 0;
+  std::vector<unsigned long long> arrived;      // last barrier epoch recorded per rank
+  std::vector<cudaEvent_t> ev;                  // [rank][2]: events of even / odd epochs
+};
+
+pic_status loopback_barrier(Ctx *ctx) {
+  LoopGroup *G = ctx->loop;
+  const int r = ctx->cfg.rank;
+  const unsigned long long e = ++ctx->peer_epoch;
+  cudaEvent_t mine = G->ev[2 * r + (e & 1)];
+  PIC_CUDA(cudaEventRecord(mine, ctx->stream));
+  std::unique_lock<std::mutex> lk(G->mu);
+  G->arrived[r] = e;
+  G->cv.notify_all();
+  for (Ctx *nb : ctx->loop_nb) {
+    if (!nb) continue;
+    const int q = nb->cfg.rank;
+    // 20 s, like the device barrier: a neighbour that never arrives is an error, not a hang
+    if (!G->cv.wait_for(lk, std::chrono::seconds(20), [&] { return G->arrived[q] >= e; }))
+      return fail(ctx, PIC_ENCCL, "loopback barrier timed out (a neighbour context stopped)");
+    // the neighbour cannot re-record this event (epoch e + 2) before it passed
+    // barrier e + 1, which needs this context's arrival there
+    PIC_CUDA(cudaStreamWaitEvent(ctx->stream, G->ev[2 * q + (e & 1)], 0));
+  }
+  return PIC_OK;
+}
+
+void loopback_release(Ctx *ctx) {
+  LoopGroup *G = ctx->loop;
+  if (!G) return;
+  ctx->loop = nullptr;
+  bool last = false;
+  {
+    std::lock_guard<std::mutex> lk(G->mu);
+    last = --G->refs == 0;
+  }
+  if (last) {
+    for (cudaEvent_t e : G->ev)
+      if (e) cudaEventDestroy(e);
+    delete G;
+  }
+}
+
+pic_status loopback_link(Ctx *const *ctxs, int n) {
+  for (int r = 0; r < n; ++r) {
+    Ctx *ctx = ctxs[r];
+    PIC_CUDA(cudaMemset(ctx->peer_ctl, 0, sizeof(PeerCtl)));
+  }
+  {
+    Ctx *ctx = ctxs[0];
+    PIC_CUDA(cudaDeviceSynchronize());
+  }
+  LoopGroup *G = new (std::nothrow) LoopGroup();
+  if (!G) return fail(ctxs[0], PIC_ENOMEM, "loopback group");
+  G->n = n;
+  G->refs = n;
+  G->arrived.assign(n, 0ull);
+  G->ev.assign(2 * n, nullptr);
+  for (int k = 0; k < 2 * n; ++k) {
+    Ctx *ctx = ctxs[k / 2];
+    if (cudaEventCreateWithFlags(&G->ev[k], cudaEventDisableTiming) != cudaSuccess) {
+      for (cudaEvent_t e : G->ev)
+        if (e) cudaEventDestroy(e);
+      delete G;
+      return fail(ctx, PIC_ECUDA, "loopback events");
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    Ctx *ctx = ctxs[r];
+    ctx->loop = G;
+    const bool per = ctx->geom.periodic[0];
+    const int left = (r > 0) ? r - 1 : (per ? n - 1 : -1);
+    const int right = (r < n - 1) ? r + 1 : (per ? 0 : -1);
+    for (int side = 0; side < 2; ++side) {
+      const int nb = side == 0 ? left : right;
+      ctx->loop_nb[side] = nb >= 0 ? ctxs[nb] : nullptr;
+      if (nb < 0) continue;
+      char *base = reinterpret_cast<char *>(ctxs[nb]->workspace);
+      fill_link(ctx, side, base, describe(ctxs[nb], base), false);
+    }
+    ctx->peer = true;
+  }
+  return PIC_OK;
+}
+
 void peer_close(Ctx *ctx) {
+  loopback_release(ctx);
   for (int side = 0; side < 2; ++side)
     if (ctx->link[side].mapped && ctx->link[side].owns_mapping) cudaIpcCloseMemHandle(ctx->link[side].mapped);
 }
@@ -233,6 +360,7 @@ __global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long 
 }
 
 pic_status peer_barrier(Ctx *ctx) {
+  if (ctx->loop) return loopback_barrier(ctx);
   ++ctx->peer_epoch;
   peer_barrier_kernel<<<1, 1, 0, ctx->stream>>>(ctx->peer_ctl->flag, ctx->link[0].flag, ctx->link[1].flag,
                                                 ctx->peer_epoch, &ctx->peer_ctl->err); ++ctx->launches;

@@ -194,6 +194,8 @@ struct Ctx {
     int64_t owned_nx = 0;
   } link[2];                         // [0] left, [1] right
   bool peer = false;
+  Ctx *loop_nb[2] = {};              // loopback transport: the neighbour contexts (same process)
+  struct LoopGroup *loop = nullptr;  // loopback transport: shared host-side barrier state (peer.cu)
   unsigned long long peer_epoch = 0;
   InjectParams inj[PIC_MAX_SPECIES];
   void *cub_temp = nullptr;
@@ -271,6 +273,7 @@ pic_status build_order(Ctx *ctx, int s);
 pic_status exchange(Ctx *ctx);
 pic_status migrate(Ctx *ctx, int s0, int s1);
 pic_status peer_setup(Ctx *ctx);
+pic_status loopback_link(Ctx *const *ctxs, int n);
 void peer_close(Ctx *ctx);
 PeerOut peer_out(const Ctx *ctx, int s);
 pic_status peer_migrate(Ctx *ctx, int s0, int s1);

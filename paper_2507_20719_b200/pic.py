@@ -28,9 +28,9 @@ PIC_OK, PIC_EINVAL, PIC_ECUDA, PIC_ENCCL, PIC_ENOMEM, PIC_ESTATE, PIC_ERANGE, PI
 STATUS_NAMES = ["PIC_OK", "PIC_EINVAL", "PIC_ECUDA", "PIC_ENCCL", "PIC_ENOMEM", "PIC_ESTATE",
                 "PIC_ERANGE", "PIC_ENONFINITE"]
 KERNEL_AUTO, KERNEL_BASIC, KERNEL_TILED = 0, 1, 2
-TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_PEER = 0, 1, 2
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_PEER, TRANSPORT_LOOPBACK = 0, 1, 2, 3
 STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "overflow", "multiwrap"]
-EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_set_stream",
+EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_loopback_link", "pic_set_stream",
            "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
            "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_gmm", "pic_moment_ptr", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
@@ -71,6 +71,7 @@ def load_library(path: str = LIB_PATH):
         lib.pic_workspace_bytes.argtypes = [P(pic_config), P(C.c_int64)]
         lib.pic_init.argtypes = [P(pic_config), vp, vp, C.c_int64, P(vp)]
         lib.pic_set_stream.argtypes = [vp, vp]
+        lib.pic_loopback_link.argtypes = [P(vp), C.c_int32]
         lib.pic_set_particles.argtypes = [vp, C.c_int32, C.c_int64, P(vp), vp]
         lib.pic_count.argtypes = [vp, C.c_int32, P(C.c_int64)]
         lib.pic_get_particles.argtypes = [vp, C.c_int32, P(vp), vp]
@@ -152,6 +153,15 @@ def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSP
     cfg.ghost, cfg.transport, cfg.kernel = ghost, transport, kernel
     cfg.relativistic = int(bool(getattr(w, "relativistic", False) if relativistic is None else relativistic))
     return cfg
+
+
+def pic_loopback_link(contexts: Sequence["Context"]):
+    """Join the slab contexts of a loopback decomposition (TRANSPORT_LOOPBACK,
+    contexts[r] = rank r, one device).  Each context must keep its own stream
+    and be stepped from its own host thread (the flag barriers spin on the
+    device, as between ranks)."""
+    arr = (C.c_void_p * len(contexts))(*[c.h.value for c in contexts])
+    _check(load_library().pic_loopback_link(arr, len(contexts)), contexts[0].h, "pic_loopback_link")
 
 
 class Context:
@@ -269,9 +279,11 @@ class Context:
                                 sg.ctypes.data, h.ctypes.data, C.byref(clipped)), self.h, "pic_gmm")
         return a, mu, sg, h, clipped.value
 
-    def moment_view(self, s: int, comp: int) -> torch.Tensor:
-        """Zero-copy [nz][ny][nx] view (raw sums x 1/V applied by the caller) of
-        moment component comp of species s, valid until the next moments call."""
+    def moment_view(self, s: int, comp: int):
+        """(view, scale): a zero-copy [nz][ny][nx] view of the RAW sums
+        sum q S {1, v, vv} of moment component comp of species s (valid until the
+        next moments call) and the R13 normalisation scale = 1/V that turns them
+        into the moment (pic_moment_ptr; the binding does no arithmetic on them)."""
         ptr = C.c_void_p()
         st = (C.c_int64 * 3)()
         org = (C.c_int64 * 3)()
@@ -283,7 +295,7 @@ class Context:
         off = (ptr.value - base.data_ptr()) // 8
         flat = base[: (base.numel() // 8) * 8].view(torch.float64)
         view = torch.as_strided(flat, (nz, ny, nx), (st[2], st[1], st[0]), off)
-        return view * scale.value
+        return view, scale.value
 
     def join_copies(self):
         """The context stream waits (on the device) for all enqueued copies."""
@@ -304,14 +316,14 @@ class Context:
 
     @property
     def transport(self) -> int:
-        """TRANSPORT_PEER / TRANSPORT_NCCL in use (nranks > 1), TRANSPORT_AUTO for one rank."""
+        """TRANSPORT_PEER / _NCCL / _LOOPBACK in use (nranks > 1), TRANSPORT_AUTO for one rank."""
         out = C.c_int32()
         _check(self.lib.pic_get_transport(self.h, C.byref(out)), self.h, "pic_get_transport")
         return out.value
 
     @property
     def peer(self) -> bool:
-        return self.transport == TRANSPORT_PEER
+        return self.transport in (TRANSPORT_PEER, TRANSPORT_LOOPBACK)
 
     def profile(self, enable: bool = True):
         _check(self.lib.pic_profile(self.h, 1 if enable else 0), self.h, "pic_profile")

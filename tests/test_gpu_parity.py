@@ -483,5 +483,68 @@ def test_moment_ptr_matches_copy_out():
     for s in range(len(parts)):
         full = ctx.get_moments(s)
         for comp in (0, 3, 9):
-            assert torch.equal(ctx.moment_view(s, comp), full[comp])
+            raw, scale = ctx.moment_view(s, comp)
+            assert raw.data_ptr() != full.data_ptr()
+            assert torch.equal(raw * scale, full[comp])
+    ctx.close()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_coalesce_overfull_and_wide_cells(kernel):
+    """R31 on every cell ("in cells with an excessive number of
+    particles, we perform pair-wise merging"): a 2000-particle cell and a cell
+    whose velocity bins lie beyond +-2^20 (and +-3e12) take the unpacked
+    global-memory path; the survivors match the oracle's coalescence exactly
+    as the 27-particle cells do."""
+    import oracle as O
+    w = I.c1(randomized=True)
+    base = I.make_species(w, device="cpu")[0]
+    sp = w.species[0]
+    dv = sp.vth / 2
+    gen = torch.Generator().manual_seed(77)
+    d = w.delta
+    # 2000 extra particles in cell (5, 6, 7)
+    n_big = 2000
+    big = {"x": (5 + torch.rand(n_big, generator=gen, dtype=torch.float64)) * d[0],
+           "y": (6 + torch.rand(n_big, generator=gen, dtype=torch.float64)) * d[1],
+           "z": (7 + torch.rand(n_big, generator=gen, dtype=torch.float64)) * d[2]}
+    for k in "uvw":
+        big[k] = sp.vth * torch.randn(n_big, generator=gen, dtype=torch.float64)
+    big["q"] = base["q"][:1].repeat(n_big) * (1 + 0.1 * torch.rand(n_big, generator=gen, dtype=torch.float64))
+    big["id"] = 10**9 + torch.arange(n_big, dtype=torch.int64)
+    # wide bins in cell (2, 3, 4): pairs at bin 2^21 and at 3e12, one at -2^21
+    wide_u = torch.tensor([2**21 + 0.25, 2**21 + 0.5, 2**21 + 0.75, 3e12, 3e12 + 0.5, -2**21 - 0.5],
+                          dtype=torch.float64) * dv
+    nw = wide_u.numel()
+    wide = {"x": torch.full((nw,), 2.5 * d[0], dtype=torch.float64) + 0.01 * torch.arange(nw) * d[0],
+            "y": torch.full((nw,), 3.5 * d[1], dtype=torch.float64),
+            "z": torch.full((nw,), 4.5 * d[2], dtype=torch.float64),
+            "u": wide_u, "v": torch.full((nw,), 0.3 * dv, dtype=torch.float64),
+            "w": torch.full((nw,), -0.3 * dv, dtype=torch.float64),
+            "q": base["q"][:1].repeat(nw), "id": 2 * 10**9 + torch.arange(nw, dtype=torch.int64)}
+    parts = {k: torch.cat([base[k], big[k], wide[k]]).contiguous() for k in base}
+    n = parts["x"].numel()
+    target = int(0.7 * n)
+    frac = (n - target) / n
+    # oracle: the same coalescence pass on the initial state
+    g = PU.oracle_grid(w)
+    P = PU.to_numpy_parts(parts)
+    st = np.zeros(n, dtype=np.int8)
+    merges = O.coalesce(g, P, st, dv, frac)
+    assert merges > 0
+    # the big cell and the wide cell both merged on the oracle side
+    merged_ids = set(P["id"][st == O.MERGED].tolist())
+    assert any(i >= 10**9 and i < 2 * 10**9 for i in merged_ids)
+    assert {2 * 10**9 + 1, 2 * 10**9 + 4} <= merged_ids
+    import dataclasses
+    wq = pic.make_config(dataclasses.replace(w, species=[sp]), capacity=[n + 64], kernel=kernel)
+    ctx = pic.Context(wq)
+    ctx.set_particles(0, {k: v.cuda() for k, v in parts.items()})
+    assert ctx.control(0, target, 0.05, 0.1, dv, 5) == 2
+    ctx.sync()
+    gp = {k: v.cpu().numpy() for k, v in ctx.get_particles(0).items()}
+    # the GPU keeps positions in cell units; compare by id
+    assert len(gp["id"]) == int((st == O.ALIVE).sum())
+    rep = {}
+    assert PU.compare_particles(w, sp, gp, P, st, rep), rep
     ctx.close()
