@@ -173,6 +173,16 @@ PIC_API pic_status pic_set_stream(pic_ctx *ctx, void *stream);
 PIC_API pic_status pic_set_particles(pic_ctx *ctx, int32_t s, int64_t n,
                              const double *const xyzuvwq[7], const int64_t *id);
 
+/* Append n particles to species s (same arrays and units as
+ * pic_set_particles; id NULL: ids continue the store's position count) and
+ * add them to the cell order.  For loading stores too large to stage in one
+ * piece (draw a sub-slab, append it, free it).  Between cycles only
+ * (PIC_ESTATE between pic_mover and pic_exchange); PIC_ERANGE if the store
+ * would exceed capacity[s].  Particles outside this rank's slab are counted
+ * as far-flyers and dropped.  Synchronises the stream.                       */
+PIC_API pic_status pic_add_particles(pic_ctx *ctx, int32_t s, int64_t n,
+                             const double *const xyzuvwq[7], const int64_t *id);
+
 /* Number of live particles of species s on this rank (synchronises the
  * stream).                                                                   */
 PIC_API pic_status pic_count(pic_ctx *ctx, int32_t s, int64_t *n);

@@ -345,6 +345,24 @@ pic_status pic_set_particles(pic_ctx *p, int32_t s, int64_t n, const double *con
   return PIC_OK;
 }
 
+pic_status pic_add_particles(pic_ctx *p, int32_t s, int64_t n, const double *const xyzuvwq[7], const int64_t *id) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  pic_status st = check_species(ctx, s, false);
+  if (st != PIC_OK) return st;
+  if (n < 0) return fail(ctx, PIC_EINVAL, "n < 0");
+  if (ctx->sp[s].moved) return fail(ctx, PIC_ESTATE, "pic_add_particles between pic_mover and pic_exchange");
+  if (n > 0) {
+    if (!xyzuvwq) return fail(ctx, PIC_EINVAL, "null particle arrays");
+    for (int k = 0; k < 7; ++k)
+      if (!xyzuvwq[k]) return fail(ctx, PIC_EINVAL, "null particle array");
+  }
+  st = append_particles(ctx, s, n, xyzuvwq, id);
+  if (st != PIC_OK) return st;
+  ctx->sp[s].deposited = false;
+  return PIC_OK;
+}
+
 pic_status pic_count(pic_ctx *p, int32_t s, int64_t *n) {
   if (!p || !n) return PIC_EINVAL;
   Ctx *ctx = C(p);

@@ -445,10 +445,10 @@ __global__ void divide_kernel(double *a, int64_t n, double d) {
        p += (int64_t)gridDim.x * blockDim.x)
     a[p] = a[p] / d;
 }
-__global__ void iota_kernel(int64_t *a, int64_t n) {
+__global__ void iota_kernel(int64_t *a, int64_t n, int64_t first = 0) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x)
-    a[p] = p;
+    a[p] = first + p;
 }
 // out[q] = src[perm[q]] * scale  (q < live count)
 __global__ void gather_scaled_kernel(const double *__restrict__ src, const uint32_t *__restrict__ perm,
@@ -485,6 +485,48 @@ pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7]
   st = zero_cell_counts(ctx, s);
   if (st != PIC_OK) return st;
   st = count_positions(ctx, s, 0, n);
+  if (st != PIC_OK) return st;
+  st = build_order(ctx, s);
+  if (st != PIC_OK) return st;
+  uint32_t nlive = 0;
+  PIC_CUDA(cudaMemcpyAsync(&nlive, sp.cell_off + ctx->geom.ncells, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));  // caller buffers may be pageable
+  sp.n = nlive;
+  return PIC_OK;
+}
+
+// Append n particles behind the store's positions [0, d_nraw) and add them to
+// the cell order as arrivals (the counts and ranks of the particles already
+// there stay valid: they are those the order was built from).
+pic_status append_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id) {
+  SpeciesStore &sp = ctx->sp[s];
+  if (!sp.order_valid) {
+    const double *none[7] = {};
+    pic_status st = load_particles(ctx, s, 0, none, nullptr);
+    if (st != PIC_OK) return st;
+  }
+  int64_t old = 0;
+  PIC_CUDA(cudaMemcpyAsync(&old, sp.d_nraw, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  PIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (old + n > sp.cap) return fail(ctx, PIC_ERANGE, "pic_add_particles: capacity exceeded");
+  if (n == 0) return PIC_OK;
+  for (int k = 0; k < 7; ++k) {
+    PIC_CUDA(cudaMemcpyAsync(sp.a[k] + old, src[k], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
+    if (k < 3) {
+      divide_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.a[k] + old, n, ctx->geom.delta[k]); ++ctx->launches;
+    }
+  }
+  if (id) {
+    PIC_CUDA(cudaMemcpyAsync(sp.id + old, id, sizeof(int64_t) * n, cudaMemcpyDefault, ctx->stream));
+  } else {
+    iota_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(sp.id + old, n, old); ++ctx->launches;
+  }
+  PIC_CUDA(cudaGetLastError());
+  sp.n_raw = std::max(sp.n_raw, old + n);
+  set_scalar_kernel<<<1, 1, 0, ctx->stream>>>(sp.d_nraw, old + n); ++ctx->launches;
+  pic_status st = recompute_keys(ctx, s, old, old + n);
+  if (st != PIC_OK) return st;
+  st = count_positions(ctx, s, old, old + n);
   if (st != PIC_OK) return st;
   st = build_order(ctx, s);
   if (st != PIC_OK) return st;

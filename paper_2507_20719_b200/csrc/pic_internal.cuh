@@ -292,6 +292,7 @@ pic_status clamp_nraw(Ctx *ctx, int s);
 pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, double dv, uint64_t seed,
                    int32_t *action);
 pic_status live_count(Ctx *ctx, int s, int64_t *n);
+pic_status append_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
 pic_status load_particles(Ctx *ctx, int s, int64_t n, const double *const src[7], const int64_t *id);
 pic_status unload_particles(Ctx *ctx, int s, double *const dst[7], int64_t *id);
 pic_status gmm_fit(Ctx *ctx, int s, int B, double vmax, int M, int n_em, double *alpha, double *mu, double *sigma,

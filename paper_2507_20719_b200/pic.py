@@ -31,7 +31,7 @@ KERNEL_AUTO, KERNEL_BASIC, KERNEL_TILED = 0, 1, 2
 TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_PEER, TRANSPORT_LOOPBACK = 0, 1, 2, 3
 STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "overflow", "multiwrap"]
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_loopback_link", "pic_set_stream",
-           "pic_set_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
+           "pic_set_particles", "pic_add_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
            "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
            "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_gmm", "pic_moment_ptr", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
@@ -73,6 +73,7 @@ def load_library(path: str = LIB_PATH):
         lib.pic_set_stream.argtypes = [vp, vp]
         lib.pic_loopback_link.argtypes = [P(vp), C.c_int32]
         lib.pic_set_particles.argtypes = [vp, C.c_int32, C.c_int64, P(vp), vp]
+        lib.pic_add_particles.argtypes = [vp, C.c_int32, C.c_int64, P(vp), vp]
         lib.pic_count.argtypes = [vp, C.c_int32, P(C.c_int64)]
         lib.pic_get_particles.argtypes = [vp, C.c_int32, P(vp), vp]
         lib.pic_set_fields.argtypes = [vp, vp]
@@ -196,6 +197,18 @@ class Context:
         if idt is not None:
             assert idt.dtype == torch.int64 and idt.is_contiguous() and idt.numel() == n
         _check(self.lib.pic_set_particles(self.h, s, n, P7, _ptr(idt)), self.h, "pic_set_particles")
+
+    def add_particles(self, s: int, parts: Dict[str, torch.Tensor]):
+        """Append particles to species s (pic_add_particles)."""
+        arrs = [parts[k] for k in "xyzuvwq"]
+        n = arrs[0].numel()
+        for a in arrs:
+            assert a.dtype == torch.float64 and a.is_contiguous() and a.numel() == n
+        P7 = (C.c_void_p * 7)(*[a.data_ptr() for a in arrs])
+        idt = parts.get("id")
+        if idt is not None:
+            assert idt.dtype == torch.int64 and idt.is_contiguous() and idt.numel() == n
+        _check(self.lib.pic_add_particles(self.h, s, n, P7, _ptr(idt)), self.h, "pic_add_particles")
 
     def count(self, s: int) -> int:
         out = C.c_int64()
