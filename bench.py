@@ -2,15 +2,18 @@
 """Bench: particle updates/s (mover + moments) of the implicit-moment PIC particle
 path on 1..8 B200, and its fraction of the HBM roofline (BASELINE.json metric).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config c3] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
-A step is one full particle cycle through the C ABI (pic_cycle = pic_mover,
-pic_moments, pic_exchange) for every species of the workload.  The default
-workload is C2 (GEM Harris sheet, 128 x 64 x 32 cells, 2 species, 125 ppc,
-65.5 M particles, 3.67 GB) per GPU; with N GPUs it is weak-scaled along x
-(128 N x 64 x 32 cells, one x-slab of C2's size per rank).  Inputs live in HBM
-and are larger than L2 (no flush needed).
+A step is one full particle cycle through the C ABI (pic_mover, pic_moments,
+pic_exchange) for every species of the workload.  The default workload is C3,
+BASELINE.json configs[2] and the largest configuration that fits one GPU: the
+weak-scaling cube of 192^3 cells per GPU, 2 species, 64 ppc (905,969,664
+particles, a 136 GB store per GPU), x-slabs of 192 cells per rank with N GPUs.
+`--config c2` is the GEM Harris sheet (configs[1]).  Inputs live in HBM and are
+far larger than L2 (no flush needed).  Besides the HBM roofline of the dominant
+kernel the line carries %fp64 (roofline_fp64) and the oracle timed on one host
+core and on all of them (cpu_baseline).
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the
 reference arm of this tier) on a bounded sample of the same workload.
@@ -38,7 +41,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c4s", "c5s"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5", "c4s", "c5s"])
     ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 basic, 2 tiled")
     ap.add_argument("--transport", type=int, default=0, help="multi-GPU: 0 auto (peer memory), 1 NCCL, 2 peer")
@@ -49,6 +52,8 @@ def parse():
     ap.add_argument("--balance", type=int, default=1, help="c4s/c5s with N>1: count-balanced slabs (1) or uniform (0)")
     ap.add_argument("--ghost", type=int, default=2)
     ap.add_argument("--ppc", type=int, default=0, help="override ppc (debug only)")
+    ap.add_argument("--c3-cells", type=int, default=192,
+                    help="c3: cells per GPU along each axis (192 = BASELINE configs[2]; smaller only for ncu clones)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -65,10 +70,12 @@ def workload(args, nranks, rank):
                 "C2 GEM double Harris sheet, 128x64x32 cells per GPU (x-slab weak scaling)") + \
             ", 2 species, 125 ppc, mass ratio 256, 3 PC iterations"
     elif args.config == "c3":
-        w = I.c3(nranks=1 if strong else nranks, ppc=args.ppc or 64)
-        per = 192 // nranks if strong else 192
-        desc = ("C3 cube 192^3 cells in total split into N x-slabs (strong scaling)" if strong else
-                "C3 weak-scaling cube 192^3 cells per GPU") + ", 2 species, 64 ppc, 3 PC iterations"
+        n3 = args.c3_cells
+        w = I.c3(nranks=1 if strong else nranks, ppc=args.ppc or 64, n_per_rank=n3)
+        per = n3 // nranks if strong else n3
+        desc = (f"C3 cube {n3}^3 cells in total split into N x-slabs (strong scaling)" if strong else
+                f"C3 weak-scaling cube {n3}^3 cells per GPU") + ", 2 species, 64 ppc, 3 PC iterations" + \
+            ("" if n3 == 192 else " (reduced clone for profiling, not BASELINE's size)")
     elif args.config == "c4":
         w = I.c4(ppc=args.ppc or 64)
         per = w.ncell[0] // nranks
@@ -226,9 +233,11 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- oracle (CPU) --
-def oracle_rate(w, parts_cpu, target_s, n_iter=3):
+def oracle_rate(w, parts_cpu, target_s, n_iter=3, all_cores=False):
     """Time the CPU oracle (mover + moments, one cycle) on a bounded sample of the
-    workload's particles; returns (updates/s, sample description, cores)."""
+    workload's particles; returns (updates/s, sample description, cores).
+    all_cores: the OpenMP build of the same source (mover over
+    particle ranges per thread, per-thread node grids merged in thread order)."""
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle as O
@@ -236,6 +245,12 @@ def oracle_rate(w, parts_cpu, target_s, n_iter=3):
     g = O.make_grid(w.ncell, w.length, w.bc, w.dt, w.c, w.planet_center, w.planet_radius)
     lo, EB = I.field_window(w.with_slab(0, w.ncell[0]) if w.slab_or_all() == (0, w.ncell[0]) else w, 2)
     F = O.FieldWindow(lo, EB.numpy())
+    cores = O.omp_threads() if all_cores else 1
+    mover = O.mover_par if all_cores else O.mover
+
+    def moments(P, st):
+        return O.moments_par(g, P, st) if all_cores else O.moments(g, P, st, with_abs=False)
+
     # the oracle deposits on the global grid; restrict the sample to this rank's
     # slab (rank 0) -- a global grid of the same shape is used for the timing
     def run(n_per_species):
@@ -244,16 +259,19 @@ def oracle_rate(w, parts_cpu, target_s, n_iter=3):
         for s, sp in enumerate(w.species):
             P = {k: parts_cpu[s][k][:n_per_species].numpy().copy() for k in "xyzuvwq"}
             st = np.zeros(len(P["x"]), dtype=np.int8)
-            O.mover(g, F, sp.qom, n_iter, P, st, relativistic=w.relativistic)
-            O.moments(g, P, st, with_abs=False)
+            mover(g, F, sp.qom, n_iter, P, st, relativistic=w.relativistic)
+            moments(P, st)
             tot += len(P["x"])
         return tot, time.perf_counter() - t0
-    n0 = min(20000, min(p["x"].numel() for p in parts_cpu))
+    nmax = min(p["x"].numel() for p in parts_cpu)
+    n0 = min(20000 * cores, nmax)
     tot, dt = run(n0)
     rate = tot / dt
-    n1 = int(min(min(p["x"].numel() for p in parts_cpu), max(n0, rate * target_s / len(w.species))))
+    n1 = int(min(nmax, max(n0, rate * target_s / len(w.species))))
     tot, dt = run(n1)
-    return tot / dt, f"{n1} particles per species (first {n1} in id order of rank 0's slab), 1 cycle, mover+moments, single thread", 1
+    how = f"OpenMP build, {cores} threads" if all_cores else "single thread"
+    return (tot / dt, f"{n1} particles per species (first {n1} in id order of rank 0's slab), 1 cycle, "
+            f"mover+moments, {how}", cores)
 
 
 def oracle_sample_parts(w, device="cpu"):
@@ -275,9 +293,9 @@ def run_reference(args):
     parts = I.make_species(sub, device="cpu")
     vals = []
     for _ in range(args.warmup):
-        oracle_rate(w, parts, min(2.0, args.cpu_seconds / 4))
+        oracle_rate(w, parts, min(2.0, args.cpu_seconds / 4), all_cores=True)
     for _ in range(args.steps):
-        r, sample, cores = oracle_rate(w, parts, args.cpu_seconds / max(1, args.steps))
+        r, sample, cores = oracle_rate(w, parts, args.cpu_seconds / max(1, args.steps), all_cores=True)
         vals.append(r)
     v = statistics.median(vals)
     # one full step of the workload (all N GPUs' particles) at the sampled rate
@@ -293,6 +311,55 @@ def run_reference(args):
             "e2e": {"value": v, "unit": "particle updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def fp64_peak_tflops(seconds=1.5):
+    """Sustained fp64 FMA throughput measured now on this GPU (tools/microbench/
+    fp64peak.cu: back-to-back DFMA launches for `seconds`), or None."""
+    import ctypes
+    from paper_2507_20719_b200 import build_lib
+    try:
+        lib = ctypes.CDLL(build_lib.FP64PEAK_LIB)
+        lib.fp64_fma_tflops.restype = ctypes.c_double
+        lib.fp64_fma_tflops.argtypes = [ctypes.c_double]
+        v = lib.fp64_fma_tflops(seconds * 1e3)
+        return v if v > 0 else None
+    except OSError:
+        return None
+
+
+def fp64_roofline(args, kname, n_alive, mover_ms_step, deposit_ms_step, rate_per_gpu, local):
+    """%fp64 beside %HBM.  flops per update of each kernel:
+    SASS-counted by ncu (2 DFMA + DADD + DMUL thread instructions + 512 per
+    DMMA.8x8x4 warp instruction, per particle of the launch) in the committed
+    capture profiles/fp64_ops.json (static: ncu cannot run inside the bench);
+    peak: the sustained DFMA rate measured in this run, with its clocks."""
+    path = os.path.join(ROOT, "profiles", "fp64_ops.json")
+    if not os.path.exists(path) or args.relativistic or args.kernel == 1:
+        return None
+    ops = json.load(open(path))
+    km = ops.get("kernels", {})
+    mov = next((v for k, v in km.items() if k.startswith(kname)), None)
+    dep = next((v for k, v in km.items() if k.startswith("deposit_tiled_kernel")), None)
+    if mov is None or dep is None:
+        return None
+    with ClockSampler(local) as clk:
+        clk.begin()
+        peak = fp64_peak_tflops()
+        clk.end()
+    if not peak:
+        return None
+    f_mov, f_dep = mov["flops_per_update"], dep["flops_per_update"]
+    achieved = n_alive * f_mov / (mover_ms_step / 1e3) / 1e12
+    return {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "flops_per_update": f_mov,
+            "deposit": {"flops_per_update": f_dep,
+                        "achieved": n_alive * f_dep / (deposit_ms_step / 1e3) / 1e12 if deposit_ms_step else None},
+            "step_frac": rate_per_gpu * (f_mov + f_dep) / (peak * 1e12),
+            "peak_kind": "measured in this run: sustained DFMA, tools/microbench/fp64peak.cu",
+            "peak_clocks": clk.summary(),
+            "ops_source": {"kind": "static ncu capture (not this run)", "file": "profiles/fp64_ops.json",
+                           "from": ops.get("source")}}
 
 
 # --------------------------------------------------------------- GPU arm ----
@@ -332,13 +399,15 @@ def main():
             raise SystemExit(f"{args.config}: store needs {need / 1e9:.1f} GB on rank {rank}, "
                              f"{free_b / 1e9:.1f} GB free: run it on more GPUs")
         ctx = pic.Context(cfg, nccl_id=nccl_id, stream=stream)
-        parts = I.make_species_chunked(w)
-        for s, p in enumerate(parts):
-            ctx.set_particles(s, p)
+        # drawn on the device sub-slab by sub-slab and appended (pic_add_particles):
+        # no host copy of the store, transient memory of one sub-slab
+        for a, b, parts in I.iter_species_chunks(w, 64_000_000, device="cuda"):
+            for s, p in enumerate(parts):
+                ctx.add_particles(s, p)
+            if want_sample and parts_cpu_sample is None:
+                parts_cpu_sample = [{k: v[:2_000_000].cpu() for k, v in p.items()} for p in parts]
+            del parts
         ctx.sync()
-        if want_sample:
-            parts_cpu_sample = [{k: v[:2_000_000].clone() for k, v in p.items()} for p in parts]
-        del parts
     else:
         parts = I.make_species(w, device="cuda")
         n_local = [p["x"].numel() for p in parts]
@@ -433,24 +502,30 @@ def main():
     deposit_ms_step = prof["deposit"][0] / args.steps
     mover_launch_ms = prof["mover"][0] / max(1, prof["mover"][1])
     achieved = n_alive * b_mover / (mover_ms_step / 1e3) / 1e9
+    # traffic: NOT measured in this run (ncu cannot run inside the bench); the
+    # DRAM bytes per update of the mover from the committed `ncu --set full`
+    # capture named in `traffic_source`, attached only when that capture is of
+    # this config and kernel family, scaled per launch (particles / species)
     traffic = None
+    traffic_src = None
     ncu_pct = None
+    kname = "mover_tiled_kernel" if args.kernel in (0, 2) else "mover_basic_kernel"
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("config") == args.config:
-                # ncu --set full capture of one mover launch (one species): DRAM bytes per
-                # particle update, scaled to this launch's particles; pipe utilisations
+            if tj.get("config") == args.config and tj.get("kernel", "mover_tiled_kernel") == kname \
+                    and not args.relativistic:
                 traffic = tj["mover_bytes_per_update"] * n_alive / n_sp
+                traffic_src = {"kind": "static ncu capture (not this run)", "file": "profiles/traffic.json",
+                               "from": tj.get("source"), "bytes_per_update": tj["mover_bytes_per_update"]}
                 ncu_pct = {k: tj[k] for k in ("mover_fp64_pipe_pct", "mover_issue_active_pct", "mover_dram_pct",
                                               "deposit_dram_pct") if k in tj}
         except Exception:
             traffic = None
-    kname = "mover_tiled_kernel" if args.kernel in (0, 2) else "mover_basic_kernel"
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic,
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "ncu_utilisation_pct": ncu_pct,
             "bytes_per_update": b_mover, "launch_ms": mover_launch_ms,
             "launches_per_step": prof["mover"][1] / args.steps,
@@ -460,6 +535,7 @@ def main():
                         "bytes_per_update": b_deposit, "ms_per_step": deposit_ms_step,
                         "achieved": n_alive * b_deposit / (deposit_ms_step / 1e3) / 1e9 if deposit_ms_step else None}}
     mover_avg = sum(mover_ms) / len(mover_ms)
+    roof64 = fp64_roofline(args, kname, n_alive, mover_ms_step, deposit_ms_step, value / world, local)
 
     # ---- e2e through the public API with host buffers (paper's discrete-GPU
     # cycle: fields host->device, moments device->host).  Every
@@ -556,9 +632,12 @@ def main():
     if parts_cpu_sample is not None:
         threads = torch.get_num_threads()
         torch.set_num_threads(1)
-        r, sample, cores = oracle_rate(w, parts_cpu_sample, args.cpu_seconds)
+        r1, sample1, _ = oracle_rate(w, parts_cpu_sample, args.cpu_seconds / 2)
+        ra, samplea, cores = oracle_rate(w, parts_cpu_sample, args.cpu_seconds / 2, all_cores=True)
         torch.set_num_threads(threads)
-        cpu = {"value": r, "unit": "particle updates/s", "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = {"value": ra, "unit": "particle updates/s", "cores": cores, "kind": "oracle", "sample": samplea,
+               "single_thread": {"value": r1, "unit": "particle updates/s", "cores": 1, "kind": "oracle",
+                                 "sample": sample1}}
 
     if rank == 0:
         line = {
@@ -571,6 +650,7 @@ def main():
                        "l2": "inputs (%.2f GB per GPU) exceed the 126 MB L2; no flush" % (n_alive * 64 / 1e9),
                        "parallelism": f"x-slabs{world}"},
             "roofline": roof,
+            "roofline_fp64": roof64,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "next2_sources": next2,

@@ -26,13 +26,18 @@ PERIODIC, OPEN = 0, 1
 ALIVE, REMOVED, BAD, MERGED = 0, 1, 2, 3
 
 
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+
+
 def build(force: bool = False) -> str:
-    """Compile oracle.c into liboracle.so with gcc (no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
+    """Compile oracle.c into liboracle.so with gcc (no FMA contraction), and the
+    same source with OpenMP into liboracle_omp.so (all-cores timing only)."""
+    for lib, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+            tmp = lib + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+                                   "-fPIC", "-shared"] + extra + ["-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, lib)
     return _LIB
 
 
@@ -170,6 +175,55 @@ def moments(g: Grid, parts: dict, status=None, with_abs: bool = True):
     if out:
         raise ValueError(f"{out} particles outside the grid in oracle.moments")
     return mom, am
+
+
+_lib_omp = None
+
+
+def _load_omp():
+    """The OpenMP build (bench.py's all-cores cpu_baseline; never a parity checker)."""
+    global _lib_omp
+    if _lib_omp is None:
+        build()
+        lib = C.CDLL(_LIB_OMP)
+        P = C.POINTER
+        d = P(C.c_double)
+        lib.oracle_omp_threads.restype = C.c_int
+        lib.oracle_mover_par.argtypes = [P(Grid), P(Field), C.c_double, C.c_int, C.c_int, C.c_int64,
+                                         d, d, d, d, d, d, P(C.c_int8)]
+        lib.oracle_mover_par.restype = C.c_int64
+        lib.oracle_moments_par.argtypes = [P(Grid), C.c_int64, d, d, d, d, d, d, d, P(C.c_int8), d]
+        lib.oracle_moments_par.restype = C.c_int64
+        _lib_omp = lib
+    return _lib_omp
+
+
+def omp_threads() -> int:
+    return int(_load_omp().oracle_omp_threads())
+
+
+def mover_par(g: Grid, F: FieldWindow, qom: float, n_iter: int, parts: dict, status=None,
+              relativistic: bool = False):
+    """`mover` on all host cores (OpenMP build; bit-identical results)."""
+    n = len(parts["x"])
+    if status is None:
+        status = np.zeros(n, dtype=np.int8)
+    bad = _load_omp().oracle_mover_par(C.byref(g), C.byref(F.c), float(qom), int(n_iter), int(bool(relativistic)),
+                                       n, *[_dptr(parts[k]) for k in "xyzuvw"],
+                                       status.ctypes.data_as(C.POINTER(C.c_int8)))
+    return status, int(bad)
+
+
+def moments_par(g: Grid, parts: dict, status=None):
+    """`moments` on all host cores: per-thread node grids merged in thread order."""
+    nx, ny, nz = node_counts(g)
+    mom = np.zeros((10, nz, ny, nx))
+    n = len(parts["x"])
+    st = status.ctypes.data_as(C.POINTER(C.c_int8)) if status is not None else None
+    out = _load_omp().oracle_moments_par(C.byref(g), n, *[_dptr(parts[k]) for k in "xyzuvwq"], st, _dptr(mom))
+    if out:
+        raise ValueError(f"{out} particles outside the grid in oracle.moments_par")
+    return mom
 
 
 def implicit_sources(g: Grid, qoms, moms, B: np.ndarray):

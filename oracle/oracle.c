@@ -328,6 +328,60 @@ int64_t oracle_moments(const oracle_grid *g, int64_t np, const double *x,
   return outside;
 }
 
+/* ------------------------------------------ all-cores timing build only -- */
+#ifdef _OPENMP
+#include <omp.h>
+/* the oracle timed on all host cores for bench.py's
+ * cpu_baseline.  Compiled only into the OpenMP build of this same source
+ * (liboracle_omp.so); the parity checker is the single-threaded build.
+ * Neither wrapper changes the arithmetic: the mover runs oracle_mover_ex on
+ * contiguous particle ranges, one per thread (every particle is independent,
+ * so the result is bit-identical); the moments run oracle_moments on the same
+ * ranges into per-thread node grids that are then added in thread order (a
+ * fixed order: the result equals the sequential sum up to reassociation,
+ * within R19).                                                              */
+/* every host core, whatever the caller's OpenMP runtime was told (torch sets
+ * the process-wide thread count of the shared libgomp) */
+int oracle_omp_threads(void) { return omp_get_num_procs(); }
+
+int64_t oracle_mover_par(const oracle_grid *g, const oracle_field *F, double qom, int n_iter, int relativistic,
+                         int64_t np, double *x, double *y, double *z, double *u, double *v, double *w,
+                         int8_t *status) {
+  int64_t bad = 0;
+  const int T = oracle_omp_threads();
+#pragma omp parallel for num_threads(T) schedule(static, 1) reduction(+ : bad)
+  for (int t = 0; t < T; ++t) {
+    const int64_t a = np * t / T, b = np * (t + 1) / T;
+    bad += oracle_mover_ex(g, F, qom, n_iter, relativistic, b - a, x + a, y + a, z + a, u + a, v + a, w + a,
+                           status + a);
+  }
+  return bad;
+}
+
+int64_t oracle_moments_par(const oracle_grid *g, int64_t np, const double *x, const double *y, const double *z,
+                           const double *u, const double *v, const double *w, const double *q,
+                           const int8_t *status, double *mom) {
+  const int64_t plane = nodes_axis(g, 0) * nodes_axis(g, 1) * nodes_axis(g, 2), M = 10 * plane;
+  const int T = oracle_omp_threads();
+  double **grid = (double **)calloc((size_t)T, sizeof(double *));
+  int64_t outside = 0;
+#pragma omp parallel for num_threads(T) schedule(static, 1) reduction(+ : outside)
+  for (int t = 0; t < T; ++t) {
+    const int64_t a = np * t / T, b = np * (t + 1) / T;
+    grid[t] = (double *)calloc((size_t)M, sizeof(double));
+    outside += oracle_moments(g, b - a, x + a, y + a, z + a, u + a, v + a, w + a, q + a,
+                              status ? status + a : NULL, grid[t], NULL);
+  }
+  /* merge in thread order, parallel over nodes */
+#pragma omp parallel for num_threads(T) schedule(static)
+  for (int64_t i = 0; i < M; ++i)
+    for (int t = 0; t < T; ++t) mom[i] += grid[t][i];
+  for (int t = 0; t < T; ++t) free(grid[t]);
+  free(grid);
+  return outside;
+}
+#endif
+
 /* Convenience for tests: unique node counts per axis.                      */
 void oracle_node_counts(const oracle_grid *g, int64_t out[3]) {
   for (int d = 0; d < 3; ++d) out[d] = nodes_axis(g, d);

@@ -64,6 +64,21 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     return lib
 
 
+FP64PEAK_SRC = os.path.join(ROOT, "tools", "microbench", "fp64peak.cu")
+FP64PEAK_LIB = os.path.join(ROOT, "tools", "microbench", "libfp64peak.so")
+
+
+def build_fp64peak(force: bool = False) -> str:
+    """The sustained-DFMA microbenchmark bench.py reports roofline_fp64 against
+    (measurement infrastructure, not part of libpic)."""
+    if force or not os.path.exists(FP64PEAK_LIB) or os.path.getmtime(FP64PEAK_LIB) < os.path.getmtime(FP64PEAK_SRC):
+        tmp = FP64PEAK_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["nvcc", "-shared", "-o", tmp, FP64PEAK_SRC, "-gencode", "arch=compute_100a,code=sm_100a",
+                               "-O3", "-Xcompiler", "-fPIC"])
+        os.replace(tmp, FP64PEAK_LIB)
+    return FP64PEAK_LIB
+
+
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]

@@ -10,6 +10,7 @@
 // order built next by pic_mover includes it.  Ghost particles that did not
 // cross the face are dropped (they were never part of the plasma).
 #include "pic_internal.cuh"
+#include "push.cuh"
 
 namespace pic {
 
@@ -74,54 +75,10 @@ __global__ void __launch_bounds__(256) inject_kernel(const InjectArgs A) {
                           A.drift[1] + A.vth * (rad1 * sin(two_pi * r[4])),
                           A.drift[2] + A.vth * (rad2 * cos(two_pi * r[6]))};
     const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
-    double xb[3] = {xn[0], xn[1], xn[2]};
-    double vb[3] = {vn[0], vn[1], vn[2]};
-    bool clamped = false;
-    if (A.rel) {
-      const double ic2 = 1.0 / (g.c * g.c);
-      const double gn = 1.0 / sqrt(1.0 - (vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2]) * ic2);
-      double gt = gn, g1 = gn, u1[3] = {gn * vn[0], gn * vn[1], gn * vn[2]};
-      for (int it = 0; it < A.n_iter; ++it) {
-        double EB[6];
-        clamped |= sample_window(g, A.F, xb, EB);
-        const double igt = 1.0 / gt;
-        double vt[3], a[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) { vt[d] = fma(A.ks, EB[d], gn * vn[d]); a[d] = A.ks_c * EB[3 + d] * igt; }
-        const double cr0 = vt[1] * a[2] - vt[2] * a[1], cr1 = vt[2] * a[0] - vt[0] * a[2], cr2 = vt[0] * a[1] - vt[1] * a[0];
-        const double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
-        const double invD = 1.0 / (gt * (1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2])));
-        vb[0] = (vt[0] + cr0 + dot * a[0]) * invD;
-        vb[1] = (vt[1] + cr1 + dot * a[1]) * invD;
-        vb[2] = (vt[2] + cr2 + dot * a[2]) * invD;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) u1[d] = 2.0 * gt * vb[d] - gn * vn[d];
-        g1 = sqrt(1.0 + (u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2]) * ic2);
-        gt = 0.5 * (gn + g1);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
-      }
-#pragma unroll
-      for (int d = 0; d < 3; ++d) { xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]); vnew[d] = u1[d] / g1; }
-    } else {
-      for (int it = 0; it < A.n_iter; ++it) {
-        double EB[6];
-        clamped |= sample_window(g, A.F, xb, EB);
-        double vt[3], a[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) { vt[d] = fma(A.ks, EB[d], vn[d]); a[d] = A.ks_c * EB[3 + d]; }
-        const double cr0 = vt[1] * a[2] - vt[2] * a[1], cr1 = vt[2] * a[0] - vt[0] * a[2], cr2 = vt[0] * a[1] - vt[1] * a[0];
-        const double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
-        const double invD = 1.0 / (1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2]));
-        vb[0] = (vt[0] + cr0 + dot * a[0]) * invD;
-        vb[1] = (vt[1] + cr1 + dot * a[1]) * invD;
-        vb[2] = (vt[2] + cr2 + dot * a[2]) * invD;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
-      }
-#pragma unroll
-      for (int d = 0; d < 3; ++d) { xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]); vnew[d] = fma(2.0, vb[d], -vn[d]); }
-    }
+    // Eq. 2 (push.cuh) with samples from the global field window
+    const WindowSampler sample{&g, A.F, A.ks, A.ks_c};
+    const bool clamped = A.rel ? push_eq2<0, 1>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew)
+                               : push_eq2<0, 0>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew);
     // only particles that crossed the face join the plasma; the others are
     // dropped without counting (R28).  NaN fails the test and is caught below.
     if (!(xnew[0] < 0.0)) {

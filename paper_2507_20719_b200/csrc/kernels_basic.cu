@@ -14,6 +14,7 @@
 // This family is the simple reference path on the GPU: correct for every
 // config, but the deposit costs 80 global atomics per particle.
 #include "pic_internal.cuh"
+#include "push.cuh"
 
 namespace pic {
 
@@ -51,66 +52,11 @@ __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
     kold = tile_key32(g, (uint32_t)((int)xn[0] - (int)g.slab_lo), (uint32_t)(int)xn[1], (uint32_t)(int)xn[2]);
     const double vn[3] = {A.src[3][p], A.src[4][p], A.src[5][p]};
     const double h[3] = {0.5 * g.dt * g.inv_delta[0], 0.5 * g.dt * g.inv_delta[1], 0.5 * g.dt * g.inv_delta[2]};
-    double xb[3] = {xn[0], xn[1], xn[2]};
-    double vb[3] = {vn[0], vn[1], vn[2]};
-    bool clamped = false;
+    // Eq. 2 (push.cuh) with samples from the global field window
+    const WindowSampler sample{&g, A.F, A.ks, A.ks_c};
     double xnew[3], vnew[3];
-    if (A.rel) {
-      // relativistic Eq. 2 (R4, R5)
-      const double ic2 = 1.0 / (g.c * g.c);
-      const double gn = 1.0 / sqrt(1.0 - (vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2]) * ic2);
-      double gt = gn, g1 = gn, u1[3] = {gn * vn[0], gn * vn[1], gn * vn[2]};
-      for (int it = 0; it < A.n_iter; ++it) {
-        double EB[6];
-        clamped |= sample_window(g, A.F, xb, EB);
-        const double igt = 1.0 / gt;
-        double vt[3], a[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) { vt[d] = fma(A.ks, EB[d], gn * vn[d]); a[d] = A.ks_c * EB[3 + d] * igt; }
-        const double cr0 = vt[1] * a[2] - vt[2] * a[1];
-        const double cr1 = vt[2] * a[0] - vt[0] * a[2];
-        const double cr2 = vt[0] * a[1] - vt[1] * a[0];
-        const double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
-        const double invD = 1.0 / (gt * (1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2])));
-        vb[0] = (vt[0] + cr0 + dot * a[0]) * invD;
-        vb[1] = (vt[1] + cr1 + dot * a[1]) * invD;
-        vb[2] = (vt[2] + cr2 + dot * a[2]) * invD;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) u1[d] = 2.0 * gt * vb[d] - gn * vn[d];
-        g1 = sqrt(1.0 + (u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2]) * ic2);
-        gt = 0.5 * (gn + g1);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
-      }
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
-        vnew[d] = u1[d] / g1;
-      }
-    } else {
-    for (int it = 0; it < A.n_iter; ++it) {
-      double EB[6];
-      clamped |= sample_window(g, A.F, xb, EB);
-      double vt[3], a[3];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) { vt[d] = fma(A.ks, EB[d], vn[d]); a[d] = A.ks_c * EB[3 + d]; }
-      const double cr0 = vt[1] * a[2] - vt[2] * a[1];
-      const double cr1 = vt[2] * a[0] - vt[0] * a[2];
-      const double cr2 = vt[0] * a[1] - vt[1] * a[0];
-      const double dot = vt[0] * a[0] + vt[1] * a[1] + vt[2] * a[2];
-      const double invD = 1.0 / (1.0 + (a[0] * a[0] + a[1] * a[1] + a[2] * a[2]));
-      vb[0] = (vt[0] + cr0 + dot * a[0]) * invD;
-      vb[1] = (vt[1] + cr1 + dot * a[1]) * invD;
-      vb[2] = (vt[2] + cr2 + dot * a[2]) * invD;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
-      vnew[d] = fma(2.0, vb[d], -vn[d]);
-    }
-    }
+    const bool clamped = A.rel ? push_eq2<0, 1>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew)
+                               : push_eq2<0, 0>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew);
     k = finish_particle(g, xnew, vnew, clamped, A.stats);
     A.dst[0][q] = xnew[0]; A.dst[1][q] = xnew[1]; A.dst[2][q] = xnew[2];
     A.dst[3][q] = vnew[0]; A.dst[4][q] = vnew[1]; A.dst[5][q] = vnew[2];

@@ -40,6 +40,7 @@
 #include <cstring>
 
 #include "pic_internal.cuh"
+#include "push.cuh"
 
 namespace pic {
 
@@ -47,8 +48,6 @@ constexpr int NB = TILE + 3;            // staged field nodes per axis: -1 .. TI
 constexpr int NB3 = NB * NB * NB;       // 343
 constexpr int MB = TILE + 1;            // deposit nodes per axis: 0 .. TILE
 constexpr int MB3 = MB * MB * MB;       // 125
-constexpr int WARPS = 8;
-constexpr int THREADS = 32 * WARPS;
 #ifndef PIC_SRC_STAGES
 #define PIC_SRC_STAGES 2
 #endif
@@ -136,17 +135,6 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, i
       " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
-}
-
-// 1/D for D >= 1 (D = 1 + |a|^2 of Eq. 2): MUFU.RCP64H seed + two Newton steps
-// (error well below 1 ulp of the 1e-12 parity budget; no IEEE slow path).
-__device__ __forceinline__ double rcp_ge1(double D) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
-  double e = fma(-D, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-D, r, 1.0);
-  return fma(r, e, r);
 }
 
 // Trilinear gather of the pre-scaled fields from the staged box.  u = position
@@ -271,11 +259,17 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       const uint32_t src_idx = pk[(ri % PK_SLOTS) * 64 + lane];
       double *d = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
 #pragma unroll
+#ifdef PIC_EXP_NO_QID
+      for (int k = 0; k < 6; ++k)
+#else
       for (int k = 0; k < 7; ++k)
+#endif
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
                      : "memory");
+#ifndef PIC_EXP_NO_QID
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 7 * 32)), "l"(A.src_id + src_idx)
                    : "memory");
+#endif
     }
   };
   for (int ri = 0; ri < PK_AHEAD; ++ri) fetch_pk(ri);
@@ -309,80 +303,22 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       // taken from the stored position, so no key array is kept; a mismatch
       // would only reclassify a stayer as an arrival or back)
       kold = tile_key32(g, (uint32_t)((int)xn[0] - (int)g.slab_lo), (uint32_t)(int)xn[1], (uint32_t)(int)xn[2]);
-      double xb[3] = {xn[0], xn[1], xn[2]};
-      double vb[3];
-      bool clamped = false;
-      const int n_iter = NIT > 0 ? NIT : A.n_iter;
+      // Eq. 2 (push.cuh); field samples from the staged box, the global window
+      // (clamped to it, R11) for iterates outside the box
+      auto sample = [&](const double xb[3], double EB[6]) -> bool {
+        const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
+        if (gather_smem(fld, u, EB)) return false;
+        return WindowSampler{&g, A.field, A.ks, A.ks_c}(xb, EB);
+      };
       double xnew[3], vnew[3];
-      if constexpr (REL == 0) {
-#pragma unroll
-        for (int it = 0; it < n_iter; ++it) {
-          double EB[6];
-          const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
-          if (!gather_smem(fld, u, EB)) {
-            clamped |= sample_window(g, A.field, xb, EB);
-#pragma unroll
-            for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
-          }
-          // Eq. 2: vt = vn + k E ; a = k B / c ; vb = (vt + vt x a + (vt.a) a) / (1 + a.a)
-          const double vt0 = vn[0] + EB[0], vt1 = vn[1] + EB[1], vt2 = vn[2] + EB[2];
-          const double a0 = EB[3], a1 = EB[4], a2 = EB[5];
-          const double dot = fma(vt0, a0, fma(vt1, a1, vt2 * a2));
-          const double D = fma(a0, a0, fma(a1, a1, fma(a2, a2, 1.0)));
-          const double invD = rcp_ge1(D);
-          vb[0] = fma(dot, a0, fma(vt1, a2, fma(-vt2, a1, vt0))) * invD;
-          vb[1] = fma(dot, a1, fma(vt2, a0, fma(-vt0, a2, vt1))) * invD;
-          vb[2] = fma(dot, a2, fma(vt0, a1, fma(-vt1, a0, vt2))) * invD;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
-          vnew[d] = fma(2.0, vb[d], -vn[d]);
-        }
-      } else {
-        // relativistic Eq. 2 (R4, R5): vt = gn vn + k E,
-        // a = k B / (c gt), D = gt (1 + a.a), u1 = 2 gt vb - gn vn,
-        // g1 = sqrt(1 + u1.u1 / c^2), gt = (gn + g1) / 2; v^{n+1} = u1 / g1
-        const double ic2 = 1.0 / (g.c * g.c);
-        const double gn = 1.0 / sqrt(1.0 - (vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2]) * ic2);
-        double gt = gn, g1 = gn, u1[3] = {gn * vn[0], gn * vn[1], gn * vn[2]};
-#pragma unroll
-        for (int it = 0; it < n_iter; ++it) {
-          double EB[6];
-          const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
-          if (!gather_smem(fld, u, EB)) {
-            clamped |= sample_window(g, A.field, xb, EB);
-#pragma unroll
-            for (int m = 0; m < 6; ++m) EB[m] *= (m < 3) ? A.ks : A.ks_c;
-          }
-          const double igt = 1.0 / gt;
-          const double vt0 = fma(gn, vn[0], EB[0]), vt1 = fma(gn, vn[1], EB[1]), vt2 = fma(gn, vn[2], EB[2]);
-          const double a0 = EB[3] * igt, a1 = EB[4] * igt, a2 = EB[5] * igt;
-          const double dot = fma(vt0, a0, fma(vt1, a1, vt2 * a2));
-          const double invD = rcp_ge1(fma(a0, a0, fma(a1, a1, fma(a2, a2, 1.0)))) * igt;
-          vb[0] = fma(dot, a0, fma(vt1, a2, fma(-vt2, a1, vt0))) * invD;
-          vb[1] = fma(dot, a1, fma(vt2, a0, fma(-vt0, a2, vt1))) * invD;
-          vb[2] = fma(dot, a2, fma(vt0, a1, fma(-vt1, a0, vt2))) * invD;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) u1[d] = fma(2.0 * gt, vb[d], -gn * vn[d]);
-          g1 = sqrt(fma(u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2], ic2, 1.0));
-          gt = 0.5 * (gn + g1);
-#pragma unroll
-          for (int d = 0; d < 3; ++d) xb[d] = fma(vb[d], h[d], xn[d]);
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          xnew[d] = fma(vb[d], 2.0 * h[d], xn[d]);
-          vnew[d] = u1[d] / g1;
-        }
-      }
+      const bool clamped = push_eq2<NIT, REL>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew);
       knew = finish_particle(g, xnew, vnew, clamped, A.stats);
       A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
       A.dst[3][p] = vnew[0]; A.dst[4][p] = vnew[1]; A.dst[5][p] = vnew[2];
+#ifndef PIC_EXP_NO_QID
       A.dst[6][p] = qv;
       A.dst_id[p] = idv;
+#endif
       A.key_new[p] = knew;
     }
     // complete the previous round's rank, then start this round's (order.cu);

@@ -328,6 +328,20 @@ def species_upper_counts(w: Workload) -> List[int]:
     return out
 
 
+def iter_species_chunks(w: Workload, chunk_particles: int = 64_000_000, device="cpu"):
+    """Yield `make_species` of consecutive sub-slabs of whole x-planes of this
+    rank's slab (each seeded by its first plane, as `make_species` seeds a
+    slab), about `chunk_particles` particles per sub-slab: the particles of a
+    slab too large to draw in one piece (C3-C5 at full size), to be appended to
+    a store one sub-slab at a time (pic_add_particles).  Yields (lo, hi, parts)."""
+    lo, hi = w.slab_or_all()
+    ub = species_upper_counts(w)
+    step = max(1, int(chunk_particles * (hi - lo) // max(1, sum(ub))))
+    for a in range(lo, hi, step):
+        b = min(hi, a + step)
+        yield a, b, make_species(w.with_slab(a, b), device=device)
+
+
 def make_species_chunked(w: Workload, chunk_particles: int = 32_000_000) -> List[dict]:
     """`make_species` for slabs too large to draw in one piece (C3-C5 at full
     size): the slab is drawn in sub-slabs of whole x-planes (each seeded by its

@@ -41,5 +41,17 @@ def test_gpu_arm_line():
     assert d["gpu_launches"] > 0 and d["value"] > 0 and d["n_gpus"] == 1
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
-    assert d["cpu_baseline"]["kind"] == "oracle"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1
+    assert cb["single_thread"]["cores"] == 1 and cb["single_thread"]["value"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_fp64_roofline_on_c3_clone():
+    d = run_bench(["--config", "c3", "--c3-cells", "48", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+                   "--no-e2e"], 900)
+    r = d["roofline_fp64"]
+    assert r is not None and r["bound"] == "alu" and r["unit"] == "TFLOP/s"
+    assert 20 < r["peak"] < 60 and 0 < r["frac"] < 1 and r["flops_per_update"] > 300
+    assert d["roofline"]["traffic"] > 0 and d["roofline"]["traffic_source"]["kind"].startswith("static")

@@ -31,7 +31,7 @@ N_NODES = 12
 
 def _box_mask(parts, node, w, half):
     """Input particles whose cell lies within `half` cells of `node` (min-image)."""
-    m = torch.ones(parts["x"].numel(), dtype=torch.bool)
+    m = torch.ones(parts["x"].numel(), dtype=torch.bool, device=parts["x"].device)
     for d, k in enumerate("xyz"):
         n = w.ncell[d]
         c = torch.floor(parts[k] / w.delta[d])
@@ -100,4 +100,103 @@ def test_c2_full_size_sampled():
             assert abs(got - float(t.sum())) <= 1e-11 * float(np.abs(t).sum()), (s, comp, got, float(t.sum()))
         del gp_dev
         torch.cuda.empty_cache()
+    ctx.close()
+
+
+# ------------------------------------------------------------------ C3 ----
+def _component(ctx, s, key, n):
+    """One array of species s's live particles (store order) on the device:
+    pic_get_particles with every other output pointer NULL (the full store
+    does not fit the device twice)."""
+    import ctypes as C
+    out = torch.empty(n, dtype=torch.int64 if key == "id" else torch.float64, device="cuda")
+    P7 = (C.c_void_p * 7)(*[out.data_ptr() if k == key else None for k in "xyzuvwq"])
+    st = ctx.lib.pic_get_particles(ctx.h, s, P7, C.c_void_p(out.data_ptr()) if key == "id" else None)
+    assert st == pic.PIC_OK, ctx.lib.pic_last_error(ctx.h)
+    return out
+
+
+def test_c3_full_size_sampled():
+    """C3 at BASELINE.json's full size (configs[2]: 192^3 cells, 2 species x
+    64 ppc = 905,969,664 particles on one GPU), loaded as bench.py loads it
+    (drawn on the device sub-slab by sub-slab, pic_add_particles) and run for
+    two cycles in bench.py's launch configuration.  The oracle checks sampled
+    outputs one by one: ~3000 particles per species by id, and 8 nodes whose
+    every contributor (the input particles within two cells; they move < 1 cell
+    in two cycles here) it moves and deposits; plus P8 for rho over all
+    particles: sum_g rho_g V = sum_p q_p of the inputs (periodic, none removed)."""
+    w = I.c3()
+    ub = I.species_upper_counts(w)
+    cap = [n + 65536 for n in ub]
+    cfg = pic.make_config(w, capacity=cap, ghost=2)
+    need = pic.pic_workspace_bytes(cfg)
+    if need > torch.cuda.mem_get_info()[0] - 20e9:
+        pytest.skip("C3 needs a 180 GB B200")
+    ctx = pic.Context(cfg)
+    rng = np.random.default_rng(31415)
+    nodes = [tuple(int(v) for v in rng.integers(0, 192, 3)) for _ in range(8)]
+    half = 2
+    gen = torch.Generator(device="cuda").manual_seed(2718)
+    keep = [[] for _ in w.species]        # host copies of the particles the oracle needs
+    qsum = [0.0 for _ in w.species]
+    p_pick = N_SAMPLE / max(ub)
+    for a, b, parts in I.iter_species_chunks(w, 64_000_000, device="cuda"):
+        for s, p in enumerate(parts):
+            ctx.add_particles(s, p)
+            qsum[s] += float(p["q"].sum().item())
+            m = torch.rand(p["x"].numel(), generator=gen, device="cuda") < p_pick
+            for node in nodes:
+                m |= _box_mask(p, node, w, half)
+            keep[s].append({k: v[m].cpu() for k, v in p.items()})
+        del parts
+    torch.cuda.empty_cache()
+    lo, EB = I.field_window(w, 2, device="cuda")
+    ctx.set_fields(EB)
+    for _ in range(CYCLES):
+        ctx.cycle()
+    stats = ctx.sync()
+    assert stats["far"] == 0 and stats["nonfinite"] == 0 and stats["removed"] == 0
+    g = PU.oracle_grid(w)
+    F = PU.oracle_field(w, 2)
+    V = w.delta[0] * w.delta[1] * w.delta[2]
+    for s, sp in enumerate(w.species):
+        sub = {k: torch.cat([c[k] for c in keep[s]]) for k in keep[s][0]}
+        # -- the oracle moves every kept particle (sample + node contributors)
+        P = PU.to_numpy_parts(sub)
+        st = np.zeros(len(P["x"]), dtype=np.int8)
+        for _ in range(CYCLES):
+            st, bad = O.mover(g, F, sp.qom, w.n_iter, P, st)
+            assert bad == 0
+        # -- moments at the sampled nodes: one deposit of the union of the boxes
+        gm = ctx.get_moments(s).cpu().numpy()
+        assert abs(float(gm[0].sum()) * V - qsum[s]) <= 1e-11 * abs(qsum[s])
+        mom, am = O.moments(g, P, st)
+        for node in nodes:
+            ix, iy, iz = node
+            o, aa, gv = mom[:, iz, iy, ix], am[:, iz, iy, ix], gm[:, iz, iy, ix]
+            assert np.all(aa > 0)
+            ratio = np.abs(gv - o) / (PU.MOM_TOL * aa)
+            assert ratio.max() <= 1.0, (s, node, ratio.max())
+        del gm, mom, am
+        # -- sampled particles by id against the GPU's particles
+        n = ctx.count(s)
+        assert n == ub[s]
+        want = torch.from_numpy(np.sort(P["id"])).cuda()
+        gid = _component(ctx, s, "id", n)
+        pos = []
+        for c0 in range(0, n, 100_000_000):
+            chunk = gid[c0:c0 + 100_000_000]
+            j = torch.searchsorted(want, chunk).clamp(max=want.numel() - 1)
+            pos.append(torch.nonzero(want[j] == chunk).flatten() + c0)
+        pos = torch.cat(pos)
+        assert pos.numel() == want.numel()
+        gsub = {"id": gid[pos].cpu().numpy()}
+        del gid
+        for k in "xyzuvwq":
+            arr = _component(ctx, s, k, n)
+            gsub[k] = arr[pos].cpu().numpy()
+            del arr
+        torch.cuda.empty_cache()
+        rep = {}
+        assert PU.compare_particles(w, sp, gsub, P, st, rep), rep
     ctx.close()

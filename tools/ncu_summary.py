@@ -27,6 +27,10 @@ KEYS = [
     "sm__cycles_elapsed.avg.per_second",
     "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
     "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "sm__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_dmul_pred_on.sum", "sm__inst_executed_pipe_tensor_subpipe_dmma.sum",
+    "sm__inst_executed_pipe_fp64.sum", "smsp__warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
 ]
 
 
@@ -37,6 +41,14 @@ def ncu_csv(rep, *args):
     out = subprocess.check_output(["ncu", "-i", rep, "--csv", "--launch-skip", str(LAUNCH), "--launch-count", "1"]
                                   + list(args), stderr=subprocess.DEVNULL).decode()
     return list(csv.reader(io.StringIO(out)))
+
+
+def fp64_flops(m):
+    """SASS-counted fp64 flops: 2 per DFMA, 1 per DADD / DMUL thread instruction,
+    512 per DMMA.8x8x4 warp instruction (8 x 8 x 4 FMAs)."""
+    g = lambda k: m.get(k, (0.0, ""))[0]
+    return (2 * g("sm__sass_thread_inst_executed_op_dfma_pred_on.sum") + g("sm__sass_thread_inst_executed_op_dadd_pred_on.sum")
+            + g("sm__sass_thread_inst_executed_op_dmul_pred_on.sum") + 512 * g("sm__inst_executed_pipe_tensor_subpipe_dmma.sum"))
 
 
 def main():
@@ -100,6 +112,7 @@ def main():
         "dram_gbs": (rd + wr) / (t_ms * 1e-3) / 1e9,
         "metrics": {k: v for k, (v, u) in m.items()},
         "warp_instr_per_particle": tot_i / a.particles,
+        "fp64_flops_per_particle": fp64_flops(m) / a.particles,
         "stall_reasons_pct": {k: round(100.0 * v / rs, 1) for k, v in reasons.most_common(10)},
     }
     with open(a.out_prefix + ".json", "w") as f:
@@ -111,7 +124,8 @@ def main():
                 f"({(rd+wr)/(t_ms*1e-3)/1e9:.0f} GB/s)\n")
         for k, (v, u) in m.items():
             f.write(f"- `{k}` = {v:g} {u}\n")
-        f.write(f"\nWarp instructions per particle: {tot_i / a.particles:.1f}\n\n")
+        f.write(f"\nWarp instructions per particle: {tot_i / a.particles:.1f}; "
+                f"fp64 flops per particle (SASS-counted): {fp64_flops(m) / a.particles:.1f}\n\n")
         f.write("Stall reasons (share of samples): " +
                 ", ".join(f"{k} {100.0*v/rs:.1f}%" for k, v in reasons.most_common(8)) + "\n\n")
         f.write("| file:line | warp instr / particle | stall % | top stall | source |\n|---|---|---|---|---|\n")
@@ -119,7 +133,7 @@ def main():
             top = max(x[5].items(), key=lambda kv: kv[1])[0] if x[5] else ""
             f.write(f"| {x[0]}:{x[1]} | {x[3]/a.particles:.2f} | {100.0*x[4]/tot_s:.1f} | {top} | `{x[2].replace('|','/')}` |\n")
     print(json.dumps({k: summary[k] for k in ("kernel", "launch_ms", "traffic_bytes_per_update", "dram_gbs",
-                                               "warp_instr_per_particle")}))
+                                               "warp_instr_per_particle", "fp64_flops_per_particle")}))
 
 
 if __name__ == "__main__":
