@@ -64,6 +64,16 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     return lib
 
 
+CHECKED_LIB = os.path.join(HERE, "libpic_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """libpic with the device bounds checks compiled in (-DPIC_CHECKED: every
+    violated index invariant is counted and pic_sync returns PIC_ECUDA) -- the
+    stand-in for compute-sanitizer, which is closed on this pool."""
+    return build(force=force, defines=("PIC_CHECKED",), out=CHECKED_LIB)
+
+
 FP64PEAK_SRC = os.path.join(ROOT, "tools", "microbench", "fp64peak.cu")
 FP64PEAK_LIB = os.path.join(ROOT, "tools", "microbench", "libfp64peak.so")
 

@@ -534,9 +534,11 @@ pic_status pic_sync(pic_ctx *p, int64_t stats[8]) {
   unsigned long long h[ST_N];
   PIC_CUDA(cudaMemcpy(h, ctx->stats, sizeof(h), cudaMemcpyDeviceToHost));
   int64_t all[ST_N];
-  for (int k = 0; k < ST_N; ++k) all[k] = (int64_t)h[k] + ctx->hstat[k];
+  for (int k = 0; k < ST_N; ++k) all[k] = (int64_t)h[k] + (k < 8 ? ctx->hstat[k] : 0);
   if (stats)
-    for (int k = 0; k < ST_N; ++k) stats[k] = all[k];
+    for (int k = 0; k < ST_PUBLIC; ++k) stats[k] = all[k];
+  if (all[ST_CHECK]) return fail(ctx, PIC_ECUDA, "checked build: " + std::to_string(all[ST_CHECK]) +
+                                                   " device bounds checks failed");
   if (ctx->peer) {
     unsigned long long perr = 0;
     PIC_CUDA(cudaMemcpy(&perr, &ctx->peer_ctl->err, sizeof(perr), cudaMemcpyDeviceToHost));

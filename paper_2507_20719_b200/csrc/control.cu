@@ -139,6 +139,8 @@ struct CoalArgs {
   // cells for coalesce_big_kernel: list[2 e] = cell, list[2 e + 1] = scratch offset
   unsigned long long *n_big, *big_used;
   int64_t *big_list;
+  int64_t cap;
+  unsigned long long *stats;
 };
 
 // Global scratch of coalesce_big_kernel, one record per particle of a listed
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(256) coalesce_big_kernel(const CoalArgs A, con
     const int64_t c = A.big_list[2 * e], off = A.big_list[2 * e + 1];
     const uint32_t q0 = A.cell_off[c];
     const int64_t nc = (int64_t)A.cell_off[c + 1] - (int64_t)q0;
+    PIC_DCHECK(off >= 0 && off + nc <= A.cap && (off + nc) / 2 <= A.cap && 2 * (int64_t)e + 1 < A.cap, A.stats);
     for (int64_t i = threadIdx.x; i < nc; i += blockDim.x) {
       const uint32_t p = A.perm[q0 + i];
       // + 0.0 maps a -0 bin to +0 (equal bins compare equal, as in the oracle)
@@ -400,6 +403,8 @@ pic_status control(Ctx *ctx, int s, int64_t target, double theta, double eps, do
     A.key_new = sp.key_new;
     A.dv = dv;
     A.frac = (double)(n - target) / (double)n;
+    A.cap = sp.cap;
+    A.stats = ctx->stats;
     A.merges = reinterpret_cast<unsigned long long *>(ctx->dev_counts + 60);
     A.n_big = reinterpret_cast<unsigned long long *>(ctx->dev_counts + 61);
     A.big_used = reinterpret_cast<unsigned long long *>(ctx->dev_counts + 62);

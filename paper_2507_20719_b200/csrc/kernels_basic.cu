@@ -35,6 +35,7 @@ struct MoverArgs {
   int rel;                    // relativistic Eq. 2 (NEXT-1)
   int peer;                   // slab leavers go straight into the neighbours' buffers (peer.cu)
   PeerOut po;
+  int64_t cap;
 };
 
 __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
@@ -47,6 +48,7 @@ __global__ void __launch_bounds__(256) mover_basic_kernel(const MoverArgs A) {
   uint32_t k = KEY_DEAD, kold = KEY_DEAD;
   if (act) {
     const uint32_t p = A.perm[q];
+    PIC_DCHECK(p < A.cap && q < A.cap, A.stats);
     const double xn[3] = {A.src[0][p], A.src[1][p], A.src[2][p]};
     // the cell of x^n (keys are always taken from the stored position)
     kold = tile_key32(g, (uint32_t)((int)xn[0] - (int)g.slab_lo), (uint32_t)(int)xn[1], (uint32_t)(int)xn[2]);
@@ -108,6 +110,7 @@ pic_status launch_mover_basic(Ctx *ctx, int s) {
   A.rel = ctx->cfg.relativistic;
   A.peer = ctx->peer;
   A.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
+  A.cap = S.cap;
   const int threads = 256;
   const int64_t blocks = std::max<int64_t>(1, (S.n_raw + threads - 1) / threads);
   {

@@ -57,7 +57,8 @@ constexpr int PERM_UNROLL = PIC_PERM_UNROLL;
 
 __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t *__restrict__ rank,
                             const uint32_t *__restrict__ cell_off, const uint32_t *__restrict__ cell_count,
-                            const int64_t *__restrict__ d_nraw, uint32_t *__restrict__ perm) {
+                            const int64_t *__restrict__ d_nraw, uint32_t *__restrict__ perm, int64_t ncells,
+                            unsigned long long *__restrict__ stats) {
   // PERM_UNROLL independent elements per thread and iteration (memory-level
   // parallelism for the dependent cell_off gather)
   const int64_t n = *d_nraw;
@@ -74,6 +75,7 @@ __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t
     for (int u = 0; u < PERM_UNROLL; ++u) {
       if (k[u] >= KEY_FIRST_RESERVED) continue;
       const uint32_t q = cell_off[k[u]] + ((r[u] & RANK_ARRIVAL) ? cell_count[k[u]] + (r[u] & ~RANK_ARRIVAL) : r[u]);
+      PIC_DCHECK(k[u] < ncells && q < cell_off[k[u] + 1], stats);
       perm[q] = (uint32_t)(p0 + u * stride);
     }
   }
@@ -104,7 +106,7 @@ pic_status build_order(Ctx *ctx, int s) {
   if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("scan: ") + cudaGetErrorString(e));
   if (sp.n_raw > 0) {
     perm_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_off, sp.cell_count,
-                                                             sp.d_nraw, sp.perm); ++ctx->launches;
+                                                             sp.d_nraw, sp.perm, nc, ctx->stats); ++ctx->launches;
   }
   PIC_CUDA(cudaGetLastError());
   sp.order_valid = true;

@@ -36,8 +36,28 @@ constexpr uint32_t KEY_FIRST_RESERVED = 0xFFFFFFFDu;
 // device counters (stats of pic_sync)
 enum Stat {
   ST_REMOVED = 0, ST_SENT = 1, ST_RECEIVED = 2, ST_FAR = 3, ST_CLAMPED = 4,
-  ST_NONFINITE = 5, ST_OVERFLOW = 6, ST_MULTIWRAP = 7, ST_N = 8
+  ST_NONFINITE = 5, ST_OVERFLOW = 6, ST_MULTIWRAP = 7,
+  ST_CHECK = 8,     // failed device bounds checks (PIC_CHECKED builds only)
+  ST_N = 9
 };
+constexpr int ST_PUBLIC = 8;   // counters returned by pic_sync
+
+// Device bounds checks of the checked build (-DPIC_CHECKED; tools/checked_run.sh):
+// every sub-array lives inside ONE workspace allocation, so an index past the
+// end of an array would silently hit its neighbour (no fault, and
+// compute-sanitizer's memcheck would not see it either).  The checked build
+// counts every violated index invariant in stats[ST_CHECK], which pic_sync turns
+// into PIC_ECUDA; the release build compiles the checks away.
+#ifdef PIC_CHECKED
+#define PIC_DCHECK(cond, stats)                                   \
+  do {                                                            \
+    if (!(cond)) atomicAdd(&(stats)[::pic::ST_CHECK], 1ull);      \
+  } while (0)
+#else
+#define PIC_DCHECK(cond, stats) \
+  do {                          \
+  } while (0)
+#endif
 
 // Grid sizing of the grid-stride kernels: multiples of the B200's 148 SMs
 // (the loops stay correct on any SM count).

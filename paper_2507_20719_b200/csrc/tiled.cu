@@ -93,6 +93,7 @@ struct MoverTArgs {
   int n_iter;
   int peer;                   // slab leavers go straight into the neighbours' buffers (peer.cu)
   PeerOut po;
+  int64_t cap;                // store capacity (bounds checks of the checked build)
 };
 
 struct DepositArgs {
@@ -102,6 +103,7 @@ struct DepositArgs {
   const uint32_t *cell_off;
   double *mom;                // ghosted moment arrays [10][m_plane]
   unsigned long long *stats;
+  int64_t cap;
 };
 
 // ------------------------------------------------------------- PTX helpers --
@@ -257,19 +259,14 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     const uint32_t q = wbeg + 32u * ri + lane;
     if (q < wend) {
       const uint32_t src_idx = pk[(ri % PK_SLOTS) * 64 + lane];
+      PIC_DCHECK(src_idx < A.cap, A.stats);
       double *d = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
 #pragma unroll
-#ifdef PIC_EXP_NO_QID
-      for (int k = 0; k < 6; ++k)
-#else
       for (int k = 0; k < 7; ++k)
-#endif
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
                      : "memory");
-#ifndef PIC_EXP_NO_QID
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 7 * 32)), "l"(A.src_id + src_idx)
                    : "memory");
-#endif
     }
   };
   for (int ri = 0; ri < PK_AHEAD; ++ri) fetch_pk(ri);
@@ -313,12 +310,11 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       double xnew[3], vnew[3];
       const bool clamped = push_eq2<NIT, REL>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew);
       knew = finish_particle(g, xnew, vnew, clamped, A.stats);
+      PIC_DCHECK(p < A.cap && (knew < g.ncells || knew >= KEY_FIRST_RESERVED), A.stats);
       A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
       A.dst[3][p] = vnew[0]; A.dst[4][p] = vnew[1]; A.dst[5][p] = vnew[2];
-#ifndef PIC_EXP_NO_QID
       A.dst[6][p] = qv;
       A.dst_id[p] = idv;
-#endif
       A.key_new[p] = knew;
     }
     // complete the previous round's rank, then start this round's (order.cu);
@@ -414,6 +410,7 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
     // cells of different warps share nodes, hence shared-memory atomics (one
     // flush per cell and warp: rare next to the per-particle work)
     const int node = ((c & 3) + (g8 & 1)) + MB * ((((c >> 2) & 3) + ((g8 >> 1) & 1)) + MB * ((c >> 4) + (g8 >> 2)));
+    PIC_DCHECK(c >= 0 && c < TILE3 && node < MB3, A.stats);
     double *dst = nacc + node * 10;
     atomicAdd(dst + 2 * j4, c0[0][0]);
     atomicAdd(dst + 2 * j4 + 1, c0[0][1]);
@@ -449,6 +446,7 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
     for (int k = 0; k < 7; ++k) s_cur[k] = s_nx[k];
     // advance the pipeline
     p_nx = p_n2;
+    PIC_DCHECK(p_nx < A.cap, A.stats);
 #pragma unroll
     for (int k = 0; k < 7; ++k) s_nx[k] = A.src[k][p_nx];
     p_n2 = (p + 64 < wend) ? A.perm[p + 64] : 0u;
@@ -608,6 +606,7 @@ pic_status launch_tiled_step(Ctx *ctx, int s) {
   A.n_iter = sp.n_iter;
   A.peer = ctx->peer;
   A.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
+  A.cap = sp.cap;
   const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap[ctx->field_cur]);
   const unsigned grid = (unsigned)ctx->geom.ntiles;
 #define PIC_LAUNCH(NIT)                                                                            \
@@ -652,6 +651,7 @@ pic_status launch_tiled_deposit(Ctx *ctx, int s) {
   A.cell_off = sp.cell_off;
   A.mom = sp.mom;
   A.stats = ctx->stats;
+  A.cap = sp.cap;
   deposit_tiled_kernel<<<(unsigned)ctx->geom.ntiles, DTHREADS, DEPOSIT_SMEM, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
