@@ -428,9 +428,22 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
     ctx->field_new = false;
     PIC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->field_ready[ctx->field_cur], 0));
   }
+  if (use_tiled(ctx)) {
+    // one launch for the species that share n_iter (species-major tiles)
+    for (int a = s0; a < s1;) {
+      int b = a + 1;
+      while (b < s1 && ctx->sp[b].n_iter == ctx->sp[a].n_iter) ++b;
+      st = launch_tiled_step(ctx, a, b);
+      if (st != PIC_OK) return st;
+      a = b;
+    }
+  } else {
+    for (int k = s0; k < s1; ++k) {
+      st = launch_mover_basic(ctx, k);
+      if (st != PIC_OK) return st;
+    }
+  }
   for (int k = s0; k < s1; ++k) {
-    st = use_tiled(ctx) ? launch_tiled_step(ctx, k) : launch_mover_basic(ctx, k);
-    if (st != PIC_OK) return st;
     ctx->sp[k].moved = true;
     ctx->sp[k].deposited = false;
   }
@@ -466,20 +479,19 @@ pic_status pic_moments(pic_ctx *p, int32_t s) {
   const int s0 = s < 0 ? 0 : s, s1 = s < 0 ? ctx->cfg.n_species : s + 1;
   for (int k = s0; k < s1; ++k)
     if (ctx->sp[k].deposited) return fail(ctx, PIC_ESTATE, "pic_moments called twice without pic_exchange");
-  for (int k = s0; k < s1; ++k) {
-    SpeciesStore &sp = ctx->sp[k];
-    {
-      PhaseTimer t(ctx, 2);
-      if (use_tiled(ctx)) {
-        st = launch_tiled_deposit(ctx, k);
-      } else {
+  {
+    PhaseTimer t(ctx, 2);
+    if (use_tiled(ctx)) {
+      st = launch_tiled_deposit(ctx, s0, s1);   // one launch, species-major tiles
+    } else {
+      for (int k = s0; k < s1 && st == PIC_OK; ++k) {
         st = zero_moments(ctx, k);
         if (st == PIC_OK) st = launch_moments_basic(ctx, k);
       }
     }
-    if (st != PIC_OK) return st;
-    sp.deposited = true;
   }
+  if (st != PIC_OK) return st;
+  for (int k = s0; k < s1; ++k) ctx->sp[k].deposited = true;
   return PIC_OK;
 }
 

@@ -284,8 +284,8 @@ inline pic_status fail(Ctx *ctx, pic_status s, const std::string &m) {
 // (implemented in the .cu files; all enqueue on ctx->stream)
 pic_status launch_mover_basic(Ctx *ctx, int s);
 pic_status launch_moments_basic(Ctx *ctx, int s);
-pic_status launch_tiled_deposit(Ctx *ctx, int s);
-pic_status launch_tiled_step(Ctx *ctx, int s);
+pic_status launch_tiled_deposit(Ctx *ctx, int s0, int s1);
+pic_status launch_tiled_step(Ctx *ctx, int s0, int s1);
 size_t order_temp_bytes(int64_t ncells);
 pic_status zero_cell_counts(Ctx *ctx, int s);
 pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to);

@@ -77,8 +77,10 @@ constexpr int NACC = PIC_DEP_NACC;               // independent MMA accumulator 
 constexpr int DWARPS = PIC_DEP_WARPS, DTHREADS = 32 * DWARPS;   // deposit CTA (one tile)
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (MB3 * 10 + DWARPS * WBUF);
 
-struct MoverTArgs {
-  Geom g;
+// Per-species arguments of the movers; one launch moves every species of
+// pic_mover (species-major blocks: blockIdx.x = s * ntiles + tile), so the
+// tail of one species' tiles overlaps the next species' first ones.
+struct MoverSp {
   const double *src[7];       // buffer A (read through perm)
   const int64_t *src_id;
   double *dst[7];             // buffer B (written in cell order)
@@ -87,23 +89,32 @@ struct MoverTArgs {
   const uint32_t *cell_off;   // tile t covers q in [cell_off[64 t], cell_off[64 (t+1)])
   uint32_t *key_new, *rank, *cell_count;
   int64_t *d_nraw;
-  const double *field;        // global window (fallback sampling)
-  unsigned long long *stats;
   double ks, ks_c;
-  int n_iter;
-  int peer;                   // slab leavers go straight into the neighbours' buffers (peer.cu)
   PeerOut po;
   int64_t cap;                // store capacity (bounds checks of the checked build)
 };
 
-struct DepositArgs {
+struct MoverTArgs {
   Geom g;
+  MoverSp sp[PIC_MAX_SPECIES];
+  const double *field;        // global window (fallback sampling)
+  unsigned long long *stats;
+  int n_iter;
+  int peer;                   // slab leavers go straight into the neighbours' buffers (peer.cu)
+};
+
+struct DepositSp {
   const double *src[7];       // particle state (buffer A after the mover)
   const uint32_t *perm;       // new order
   const uint32_t *cell_off;
   double *mom;                // ghosted moment arrays [10][m_plane]
-  unsigned long long *stats;
   int64_t cap;
+};
+
+struct DepositArgs {
+  Geom g;
+  DepositSp sp[PIC_MAX_SPECIES];
+  unsigned long long *stats;
 };
 
 // ------------------------------------------------------------- PTX helpers --
@@ -202,9 +213,11 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
   uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_base + MW * MOVER_WARP_STAGE);
   const Geom &g = A.g;
 
-  const int tile = blockIdx.x;
-  if (tile == 0 && threadIdx.x == 0) *A.d_nraw = A.cell_off[g.ncells];
-  const uint32_t p0 = A.cell_off[(int64_t)tile * TILE3], p1 = A.cell_off[(int64_t)(tile + 1) * TILE3];
+  const int sp_i = (int)(blockIdx.x / (unsigned)g.ntiles);
+  const int tile = (int)(blockIdx.x - (unsigned)sp_i * (unsigned)g.ntiles);
+  const MoverSp &S = A.sp[sp_i];
+  if (tile == 0 && threadIdx.x == 0) *S.d_nraw = S.cell_off[g.ncells];
+  const uint32_t p0 = S.cell_off[(int64_t)tile * TILE3], p1 = S.cell_off[(int64_t)(tile + 1) * TILE3];
   if (p0 == p1) return;
   const int tx = (int)(tile % g.nt[0]);
   const int ty = (int)((tile / g.nt[0]) % g.nt[1]);
@@ -227,7 +240,7 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
   }
   mbar_wait(mbar, 0);
   {
-    for (int i = tid; i < NB3 * 6; i += MT) fld[i] *= ((i % 6) < 3) ? A.ks : A.ks_c;
+    for (int i = tid; i < NB3 * 6; i += MT) fld[i] *= ((i % 6) < 3) ? S.ks : S.ks_c;
   }
   __syncthreads();
 
@@ -252,20 +265,20 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     const uint32_t q = wbeg + 32u * ri + lane;
     if (q < wend) {
       uint32_t *slot = pk + (ri % PK_SLOTS) * 64 + lane;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(A.perm + q) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot)), "l"(S.perm + q) : "memory");
     }
   };
   auto fetch_src = [&](int ri) {       // sources of round ri (its perm is already in the ring)
     const uint32_t q = wbeg + 32u * ri + lane;
     if (q < wend) {
       const uint32_t src_idx = pk[(ri % PK_SLOTS) * 64 + lane];
-      PIC_DCHECK(src_idx < A.cap, A.stats);
+      PIC_DCHECK(src_idx < S.cap, A.stats);
       double *d = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
 #pragma unroll
       for (int k = 0; k < 7; ++k)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(A.src[k] + src_idx)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(S.src[k] + src_idx)
                      : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 7 * 32)), "l"(A.src_id + src_idx)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 7 * 32)), "l"(S.src_id + src_idx)
                    : "memory");
     }
   };
@@ -305,32 +318,32 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       auto sample = [&](const double xb[3], double EB[6]) -> bool {
         const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
         if (gather_smem(fld, u, EB)) return false;
-        return WindowSampler{&g, A.field, A.ks, A.ks_c}(xb, EB);
+        return WindowSampler{&g, A.field, S.ks, S.ks_c}(xb, EB);
       };
       double xnew[3], vnew[3];
       const bool clamped = push_eq2<NIT, REL>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew);
       knew = finish_particle(g, xnew, vnew, clamped, A.stats);
-      PIC_DCHECK(p < A.cap && (knew < g.ncells || knew >= KEY_FIRST_RESERVED), A.stats);
-      A.dst[0][p] = xnew[0]; A.dst[1][p] = xnew[1]; A.dst[2][p] = xnew[2];
-      A.dst[3][p] = vnew[0]; A.dst[4][p] = vnew[1]; A.dst[5][p] = vnew[2];
-      A.dst[6][p] = qv;
-      A.dst_id[p] = idv;
-      A.key_new[p] = knew;
+      PIC_DCHECK(p < S.cap && (knew < g.ncells || knew >= KEY_FIRST_RESERVED), A.stats);
+      S.dst[0][p] = xnew[0]; S.dst[1][p] = xnew[1]; S.dst[2][p] = xnew[2];
+      S.dst[3][p] = vnew[0]; S.dst[4][p] = vnew[1]; S.dst[5][p] = vnew[2];
+      S.dst[6][p] = qv;
+      S.dst_id[p] = idv;
+      S.key_new[p] = knew;
     }
     // complete the previous round's rank, then start this round's (order.cu);
     // leavers and removed particles are not counted
     if (r0 != wbeg) {
       const uint32_t r = count_rank_finish(tk);
-      if (tk.counted) A.rank[pr_p] = r;
+      if (tk.counted) S.rank[pr_p] = r;
     }
-    tk = count_rank_issue(A.cell_count, g.ncells, knew, act && knew < KEY_FIRST_RESERVED, knew != kold);
+    tk = count_rank_issue(S.cell_count, g.ncells, knew, act && knew < KEY_FIRST_RESERVED, knew != kold);
     pr_p = p;
     if (A.peer && __any_sync(0xffffffffu, knew == KEY_LEFT || knew == KEY_RIGHT))
-      send_leavers_peer(A.po, knew, A.dst, A.dst_id, p, A.stats);
+      send_leavers_peer(S.po, knew, S.dst, S.dst_id, p, A.stats);
   }
   if (wbeg < wend) {
     const uint32_t r = count_rank_finish(tk);
-    if (tk.counted) A.rank[pr_p] = r;
+    if (tk.counted) S.rank[pr_p] = r;
   }
 }
 
@@ -346,8 +359,10 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
   double *nacc = reinterpret_cast<double *>(smem_raw);  // node sums of the tile box [MB^3][10]
   double *wbuf = nacc + MB3 * 10;
   const Geom &g = A.g;
-  const int tile = blockIdx.x;
-  const uint32_t *coff = A.cell_off + (int64_t)tile * TILE3;   // 65 offsets of this tile's cells
+  const int sp_i = (int)(blockIdx.x / (unsigned)g.ntiles);
+  const int tile = (int)(blockIdx.x - (unsigned)sp_i * (unsigned)g.ntiles);
+  const DepositSp &S = A.sp[sp_i];
+  const uint32_t *coff = S.cell_off + (int64_t)tile * TILE3;   // 65 offsets of this tile's cells
   const uint32_t p0 = coff[0], p1 = coff[TILE3];
   if (p0 == p1) return;
   const int tx = (int)(tile % g.nt[0]);
@@ -433,10 +448,10 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
   double s_nx[7];
   {
     const uint32_t p = wbeg + lane;
-    if (p < wend) p_nx = A.perm[p];
-    if (p + 32 < wend) p_n2 = A.perm[p + 32];
+    if (p < wend) p_nx = S.perm[p];
+    if (p + 32 < wend) p_n2 = S.perm[p + 32];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s_nx[k] = A.src[k][p_nx];
+    for (int k = 0; k < 7; ++k) s_nx[k] = S.src[k][p_nx];
   }
   for (uint32_t r0 = wbeg; r0 < wend; r0 += 32) {
     const uint32_t p = r0 + lane;
@@ -446,10 +461,10 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
     for (int k = 0; k < 7; ++k) s_cur[k] = s_nx[k];
     // advance the pipeline
     p_nx = p_n2;
-    PIC_DCHECK(p_nx < A.cap, A.stats);
+    PIC_DCHECK(p_nx < S.cap, A.stats);
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s_nx[k] = A.src[k][p_nx];
-    p_n2 = (p + 64 < wend) ? A.perm[p + 64] : 0u;
+    for (int k = 0; k < 7; ++k) s_nx[k] = S.src[k][p_nx];
+    p_n2 = (p + 64 < wend) ? S.perm[p + 64] : 0u;
     // inactive lanes carry zeros (q = 0: every value is 0, the weights finite)
     // the particle's cell in the tile, from its position (the order's cell:
     // keys are taken from positions; clamped to the tile, where a cell one off
@@ -539,7 +554,7 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
       if (m == 0) atomicAdd(&A.stats[ST_FAR], 1ull);
       continue;
     }
-    atomicAdd(A.mom + m * g.m_plane + node, v);
+    atomicAdd(S.mom + m * g.m_plane + node, v);
   }
 }
 
@@ -577,38 +592,43 @@ static pic_status make_tmap(Ctx *ctx) {
   return PIC_OK;
 }
 
-// pic_mover, tiled family: move through the current order into buffer B, rank
-// the new keys and swap buffers; pic_mover then migrates slab leavers
-// (multi-rank) and builds the next order (order.cu).
-pic_status launch_tiled_step(Ctx *ctx, int s) {
-  SpeciesStore &sp = ctx->sp[s];
+// pic_mover, tiled family: move species [s0, s1) (one launch, species-major
+// blocks) through the current order into buffer B, rank the new keys and swap
+// buffers; pic_mover then migrates slab leavers (multi-rank) and builds the
+// next order (order.cu).  The species of one launch share n_iter.
+pic_status launch_tiled_step(Ctx *ctx, int s0, int s1) {
   if (!ctx->tmap_ok) {
     pic_status st = make_tmap(ctx);
     if (st != PIC_OK) return st;
   }
-  pic_status st = zero_cell_counts(ctx, s);
-  if (st != PIC_OK) return st;
   MoverTArgs A;
   A.g = ctx->geom;
-  for (int k = 0; k < 7; ++k) { A.src[k] = sp.a[k]; A.dst[k] = sp.b[k]; }
-  A.src_id = sp.id;
-  A.dst_id = sp.id_b;
-  A.perm = sp.perm;
-  A.cell_off = sp.cell_off;
-  A.key_new = sp.key_new;
-  A.rank = sp.rank;
-  A.cell_count = sp.cell_count;
-  A.d_nraw = sp.d_nraw;
+  for (int s = s0; s < s1; ++s) {
+    SpeciesStore &sp = ctx->sp[s];
+    pic_status st = zero_cell_counts(ctx, s);
+    if (st != PIC_OK) return st;
+    MoverSp &S = A.sp[s - s0];
+    for (int k = 0; k < 7; ++k) { S.src[k] = sp.a[k]; S.dst[k] = sp.b[k]; }
+    S.src_id = sp.id;
+    S.dst_id = sp.id_b;
+    S.perm = sp.perm;
+    S.cell_off = sp.cell_off;
+    S.key_new = sp.key_new;
+    S.rank = sp.rank;
+    S.cell_count = sp.cell_count;
+    S.d_nraw = sp.d_nraw;
+    S.ks = sp.qom * (ctx->geom.dt * 0.5);
+    S.ks_c = S.ks / ctx->geom.c;
+    S.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
+    S.cap = sp.cap;
+    if (sp.n_iter != ctx->sp[s0].n_iter) return fail(ctx, PIC_EINVAL, "one mover launch needs one n_iter");
+  }
   A.field = ctx->field();
   A.stats = ctx->stats;
-  A.ks = sp.qom * (ctx->geom.dt * 0.5);
-  A.ks_c = A.ks / ctx->geom.c;
-  A.n_iter = sp.n_iter;
+  A.n_iter = ctx->sp[s0].n_iter;
   A.peer = ctx->peer;
-  A.po = ctx->peer ? peer_out(ctx, s) : PeerOut{};
-  A.cap = sp.cap;
   const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(ctx->tmap[ctx->field_cur]);
-  const unsigned grid = (unsigned)ctx->geom.ntiles;
+  const unsigned grid = (unsigned)(ctx->geom.ntiles * (s1 - s0));
 #define PIC_LAUNCH(NIT)                                                                            \
   do {                                                                                             \
     if (ctx->cfg.relativistic)                                                                     \
@@ -618,7 +638,7 @@ pic_status launch_tiled_step(Ctx *ctx, int s) {
   } while (0)
   {
     PhaseTimer t(ctx, 0);
-    switch (sp.n_iter) {
+    switch (A.n_iter) {
       case 1: PIC_LAUNCH(1); break;
       case 2: PIC_LAUNCH(2); break;
       case 3: PIC_LAUNCH(3); break;
@@ -629,30 +649,34 @@ pic_status launch_tiled_step(Ctx *ctx, int s) {
 #undef PIC_LAUNCH
   ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
-  sp.swap_buffers();
+  for (int s = s0; s < s1; ++s) ctx->sp[s].swap_buffers();
   return PIC_OK;
 }
 
-// pic_moments, tiled family: deposit over the new order (requires the order
-// built by pic_mover after migration, so arrivals are included and leavers are
-// deposited by their new owner only).
-pic_status launch_tiled_deposit(Ctx *ctx, int s) {
-  SpeciesStore &sp = ctx->sp[s];
+// pic_moments, tiled family: deposit species [s0, s1) (one launch) over the new
+// order (requires the order built by pic_mover after migration, so arrivals are
+// included and leavers are deposited by their new owner only).
+pic_status launch_tiled_deposit(Ctx *ctx, int s0, int s1) {
   if (!ctx->tmap_ok) {
     pic_status st = make_tmap(ctx);
     if (st != PIC_OK) return st;
   }
-  pic_status st = zero_moments(ctx, s);
-  if (st != PIC_OK) return st;
   DepositArgs A;
   A.g = ctx->geom;
-  for (int k = 0; k < 7; ++k) A.src[k] = sp.a[k];
-  A.perm = sp.perm;
-  A.cell_off = sp.cell_off;
-  A.mom = sp.mom;
+  for (int s = s0; s < s1; ++s) {
+    SpeciesStore &sp = ctx->sp[s];
+    pic_status st = zero_moments(ctx, s);
+    if (st != PIC_OK) return st;
+    DepositSp &S = A.sp[s - s0];
+    for (int k = 0; k < 7; ++k) S.src[k] = sp.a[k];
+    S.perm = sp.perm;
+    S.cell_off = sp.cell_off;
+    S.mom = sp.mom;
+    S.cap = sp.cap;
+  }
   A.stats = ctx->stats;
-  A.cap = sp.cap;
-  deposit_tiled_kernel<<<(unsigned)ctx->geom.ntiles, DTHREADS, DEPOSIT_SMEM, ctx->stream>>>(A); ++ctx->launches;
+  deposit_tiled_kernel<<<(unsigned)(ctx->geom.ntiles * (s1 - s0)), DTHREADS, DEPOSIT_SMEM, ctx->stream>>>(A);
+  ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }
