@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle CPU time")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1: time the step as pic_cycle replayed from CUDA graphs where libpic allows it "
+                         "(the per-kernel roofline then comes from a second, profiled pass of the same steps)")
     return ap.parse_args()
 
 
@@ -381,7 +384,9 @@ def main():
 
     w, desc = workload(args, world, rank)
     nccl_id = decomp.broadcast_nccl_id(pic.pic_nccl_id) if world > 1 else None
-    stream = torch.cuda.current_stream()
+    # the context runs on a stream of its own (CUDA-graph capture of whole
+    # cycles needs one); torch work is ordered against it by synchronisation
+    stream = torch.cuda.Stream()
     parts_cpu_sample = None
     want_sample = rank == 0 and world == 1 and not args.no_cpu_baseline
     if args.config in ("c3", "c4", "c5"):
@@ -402,6 +407,7 @@ def main():
         # drawn on the device sub-slab by sub-slab and appended (pic_add_particles):
         # no host copy of the store, transient memory of one sub-slab
         for a, b, parts in I.iter_species_chunks(w, 64_000_000, device="cuda"):
+            torch.cuda.synchronize()     # drawn on torch's stream, copied on libpic's
             for s, p in enumerate(parts):
                 ctx.add_particles(s, p)
             if want_sample and parts_cpu_sample is None:
@@ -410,6 +416,7 @@ def main():
         ctx.sync()
     else:
         parts = I.make_species(w, device="cuda")
+        torch.cuda.synchronize()         # drawn on torch's stream, copied on libpic's
         n_local = [p["x"].numel() for p in parts]
         face = w.ncell[1] * w.ncell[2]
         cap = [int(n * (1.35 if args.control else 1.08)) + 65536 + (4 * face * 64 if args.config == "c4s" else 0)
@@ -429,6 +436,7 @@ def main():
         del parts
     torch.cuda.empty_cache()
     lo, EB = I.field_window(w, args.ghost, device="cuda")
+    torch.cuda.synchronize()
     ctx.set_fields(EB)
 
     def barrier():
@@ -443,14 +451,17 @@ def main():
     ctx.sync()
     n_alive = sum(ctx.count(s) for s in range(len(w.species)))
 
-    # ---- timed region (device time, CUDA events on the context stream)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = ctx.launch_count()
-    ctx.profile(True)        # CUDA events around each phase, on the libpic stream
-    with ClockSampler(local) as clk:
+    # ---- timed region (device time, CUDA events on the context stream).  With
+    # --graph 1 the step is pic_cycle (replayed from CUDA graphs when libpic
+    # allows it: peer transport or one rank, no injection), timed alone; the
+    # per-phase kernel times (roofline, phase_ms) come from a second pass of the
+    # same number of steps with CUDA events around every phase (pic_profile,
+    # no graphs).  With --graph 0 one profiled pass gives both.
+    def profiled_pass():
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+               torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        ctx.profile(True)
         barrier()
-        clk.begin()
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
@@ -464,19 +475,43 @@ def main():
             e2.record(stream)
         end.record(stream)
         barrier()
-        clk.end()
-    launches = ctx.launch_count() - launches0
-    prof = ctx.profile_read()
-    ctx.profile(False)
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        return start.elapsed_time(end), prof, ([a.elapsed_time(b) for a, b, c in ev], [b.elapsed_time(c) for a, b, c in ev])
+
+    use_graph = bool(args.graph)
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        if use_graph:
+            ctx.set_graph(True)
+            ctx.cycle()            # capture (or plain fallback), untimed
+            ctx.cycle()
+            barrier()
+            clk.begin()
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            launches0 = ctx.launch_count()
+            start.record(stream)
+            for k in range(args.steps):
+                ctx.cycle()
+            end.record(stream)
+            barrier()
+            clk.end()
+            t_ms = start.elapsed_time(end)
+            launches = ctx.launch_count() - launches0
+            ctx.set_graph(False)
+            _, prof, (mover_ms, rest_ms) = profiled_pass()
+        else:
+            clk.begin()
+            t_ms, prof, (mover_ms, rest_ms) = profiled_pass()
+            clk.end()
+            launches = ctx.launch_count() - launches0
     kps = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
     kps_ranks = [kps]
     if world > 1:
         kps_ranks = [None] * world
         dist.all_gather_object(kps_ranks, kps)
     stats = ctx.sync()
-    t_ms = start.elapsed_time(end)
-    mover_ms = [a.elapsed_time(b) for a, b, c in ev]
-    rest_ms = [b.elapsed_time(c) for a, b, c in ev]
     tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
     tot = torch.tensor([float(n_alive)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -549,6 +584,10 @@ def main():
         shape = ctx.moment_shape()
         mom_h = [torch.empty((10, shape[2], shape[1], shape[0]), dtype=torch.float64).pin_memory()
                  for _ in range(n_sp)]
+        ctx.set_graph(use_graph)
+        for _ in range(4):       # untimed: capture the graphs of both field buffers x store parities
+            ctx.set_fields(EB_h)
+            ctx.cycle()
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -648,7 +687,10 @@ def main():
             "config": {"workload": desc, "particles_per_gpu": n_alive, "cells_per_gpu": [w.slab_or_all()[1] - w.slab_or_all()[0]] + list(w.ncell[1:]),
                        "kernel": ["auto", "basic", "tiled"][args.kernel], "transport": (["nccl", "peer"][int(ctx.peer)] if world > 1 else None),
                        "l2": "inputs (%.2f GB per GPU) exceed the 126 MB L2; no flush" % (n_alive * 64 / 1e9),
-                       "parallelism": f"x-slabs{world}"},
+                       "parallelism": f"x-slabs{world}",
+                       "step": ("pic_cycle, replayed from CUDA graphs where libpic allows (pic_set_graph); kernel "
+                                "times from a second, profiled pass" if use_graph else
+                                "pic_mover + pic_moments + pic_exchange, plain launches, profiled")},
             "roofline": roof,
             "roofline_fp64": roof64,
             "cpu_baseline": cpu,

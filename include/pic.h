@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define PIC_ABI_VERSION 4
+#define PIC_ABI_VERSION 5
 #define PIC_MAX_SPECIES 8
 #define PIC_NCCL_ID_BYTES 128
 #define PIC_N_MOMENTS 10  /* rho, Jx, Jy, Jz, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz (R16) */
@@ -127,6 +127,14 @@ typedef struct {
   int32_t relativistic;          /* 0: gamma == 1 limit of Eq. 2 (R3, the hot path);
                                     1: relativistic Eq. 2 with gamma (NEXT-1, R4-R6);
                                     |v| >= c is then a non-finite update (R23)    */
+  int32_t far_hops;              /* peer / loopback transports: extra forwarding
+                                    rounds per pic_mover for particles that cross
+                                    more than one slab in one step (R22); a
+                                    particle still not home after them is dropped
+                                    and counted as a far-flyer (PIC_ERANGE).  0
+                                    (default): one hop; each extra round costs a
+                                    barrier even when nothing is forwarded.
+                                    0 <= far_hops < nranks.                       */
 } pic_config;
 
 /* ABI version (PIC_ABI_VERSION).                                             */
@@ -234,6 +242,17 @@ PIC_API pic_status pic_exchange(pic_ctx *ctx);
 /* Shorthand for one full cycle: pic_mover(-1), pic_moments(-1),
  * pic_exchange.                                                              */
 PIC_API pic_status pic_cycle(pic_ctx *ctx);
+
+/* CUDA graphs for pic_cycle (enable != 0; default off): the first pic_cycle
+ * of each (field buffer, store buffer) combination is captured into a CUDA
+ * graph and later cycles replay it — one launch instead of ~20 kernel launches
+ * per cycle, for small per-GPU problems where launch gaps matter.  pic_cycle
+ * falls back to plain launches (same results) whenever a host decision sits
+ * inside the cycle: the NCCL or loopback transports, inflow injection,
+ * pic_profile enabled, a species between pic_mover and pic_exchange, or the
+ * legacy default stream as the context stream (capture needs its own stream).
+ * The separate pic_mover / pic_moments / pic_exchange calls never use graphs. */
+PIC_API pic_status pic_set_graph(pic_ctx *ctx, int32_t enable);
 
 /* Node counts of the moment output of this rank: out[0] = owned x-planes
  * (slab_hi - slab_lo, +1 on the last rank when x is open), out[1], out[2] =

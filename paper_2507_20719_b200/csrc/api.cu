@@ -57,6 +57,9 @@ pic_status validate(const pic_config *c, std::string *why) {
   if (c->transport < PIC_TRANSPORT_AUTO || c->transport > PIC_TRANSPORT_LOOPBACK) { *why = "bad transport"; return PIC_EINVAL; }
   if (c->kernel < 0 || c->kernel > 2) { *why = "bad kernel"; return PIC_EINVAL; }
   if (c->relativistic != 0 && c->relativistic != 1) { *why = "relativistic must be 0 or 1"; return PIC_EINVAL; }
+  if (c->far_hops < 0 || (c->far_hops > 0 && c->far_hops >= c->nranks)) {
+    *why = "far_hops must be in [0, nranks)"; return PIC_EINVAL;
+  }
   return PIC_OK;
 }
 
@@ -77,6 +80,7 @@ void make_geom(const pic_config *c, Geom *g) {
   g->slab_hi = c->slab_hi;
   g->G = c->ghost;
   g->multi_rank = c->nranks > 1;
+  g->far_hops = c->far_hops;
   const int64_t G = c->ghost;
   g->f_lo[0] = c->slab_lo - G; g->f_lo[1] = -G; g->f_lo[2] = -G;
   g->f_n[0] = c->slab_hi - c->slab_lo + 1 + 2 * G;
@@ -172,6 +176,12 @@ int64_t plan(const pic_config *c, const Geom &g, Ctx *ctx, char *base, size_t cu
     ctx->mig_recv[0] = (double *)(base + om[2]);
     ctx->mig_recv[1] = (double *)(base + om[3]);
     ctx->mig_cap = mig_cap;
+    // the peer transports never use the send buffers: they hold the forwarded
+    // far-flyers, [hop parity] halves of mig_send[from side]
+    ctx->fwd_cap = mig_cap / 2;
+    for (int par = 0; par < 2; ++par)
+      for (int side = 0; side < 2; ++side)
+        ctx->fwd_recv[par][side] = ctx->mig_send[side] + (int64_t)par * MIG_REC * (mig_cap / 2) * c->n_species;
     ctx->pack = (double *)(base + opack);
     ctx->src_buf = (double *)(base + osrc);
     ctx->gmm_buf = (double *)(base + ogmm);
@@ -453,8 +463,12 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
     st = inject(ctx, k);
     if (st != PIC_OK) return st;
   }
-  // the field buffer may be refilled once these movers are done
-  PIC_CUDA(cudaEventRecord(ctx->field_free[ctx->field_cur], ctx->stream));
+  // the field buffer may be refilled once these movers are done (a cycle being
+  // captured into a graph records this after the graph launch instead)
+  cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+  PIC_CUDA(cudaStreamIsCapturing(ctx->stream, &cap_st));
+  if (cap_st == cudaStreamCaptureStatusNone)
+    PIC_CUDA(cudaEventRecord(ctx->field_free[ctx->field_cur], ctx->stream));
   // slab leavers go to their neighbour right after the mover (Alg. 1: the
   // particle communication follows the push), every species in one NCCL group
   // per message; the receiver deposits them like its own particles
@@ -511,12 +525,95 @@ pic_status pic_exchange(pic_ctx *p) {
   return PIC_OK;
 }
 
-pic_status pic_cycle(pic_ctx *p) {
+static pic_status cycle_plain(pic_ctx *p) {
   pic_status st = pic_mover(p, -1);
   if (st != PIC_OK) return st;
   st = pic_moments(p, -1);
   if (st != PIC_OK) return st;
   return pic_exchange(p);
+}
+
+// A cycle can be replayed from a CUDA graph when every kernel argument is fixed
+// by (field buffer, store buffer parity) and no host decision sits inside it:
+// one rank or the peer transport (the NCCL transport learns the migration
+// counts on the host; the loopback barrier is a host handshake), no inflow
+// injection (its draws are keyed by the host's cycle counter), no profiling
+// events, and every species in one state.
+static bool graph_ok(const Ctx *ctx) {
+  if (ctx->prof_on) return false;
+  // stream capture needs a stream of its own (not the legacy default stream)
+  if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy || ctx->stream == cudaStreamPerThread) return false;
+  if (ctx->cfg.nranks > 1 && (!ctx->peer || ctx->loop)) return false;
+  for (int s = 0; s < ctx->cfg.n_species; ++s) {
+    const SpeciesStore &sp = ctx->sp[s];
+    if (ctx->inj[s].ppc > 0 || sp.moved || sp.deposited || !sp.order_valid) return false;
+  }
+  return ctx->fields_set;
+}
+
+static pic_status cycle_graph(pic_ctx *p) {
+  Ctx *ctx = C(p);
+  if (ctx->field_new) {            // as pic_mover: switch to the freshly copied field buffer
+    ctx->field_cur ^= 1;
+    ctx->field_new = false;
+    PIC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->field_ready[ctx->field_cur], 0));
+  }
+  Ctx::CycleGraph *G = nullptr;
+  for (auto &g : ctx->graphs)
+    if (g.exec && g.field_cur == ctx->field_cur && g.a0 == ctx->sp[0].a[0]) G = &g;
+  if (G) {
+    PIC_CUDA(cudaGraphLaunch((cudaGraphExec_t)G->exec, ctx->stream));
+    PIC_CUDA(cudaEventRecord(ctx->field_free[ctx->field_cur], ctx->stream));
+    // the host-side effects of the replayed cycle
+    for (int s = 0; s < ctx->cfg.n_species; ++s) ctx->sp[s].swap_buffers();
+    ctx->launches += G->launches;
+    ctx->cycle++;
+    return PIC_OK;
+  }
+  for (auto &g : ctx->graphs)
+    if (!g.exec) G = &g;
+  if (!G) return cycle_plain(p);   // (cannot happen: at most 2 x 2 keys)
+  // grid sizes of the grid-stride kernels from the capacity (the host's
+  // running upper bound of the store is not advanced by replays)
+  for (int s = 0; s < ctx->cfg.n_species; ++s) ctx->sp[s].n_raw = ctx->sp[s].cap;
+  const int field_cur = ctx->field_cur;
+  const double *a0 = ctx->sp[0].a[0];
+  const int64_t l0 = ctx->launches;
+  PIC_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  pic_status st = cycle_plain(p);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (st != PIC_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  G->exec = exec;
+  G->field_cur = field_cur;
+  G->a0 = a0;
+  G->launches = ctx->launches - l0;
+  // the capture enqueued nothing: run the captured cycle (host state already advanced)
+  PIC_CUDA(cudaGraphLaunch(exec, ctx->stream));
+  PIC_CUDA(cudaEventRecord(ctx->field_free[field_cur], ctx->stream));
+  return PIC_OK;
+}
+
+pic_status pic_cycle(pic_ctx *p) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  if (ctx->graph_on && graph_ok(ctx)) return cycle_graph(p);
+  return cycle_plain(p);
+}
+
+pic_status pic_set_graph(pic_ctx *p, int32_t enable) {
+  if (!p) return PIC_EINVAL;
+  Ctx *ctx = C(p);
+  ctx->graph_on = enable != 0;
+  return PIC_OK;
 }
 
 pic_status pic_moment_shape(const pic_ctx *p, int64_t out[3]) {
@@ -713,6 +810,8 @@ pic_status pic_destroy(pic_ctx *p) {
   }
   if (ctx->copies_done) cudaEventDestroy(ctx->copies_done);
   if (ctx->fields_done) cudaEventDestroy(ctx->fields_done);
+  for (auto &g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy((cudaGraphExec_t)g.exec);
   peer_close(ctx);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
   for (auto &v : ctx->prof_ev)

@@ -61,6 +61,8 @@ struct PeerDesc {
   int64_t ghost_x;             // array x index of node slab_hi (the plane the right neighbour pulls)
   int64_t src_off;             // NEXT-2 sources buffer (J-hat at 9 x owned nodes)
   int64_t owned_nx;            // owned x node planes (pic_moment_shape x)
+  int64_t fwd_off[2][2];       // forwarded far-flyers: [hop parity][from side]
+  int64_t fwd_cap;
 };
 
 static unsigned grid_for(int64_t total) {
@@ -91,6 +93,9 @@ static PeerDesc describe(Ctx *ctx, char *b) {
   int64_t shape[3];
   pic_moment_shape((const pic_ctx *)ctx, shape);
   d.owned_nx = shape[0];
+  for (int par = 0; par < 2; ++par)
+    for (int side = 0; side < 2; ++side) d.fwd_off[par][side] = reinterpret_cast<char *>(ctx->fwd_recv[par][side]) - b;
+  d.fwd_cap = ctx->fwd_cap;
   return d;
 }
 
@@ -113,6 +118,11 @@ static void fill_link(Ctx *ctx, int side, char *mapped, const PeerDesc &d, bool 
   L.ghost_x = d.ghost_x;
   L.src = reinterpret_cast<double *>(mapped + d.src_off);
   L.owned_nx = d.owned_nx;
+  for (int par = 0; par < 2; ++par) {
+    L.fcnt[par] = &pc->fcnt[par][from][0];
+    L.frecv[par] = reinterpret_cast<double *>(mapped + d.fwd_off[par][from]);
+  }
+  L.fwd_cap = d.fwd_cap;
 }
 
 pic_status peer_setup(Ctx *ctx) {
@@ -342,9 +352,13 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// The epoch lives in device memory (PeerCtl::epoch, advanced by this kernel
+// only): every rank runs the same sequence of barriers, and a barrier captured
+// in a CUDA graph (pic_set_graph) advances it on every replay.
 __global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long long *left_flag,
-                                    unsigned long long *right_flag, unsigned long long epoch,
+                                    unsigned long long *right_flag, unsigned long long *own_epoch,
                                     unsigned long long *err) {
+  const unsigned long long epoch = ++*own_epoch;
   __threadfence_system();
   if (left_flag) st_release_sys(left_flag, epoch);
   if (right_flag) st_release_sys(right_flag, epoch);
@@ -361,9 +375,8 @@ __global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long 
 
 pic_status peer_barrier(Ctx *ctx) {
   if (ctx->loop) return loopback_barrier(ctx);
-  ++ctx->peer_epoch;
   peer_barrier_kernel<<<1, 1, 0, ctx->stream>>>(ctx->peer_ctl->flag, ctx->link[0].flag, ctx->link[1].flag,
-                                                ctx->peer_epoch, &ctx->peer_ctl->err); ++ctx->launches;
+                                                &ctx->peer_ctl->epoch, &ctx->peer_ctl->err); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }
@@ -376,40 +389,56 @@ struct ArriveArgs {
   uint32_t *key_new[PIC_MAX_SPECIES], *rank[PIC_MAX_SPECIES], *cell_count[PIC_MAX_SPECIES];
   int64_t *d_nraw[PIC_MAX_SPECIES];
   int64_t cap[PIC_MAX_SPECIES];
-  const double *recv[2];           // own receive records, [from][species][MIG_REC * mig_cap]
-  int64_t mig_cap;
-  PeerCtl *ctl;
+  const double *recv[2];           // own receive records, [from][species][MIG_REC * rcap]
+  int64_t rcap;
+  unsigned long long *rcnt[2];     // their counts, [from][species]
+  // far-flyers not owned here go on (hop < far_hops) into the neighbour's
+  // forward region of this hop's parity; after the last hop they are dropped
+  int forward;
+  double *fwd[2];                  // neighbour's region from me, [side][species][MIG_REC * fcap]
+  unsigned long long *fcnt[2];     // its counts, [side][species]
+  int64_t fcap;
   unsigned long long *stats;
   int s0;
 };
 
 // blockIdx.y = species - s0.  Arrival i < n_from_left comes from the left
 // buffer, the rest from the right one; appended at d_nraw + i and ranked into
-// the cell counts as an arrival (order.cu).
+// the cell counts as an arrival (order.cu).  Records whose position is not in
+// this slab (they crossed more than one slab) are forwarded in their direction
+// or counted as far-flyers (R22).
 __global__ void arrive_kernel(const ArriveArgs A) {
   const int s = A.s0 + blockIdx.y;
-  const int64_t c0 = min((int64_t)A.ctl->cnt[0][s], A.mig_cap), c1 = min((int64_t)A.ctl->cnt[1][s], A.mig_cap);
+  const int64_t c0 = min((int64_t)A.rcnt[0][s], A.rcap), c1 = min((int64_t)A.rcnt[1][s], A.rcap);
   const int64_t n = c0 + c1, base = *A.d_nraw[s];
   const Geom &g = A.g;
+  const unsigned lane = threadIdx.x & 31u;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < n; w0 += stride) {
     const int64_t i = w0 + threadIdx.x;
     uint32_t k = KEY_DEAD;
     const int64_t at = base + i;
     const bool act = i < n;
+    int fwd_side = -1;
+    double v[7];
+    int64_t idv = 0;
     if (act) {
-      const double *rec = i < c0 ? A.recv[0] + ((int64_t)s * A.mig_cap + i) * MIG_REC
-                                 : A.recv[1] + ((int64_t)s * A.mig_cap + (i - c0)) * MIG_REC;
-      double v[7];
+      const double *rec = i < c0 ? A.recv[0] + ((int64_t)s * A.rcap + i) * MIG_REC
+                                 : A.recv[1] + ((int64_t)s * A.rcap + (i - c0)) * MIG_REC;
 #pragma unroll
       for (int c = 0; c < 7; ++c) v[c] = rec[c];
-      const int64_t idv = __double_as_longlong(rec[7]);
+      idv = __double_as_longlong(rec[7]);
       const int64_t cx = (int64_t)floor(v[0]), cy = (int64_t)floor(v[1]), cz = (int64_t)floor(v[2]);
+      const bool mine = cx >= g.slab_lo && cx < g.slab_hi && cy >= 0 && cy < g.ncell[1] && cz >= 0 && cz < g.ncell[2];
       if (at >= A.cap[s]) {
         atomicAdd(&A.stats[ST_OVERFLOW], 1ull);
       } else {
-        if (cx >= g.slab_lo && cx < g.slab_hi && cy >= 0 && cy < g.ncell[1] && cz >= 0 && cz < g.ncell[2]) {
+        if (mine) {
           k = tile_key(g, cx - g.slab_lo, cy, cz);
+        } else if (A.forward && A.fwd[i < c0 ? 1 : 0]) {
+          // onward in the direction of motion: a record from the left neighbour
+          // moves right (and vice versa), also across the periodic seam
+          fwd_side = i < c0 ? 1 : 0;
         } else {
           atomicAdd(&A.stats[ST_FAR], 1ull);
         }
@@ -419,7 +448,31 @@ __global__ void arrive_kernel(const ArriveArgs A) {
         A.key_new[s][at] = k;
       }
     }
+    // forwarding: one remote atomic per warp and side reserves the slots
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const unsigned mask = __ballot_sync(0xffffffffu, fwd_side == side);
+      if (!mask) continue;
+      const int leader = __ffs(mask) - 1;
+      unsigned long long slot0 = 0;
+      if ((int)lane == leader) slot0 = atomicAdd(A.fcnt[side] + s, (unsigned long long)__popc(mask));
+      slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+      if (fwd_side == side) {
+        const int64_t slot = (int64_t)slot0 + __popc(mask & ((1u << lane) - 1u));
+        if (slot < A.fcap) {
+          double *rec = A.fwd[side] + ((int64_t)s * A.fcap + slot) * MIG_REC;
+#pragma unroll
+          for (int c = 0; c < 7; ++c) rec[c] = v[c];
+          rec[7] = __longlong_as_double(idv);
+          __threadfence_system();
+        } else {
+          atomicAdd(&A.stats[ST_OVERFLOW], 1ull);
+        }
+      }
+    }
     const bool counted = act && k < KEY_FIRST_RESERVED;
+    const unsigned nrecv = __popc(__ballot_sync(0xffffffffu, counted));
+    if (lane == 0 && nrecv) atomicAdd(&A.stats[ST_RECEIVED], (unsigned long long)nrecv);
     const uint32_t r = count_rank(A.cell_count[s], g.ncells, k, counted, true);
     if (counted) A.rank[s][at] = r;
   }
@@ -428,46 +481,67 @@ __global__ void arrive_kernel(const ArriveArgs A) {
 __global__ void arrive_finish_kernel(const ArriveArgs A, int S) {
   const int s = A.s0 + threadIdx.x;
   if (threadIdx.x >= S) return;
-  const int64_t c0 = min((int64_t)A.ctl->cnt[0][s], A.mig_cap), c1 = min((int64_t)A.ctl->cnt[1][s], A.mig_cap);
+  const int64_t c0 = min((int64_t)A.rcnt[0][s], A.rcap), c1 = min((int64_t)A.rcnt[1][s], A.rcap);
   const int64_t n = c0 + c1;
   *A.d_nraw[s] = min(*A.d_nraw[s] + n, A.cap[s]);
-  atomicAdd(&A.stats[ST_RECEIVED], (unsigned long long)n);
-  A.ctl->cnt[0][s] = 0;
-  A.ctl->cnt[1][s] = 0;
+  A.rcnt[0][s] = 0;
+  A.rcnt[1][s] = 0;
 }
 
-// After the movers of species [s0, s1): barrier, append + rank the arrivals.
+// After the movers of species [s0, s1): barrier, append + rank the arrivals;
+// with far_hops > 0 as many more rounds (barrier, then the forwarded records)
+// for particles that crossed more than one slab.
 pic_status peer_migrate(Ctx *ctx, int s0, int s1) {
-  {
-    PhaseTimer t(ctx, 4);
-    pic_status st = peer_barrier(ctx);
-    if (st != PIC_OK) return st;
+  const int hops = ctx->cfg.far_hops;
+  for (int hop = 0; hop <= hops; ++hop) {
+    {
+      PhaseTimer t(ctx, 4);
+      pic_status st = peer_barrier(ctx);
+      if (st != PIC_OK) return st;
+    }
+    PhaseTimer t(ctx, 5);
+    ArriveArgs A;
+    A.g = ctx->geom;
+    for (int s = s0; s < s1; ++s) {
+      SpeciesStore &sp = ctx->sp[s];
+      for (int k = 0; k < 7; ++k) A.a[s][k] = sp.a[k];
+      A.id[s] = sp.id;
+      A.key_new[s] = sp.key_new;
+      A.rank[s] = sp.rank;
+      A.cell_count[s] = sp.cell_count;
+      A.d_nraw[s] = sp.d_nraw;
+      A.cap[s] = sp.cap;
+      // the host no longer knows the live count exactly: keep an upper bound for grid sizes
+      sp.n_raw = std::min<int64_t>(sp.cap, sp.n_raw + 2 * (hop == 0 ? ctx->mig_cap : ctx->fwd_cap));
+    }
+    if (hop == 0) {
+      A.recv[0] = ctx->mig_recv[0];
+      A.recv[1] = ctx->mig_recv[1];
+      A.rcap = ctx->mig_cap;
+      A.rcnt[0] = ctx->peer_ctl->cnt[0];
+      A.rcnt[1] = ctx->peer_ctl->cnt[1];
+    } else {
+      const int par = (hop - 1) & 1;
+      A.recv[0] = ctx->fwd_recv[par][0];
+      A.recv[1] = ctx->fwd_recv[par][1];
+      A.rcap = ctx->fwd_cap;
+      A.rcnt[0] = ctx->peer_ctl->fcnt[par][0];
+      A.rcnt[1] = ctx->peer_ctl->fcnt[par][1];
+    }
+    A.forward = hop < hops;
+    for (int side = 0; side < 2; ++side) {
+      const Ctx::PeerLink &L = ctx->link[side];
+      A.fwd[side] = (A.forward && L.mapped) ? L.frecv[hop & 1] : nullptr;
+      A.fcnt[side] = (A.forward && L.mapped) ? L.fcnt[hop & 1] : nullptr;
+    }
+    A.fcap = ctx->fwd_cap;
+    A.stats = ctx->stats;
+    A.s0 = s0;
+    dim3 grid(kSMs, s1 - s0);
+    arrive_kernel<<<grid, 256, 0, ctx->stream>>>(A); ++ctx->launches;
+    arrive_finish_kernel<<<1, 32, 0, ctx->stream>>>(A, s1 - s0); ++ctx->launches;
+    PIC_CUDA(cudaGetLastError());
   }
-  PhaseTimer t(ctx, 5);
-  ArriveArgs A;
-  A.g = ctx->geom;
-  for (int s = s0; s < s1; ++s) {
-    SpeciesStore &sp = ctx->sp[s];
-    for (int k = 0; k < 7; ++k) A.a[s][k] = sp.a[k];
-    A.id[s] = sp.id;
-    A.key_new[s] = sp.key_new;
-    A.rank[s] = sp.rank;
-    A.cell_count[s] = sp.cell_count;
-    A.d_nraw[s] = sp.d_nraw;
-    A.cap[s] = sp.cap;
-    // the host no longer knows the live count exactly: keep an upper bound for grid sizes
-    sp.n_raw = std::min<int64_t>(sp.cap, sp.n_raw + 2 * ctx->mig_cap);
-  }
-  A.recv[0] = ctx->mig_recv[0];
-  A.recv[1] = ctx->mig_recv[1];
-  A.mig_cap = ctx->mig_cap;
-  A.ctl = ctx->peer_ctl;
-  A.stats = ctx->stats;
-  A.s0 = s0;
-  dim3 grid(kSMs, s1 - s0);
-  arrive_kernel<<<grid, 256, 0, ctx->stream>>>(A); ++ctx->launches;
-  arrive_finish_kernel<<<1, 32, 0, ctx->stream>>>(A, s1 - s0); ++ctx->launches;
-  PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }
 

@@ -71,8 +71,10 @@ constexpr int MIG_REC = 8;
 struct PeerCtl {
   unsigned long long flag[2];      // barrier epochs: [0] from the left neighbour, [1] from the right
   unsigned long long err;          // barrier timeouts
-  unsigned long long pad;
+  unsigned long long epoch;        // own barrier epoch (advanced by the own barrier kernel only)
   unsigned long long cnt[2][PIC_MAX_SPECIES];   // arrivals reserved by [0] left / [1] right neighbour
+  // forwarded far-flyers (R22, far_hops > 0): [hop parity][from side][species]
+  unsigned long long fcnt[2][2][PIC_MAX_SPECIES];
 };
 
 // What a sender needs to write one species' leavers into its neighbours'
@@ -96,6 +98,7 @@ struct Geom {
   int64_t slab_lo, slab_hi;
   int32_t G;
   int32_t multi_rank;     // nranks > 1 (slab leavers migrate)
+  int32_t far_hops;       // forwarding rounds for far-flyers (peer / loopback transports)
   // field window
   int64_t f_lo[3];        // global node index of window element 0
   int64_t f_n[3];         // window nodes per axis
@@ -212,11 +215,25 @@ struct Ctx {
     int64_t m_plane = 0, m_nx = 0, ghost_x = 0;
     double *src = nullptr;           // its NEXT-2 sources buffer
     int64_t owned_nx = 0;
+    unsigned long long *fcnt[2] = {};  // my forward slots in its PeerCtl, per hop parity
+    double *frecv[2] = {};           // its forward records from me, per hop parity
+    int64_t fwd_cap = 0;
   } link[2];                         // [0] left, [1] right
+  double *fwd_recv[2][2] = {};       // own forward regions [hop parity][from side] (in mig_send)
+  int64_t fwd_cap = 0;               // records per region and species
   bool peer = false;
   Ctx *loop_nb[2] = {};              // loopback transport: the neighbour contexts (same process)
   struct LoopGroup *loop = nullptr;  // loopback transport: shared host-side barrier state (peer.cu)
-  unsigned long long peer_epoch = 0;
+  unsigned long long peer_epoch = 0;   // loopback transport: host-side barrier epochs
+  // CUDA graphs of whole cycles (pic_set_graph): one per (field buffer, store
+  // buffer parity), since the kernels' arguments differ only in those
+  bool graph_on = false;
+  struct CycleGraph {
+    void *exec = nullptr;            // cudaGraphExec_t
+    int field_cur = -1;
+    const double *a0 = nullptr;      // species 0 buffer A at capture
+    int64_t launches = 0;
+  } graphs[4];
   InjectParams inj[PIC_MAX_SPECIES];
   void *cub_temp = nullptr;
   size_t cub_bytes = 0;
@@ -431,10 +448,10 @@ __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3
     k = KEY_DEAD;
   } else if (g.multi_rank && x_pre < (double)g.slab_lo) {
     k = KEY_LEFT;
-    if (x_pre < (double)(g.slab_lo - g.G)) atomicAdd(&stats[ST_FAR], 1ull);
+    if (g.far_hops == 0 && x_pre < (double)(g.slab_lo - g.G)) atomicAdd(&stats[ST_FAR], 1ull);
   } else if (g.multi_rank && x_pre >= (double)g.slab_hi) {
     k = KEY_RIGHT;
-    if (x_pre >= (double)(g.slab_hi + g.G)) atomicAdd(&stats[ST_FAR], 1ull);
+    if (g.far_hops == 0 && x_pre >= (double)(g.slab_hi + g.G)) atomicAdd(&stats[ST_FAR], 1ull);
   } else {
     const int cx = (int)xnew[0], cy = (int)xnew[1], cz = (int)xnew[2];
     k = tile_key32(g, (uint32_t)(cx - (int)g.slab_lo), (uint32_t)cy, (uint32_t)cz);

@@ -542,8 +542,10 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
   if (cur >= 0) flush(cur);
   __syncthreads();
 
-  // node sums of the tile -> global moments (tile faces are shared with
-  // neighbour tiles: atomics); one (node, moment) pair per thread
+  // node sums of the tile -> global moments; one (node, moment) pair per
+  // thread.  Nodes on the tile's faces are shared with neighbour tiles
+  // (atomics); the 3^3 interior nodes belong to this tile's cells only, so a
+  // plain store into the zeroed array suffices.
   for (int i = tid; i < MB3 * 10; i += DTHREADS) {
     const int n = i / 10, m = i - 10 * n;
     const int bx = n % MB, by = (n / MB) % MB, bz = n / (MB * MB);
@@ -554,7 +556,11 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
       if (m == 0) atomicAdd(&A.stats[ST_FAR], 1ull);
       continue;
     }
-    atomicAdd(S.mom + m * g.m_plane + node, v);
+    const bool interior = bx > 0 && bx < TILE && by > 0 && by < TILE && bz > 0 && bz < TILE;
+    if (interior)
+      S.mom[m * g.m_plane + node] = v;
+    else
+      atomicAdd(S.mom + m * g.m_plane + node, v);
   }
 }
 

@@ -32,7 +32,7 @@ TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_PEER, TRANSPORT_LOOPBACK = 0, 1, 2, 3
 STAT_NAMES = ["removed", "sent", "received", "far", "clamped", "nonfinite", "overflow", "multiwrap"]
 EXPORTS = ["pic_abi_version", "pic_nccl_id", "pic_workspace_bytes", "pic_init", "pic_loopback_link", "pic_set_stream",
            "pic_set_particles", "pic_add_particles", "pic_count", "pic_get_particles", "pic_set_fields", "pic_mover",
-           "pic_moments", "pic_exchange", "pic_cycle", "pic_moment_shape", "pic_get_moments",
+           "pic_moments", "pic_exchange", "pic_cycle", "pic_set_graph", "pic_moment_shape", "pic_get_moments",
            "pic_sync", "pic_get_moments_async", "pic_join_copies", "pic_implicit_sources", "pic_set_injection", "pic_control", "pic_gmm", "pic_moment_ptr", "pic_get_transport", "pic_launch_count", "pic_profile", "pic_profile_read", "pic_last_error", "pic_destroy"]
 
 
@@ -45,6 +45,7 @@ class pic_config(C.Structure):
         ("planet_center", C.c_double * 3), ("planet_radius", C.c_double),
         ("rank", C.c_int32), ("nranks", C.c_int32), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64),
         ("ghost", C.c_int32), ("transport", C.c_int32), ("kernel", C.c_int32), ("relativistic", C.c_int32),
+        ("far_hops", C.c_int32),
     ]
 
 
@@ -81,6 +82,7 @@ def load_library(path: str = LIB_PATH):
         lib.pic_moments.argtypes = [vp, C.c_int32]
         lib.pic_exchange.argtypes = [vp]
         lib.pic_cycle.argtypes = [vp]
+        lib.pic_set_graph.argtypes = [vp, C.c_int32]
         lib.pic_moment_shape.argtypes = [vp, P(C.c_int64)]
         lib.pic_get_moments.argtypes = [vp, C.c_int32, vp]
         lib.pic_sync.argtypes = [vp, P(C.c_int64)]
@@ -135,7 +137,7 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSPORT_AUTO, kernel=KERNEL_AUTO,
-                n_iter=None, relativistic=None) -> pic_config:
+                n_iter=None, relativistic=None, far_hops=0) -> pic_config:
     """pic_config from an inputs.Workload (marshalling only)."""
     cfg = pic_config()
     lo, hi = w.slab_or_all()
@@ -153,6 +155,7 @@ def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSP
     cfg.rank, cfg.nranks, cfg.slab_lo, cfg.slab_hi = rank, nranks, lo, hi
     cfg.ghost, cfg.transport, cfg.kernel = ghost, transport, kernel
     cfg.relativistic = int(bool(getattr(w, "relativistic", False) if relativistic is None else relativistic))
+    cfg.far_hops = int(far_hops)
     return cfg
 
 
@@ -239,6 +242,10 @@ class Context:
 
     def cycle(self):
         _check(self.lib.pic_cycle(self.h), self.h, "pic_cycle")
+
+    def set_graph(self, enable: bool = True):
+        """pic_set_graph: replay whole cycles from CUDA graphs where possible."""
+        _check(self.lib.pic_set_graph(self.h, 1 if enable else 0), self.h, "pic_set_graph")
 
     def moment_shape(self):
         out = (C.c_int64 * 3)()

@@ -25,7 +25,7 @@ import slab_parity as SP  # noqa: E402
 from paper_2507_20719_b200 import decomp, inputs as I, pic  # noqa: E402
 
 
-def run_case(name, w, cycles, kernel, transport, rank, world, inject=None, orc_cache=None):
+def run_case(name, w, cycles, kernel, transport, rank, world, inject=None, orc_cache=None, graph=False):
     bounds = decomp.uniform_bounds(w.ncell[0], world)
     lo, hi = bounds[rank], bounds[rank + 1]
     parts_all, per_rank = SP.split_inputs(w, bounds)
@@ -34,14 +34,18 @@ def run_case(name, w, cycles, kernel, transport, rank, world, inject=None, orc_c
     nid = decomp.broadcast_nccl_id(pic.pic_nccl_id)
     cfg = pic.make_config(wr, rank=rank, nranks=world, capacity=SP.capacity(parts_all), ghost=2, kernel=kernel,
                           transport=transport)
-    ctx = pic.Context(cfg, nccl_id=nid)
+    ctx = pic.Context(cfg, nccl_id=nid, stream=torch.cuda.Stream() if graph else None)
+    ctx.set_graph(graph)
     assert ctx.transport == transport
+    mine = [{k: v.cuda() for k, v in p.items()} for p in mine]
+    torch.cuda.synchronize()          # torch's copies before libpic's stream reads them
     for s, p in enumerate(mine):
-        ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+        ctx.set_particles(s, p)
         if inject:
             ctx.set_injection(s, inject["ppc"], w.species[s].vth, inject["drift"], float(parts_all[s]["q"][0]),
                               500 + s)
     _, EB = I.field_window(wr, 2, device="cpu")
+    torch.cuda.synchronize()
     ctx.set_fields(EB.cuda())
     torch.cuda.synchronize()
     dist.barrier()           # every rank is set up before the first collective cycle
@@ -95,6 +99,17 @@ def main():
                     ok, reps = res
                     all_ok &= ok
                     reports += reps
+    # whole cycles replayed from CUDA graphs over the peer transport (device-side
+    # barrier epochs advance on every replay)
+    for name, w, cyc, *inj in cases[:2]:
+        res = run_case(name, w, cyc + 2, pic.KERNEL_TILED, pic.TRANSPORT_PEER, rank, world, orc_cache=orc_cache,
+                       graph=True)
+        if rank == 0:
+            ok, reps = res
+            for r in reps:
+                r["graph"] = True
+            all_ok &= ok
+            reports += reps
     if rank == 0:
         txt = json.dumps({"ok": bool(all_ok), "reports": reports}, indent=1)
         print(txt)

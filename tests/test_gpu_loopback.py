@@ -3,7 +3,7 @@ P = 2, 3, 4 x-slab contexts of one process share the device through the
 loopback transport (pic_loopback_link).  Each context runs on its own stream,
 driven by its own host thread like a rank, and the peer transport's kernels
 run unchanged: the mover writes slab leavers into the neighbour's receive
-buffer (send_leavers_peer), the flag barriers publish them, arrive_kernel
+buffer (send_leavers_peer), event-handshake barriers publish them, arrive_kernel
 appends and ranks them, ghost_pull_kernel sums the shared node planes, and
 pic_implicit_sources reads the neighbour's planes.  The union of the slabs is
 compared with the single-process CPU oracle (exiting
@@ -37,7 +37,7 @@ def _oracle(name):
     return SP.oracle_reference(w, parts_all, cycles, inject)
 
 
-def run_loopback(w, cycles, world, kernel, inject=None, bounds=None, sources=True):
+def run_loopback(w, cycles, world, kernel, inject=None, bounds=None, sources=True, far_hops=0, check=True):
     """The loopback decomposition of workload w: returns gathered[r] =
     ([(particles, moments)] per species, stats, sources) like mr_parity."""
     bounds = bounds or decomp.uniform_bounds(w.ncell[0], world)
@@ -48,15 +48,18 @@ def run_loopback(w, cycles, world, kernel, inject=None, bounds=None, sources=Tru
     for r in range(world):
         wr = w.with_slab(bounds[r], bounds[r + 1])
         cfg = pic.make_config(wr, rank=r, nranks=world, capacity=cap, ghost=2, kernel=kernel,
-                              transport=pic.TRANSPORT_LOOPBACK)
+                              transport=pic.TRANSPORT_LOOPBACK, far_hops=far_hops)
         ctx = pic.Context(cfg, stream=streams[r])
-        for s, p in enumerate(per_rank[r]):
-            ctx.set_particles(s, {k: v.cuda() for k, v in p.items()})
+        dev = [{k: v.cuda() for k, v in p.items()} for p in per_rank[r]]
+        _, EB = I.field_window(wr, 2, device="cpu")
+        EB = EB.cuda()
+        torch.cuda.synchronize()      # torch's copies before libpic's stream reads them
+        for s, p in enumerate(dev):
+            ctx.set_particles(s, p)
             if inject:
                 ctx.set_injection(s, inject["ppc"], w.species[s].vth, inject["drift"], float(parts_all[s]["q"][0]),
                                   500 + s)
-        _, EB = I.field_window(wr, 2, device="cpu")
-        ctx.set_fields(EB.cuda())
+        ctx.set_fields(EB)
         ctxs.append(ctx)
     pic.pic_loopback_link(ctxs)
     assert all(c.transport == pic.TRANSPORT_LOOPBACK for c in ctxs)
@@ -70,7 +73,7 @@ def run_loopback(w, cycles, world, kernel, inject=None, bounds=None, sources=Tru
                 ctx = ctxs[r]
                 for _ in range(cycles):
                     ctx.cycle()
-                stats = ctx.sync()
+                stats = ctx.sync(raise_on_error=check)
                 src = tuple(t.cpu().numpy() for t in ctx.implicit_sources()) if sources else None
                 out[r] = (stats, src)
         except Exception as e:  # noqa: BLE001
@@ -163,3 +166,58 @@ def test_loopback_link_rejects_bad_groups():
     assert e.value.status == pic.PIC_EINVAL
     a.close()
     b.close()
+
+
+def _with_fast_particles(w, n_fast=24, seed=9):
+    """The workload's particles plus particles that cross 1.5 to 2.5 slabs of a
+    P = 4 split in one step (6 to 10 cells along +-x)."""
+    base = I.make_species
+    def make(wl, device="cpu"):
+        parts = base(wl, device=device)
+        g = torch.Generator().manual_seed(seed)
+        out = []
+        for s, p in enumerate(parts):
+            n = n_fast
+            cells = 6 + 4 * torch.rand(n, generator=g, dtype=torch.float64)
+            sign = torch.where(torch.rand(n, generator=g) < 0.5, -1.0, 1.0).to(torch.float64)
+            u = sign * cells * w.delta[0] / w.dt
+            extra = {"x": torch.rand(n, generator=g, dtype=torch.float64) * w.length[0],
+                     "y": torch.rand(n, generator=g, dtype=torch.float64) * w.length[1],
+                     "z": torch.rand(n, generator=g, dtype=torch.float64) * w.length[2],
+                     "u": u, "v": torch.zeros(n, dtype=torch.float64), "w": torch.zeros(n, dtype=torch.float64),
+                     "q": p["q"][:n].clone(), "id": torch.arange(n, dtype=torch.int64) + (1 << 52) + 1000 * s}
+            out.append({k: torch.cat([p[k], extra[k].to(p[k].device)]).contiguous() for k in p})
+        return out
+    return make
+
+
+@pytest.mark.parametrize("kernel", [pic.KERNEL_TILED, pic.KERNEL_BASIC])
+def test_loopback_far_flyers_are_forwarded(kernel):
+    """R22: particles that cross more than one slab in one step reach their
+    owner through far_hops forwarding rounds (each receiver passes a record it
+    does not own onward in its direction of motion) and match the oracle.
+    Uniform fields (C1), so an iterate sampled beyond the field window (clamped,
+    R11) sees the same field as the oracle's."""
+    w = I.c1()
+    orig = I.make_species
+    I.make_species = _with_fast_particles(w)
+    try:
+        gathered, parts_all = run_loopback(w, 2, 4, kernel, sources=False, far_hops=2)
+    finally:
+        I.make_species = orig
+    orc = SP.oracle_reference(w, parts_all, 2)
+    ok, reps = SP.check_union("c1-far", w, gathered, orc, kernel=kernel, transport="loopback", world=4)
+    assert ok, reps
+    assert sum(g[1]["far"] for g in gathered) == 0
+    assert sum(g[1]["sent"] for g in gathered) == sum(g[1]["received"] for g in gathered)
+
+
+def test_loopback_far_flyers_without_forwarding_are_reported():
+    w = I.c1()
+    orig = I.make_species
+    I.make_species = _with_fast_particles(w)
+    try:
+        gathered, _ = run_loopback(w, 1, 4, pic.KERNEL_TILED, sources=False, far_hops=0, check=False)
+    finally:
+        I.make_species = orig
+    assert sum(g[1]["far"] for g in gathered) > 0

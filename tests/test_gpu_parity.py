@@ -548,3 +548,38 @@ def test_coalesce_overfull_and_wide_cells(kernel):
     rep = {}
     assert PU.compare_particles(w, sp, gp, P, st, rep), rep
     ctx.close()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_graph_cycles_match_the_oracle(kernel):
+    """pic_set_graph: cycles replayed from CUDA graphs (one per field buffer x
+    store buffer parity; new fields every other cycle switch the field buffer)
+    give the oracle's particles and moments like plain launches."""
+    w = I.c1(randomized=True)
+    parts = I.make_species(w, device="cpu")
+    cycles = 6
+    orc = PU.run_oracle(w, parts, cycles)
+    cap = [p["x"].numel() + 64 for p in parts]
+    stream = torch.cuda.Stream()
+    ctx = pic.Context(pic.make_config(w, capacity=cap, kernel=kernel), stream=stream)
+    dev = [{k: v.cuda() for k, v in p.items()} for p in parts]
+    EB = I.field_window(w, 2)[1].cuda()
+    torch.cuda.synchronize()          # torch's copies before libpic's stream reads them
+    for s, p in enumerate(dev):
+        ctx.set_particles(s, p)
+    ctx.set_fields(EB)
+    ctx.set_graph(True)
+    l0 = ctx.launch_count()
+    for c in range(cycles):
+        if c % 2 == 1:
+            ctx.set_fields(EB)
+        ctx.cycle()
+    ctx.sync()
+    assert ctx.launch_count() > l0
+    for s, sp in enumerate(w.species):
+        gp = {k: v.cpu().numpy() for k, v in ctx.get_particles(s).items()}
+        gm = ctx.get_moments(s).cpu().numpy()
+        rep = {"species": sp.name}
+        assert PU.compare_particles(w, sp, gp, orc[s][0], orc[s][1], rep), rep
+        assert PU.compare_moments(gm, orc[s][2], orc[s][3], rep), rep
+    ctx.close()

@@ -85,11 +85,16 @@ def loopback_pair():
         cfg = pic.make_config(wr, rank=r, nranks=2, capacity=[p["x"].numel() + 4096 for p in parts_all],
                               transport=pic.TRANSPORT_LOOPBACK)
         ctx = pic.Context(cfg, stream=streams[r])
+        dev = []
         for s, p in enumerate(parts_all):
             cx = torch.floor(p["x"] / w.delta[0]).to(torch.int64)
             own = decomp.owner_of_cells(cx, bounds) == r
-            ctx.set_particles(s, {k: v[own].contiguous().cuda() for k, v in p.items()})
-        ctx.set_fields(I.field_window(wr, 2, device="cuda")[1])
+            dev.append({k: v[own].contiguous().cuda() for k, v in p.items()})
+        EB = I.field_window(wr, 2, device="cuda")[1]
+        torch.cuda.synchronize()      # torch's work before libpic's stream reads it
+        for s, p in enumerate(dev):
+            ctx.set_particles(s, p)
+        ctx.set_fields(EB)
         ctxs.append(ctx)
     pic.pic_loopback_link(ctxs)
     torch.cuda.synchronize()
