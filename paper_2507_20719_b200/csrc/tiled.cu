@@ -75,14 +75,7 @@ constexpr int NACC = PIC_DEP_NACC;               // independent MMA accumulator 
 #define PIC_DEP_MINB 3
 #endif
 constexpr int DWARPS = PIC_DEP_WARPS, DTHREADS = 32 * DWARPS;   // deposit CTA (one tile)
-#ifdef PIC_DEP_CELLSUMS
-// per-cell corner sums [64 cells][8 corners x 10 moments]: every cell is
-// flushed once, by the one warp that owns it, with plain stores; the epilogue
-// adds each node's (up to 8) adjacent cells in a fixed order
-constexpr size_t DEPOSIT_SMEM = sizeof(double) * (TILE3 * 80 + DWARPS * WBUF);
-#else
 constexpr size_t DEPOSIT_SMEM = sizeof(double) * (MB3 * 10 + DWARPS * WBUF);
-#endif
 
 // Per-species arguments of the movers; one launch moves every species of
 // pic_mover (species-major blocks: blockIdx.x = s * ntiles + tile), so the
@@ -363,13 +356,8 @@ __device__ __forceinline__ int stage_slot(int p, int k) {
 
 __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(const DepositArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-#ifdef PIC_DEP_CELLSUMS
-  double *csum = reinterpret_cast<double *>(smem_raw);  // corner sums of the tile's cells [64][80]
-  double *wbuf = csum + TILE3 * 80;
-#else
   double *nacc = reinterpret_cast<double *>(smem_raw);  // node sums of the tile box [MB^3][10]
   double *wbuf = nacc + MB3 * 10;
-#endif
   const Geom &g = A.g;
   const int sp_i = (int)(blockIdx.x / (unsigned)g.ntiles);
   const int tile = (int)(blockIdx.x - (unsigned)sp_i * (unsigned)g.ntiles);
@@ -382,11 +370,7 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
   const int tz = (int)(tile / (g.nt[0] * g.nt[1]));
   const int64_t ox = g.slab_lo + (int64_t)tx * TILE, oy = (int64_t)ty * TILE, oz = (int64_t)tz * TILE;
   const int tid = threadIdx.x;
-#ifdef PIC_DEP_CELLSUMS
-  for (int i = tid; i < TILE3 * 80 / 2; i += DTHREADS) reinterpret_cast<double2 *>(csum)[i] = make_double2(0.0, 0.0);
-#else
   for (int i = tid; i < MB3 * 10; i += DTHREADS) nacc[i] = 0.0;
-#endif
   __syncthreads();
 
   // warp ranges are aligned to cell boundaries, so every cell belongs to one
@@ -440,12 +424,6 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
     // corner g8 of cell c is node (cx + gx, cy + gy, cz + gz) of the tile box;
     // cells of different warps share nodes, hence shared-memory atomics (one
     // flush per cell and warp: rare next to the per-particle work)
-#ifdef PIC_DEP_CELLSUMS
-    PIC_DCHECK(c >= 0 && c < TILE3, A.stats);
-    double *dst = csum + c * 80 + g8 * 10;
-    *reinterpret_cast<double2 *>(dst + 2 * j4) = make_double2(c0[0][0], c0[0][1]);
-    if (j4 == 0) *reinterpret_cast<double2 *>(dst + 8) = make_double2(c1[0][0], c1[0][1]);
-#else
     const int node = ((c & 3) + (g8 & 1)) + MB * ((((c >> 2) & 3) + ((g8 >> 1) & 1)) + MB * ((c >> 4) + (g8 >> 2)));
     PIC_DCHECK(c >= 0 && c < TILE3 && node < MB3, A.stats);
     double *dst = nacc + node * 10;
@@ -455,7 +433,6 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
       atomicAdd(dst + 8, c1[0][0]);
       atomicAdd(dst + 9, c1[0][1]);
     }
-#endif
 #pragma unroll
     for (int a = 0; a < NACC; ++a) c0[a][0] = c0[a][1] = c1[a][0] = c1[a][1] = 0.0;
   };
@@ -555,14 +532,8 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
           const int pi = 4 * t + j4;
           const int o = 32 * t + ((t & 1) ? rs1 : rs0);
           const double a = (pi >= b && pi < e) ? Ss[o] : 0.0;
-          // alternate accumulator sets (static indices: no local-memory array)
-          if (NACC > 1 && (t & 1)) {
-            mma(c0[NACC > 1 ? 1 : 0], a, Vs[o]);
-            mma(c1[NACC > 1 ? 1 : 0], a, V2[8 * t + v2off]);
-          } else {
-            mma(c0[0], a, Vs[o]);
-            mma(c1[0], a, V2[8 * t + v2off]);
-          }
+          mma(c0[0], a, Vs[o]);
+          mma(c1[0], a, V2[8 * t + v2off]);
         }
       }
     }
@@ -578,17 +549,7 @@ __global__ void __launch_bounds__(DTHREADS, PIC_DEP_MINB) deposit_tiled_kernel(c
   for (int i = tid; i < MB3 * 10; i += DTHREADS) {
     const int n = i / 10, m = i - 10 * n;
     const int bx = n % MB, by = (n / MB) % MB, bz = n / (MB * MB);
-#ifdef PIC_DEP_CELLSUMS
-    double v = 0.0;
-    for (int cz = max(bz - 1, 0); cz <= min(bz, TILE - 1); ++cz)
-      for (int cy = max(by - 1, 0); cy <= min(by, TILE - 1); ++cy)
-        for (int cx = max(bx - 1, 0); cx <= min(bx, TILE - 1); ++cx) {
-          const int corner = (bx - cx) + 2 * (by - cy) + 4 * (bz - cz);
-          v += csum[(cx + TILE * (cy + TILE * cz)) * 80 + corner * 10 + m];
-        }
-#else
     const double v = nacc[i];
-#endif
     if (v == 0.0) continue;
     const int64_t node = moment_node(g, ox + bx, oy + by, oz + bz);
     if (node < 0) {
