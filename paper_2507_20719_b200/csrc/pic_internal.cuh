@@ -394,8 +394,15 @@ __device__ __forceinline__ uint32_t tile_key32(const Geom &g, uint32_t lx, uint3
 // the rare flagged path.  Fast path: the particle is still inside this rank's
 // slab and the domain (no wrap, no leaver, no open face) and outside the planet,
 // which is every particle but the few that cross a face this step.
+// `old_cell` (optional): the particle's cell before the push and its key; a
+// particle still in that cell keeps the key without recomputing it.
+struct OldCell {
+  int c[3];
+  uint32_t key;
+};
 __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3], const double vnew[3],
-                                                   bool clamped, unsigned long long *__restrict__ stats) {
+                                                   bool clamped, unsigned long long *__restrict__ stats,
+                                                   const OldCell *old_cell = nullptr) {
   if (xnew[0] >= (double)g.slab_lo && xnew[0] < (double)g.slab_hi && xnew[1] >= 0.0 &&
       xnew[1] < (double)g.ncell[1] && xnew[2] >= 0.0 && xnew[2] < (double)g.ncell[2]) {
     bool hit = false;
@@ -411,6 +418,7 @@ __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3
     if (!hit) {
       if (clamped) atomicAdd(&stats[ST_CLAMPED], 1ull);
       const int cx = (int)xnew[0], cy = (int)xnew[1], cz = (int)xnew[2];
+      if (old_cell && cx == old_cell->c[0] && cy == old_cell->c[1] && cz == old_cell->c[2]) return old_cell->key;
       return tile_key32(g, (uint32_t)(cx - (int)g.slab_lo), (uint32_t)cy, (uint32_t)cz);
     }
   }

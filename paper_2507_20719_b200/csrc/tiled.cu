@@ -239,8 +239,12 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
                 mbar);
   }
   mbar_wait(mbar, 0);
-  {
-    for (int i = tid; i < NB3 * 6; i += MT) fld[i] *= ((i % 6) < 3) ? S.ks : S.ks_c;
+  for (int nd = tid; nd < NB3; nd += MT) {   // E' = k E, a = k B / c (48 B per node)
+    double2 *f2 = reinterpret_cast<double2 *>(fld + 6 * nd);
+    double2 e0 = f2[0], e1 = f2[1], e2 = f2[2];
+    e0.x *= S.ks; e0.y *= S.ks; e1.x *= S.ks;
+    e1.y *= S.ks_c; e2.x *= S.ks_c; e2.y *= S.ks_c;
+    f2[0] = e0; f2[1] = e1; f2[2] = e2;
   }
   __syncthreads();
 
@@ -312,7 +316,14 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       // the cell of x^n (the key the order was built from: keys are always
       // taken from the stored position, so no key array is kept; a mismatch
       // would only reclassify a stayer as an arrival or back)
-      kold = tile_key32(g, (uint32_t)((int)xn[0] - (int)g.slab_lo), (uint32_t)(int)xn[1], (uint32_t)(int)xn[2]);
+      // (this tile's cell: key = tile * 64 + local cell, no division)
+      OldCell oc;
+      oc.c[0] = (int)xn[0];
+      oc.c[1] = (int)xn[1];
+      oc.c[2] = (int)xn[2];
+      oc.key = (uint32_t)tile * TILE3 +
+               (uint32_t)(((oc.c[0] - (int)ox) & 3) + 4 * ((oc.c[1] - (int)oy) & 3) + 16 * ((oc.c[2] - (int)oz) & 3));
+      kold = oc.key;
       // Eq. 2 (push.cuh); field samples from the staged box, the global window
       // (clamped to it, R11) for iterates outside the box
       auto sample = [&](const double xb[3], double EB[6]) -> bool {
@@ -322,7 +333,7 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       };
       double xnew[3], vnew[3];
       const bool clamped = push_eq2<NIT, REL>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew);
-      knew = finish_particle(g, xnew, vnew, clamped, A.stats);
+      knew = finish_particle(g, xnew, vnew, clamped, A.stats, &oc);
       PIC_DCHECK(p < S.cap && (knew < g.ncells || knew >= KEY_FIRST_RESERVED), A.stats);
       S.dst[0][p] = xnew[0]; S.dst[1][p] = xnew[1]; S.dst[2][p] = xnew[2];
       S.dst[3][p] = vnew[0]; S.dst[4][p] = vnew[1]; S.dst[5][p] = vnew[2];
