@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define PIC_ABI_VERSION 5
+#define PIC_ABI_VERSION 6
 #define PIC_MAX_SPECIES 8
 #define PIC_NCCL_ID_BYTES 128
 #define PIC_N_MOMENTS 10  /* rho, Jx, Jy, Jz, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz (R16) */
@@ -135,6 +135,10 @@ typedef struct {
                                     (default): one hop; each extra round costs a
                                     barrier even when nothing is forwarded.
                                     0 <= far_hops < nranks.                       */
+  int32_t barrier_timeout_ms;    /* peer / loopback transports: a neighbour that
+                                    does not reach a barrier within this time is
+                                    reported (PIC_ENCCL) instead of hanging; 0 =
+                                    default 20000                                 */
 } pic_config;
 
 /* ABI version (PIC_ABI_VERSION).                                             */

@@ -57,6 +57,7 @@ pic_status validate(const pic_config *c, std::string *why) {
   if (c->transport < PIC_TRANSPORT_AUTO || c->transport > PIC_TRANSPORT_LOOPBACK) { *why = "bad transport"; return PIC_EINVAL; }
   if (c->kernel < 0 || c->kernel > 2) { *why = "bad kernel"; return PIC_EINVAL; }
   if (c->relativistic != 0 && c->relativistic != 1) { *why = "relativistic must be 0 or 1"; return PIC_EINVAL; }
+  if (c->barrier_timeout_ms < 0) { *why = "barrier_timeout_ms must be >= 0"; return PIC_EINVAL; }
   if (c->far_hops < 0 || (c->far_hops > 0 && c->far_hops >= c->nranks)) {
     *why = "far_hops must be in [0, nranks)"; return PIC_EINVAL;
   }

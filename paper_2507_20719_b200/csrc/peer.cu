@@ -232,6 +232,10 @@ pic_status peer_setup(Ctx *ctx) {
 // thread waits until both neighbours have recorded theirs for the same epoch,
 // and its stream waits on those events.  Each context is driven by its own
 // host thread, as a rank would be.
+static int barrier_timeout_ms(const Ctx *ctx) {
+  return ctx->cfg.barrier_timeout_ms > 0 ? ctx->cfg.barrier_timeout_ms : 20000;
+}
+
 struct LoopGroup {
   std::mutex mu;
   std::condition_variable cv;
@@ -252,8 +256,8 @@ pic_status loopback_barrier(Ctx *ctx) {
   for (Ctx *nb : ctx->loop_nb) {
     if (!nb) continue;
     const int q = nb->cfg.rank;
-    // 20 s, like the device barrier: a neighbour that never arrives is an error, not a hang
-    if (!G->cv.wait_for(lk, std::chrono::seconds(20), [&] { return G->arrived[q] >= e; }))
+    // like the device barrier: a neighbour that never arrives is an error, not a hang
+    if (!G->cv.wait_for(lk, std::chrono::milliseconds(barrier_timeout_ms(ctx)), [&] { return G->arrived[q] >= e; }))
       return fail(ctx, PIC_ENCCL, "loopback barrier timed out (a neighbour context stopped)");
     // the neighbour cannot re-record this event (epoch e + 2) before it passed
     // barrier e + 1, which needs this context's arrival there
@@ -357,7 +361,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // in a CUDA graph (pic_set_graph) advances it on every replay.
 __global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long long *left_flag,
                                     unsigned long long *right_flag, unsigned long long *own_epoch,
-                                    unsigned long long *err) {
+                                    unsigned long long *err, unsigned long long timeout_ns) {
   const unsigned long long epoch = ++*own_epoch;
   __threadfence_system();
   if (left_flag) st_release_sys(left_flag, epoch);
@@ -365,7 +369,7 @@ __global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long 
   const unsigned long long t0 = global_ns();
   // own_flag[0] is written by the left neighbour, own_flag[1] by the right one
   while ((left_flag && ld_acquire_sys(own_flag) < epoch) || (right_flag && ld_acquire_sys(own_flag + 1) < epoch)) {
-    if (global_ns() - t0 > 20ull * 1000 * 1000 * 1000) {   // 20 s: a neighbour is gone
+    if (global_ns() - t0 > timeout_ns) {   // a neighbour is gone
       atomicAdd(err, 1ull);
       break;
     }
@@ -376,7 +380,8 @@ __global__ void peer_barrier_kernel(unsigned long long *own_flag, unsigned long 
 pic_status peer_barrier(Ctx *ctx) {
   if (ctx->loop) return loopback_barrier(ctx);
   peer_barrier_kernel<<<1, 1, 0, ctx->stream>>>(ctx->peer_ctl->flag, ctx->link[0].flag, ctx->link[1].flag,
-                                                &ctx->peer_ctl->epoch, &ctx->peer_ctl->err); ++ctx->launches;
+                                                &ctx->peer_ctl->epoch, &ctx->peer_ctl->err,
+                                                1000000ull * (unsigned long long)barrier_timeout_ms(ctx)); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   return PIC_OK;
 }

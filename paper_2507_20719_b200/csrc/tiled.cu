@@ -171,19 +171,22 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
   const int base = ((i[2] * NB + i[1]) * NB + i[0]) * 6;
 #pragma unroll
   for (int m = 0; m < 6; ++m) out[m] = 0.0;
+  auto accumulate = [&](const double *cell) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int off = base + 6 * ((c & 1) + NB * ((c >> 1) & 1) + NB * NB * (c >> 2));
-    const double2 a = *reinterpret_cast<const double2 *>(fld + off);
-    const double2 b = *reinterpret_cast<const double2 *>(fld + off + 2);
-    const double2 e = *reinterpret_cast<const double2 *>(fld + off + 4);
-    out[0] = fma(S[c], a.x, out[0]);
-    out[1] = fma(S[c], a.y, out[1]);
-    out[2] = fma(S[c], b.x, out[2]);
-    out[3] = fma(S[c], b.y, out[3]);
-    out[4] = fma(S[c], e.x, out[4]);
-    out[5] = fma(S[c], e.y, out[5]);
-  }
+    for (int c = 0; c < 8; ++c) {
+      const double *nd = cell + 6 * ((c & 1) + NB * ((c >> 1) & 1) + NB * NB * (c >> 2));
+      const double2 a = *reinterpret_cast<const double2 *>(nd);
+      const double2 b = *reinterpret_cast<const double2 *>(nd + 2);
+      const double2 e = *reinterpret_cast<const double2 *>(nd + 4);
+      out[0] = fma(S[c], a.x, out[0]);
+      out[1] = fma(S[c], a.y, out[1]);
+      out[2] = fma(S[c], b.x, out[2]);
+      out[3] = fma(S[c], b.y, out[3]);
+      out[4] = fma(S[c], e.x, out[4]);
+      out[5] = fma(S[c], e.y, out[5]);
+    }
+  };
+  accumulate(fld + base);
   return true;
 }
 

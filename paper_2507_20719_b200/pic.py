@@ -45,7 +45,7 @@ class pic_config(C.Structure):
         ("planet_center", C.c_double * 3), ("planet_radius", C.c_double),
         ("rank", C.c_int32), ("nranks", C.c_int32), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64),
         ("ghost", C.c_int32), ("transport", C.c_int32), ("kernel", C.c_int32), ("relativistic", C.c_int32),
-        ("far_hops", C.c_int32),
+        ("far_hops", C.c_int32), ("barrier_timeout_ms", C.c_int32),
     ]
 
 
@@ -137,7 +137,7 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSPORT_AUTO, kernel=KERNEL_AUTO,
-                n_iter=None, relativistic=None, far_hops=0) -> pic_config:
+                n_iter=None, relativistic=None, far_hops=0, barrier_timeout_ms=0) -> pic_config:
     """pic_config from an inputs.Workload (marshalling only)."""
     cfg = pic_config()
     lo, hi = w.slab_or_all()
@@ -156,6 +156,7 @@ def make_config(w, *, rank=0, nranks=1, capacity=None, ghost=2, transport=TRANSP
     cfg.ghost, cfg.transport, cfg.kernel = ghost, transport, kernel
     cfg.relativistic = int(bool(getattr(w, "relativistic", False) if relativistic is None else relativistic))
     cfg.far_hops = int(far_hops)
+    cfg.barrier_timeout_ms = int(barrier_timeout_ms)
     return cfg
 
 

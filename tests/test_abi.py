@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.pic_abi_version() == 5
+    assert lib.pic_abi_version() == 6
 
 
 def test_struct_layout_matches_header():

@@ -221,3 +221,33 @@ def test_loopback_far_flyers_without_forwarding_are_reported():
     finally:
         I.make_species = orig
     assert sum(g[1]["far"] for g in gathered) > 0
+
+
+def test_loopback_barrier_timeout_is_an_error_not_a_hang():
+    """A neighbour that never reaches the barrier: pic_mover reports PIC_ENCCL
+    after barrier_timeout_ms instead of waiting forever."""
+    import time
+    w = I.c1()
+    bounds = decomp.uniform_bounds(w.ncell[0], 2)
+    parts_all, per_rank = SP.split_inputs(w, bounds)
+    ctxs = []
+    for r in range(2):
+        wr = w.with_slab(bounds[r], bounds[r + 1])
+        cfg = pic.make_config(wr, rank=r, nranks=2, capacity=SP.capacity(parts_all), transport=pic.TRANSPORT_LOOPBACK,
+                              barrier_timeout_ms=500)
+        ctx = pic.Context(cfg, stream=torch.cuda.Stream())
+        dev = [{k: v.cuda() for k, v in p.items()} for p in per_rank[r]]
+        EB = I.field_window(wr, 2, device="cuda")[1]
+        torch.cuda.synchronize()
+        for s, p in enumerate(dev):
+            ctx.set_particles(s, p)
+        ctx.set_fields(EB)
+        ctxs.append(ctx)
+    pic.pic_loopback_link(ctxs)
+    t0 = time.time()
+    with pytest.raises(pic.PicError) as e:
+        ctxs[0].mover(-1)            # rank 1 never moves
+    assert e.value.status == pic.PIC_ENCCL
+    assert 0.4 < time.time() - t0 < 10
+    for c in ctxs:
+        c.close()
