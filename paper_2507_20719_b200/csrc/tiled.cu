@@ -190,6 +190,107 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
   return true;
 }
 
+// PIC_GATHER_MMA = 1 selects gather_mma below in the gamma == 1 mover.  It is
+// correct (parity green) but measured 2.1x slower than the per-lane gather
+// (C2: mover 5.59 vs 2.66 ms per step): its shuffles, weights,
+// dependent DMMA pairs and transpose lengthen every iterate's critical path,
+// and the mover is latency-bound at 16 warps per SM.  Kept as the measured
+// alternative; off by default.
+#ifndef PIC_GATHER_MMA
+#define PIC_GATHER_MMA 0
+#endif
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+// The trilinear gather of the staged box as a contraction on the fp64 tensor
+// cores (warp-collective: all 32 lanes call it, each with its own particle's
+// position).  For the particles of one cell the gather is the matrix product
+//   EB[particle][component] = sum_corner S[particle][corner] F[corner][component]
+// with the cell's 8 corner nodes F (8 x 6, padded to 8 x 8) shared by all of
+// them: mma.m8n8k4 with M = 8 particles, K = 4 corners (two K-steps: z = 0, 1),
+// N = 8 components.  F is the B operand, two doubles per lane read from shared
+// memory once per distinct cell of the warp — instead of all 48 values into
+// every lane (the 128 B/clk shared-memory crossbar bound of the per-lane gather).
+// Lane L = 4 g + j owns particle (t = j, g) — row g of M-tile t; the A operand
+// of lane (g, j) is the weight of corner (kk, j) of particle (t, g), computed
+// from that particle's fractional position (shuffled within the quad); the C
+// fragment (components 2j, 2j+1 of particle (t, g)) is transposed back to its
+// owner within the quad.  A particle whose cell is not in the box returns false
+// (the caller samples the global window).
+__device__ __forceinline__ bool gather_mma(const double *__restrict__ fld, const double u[3], double out[6]) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u, j = lane & 3u, gq = lane >> 2;
+  const unsigned quad = lane & ~3u;
+  double f[3];
+  int i[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double fl = floor(u[d]);
+    f[d] = u[d] - fl;
+    i[d] = (int)fl;
+  }
+  const bool inbox = (unsigned)i[0] <= (unsigned)(NB - 2) && (unsigned)i[1] <= (unsigned)(NB - 2) &&
+                     (unsigned)i[2] <= (unsigned)(NB - 2);
+  const int cell = inbox ? ((i[2] * NB + i[1]) * NB + i[0]) * 6 : -1;
+  // A operands: a[t][kk] = weight of corner (x = j & 1, y = j >> 1, z = kk) of
+  // the particle of lane quad + t
+  double a[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const double fx = __shfl_sync(FULL, f[0], quad | t);
+    const double fy = __shfl_sync(FULL, f[1], quad | t);
+    const double fz = __shfl_sync(FULL, f[2], quad | t);
+    const double wx = (j & 1u) ? fx : 1.0 - fx;
+    const double wy = (j & 2u) ? fy : 1.0 - fy;
+    const double wxy = wx * wy;
+    a[t][0] = wxy * (1.0 - fz);
+    a[t][1] = wxy * fz;
+  }
+  // one pair of B fragments and 8 DMMAs per distinct cell of the warp
+  double ck[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) ck[t][0] = ck[t][1] = 0.0;
+  unsigned todo = __ballot_sync(FULL, inbox);
+  const int off0 = 6 * ((j & 1u) + NB * (j >> 1)), off1 = off0 + 6 * NB * NB;
+  while (todo) {
+    const int cur = __shfl_sync(FULL, cell, __ffs(todo) - 1);
+    const unsigned in_cur = __ballot_sync(FULL, cell == cur);
+    todo &= ~in_cur;
+    const double b0 = gq < 6 ? fld[cur + off0 + gq] : 0.0;
+    const double b1 = gq < 6 ? fld[cur + off1 + gq] : 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      double c[2] = {0.0, 0.0};
+      dmma_884(c, a[t][0], b0);
+      dmma_884(c, a[t][1], b1);
+      if ((in_cur >> (quad | t)) & 1u) {
+        ck[t][0] = c[0];
+        ck[t][1] = c[1];
+      }
+    }
+  }
+  // in-quad transpose: lane j holds components (2j, 2j+1) of the particles of
+  // lanes quad + t; in round r it sends the pair of owner (j + r) & 3 and
+  // receives, as owner, the pair computed by lane (j - r) & 3
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const unsigned tsend = (j + (unsigned)r) & 3u;
+    double s0 = ck[0][0], s1 = ck[0][1];
+    if (tsend == 1u) { s0 = ck[1][0]; s1 = ck[1][1]; }
+    if (tsend == 2u) { s0 = ck[2][0]; s1 = ck[2][1]; }
+    if (tsend == 3u) { s0 = ck[3][0]; s1 = ck[3][1]; }
+    const unsigned src = (j - (unsigned)r) & 3u;
+    const double r0 = r == 0 ? s0 : __shfl_sync(FULL, s0, quad | src);
+    const double r1 = r == 0 ? s1 : __shfl_sync(FULL, s1, quad | src);
+    if (src == 0u) { out[0] = r0; out[1] = r1; }
+    if (src == 1u) { out[2] = r0; out[3] = r1; }
+    if (src == 2u) { out[4] = r0; out[5] = r1; }
+  }
+  return inbox;
+}
+
 // ----------------------------------------------------------------- mover ----
 #ifndef PIC_MOVER_MINB
 #define PIC_MOVER_MINB 2
@@ -311,11 +412,16 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     asm volatile("cp.async.wait_group %0;" ::"n"(SRC_STAGES - 1) : "memory");
     const double *sv = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
     uint32_t knew = KEY_DEAD;
-    if (act) {
-      const double qv = sv[6 * 32];
-      const int64_t idv = __double_as_longlong(sv[7 * 32]);
-      const double xn[3] = {sv[0], sv[32], sv[64]};
-      const double vn[3] = {sv[96], sv[128], sv[160]};
+    constexpr bool kMma = PIC_GATHER_MMA && REL == 0;
+    // with the tensor-core gather every lane pushes (warp-collective samples):
+    // a lane past the end of the range pushes a particle at rest in the tile's
+    // first cell and drops the result
+    if (kMma || act) {
+      const double qv = act ? sv[6 * 32] : 0.0;
+      const int64_t idv = act ? __double_as_longlong(sv[7 * 32]) : 0;
+      const double xn[3] = {act ? sv[0] : (double)ox + 0.5, act ? sv[32] : (double)oy + 0.5,
+                            act ? sv[64] : (double)oz + 0.5};
+      const double vn[3] = {act ? sv[96] : 0.0, act ? sv[128] : 0.0, act ? sv[160] : 0.0};
       // the cell of x^n (the key the order was built from: keys are always
       // taken from the stored position, so no key array is kept; a mismatch
       // would only reclassify a stayer as an arrival or back)
@@ -326,23 +432,30 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
       oc.c[2] = (int)xn[2];
       oc.key = (uint32_t)tile * TILE3 +
                (uint32_t)(((oc.c[0] - (int)ox) & 3) + 4 * ((oc.c[1] - (int)oy) & 3) + 16 * ((oc.c[2] - (int)oz) & 3));
-      kold = oc.key;
-      // Eq. 2 (push.cuh); field samples from the staged box, the global window
-      // (clamped to it, R11) for iterates outside the box
+      if (act) kold = oc.key;
+      // Eq. 2 (push.cuh); field samples from the staged box (tensor-core gather
+      // or per-lane loads), the global window (clamped to it, R11) for iterates
+      // outside the box
       auto sample = [&](const double xb[3], double EB[6]) -> bool {
         const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
-        if (gather_smem(fld, u, EB)) return false;
+        if constexpr (kMma) {
+          if (gather_mma(fld, u, EB)) return false;
+        } else {
+          if (gather_smem(fld, u, EB)) return false;
+        }
         return WindowSampler{&g, A.field, S.ks, S.ks_c}(xb, EB);
       };
       double xnew[3], vnew[3];
       const bool clamped = push_eq2<NIT, REL>(xn, vn, h, g.c, A.n_iter, sample, xnew, vnew);
-      knew = finish_particle(g, xnew, vnew, clamped, A.stats, &oc);
-      PIC_DCHECK(p < S.cap && (knew < g.ncells || knew >= KEY_FIRST_RESERVED), A.stats);
-      S.dst[0][p] = xnew[0]; S.dst[1][p] = xnew[1]; S.dst[2][p] = xnew[2];
-      S.dst[3][p] = vnew[0]; S.dst[4][p] = vnew[1]; S.dst[5][p] = vnew[2];
-      S.dst[6][p] = qv;
-      S.dst_id[p] = idv;
-      S.key_new[p] = knew;
+      if (act) knew = finish_particle(g, xnew, vnew, clamped, A.stats, &oc);
+      if (act) {
+        PIC_DCHECK(p < S.cap && (knew < g.ncells || knew >= KEY_FIRST_RESERVED), A.stats);
+        S.dst[0][p] = xnew[0]; S.dst[1][p] = xnew[1]; S.dst[2][p] = xnew[2];
+        S.dst[3][p] = vnew[0]; S.dst[4][p] = vnew[1]; S.dst[5][p] = vnew[2];
+        S.dst[6][p] = qv;
+        S.dst_id[p] = idv;
+        S.key_new[p] = knew;
+      }
     }
     // complete the previous round's rank, then start this round's (order.cu);
     // leavers and removed particles are not counted
