@@ -462,6 +462,7 @@ def main():
                torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         ctx.profile(True)
         barrier()
+        torch.cuda.nvtx.range_push("bench_steps")   # ncu --nvtx --nvtx-include "bench_steps/"
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
@@ -475,6 +476,7 @@ def main():
             e2.record(stream)
         end.record(stream)
         barrier()
+        torch.cuda.nvtx.range_pop()
         prof = ctx.profile_read()
         ctx.profile(False)
         return start.elapsed_time(end), prof, ([a.elapsed_time(b) for a, b, c in ev], [b.elapsed_time(c) for a, b, c in ev])

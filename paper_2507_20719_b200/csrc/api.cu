@@ -434,6 +434,10 @@ pic_status pic_mover(pic_ctx *p, int32_t s) {
   for (int k = s0; k < s1; ++k)
     if (ctx->sp[k].moved || !ctx->sp[k].order_valid)
       return fail(ctx, PIC_ESTATE, "pic_mover called twice without pic_exchange");
+  for (int k = s0; k < s1; ++k) {
+    st = ensure_order(ctx, k);
+    if (st != PIC_OK) return st;
+  }
   if (ctx->field_new) {
     ctx->field_cur ^= 1;
     ctx->field_new = false;
@@ -494,6 +498,10 @@ pic_status pic_moments(pic_ctx *p, int32_t s) {
   const int s0 = s < 0 ? 0 : s, s1 = s < 0 ? ctx->cfg.n_species : s + 1;
   for (int k = s0; k < s1; ++k)
     if (ctx->sp[k].deposited) return fail(ctx, PIC_ESTATE, "pic_moments called twice without pic_exchange");
+  for (int k = s0; k < s1; ++k) {
+    st = ensure_order(ctx, k);
+    if (st != PIC_OK) return st;
+  }
   {
     PhaseTimer t(ctx, 2);
     if (use_tiled(ctx)) {
@@ -547,7 +555,7 @@ static bool graph_ok(const Ctx *ctx) {
   if (ctx->cfg.nranks > 1 && (!ctx->peer || ctx->loop)) return false;
   for (int s = 0; s < ctx->cfg.n_species; ++s) {
     const SpeciesStore &sp = ctx->sp[s];
-    if (ctx->inj[s].ppc > 0 || sp.moved || sp.deposited || !sp.order_valid) return false;
+    if (ctx->inj[s].ppc > 0 || sp.moved || sp.deposited || !sp.order_valid || sp.order_dirty) return false;
   }
   return ctx->fields_set;
 }
@@ -716,6 +724,8 @@ pic_status pic_gmm(pic_ctx *p, int32_t s, int32_t B, double vmax, int32_t M, int
   if (st != PIC_OK) return st;
   if (ctx->sp[s].moved || !ctx->sp[s].order_valid)
     return fail(ctx, PIC_ESTATE, "pic_gmm runs between cycles (after pic_exchange)");
+  st = ensure_order(ctx, s);
+  if (st != PIC_OK) return st;
   return gmm_fit(ctx, s, B, vmax, M, n_em, alpha, mu, sigma, hist, clipped);
 }
 

@@ -528,17 +528,15 @@ pic_status append_particles(Ctx *ctx, int s, int64_t n, const double *const src[
   if (st != PIC_OK) return st;
   st = count_positions(ctx, s, old, old + n);
   if (st != PIC_OK) return st;
-  st = build_order(ctx, s);
-  if (st != PIC_OK) return st;
-  uint32_t nlive = 0;
-  PIC_CUDA(cudaMemcpyAsync(&nlive, sp.cell_off + ctx->geom.ncells, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  sp.order_dirty = true;   // built once, by the next call that needs the order
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));  // caller buffers may be pageable
-  sp.n = nlive;
   return PIC_OK;
 }
 
 pic_status live_count(Ctx *ctx, int s, int64_t *n) {
   SpeciesStore &sp = ctx->sp[s];
+  pic_status st = ensure_order(ctx, s);
+  if (st != PIC_OK) return st;
   uint32_t nlive = 0;
   PIC_CUDA(cudaMemcpyAsync(&nlive, sp.cell_off + ctx->geom.ncells, 4, cudaMemcpyDeviceToHost, ctx->stream));
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));

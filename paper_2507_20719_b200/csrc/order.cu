@@ -110,7 +110,12 @@ pic_status build_order(Ctx *ctx, int s) {
   }
   PIC_CUDA(cudaGetLastError());
   sp.order_valid = true;
+  sp.order_dirty = false;
   return PIC_OK;
+}
+
+pic_status ensure_order(Ctx *ctx, int s) {
+  return ctx->sp[s].order_dirty ? build_order(ctx, s) : PIC_OK;
 }
 
 }  // namespace pic

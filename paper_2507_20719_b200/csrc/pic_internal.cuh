@@ -153,6 +153,7 @@ struct SpeciesStore {
   int32_t n_iter = 3;
   bool moved = false, deposited = false;
   bool order_valid = false;
+  bool order_dirty = false;  // positions appended since the last order build (ensure_order)
   void swap_buffers() {
     for (int k = 0; k < 7; ++k) { double *t = a[k]; a[k] = b[k]; b[k] = t; }
     int64_t *t = id; id = id_b; id_b = t;
@@ -307,6 +308,9 @@ size_t order_temp_bytes(int64_t ncells);
 pic_status zero_cell_counts(Ctx *ctx, int s);
 pic_status count_positions(Ctx *ctx, int s, int64_t from, int64_t to);
 pic_status build_order(Ctx *ctx, int s);
+// Rebuild the cell order if particles were appended since the last build
+// (pic_add_particles defers it, so loading a store chunk by chunk builds it once).
+pic_status ensure_order(Ctx *ctx, int s);
 pic_status exchange(Ctx *ctx);
 pic_status migrate(Ctx *ctx, int s0, int s1);
 pic_status peer_setup(Ctx *ctx);
