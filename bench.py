@@ -553,7 +553,8 @@ def main():
             tj = json.load(open(tpath))
             if tj.get("config") == args.config and tj.get("kernel", "mover_tiled_kernel") == kname \
                     and not args.relativistic:
-                traffic = tj["mover_bytes_per_update"] * n_alive / n_sp
+                # per launch: one mover launch moves every species sharing n_iter
+                traffic = tj["mover_bytes_per_update"] * n_alive / max(1.0, prof["mover"][1] / args.steps)
                 traffic_src = {"kind": "static ncu capture (not this run)", "file": "profiles/traffic.json",
                                "from": tj.get("source"), "bytes_per_update": tj["mover_bytes_per_update"]}
                 ncu_pct = {k: tj[k] for k in ("mover_fp64_pipe_pct", "mover_issue_active_pct", "mover_dram_pct",
