@@ -28,3 +28,20 @@ def test_multirank_parity(nproc):
         assert rep["ok"], rep
         assert any(x.get("sent", 0) > 0 for x in rep["reports"])
         assert any("sources_ok" in x for x in rep["reports"])
+
+
+@pytest.mark.parametrize("config", ["c4"])
+def test_multirank_fullsize_sampled(config):
+    """C4 at full size (4.29e9 particles, open faces, absorbing planet,
+    count-balanced slabs) on 4 GPUs, sampled against the oracle (mr_fullsize.py)."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "rep.json")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+               "--master-addr", "127.0.0.1", "--master-port", "29571",
+               os.path.join(HERE, "mr_fullsize.py"), "--config", config, "--out", out]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
+        assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+        rep = json.load(open(out))
+        assert rep["ok"], rep
