@@ -175,7 +175,10 @@ PIC_API pic_status pic_loopback_link(pic_ctx *const *ctxs, int32_t n);
  * stream).  NULL = the legacy default stream.                                */
 PIC_API pic_status pic_set_stream(pic_ctx *ctx, void *stream);
 
-/* Load n particles of species s, replacing the previous ones.  xyzuvwq[7]:
+/* Load n particles of species s, replacing the previous ones (the particle
+ * state of Eq. 1: x_p, v_p and the charge q_s w_p of the
+ * statistical weights; kept in GPU memory).
+ * xyzuvwq[7]:
  * host or device fp64 arrays x, y, z, u, v, w (velocity) and q (per-particle
  * charge q_s w_p, R14); id: host or device int64 ids (may be NULL: ids
  * become 0..n-1).  Particles must lie in this rank's slab [slab_lo, slab_hi)
@@ -186,8 +189,9 @@ PIC_API pic_status pic_set_particles(pic_ctx *ctx, int32_t s, int64_t n,
                              const double *const xyzuvwq[7], const int64_t *id);
 
 /* Append n particles to species s (same arrays and units as
- * pic_set_particles; id NULL: ids continue the store's position count) and
- * add them to the cell order.  For loading stores too large to stage in one
+ * pic_set_particles; id NULL: ids continue the store's
+ * position count) and count them into the cell order (built once, by the next
+ * call that needs it).  For loading stores too large to stage in one
  * piece (draw a sub-slab, append it, free it).  Between cycles only
  * (PIC_ESTATE between pic_mover and pic_exchange); PIC_ERANGE if the store
  * would exceed capacity[s].  Particles outside this rank's slab are counted
@@ -243,11 +247,14 @@ PIC_API pic_status pic_moments(pic_ctx *ctx, int32_t s);
  * Asynchronous; latched device errors are returned by pic_sync.              */
 PIC_API pic_status pic_exchange(pic_ctx *ctx);
 
-/* Shorthand for one full cycle: pic_mover(-1), pic_moments(-1),
- * pic_exchange.                                                              */
+/* One full particle cycle of Alg. 1 (phases 1-2):
+ * pic_mover(-1), pic_moments(-1), pic_exchange (errors as those calls; the
+ * first failing status is returned).  Replayed from a CUDA graph when
+ * pic_set_graph allows it.                                                    */
 PIC_API pic_status pic_cycle(pic_ctx *ctx);
 
-/* CUDA graphs for pic_cycle (enable != 0; default off): the first pic_cycle
+/* Implementation control (no paper passage).
+ * CUDA graphs for pic_cycle (enable != 0; default off): the first pic_cycle
  * of each (field buffer, store buffer) combination is captured into a CUDA
  * graph and later cycles replay it — one launch instead of ~20 kernel launches
  * per cycle, for small per-GPU problems where launch gaps matter.  pic_cycle
