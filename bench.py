@@ -670,7 +670,7 @@ def main():
         next4 = {"what": "pic_gmm per species: 24^3 velocity bins, 4 components, 50 EM iterations (host-timed, synchronous)",
                  "fits": res}
 
-    cpu = None
+    cpu = cpu1 = None
     if parts_cpu_sample is not None:
         threads = torch.get_num_threads()
         torch.set_num_threads(1)
@@ -680,6 +680,7 @@ def main():
         cpu = {"value": ra, "unit": "particle updates/s", "cores": cores, "kind": "oracle", "sample": samplea,
                "single_thread": {"value": r1, "unit": "particle updates/s", "cores": 1, "kind": "oracle",
                                  "sample": sample1}}
+        cpu1 = dict(cpu["single_thread"])
 
     if rank == 0:
         line = {
@@ -696,7 +697,8 @@ def main():
                                 "pic_mover + pic_moments + pic_exchange, plain launches, profiled")},
             "roofline": roof,
             "roofline_fp64": roof64,
-            "cpu_baseline": cpu,
+            "cpu_baseline": cpu,                  # the oracle on every host core (OpenMP build)
+            "cpu_baseline_1core": cpu1,           # the single-threaded parity checker
             "e2e": e2e,
             "next2_sources": next2,
             "next3_control": next3,
