@@ -697,6 +697,8 @@ def main():
                                 "pic_mover + pic_moments + pic_exchange, plain launches, profiled")},
             "roofline": roof,
             "roofline_fp64": roof64,
+            "parity_report": "profiles/r02_parity_report.json (tools/parity_report.py: max error / bound per "
+                             "config clone, kernel family and species; not run by the bench)",
             "cpu_baseline": cpu,                  # the oracle on every host core (OpenMP build)
             "cpu_baseline_1core": cpu1,           # the single-threaded parity checker
             "e2e": e2e,

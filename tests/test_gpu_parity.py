@@ -583,3 +583,24 @@ def test_graph_cycles_match_the_oracle(kernel):
         assert PU.compare_particles(w, sp, gp, orc[s][0], orc[s][1], rep), rep
         assert PU.compare_moments(gm, orc[s][2], orc[s][3], rep), rep
     ctx.close()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_run_to_run_determinism(kernel):
+    """SURVEY.md §5 (race detection): the mover is per-particle pure, so two runs
+    of the same inputs give every particle (by id) bit for bit the same state,
+    whatever order the atomics built; the moments differ only by the order of
+    their fp64 sums."""
+    w = I.c2(nx_per_rank=16, ppc=27)
+    parts = I.make_species(w, device="cpu")
+    a, _ = run_gpu(w, parts, 3, kernel)
+    b, _ = run_gpu(w, parts, 3, kernel)
+    for s in range(len(parts)):
+        ga, gb = a[s][0], b[s][0]
+        oa, ob = np.argsort(ga["id"]), np.argsort(gb["id"])
+        assert np.array_equal(ga["id"][oa], gb["id"][ob])
+        for k in "xyzuvwq":
+            assert np.array_equal(ga[k][oa], gb[k][ob]), k
+        ma, mb = a[s][1], b[s][1]
+        scale = np.abs(ma).max(axis=(1, 2, 3), keepdims=True)
+        assert np.all(np.abs(ma - mb) <= 1e-12 * scale)
