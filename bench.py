@@ -236,6 +236,22 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- oracle (CPU) --
+_ORACLE_SETUP = {}
+
+
+def oracle_setup(w):
+    """The oracle's grid and field window of workload w (built once per process:
+    the field window of a full-size workload takes seconds on the host)."""
+    import oracle as O
+    from paper_2507_20719_b200 import inputs as I
+    key = (w.name, tuple(w.ncell), w.slab_or_all())
+    if key not in _ORACLE_SETUP:
+        g = O.make_grid(w.ncell, w.length, w.bc, w.dt, w.c, w.planet_center, w.planet_radius)
+        lo, EB = I.field_window(w.with_slab(0, w.ncell[0]) if w.slab_or_all() == (0, w.ncell[0]) else w, 2)
+        _ORACLE_SETUP[key] = (g, O.FieldWindow(lo, EB.numpy()))
+    return _ORACLE_SETUP[key]
+
+
 def oracle_rate(w, parts_cpu, target_s, n_iter=3, all_cores=False):
     """Time the CPU oracle (mover + moments, one cycle) on a bounded sample of the
     workload's particles; returns (updates/s, sample description, cores).
@@ -244,10 +260,7 @@ def oracle_rate(w, parts_cpu, target_s, n_iter=3, all_cores=False):
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle as O
-    from paper_2507_20719_b200 import inputs as I
-    g = O.make_grid(w.ncell, w.length, w.bc, w.dt, w.c, w.planet_center, w.planet_radius)
-    lo, EB = I.field_window(w.with_slab(0, w.ncell[0]) if w.slab_or_all() == (0, w.ncell[0]) else w, 2)
-    F = O.FieldWindow(lo, EB.numpy())
+    g, F = oracle_setup(w)
     cores = O.omp_threads() if all_cores else 1
     mover = O.mover_par if all_cores else O.mover
 

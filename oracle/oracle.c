@@ -361,23 +361,58 @@ int64_t oracle_mover_par(const oracle_grid *g, const oracle_field *F, double qom
 int64_t oracle_moments_par(const oracle_grid *g, int64_t np, const double *x, const double *y, const double *z,
                            const double *u, const double *v, const double *w, const double *q,
                            const int8_t *status, double *mom) {
-  const int64_t plane = nodes_axis(g, 0) * nodes_axis(g, 1) * nodes_axis(g, 2), M = 10 * plane;
+  const int64_t nn[3] = {nodes_axis(g, 0), nodes_axis(g, 1), nodes_axis(g, 2)};
+  const int64_t plane = nn[0] * nn[1] * nn[2], M = 10 * plane;
   const int T = oracle_omp_threads();
   double **grid = (double **)calloc((size_t)T, sizeof(double *));
+  /* node indices each thread touched, per axis (a cell and the next node,
+   * periodic wrap included): the merge reads only their product, so a sample
+   * that occupies a few planes of a large grid costs no full-grid pass; the
+   * per-thread grids are calloc'ed, i.e. untouched pages are never materialised */
+  unsigned char **touched = (unsigned char **)calloc((size_t)T, sizeof(unsigned char *));
+  const double *pos[3] = {x, y, z};
   int64_t outside = 0;
 #pragma omp parallel for num_threads(T) schedule(static, 1) reduction(+ : outside)
   for (int t = 0; t < T; ++t) {
     const int64_t a = np * t / T, b = np * (t + 1) / T;
     grid[t] = (double *)calloc((size_t)M, sizeof(double));
+    touched[t] = (unsigned char *)calloc((size_t)(nn[0] + nn[1] + nn[2]), 1);
     outside += oracle_moments(g, b - a, x + a, y + a, z + a, u + a, v + a, w + a, q + a,
                               status ? status + a : NULL, grid[t], NULL);
+    unsigned char *tc = touched[t];
+    for (int d = 0, o = 0; d < 3; o += (int)nn[d], ++d) {
+      const double dl = g->len[d] / (double)g->ncell[d];
+      for (int64_t p = a; p < b; ++p) {
+        if (status && status[p] != ORACLE_ALIVE) continue;
+        int64_t c = (int64_t)floor(pos[d][p] / dl);
+        if (c < 0 || c >= g->ncell[d]) continue;
+        tc[o + c] = 1;
+        tc[o + ((g->bc[d] == 0 && c + 1 == nn[d]) ? 0 : c + 1)] = 1;
+      }
+    }
   }
-  /* merge in thread order, parallel over nodes */
+  /* merge in thread order (every node adds threads 0, 1, ... in turn) */
+  for (int t = 0; t < T; ++t) {
+    const unsigned char *tx = touched[t], *ty = tx + nn[0], *tz = ty + nn[1];
 #pragma omp parallel for num_threads(T) schedule(static)
-  for (int64_t i = 0; i < M; ++i)
-    for (int t = 0; t < T; ++t) mom[i] += grid[t][i];
-  for (int t = 0; t < T; ++t) free(grid[t]);
+    for (int64_t k = 0; k < nn[2]; ++k) {
+      if (!tz[k]) continue;
+      for (int64_t j = 0; j < nn[1]; ++j) {
+        if (!ty[j]) continue;
+        for (int64_t i = 0; i < nn[0]; ++i) {
+          if (!tx[i]) continue;
+          const int64_t node = (k * nn[1] + j) * nn[0] + i;
+          for (int m = 0; m < 10; ++m) mom[m * plane + node] += grid[t][m * plane + node];
+        }
+      }
+    }
+  }
+  for (int t = 0; t < T; ++t) {
+    free(grid[t]);
+    free(touched[t]);
+  }
   free(grid);
+  free(touched);
   return outside;
 }
 #endif
