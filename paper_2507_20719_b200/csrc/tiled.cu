@@ -190,98 +190,6 @@ __device__ __forceinline__ bool gather_smem(const double *__restrict__ fld, cons
   return true;
 }
 
-// Field-split pair gather (PIC_GATHER_PAIR = 1; warp-collective, lanes paired
-// L, L ^ 1).  The per-lane gather delivers all 48 corner values to every lane
-// (the shared-memory crossbar bound).  Here the even lane
-// interpolates E and the odd lane B, each for BOTH particles of the pair: a
-// lane reads 3 of each node's 6 values (one LDS.128 + one LDS.64 instead of
-// three LDS.128), the partner's position comes in with three 64-bit shuffles and
-// the partner's half of the result goes back with three more.  Needs the node
-// layout (E_x, E_y, B_x, B_y, E_z, B_z) (the prescale writes it): the lane's
-// pair is at 2 h, its single at 4 + h (h = lane & 1).  When the partner's cell
-// differs (rare: the order is sorted by cell) a second pass reads the
-// partner's cell.  Returns false if the lane's own particle is not in the box.
-__device__ __forceinline__ bool gather_pair(const double *__restrict__ fld, const double u[3], double out[6]) {
-  constexpr unsigned FULL = 0xffffffffu;
-  const int hb = (int)(threadIdx.x & 1u);
-  double up[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) up[d] = __shfl_xor_sync(FULL, u[d], 1);
-  double f[3], fp[3];
-  int i[3], ip[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double fl = floor(u[d]), flp = floor(up[d]);
-    f[d] = u[d] - fl;
-    fp[d] = up[d] - flp;
-    i[d] = (int)fl;
-    ip[d] = (int)flp;
-  }
-  const bool in_own = (unsigned)i[0] <= (unsigned)(NB - 2) && (unsigned)i[1] <= (unsigned)(NB - 2) &&
-                      (unsigned)i[2] <= (unsigned)(NB - 2);
-  const bool in_par = (unsigned)ip[0] <= (unsigned)(NB - 2) && (unsigned)ip[1] <= (unsigned)(NB - 2) &&
-                      (unsigned)ip[2] <= (unsigned)(NB - 2);
-  const int b_own = ((i[2] * NB + i[1]) * NB + i[0]) * 6;
-  const int b_par = ((ip[2] * NB + ip[1]) * NB + ip[0]) * 6;
-  double S[8], Sp[8];
-  {
-    const double gx = 1.0 - f[0], gy = 1.0 - f[1], gz = 1.0 - f[2];
-    const double w00 = gy * gz, w10 = f[1] * gz, w01 = gy * f[2], w11 = f[1] * f[2];
-    S[0] = gx * w00; S[1] = f[0] * w00; S[2] = gx * w10; S[3] = f[0] * w10;
-    S[4] = gx * w01; S[5] = f[0] * w01; S[6] = gx * w11; S[7] = f[0] * w11;
-  }
-  {
-    const double gx = 1.0 - fp[0], gy = 1.0 - fp[1], gz = 1.0 - fp[2];
-    const double w00 = gy * gz, w10 = fp[1] * gz, w01 = gy * fp[2], w11 = fp[1] * fp[2];
-    Sp[0] = gx * w00; Sp[1] = fp[0] * w00; Sp[2] = gx * w10; Sp[3] = fp[0] * w10;
-    Sp[4] = gx * w01; Sp[5] = fp[0] * w01; Sp[6] = gx * w11; Sp[7] = fp[0] * w11;
-  }
-  // main pass over the own cell (the partner's if the own is outside the box);
-  // ap is right when both are in one cell or the own is outside
-  const int bm = in_own ? b_own : (in_par ? b_par : 0);
-  const double *cm = fld + bm;
-  double ao[3] = {0.0, 0.0, 0.0}, ap[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const double *nd = cm + 6 * ((c & 1) + NB * ((c >> 1) & 1) + NB * NB * (c >> 2));
-    const double2 pr = *reinterpret_cast<const double2 *>(nd + 2 * hb);
-    const double s = nd[4 + hb];
-    ao[0] = fma(S[c], pr.x, ao[0]);
-    ao[1] = fma(S[c], pr.y, ao[1]);
-    ao[2] = fma(S[c], s, ao[2]);
-    ap[0] = fma(Sp[c], pr.x, ap[0]);
-    ap[1] = fma(Sp[c], pr.y, ap[1]);
-    ap[2] = fma(Sp[c], s, ap[2]);
-  }
-  if (in_own && in_par && b_par != b_own) {
-    const double *cp = fld + b_par;
-    ap[0] = ap[1] = ap[2] = 0.0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const double *nd = cp + 6 * ((c & 1) + NB * ((c >> 1) & 1) + NB * NB * (c >> 2));
-      const double2 pr = *reinterpret_cast<const double2 *>(nd + 2 * hb);
-      const double s = nd[4 + hb];
-      ap[0] = fma(Sp[c], pr.x, ap[0]);
-      ap[1] = fma(Sp[c], pr.y, ap[1]);
-      ap[2] = fma(Sp[c], s, ap[2]);
-    }
-  }
-  // the partner computed my other half
-  double r[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) r[k] = __shfl_xor_sync(FULL, ap[k], 1);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    out[k] = hb ? r[k] : ao[k];
-    out[3 + k] = hb ? ao[k] : r[k];
-  }
-  return in_own;
-}
-
-#ifndef PIC_GATHER_PAIR
-#define PIC_GATHER_PAIR 0
-#endif
-
 // PIC_GATHER_MMA = 1 selects gather_mma below in the gamma == 1 mover.  It is
 // correct (parity green) but measured 2.1x slower than the per-lane gather
 // (C2: mover 5.59 vs 2.66 ms per step): its shuffles, weights,
@@ -403,7 +311,6 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     mover_tiled_kernel(const __grid_constant__ CUtensorMap tmap, const MoverTArgs A) {
   constexpr int MW = MOVER_WARPS;
   constexpr int MT = MOVER_THREADS;
-  constexpr bool kPair = PIC_GATHER_PAIR && REL == 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *fld = reinterpret_cast<double *>(smem_raw);              // staged node box
   double *stage_base = fld + NB3 * 6;
@@ -441,11 +348,7 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     double2 e0 = f2[0], e1 = f2[1], e2 = f2[2];
     e0.x *= S.ks; e0.y *= S.ks; e1.x *= S.ks;
     e1.y *= S.ks_c; e2.x *= S.ks_c; e2.y *= S.ks_c;
-    if constexpr (kPair) {   // (E_x, E_y, B_x, B_y, E_z, B_z) for gather_pair
-      f2[0] = e0; f2[1] = make_double2(e1.y, e2.x); f2[2] = make_double2(e1.x, e2.y);
-    } else {
-      f2[0] = e0; f2[1] = e1; f2[2] = e2;
-    }
+    f2[0] = e0; f2[1] = e1; f2[2] = e2;
   }
   __syncthreads();
 
@@ -510,10 +413,10 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     const double *sv = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
     uint32_t knew = KEY_DEAD;
     constexpr bool kMma = PIC_GATHER_MMA && REL == 0;
-    // with the tensor-core or the pair gather every lane pushes (warp-collective samples):
+    // with the tensor-core gather every lane pushes (warp-collective samples):
     // a lane past the end of the range pushes a particle at rest in the tile's
     // first cell and drops the result
-    if (kMma || kPair || act) {
+    if (kMma || act) {
       const double qv = act ? sv[6 * 32] : 0.0;
       const int64_t idv = act ? __double_as_longlong(sv[7 * 32]) : 0;
       const double xn[3] = {act ? sv[0] : (double)ox + 0.5, act ? sv[32] : (double)oy + 0.5,
@@ -537,8 +440,6 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
         const double u[3] = {xb[0] - bo[0], xb[1] - bo[1], xb[2] - bo[2]};
         if constexpr (kMma) {
           if (gather_mma(fld, u, EB)) return false;
-        } else if constexpr (kPair) {
-          if (gather_pair(fld, u, EB)) return false;
         } else {
           if (gather_smem(fld, u, EB)) return false;
         }
