@@ -2,11 +2,11 @@
 // indirection (not a step of the paper, which sorts only
 // for coalescence).
 //
-// The mover ranks every particle that stays on this rank within its new cell
-// (count_rank, warp-aggregated atomics on cell_count) while it moves; the
-// exchange ranks received particles the same way.  build_order then turns the
-// counts into cell offsets (exclusive scan) and scatters perm[cell_off[k] +
-// rank] = position.  The next mover gathers its inputs through perm and writes
+// The mover counts every particle that stays on this rank in its new cell
+// and ranks those that kept their cell (count_rank); the exchange counts
+// received particles the same way.  build_order then turns the counts into
+// cell offsets (exclusive scan) and scatters perm[cell_off[k] + rank] =
+// position, arrivals after each cell's stayers.  The next mover gathers its inputs through perm and writes
 // them in that order, so no separate permutation pass over the particle data
 // is ever needed (≈ 12 B / particle of order metadata instead of a radix sort
 // + gather of all arrays).  No key array is kept: a particle's cell always
@@ -55,10 +55,14 @@ __global__ void total_kernel(const uint32_t *__restrict__ cell_count, uint32_t *
 #endif
 constexpr int PERM_UNROLL = PIC_PERM_UNROLL;
 
+// Stayers go to cell_off[k] + rank; arrivals after the cell's stayers, in the
+// order of an atomic cursor per cell (`cursor`, zeroed after the scan).  (A
+// warp-aggregated cursor atomic measured slower: its warp-collective match
+// serialises the unrolled gathers.)
 __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t *__restrict__ rank,
                             const uint32_t *__restrict__ cell_off, const uint32_t *__restrict__ cell_count,
-                            const int64_t *__restrict__ d_nraw, uint32_t *__restrict__ perm, int64_t ncells,
-                            unsigned long long *__restrict__ stats) {
+                            uint32_t *__restrict__ cursor, const int64_t *__restrict__ d_nraw,
+                            uint32_t *__restrict__ perm, int64_t ncells, unsigned long long *__restrict__ stats) {
   // PERM_UNROLL independent elements per thread and iteration (memory-level
   // parallelism for the dependent cell_off gather)
   const int64_t n = *d_nraw;
@@ -74,7 +78,8 @@ __global__ void perm_kernel(const uint32_t *__restrict__ key_new, const uint32_t
 #pragma unroll
     for (int u = 0; u < PERM_UNROLL; ++u) {
       if (k[u] >= KEY_FIRST_RESERVED) continue;
-      const uint32_t q = cell_off[k[u]] + ((r[u] & RANK_ARRIVAL) ? cell_count[k[u]] + (r[u] & ~RANK_ARRIVAL) : r[u]);
+      const uint32_t q =
+          cell_off[k[u]] + ((r[u] & RANK_ARRIVAL) ? cell_count[k[u]] + atomicAdd(cursor + k[u], 1u) : r[u]);
       PIC_DCHECK(k[u] < ncells && q < cell_off[k[u] + 1], stats);
       perm[q] = (uint32_t)(p0 + u * stride);
     }
@@ -105,8 +110,11 @@ pic_status build_order(Ctx *ctx, int s) {
                                                 ctx->stream);
   if (e != cudaSuccess) return fail(ctx, PIC_ECUDA, std::string("scan: ") + cudaGetErrorString(e));
   if (sp.n_raw > 0) {
+    // the scan input is dead now: it becomes the arrivals' cursor
+    PIC_CUDA(cudaMemsetAsync(sp.cell_tot, 0, sizeof(uint32_t) * (nc + 1), ctx->stream));
     perm_kernel<<<grid_for(sp.n_raw), 256, 0, ctx->stream>>>(sp.key_new, sp.rank, sp.cell_off, sp.cell_count,
-                                                             sp.d_nraw, sp.perm, nc, ctx->stats); ++ctx->launches;
+                                                             sp.cell_tot, sp.d_nraw, sp.perm, nc, ctx->stats);
+    ++ctx->launches;
   }
   PIC_CUDA(cudaGetLastError());
   sp.order_valid = true;

@@ -472,14 +472,22 @@ __device__ __forceinline__ uint32_t finish_particle(const Geom &g, double xnew[3
   return k;
 }
 
-// Rank of a live particle within its cell for the counting sort: the lanes of
-// a warp holding the same key share one global atomicAdd.  Particles that kept
-// their cell ("stayers") and arrivals are counted separately so that, in the
-// next order, every cell lists its stayers first, in their previous order (a
-// contiguous run of the previous store: coalesced gathers), then its arrivals;
-// arrivals carry bit 31 in the rank.  All 32 lanes must call it; `counted ==
-// false` lanes get no rank.
+// Rank of a live particle within its cell for the counting sort.  Particles
+// that kept their cell ("stayers") and arrivals are counted separately so
+// that, in the next order, every cell lists its stayers first, in their
+// previous order (a contiguous run of the previous store: coalesced gathers),
+// then its arrivals.  A stayer gets its rank among the cell's stayers here
+// (the lanes of a warp holding the same key share one atomicAdd).  An arrival
+// is only counted (a reduction without return, so no kernel waits for it) and
+// gets the rank RANK_ARRIVAL; perm_kernel places it after the cell's stayers
+// with an atomic cursor.  All 32 lanes must call it; `counted == false` lanes
+// get no rank.
 constexpr uint32_t RANK_ARRIVAL = 0x80000000u;
+// a reduction without return (RED): atomicAdd with an unused result still
+// compiles to an ATOMG that later instructions wait for
+__device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t count_rank(uint32_t *__restrict__ cell_count, int64_t ncells, uint32_t k,
                                                bool counted, bool arrival) {
   const unsigned kk = counted ? (k | (arrival ? RANK_ARRIVAL : 0u)) : 0xFFFFFFFFu;
@@ -487,22 +495,32 @@ __device__ __forceinline__ uint32_t count_rank(uint32_t *__restrict__ cell_count
   const unsigned lane = threadIdx.x & 31u;
   const int leader = __ffs(peers) - 1;
   uint32_t base = 0;
-  if (counted && (int)lane == leader)
-    base = atomicAdd(cell_count + (arrival ? ncells + 1 : 0) + k, (unsigned)__popc(peers));
+  if (counted && (int)lane == leader) {
+    if (arrival)
+      red_add_u32(cell_count + ncells + 1 + k, (unsigned)__popc(peers));
+    else
+      base = atomicAdd(cell_count + k, (unsigned)__popc(peers));
+  }
   base = __shfl_sync(0xffffffffu, base, leader);
-  return (base + (uint32_t)__popc(peers & ((1u << lane) - 1u))) | (arrival ? RANK_ARRIVAL : 0u);
+  return arrival ? RANK_ARRIVAL : base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
 }
 
-// The same rank in two halves, so that the atomic's return latency can be
-// hidden behind unrelated work: count_rank_issue starts the warp-aggregated
-// atomic, count_rank_finish (called later by all 32 lanes) completes the rank.
+// The tiled mover's rank, in two halves: a stayer's cell belongs to the
+// CTA's own tile, and no other CTA counts stayers of that tile, so stayers are
+// counted in shared memory (`scnt`, the tile's 64 cells; the CTA stores the
+// totals at its end) and the short shared atomic's latency is hidden behind
+// the next round (count_rank_finish, called later by all 32 lanes).
+// Arrivals are counted with a global reduction, as in count_rank.  (A global
+// atomic with return here held every round: ptxas shares its scoreboard with
+// the next round's loads.)
 struct RankTicket {
-  uint32_t base;      // atomic result (leader lanes), consumed in finish
+  uint32_t base;      // shared atomic result (leader lanes), consumed in finish
   unsigned peers;
   int leader;
   bool counted, arrival;
 };
-__device__ __forceinline__ RankTicket count_rank_issue(uint32_t *__restrict__ cell_count, int64_t ncells,
+__device__ __forceinline__ RankTicket count_rank_issue(uint32_t *__restrict__ scnt, uint32_t tile_key0,
+                                                       uint32_t *__restrict__ cell_count, int64_t ncells,
                                                        uint32_t k, bool counted, bool arrival) {
   RankTicket t;
   const unsigned kk = counted ? (k | (arrival ? RANK_ARRIVAL : 0u)) : 0xFFFFFFFFu;
@@ -511,14 +529,18 @@ __device__ __forceinline__ RankTicket count_rank_issue(uint32_t *__restrict__ ce
   t.counted = counted;
   t.arrival = arrival;
   t.base = 0;
-  if (counted && (int)(threadIdx.x & 31u) == t.leader)
-    t.base = atomicAdd(cell_count + (arrival ? ncells + 1 : 0) + k, (unsigned)__popc(t.peers));
+  if (counted && (int)(threadIdx.x & 31u) == t.leader) {
+    if (arrival)
+      red_add_u32(cell_count + ncells + 1 + k, (unsigned)__popc(t.peers));
+    else
+      t.base = atomicAdd(scnt + (k - tile_key0), (unsigned)__popc(t.peers));
+  }
   return t;
 }
 __device__ __forceinline__ uint32_t count_rank_finish(const RankTicket &t) {
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t base = __shfl_sync(0xffffffffu, t.base, t.leader);
-  return (base + (uint32_t)__popc(t.peers & ((1u << lane) - 1u))) | (t.arrival ? RANK_ARRIVAL : 0u);
+  return t.arrival ? RANK_ARRIVAL : base + (uint32_t)__popc(t.peers & ((1u << lane) - 1u));
 }
 
 // Peer transport, warp-collective (all 32 lanes): lanes whose new key is
