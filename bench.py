@@ -39,7 +39,7 @@ B_ALG_PARTICLE = 104.0       # read x,v,q (56 B) + write x,v (48 B) per update (
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5", "c4s", "c5s"])
     ap.add_argument("--impl", default="pic", choices=["pic", "reference"])
