@@ -25,3 +25,21 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _release_gpu_memory(request):
+    """GPU tests that run libpic in-process hold up to ~140 GB of workspace in
+    torch's caching allocator; hand it back to the driver after every GPU test
+    so that the next one (or a multi-rank subprocess on the same device) can
+    allocate its own."""
+    yield
+    if "gpu" not in request.keywords:
+        return
+    import gc
+
+    import torch
+    if torch.cuda.is_available():
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
