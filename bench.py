@@ -587,6 +587,23 @@ def main():
                         "achieved": n_alive * b_deposit / (deposit_ms_step / 1e3) / 1e9 if deposit_ms_step else None}}
     mover_avg = sum(mover_ms) / len(mover_ms)
     roof64 = fp64_roofline(args, kname, n_alive, mover_ms_step, deposit_ms_step, value / world, local)
+    # the mover's binding unit: the shared-memory crossbar,
+    # 128 B per SM cycle (B300_MICROARCH.md "LDS/STS"; a broadcast counts as
+    # one access).  Wavefronts per update from the same static ncu capture as
+    # `traffic`; the time is this run's, the peak at this run's median SM clock.
+    roof_smem = None
+    sm_mhz = clk.summary().get("sm_mhz")
+    if traffic_src is not None and tj.get("mover_smem_wavefronts_per_update") and sm_mhz:
+        wf = tj["mover_smem_wavefronts_per_update"]
+        got = wf * 128 * n_alive / (mover_ms_step / 1e3) / 1e9
+        n_sms = torch.cuda.get_device_properties(local).multi_processor_count
+        top = 128 * n_sms * sm_mhz * 1e6 / 1e9
+        roof_smem = {"bound": "smem", "kernel": kname, "achieved": got, "peak": top, "unit": "GB/s",
+                     "frac": got / top, "wavefronts_per_update": wf,
+                     "peak_kind": "128 B/cycle/SM x %d SMs x the median SM clock of this run (%.0f MHz)"
+                                  % (n_sms, sm_mhz),
+                     "wavefronts_source": {"kind": "static ncu capture (not this run)",
+                                           "file": "profiles/traffic.json", "from": tj.get("source")}}
 
     # ---- e2e through the public API with host buffers (paper's discrete-GPU
     # cycle: fields host->device, moments device->host).  Every
@@ -710,6 +727,7 @@ def main():
                                 "pic_mover + pic_moments + pic_exchange, plain launches, profiled")},
             "roofline": roof,
             "roofline_fp64": roof64,
+            "roofline_smem": roof_smem,
             "parity_report": "profiles/r02_parity_report.json (tools/parity_report.py: max error / bound per "
                              "config clone, kernel family and species; not run by the bench)",
             "cpu_baseline": cpu,                  # the oracle on every host core (OpenMP build)
