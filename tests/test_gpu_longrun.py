@@ -8,8 +8,7 @@ GPU by id: within the north_star tolerances (1e-12) through 50 cycles.  The two
 fp64 implementations round differently (FMA contraction), and the electrons'
 orbits in the Harris sheet amplify those differences: measured worst velocity
 error / 1e-12 = 0.21, 0.44, 2.09 at cycles 25, 50, 100 (ions 0.009 at 100,
-positions <= 0.03), so at 100 cycles the bound is 10x (10 times the rate of
-growth is a bug, not rounding).
+positions <= 0.03), so at 100 cycles the test bounds the ratios by 10.
 """
 import numpy as np
 import pytest
