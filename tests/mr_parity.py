@@ -78,6 +78,8 @@ def run_case(name, w, cycles, kernel, transport, rank, world, inject=None, orc_c
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--long", type=int, default=0,
+                    help="only C1r for this many cycles, replayed from CUDA graphs over the peer transport")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -88,9 +90,19 @@ def main():
              ("c4s", I.c4(ncell=(32, 16, 16), ppc=8), 4),
              ("c5s", I.c5(ncell=(64, 32, 32), wind_ppc=2, inner_ppc=1, planet_ppc=16), 3)]
     all_ok, reports = True, []
+    if args.long:
+        # many replays of the same graphs: the device-side barrier epochs, the
+        # peer receive buffers and the forward rounds over a long run
+        res = run_case("c1r-long", I.c1(randomized=True), args.long, pic.KERNEL_TILED, pic.TRANSPORT_PEER, rank,
+                       world, orc_cache={}, graph=True)
+        if rank == 0:
+            all_ok, reports = res
+            for r in reports:
+                r["graph"] = True
+        cases = []
     inj_case = ("c4inj", I.c4(ncell=(32, 16, 16), ppc=8), 3, {"ppc": 8, "drift": (0.15, 0.0, 0.0)})
     orc_cache = {}
-    for transport in (pic.TRANSPORT_PEER, pic.TRANSPORT_NCCL):
+    for transport in (pic.TRANSPORT_PEER, pic.TRANSPORT_NCCL) if cases else ():
         for kernel in (pic.KERNEL_TILED, pic.KERNEL_BASIC):
             for name, w, cyc, *inj in cases + [inj_case]:
                 res = run_case(name, w, cyc, kernel, transport, rank, world, inject=inj[0] if inj else None,

@@ -45,3 +45,21 @@ def test_multirank_fullsize_sampled(config):
         assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
         rep = json.load(open(out))
         assert rep["ok"], rep
+
+
+def test_multirank_long_graph_run():
+    """C1r for 40 cycles replayed from CUDA graphs over the peer transport on
+    2 GPUs (every replay advances the device-side barrier epochs and reuses the
+    receive buffers), checked against the oracle by id."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "rep.json")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr", "127.0.0.1", "--master-port", "29583",
+               os.path.join(HERE, "mr_parity.py"), "--long", "40", "--out", out]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+        rep = json.load(open(out))
+        assert rep["ok"], rep
+        assert any(x.get("sent", 0) > 0 for x in rep["reports"])
