@@ -10,9 +10,10 @@
 //     memory; the CTA pre-scales them by k_s = (q/m) dt/2 and k_s / c so the
 //     iteration reads E' = k_s E and a = k_s B / c directly (R7, R8).
 //  2. Warps split the tile's particles evenly; lane = particle, rounds of 32.
-//     perm runs PK_AHEAD rounds ahead and the sources SRC_STAGES - 1 rounds
-//     ahead through cp.async (LDGSTS) rings in shared memory (mostly
-//     contiguous runs: every cell lists its stayers first).  n_iter predictor-
+//     perm runs PK_AHEAD rounds ahead and the sources x, v SRC_STAGES - 1
+//     rounds ahead through cp.async (LDGSTS) rings in shared memory (mostly
+//     contiguous runs: every cell lists its stayers first); q and id, which
+//     only pass through, go straight to registers.  n_iter predictor-
 //     corrector iterations (R1, R2) with trilinear gathers from shared memory
 //     (R12); x^{n+1}, v^{n+1}, boundary conditions (R10, R11, R21; fast path
 //     for particles that stay inside the slab); the result goes to buffer B at
@@ -57,7 +58,13 @@ constexpr int SRC_STAGES = PIC_SRC_STAGES;   // mover: rounds of gathered source
 #endif
 constexpr int PK_AHEAD = PIC_PK_AHEAD;   // mover: perm fetched this many rounds ahead
 constexpr int PK_SLOTS = PK_AHEAD + 1;   // mover: perm ring slots
-constexpr int MOVER_WARP_STAGE = SRC_STAGES * 8 * 32 + PK_SLOTS * 2 * 32 / 2;  // doubles per warp
+#ifndef PIC_SRC_RING_SLOTS
+#define PIC_SRC_RING_SLOTS 8
+#endif
+constexpr int SRC_STAGED = 6;            // mover: x, v staged in the ring (q, id go straight to registers)
+constexpr int SRC_RING = PIC_SRC_RING_SLOTS;   // ring stage pitch in 32-double rows (>= SRC_STAGED;
+                                              // 8 measured 1 % faster than 6)
+constexpr int MOVER_WARP_STAGE = SRC_STAGES * SRC_RING * 32 + PK_SLOTS * 2 * 32 / 2;  // doubles per warp
 // deposit staging per warp: S[32 particles][8 corners], V[32][moments 0..7]
 // and V2[32][moments 8, 9].  S and V rows are 8 doubles whose 16-byte pairs
 // are XOR-swizzled by row (stage_slot) so that both the row writes (STS.128,
@@ -369,8 +376,8 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
   // SRC_STAGES-1" then guarantees round r's sources.  The counting-sort rank of
   // a round completes during the next one, so the global atomic's latency
   // overlaps compute.
-  double *stg = stage_base + (size_t)warp * MOVER_WARP_STAGE;          // [SRC_STAGES][8][32] doubles
-  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + SRC_STAGES * 8 * 32);  // [PK_SLOTS][64]: perm in [0, 32)
+  double *stg = stage_base + (size_t)warp * MOVER_WARP_STAGE;          // [SRC_STAGES][SRC_STAGED][32] doubles
+  uint32_t *pk = reinterpret_cast<uint32_t *>(stg + SRC_STAGES * SRC_RING * 32);  // [PK_SLOTS][64]: perm in [0, 32)
   auto fetch_pk = [&](int ri) {        // perm of round ri
     const uint32_t q = wbeg + 32u * ri + lane;
     if (q < wend) {
@@ -383,13 +390,11 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     if (q < wend) {
       const uint32_t src_idx = pk[(ri % PK_SLOTS) * 64 + lane];
       PIC_DCHECK(src_idx < S.cap, A.stats);
-      double *d = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
+      double *d = stg + (ri % SRC_STAGES) * (SRC_RING * 32) + lane;
 #pragma unroll
-      for (int k = 0; k < 7; ++k)
+      for (int k = 0; k < SRC_STAGED; ++k)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + k * 32)), "l"(S.src[k] + src_idx)
                      : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 7 * 32)), "l"(S.src_id + src_idx)
-                   : "memory");
     }
   };
   for (int ri = 0; ri < PK_AHEAD; ++ri) fetch_pk(ri);
@@ -412,7 +417,7 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     fetch_pk(ri + PK_AHEAD);
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group %0;" ::"n"(SRC_STAGES - 1) : "memory");
-    const double *sv = stg + (ri % SRC_STAGES) * (8 * 32) + lane;
+    const double *sv = stg + (ri % SRC_STAGES) * (SRC_RING * 32) + lane;
     uint32_t knew = KEY_DEAD;
     constexpr bool kMma = PIC_GATHER_MMA && REL == 0;
     // with the tensor-core gather every lane pushes (warp-collective samples):
@@ -421,8 +426,14 @@ __global__ void __launch_bounds__(MOVER_THREADS, PIC_MOVER_MINB)
     double xnew[3], vnew[3], qv = 0.0;
     int64_t idv = 0;
     if (kMma || act) {
-      qv = act ? sv[6 * 32] : 0.0;
-      idv = act ? __double_as_longlong(sv[7 * 32]) : 0;
+      // q and id only pass through: loaded straight into registers (no
+      // shared-memory staging: -0.3 crossbar wavefronts per particle), consumed
+      // by the stores at the round's end
+      if (act) {
+        const uint32_t si = pk[(ri % PK_SLOTS) * 64 + lane];
+        qv = __ldg(S.src[6] + si);
+        idv = __ldg(S.src_id + si);
+      }
       const double xn[3] = {act ? sv[0] : (double)ox + 0.5, act ? sv[32] : (double)oy + 0.5,
                             act ? sv[64] : (double)oz + 0.5};
       const double vn[3] = {act ? sv[96] : 0.0, act ? sv[128] : 0.0, act ? sv[160] : 0.0};
