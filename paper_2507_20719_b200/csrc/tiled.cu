@@ -17,8 +17,10 @@
 //     corrector iterations (R1, R2) with trilinear gathers from shared memory
 //     (R12); x^{n+1}, v^{n+1}, boundary conditions (R10, R11, R21; fast path
 //     for particles that stay inside the slab); the result goes to buffer B at
-//     q and the new cell key is ranked for the counting sort of the next order
-//     (the rank atomic of a round completes during the next one).  With the
+//     q and the new cell key is counted for the counting sort of the next
+//     order (a particle that keeps its cell is ranked with a shared-memory
+//     atomic that completes during the next round; an arrival is only
+//     counted, with a global reduction).  With the
 //     peer transport, slab leavers are written straight into the neighbour's
 //     receive buffer (send_leavers_peer).  REL = 1 instantiates the
 //     relativistic Eq. 2 (NEXT-1).
