@@ -6,10 +6,10 @@
 // and ranks those that kept their cell (count_rank); the exchange counts
 // received particles the same way.  build_order then turns the counts into
 // cell offsets (exclusive scan) and scatters perm[cell_off[k] + rank] =
-// position, arrivals after each cell's stayers.  The next mover gathers its inputs through perm and writes
-// them in that order, so no separate permutation pass over the particle data
-// is ever needed (≈ 12 B / particle of order metadata instead of a radix sort
-// + gather of all arrays).  No key array is kept: a particle's cell always
+// position, arrivals after each cell's stayers.  The next mover gathers its
+// inputs through perm and writes them in that order, so no separate
+// permutation pass over the particle data is ever needed (≈ 12 B / particle of
+// order metadata instead of a radix sort + gather of all arrays).  No key array is kept: a particle's cell always
 // follows from its stored position.  Removed particles and slab leavers are
 // not counted and so drop out of the next order.
 #include <cub/device/device_scan.cuh>
