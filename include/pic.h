@@ -301,8 +301,10 @@ PIC_API pic_status pic_get_moments_async(pic_ctx *ctx, int32_t s, double *out);
  * Central differences (periodic wrap; one-sided at open-axis boundary nodes).
  * nranks > 1: COLLECTIVE with the peer transport (the x derivatives at a slab
  * face read the neighbour's adjacent owned plane from its mapped workspace,
- * behind a flag barrier); the NCCL transport returns PIC_EINVAL.
- * Synchronises.                                                              */
+ * behind a flag barrier); the NCCL transport returns PIC_EINVAL.  Device
+ * buffers for chi and rho_hat are written in place by the kernels; host
+ * buffers (and J_hat, staged in the workspace for the neighbours) are filled
+ * by copies.  Synchronises.                                                  */
 PIC_API pic_status pic_implicit_sources(pic_ctx *ctx, double *chi, double *rho_hat, double *J_hat);
 
 /* NEXT-3: inflow injection at the x = 0 face of an open x axis (PAPER.md:

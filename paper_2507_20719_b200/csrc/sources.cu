@@ -21,6 +21,7 @@ struct SourcesArgs {
   const double *field;                  // window [z][y][x][6]
   int64_t n[3];                         // owned nodes
   double invV;
+  double inv_delta[3], inv_2delta[3];   // stencil factors (one-sided, central)
   double *chi, *rho_hat, *J_hat;        // [9][n], [n], [3][n] (owned-node layout)
   // x neighbours (multi-rank, peer transport): their moment arrays and J-hat
   int has_nb[2];                        // [0] left, [1] right
@@ -41,9 +42,8 @@ __device__ __forceinline__ int64_t src_node(const SourcesArgs &A, int64_t i, int
 template <class F>
 __device__ __forceinline__ double node_diff(const SourcesArgs &A, const int64_t c[3], int axis, F f) {
   const int64_t n = A.n[axis];
-  const double delta = A.g.delta[axis];
   int64_t lo[3] = {c[0], c[1], c[2]}, hi[3] = {c[0], c[1], c[2]};
-  double h = 2.0 * delta;
+  double ih = A.inv_2delta[axis];   // 1 / (2 delta), or 1 / delta one-sided
   if (axis == 0 && A.g.multi_rank) {
     const bool L = c[0] == 0, R = c[0] == n - 1;
     if ((!L || A.has_nb[0]) && (!R || A.has_nb[1])) {
@@ -51,25 +51,25 @@ __device__ __forceinline__ double node_diff(const SourcesArgs &A, const int64_t 
       hi[0] = c[0] + 1;   // n: right neighbour
     } else if (L) {       // global open face: one-sided (R27)
       hi[0] = 1;          // (== n with one owned plane: the right neighbour)
-      h = delta;
+      ih = A.inv_delta[axis];
     } else {
       lo[0] = n - 2;
-      h = delta;
+      ih = A.inv_delta[axis];
     }
   } else if (A.g.periodic[axis]) {
     lo[axis] = c[axis] == 0 ? n - 1 : c[axis] - 1;
     hi[axis] = c[axis] == n - 1 ? 0 : c[axis] + 1;
   } else if (c[axis] == 0) {
     hi[axis] = 1;
-    h = delta;
+    ih = A.inv_delta[axis];
   } else if (c[axis] == n - 1) {
     lo[axis] = n - 2;
-    h = delta;
+    ih = A.inv_delta[axis];
   } else {
     lo[axis] = c[axis] - 1;
     hi[axis] = c[axis] + 1;
   }
-  return (f(hi) - f(lo)) / h;
+  return (f(hi) - f(lo)) * ih;
 }
 
 __device__ __forceinline__ void apply_R(const double a[3], const double x[3], double out[3]) {
@@ -87,8 +87,12 @@ __global__ void chi_jhat_kernel(const SourcesArgs A) {
   const int64_t total = A.n[0] * A.n[1] * A.n[2];
   const double dt = A.g.dt;
   const double four_pi = 4.0 * 3.14159265358979323846;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c[3] = {t % A.n[0], (t / A.n[0]) % A.n[1], t / (A.n[0] * A.n[1])};
+  {
+    // one thread per owned node: x from the block row, y and z from the grid
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n[0]) return;
+    const int64_t c[3] = {i, (int64_t)blockIdx.y, (int64_t)blockIdx.z};
+    const int64_t t = (c[2] * A.n[1] + c[1]) * A.n[0] + c[0];
     // B at the node from the field window (global node slab_lo + i, j, k)
     const double *fw = A.field + 6 * (((c[2] - A.g.f_lo[2]) * A.g.f_n[1] + (c[1] - A.g.f_lo[1])) * A.g.f_n[0] +
                                       (A.g.slab_lo + c[0] - A.g.f_lo[0]));
@@ -146,8 +150,11 @@ __global__ void chi_jhat_kernel(const SourcesArgs A) {
 
 __global__ void rho_hat_kernel(const SourcesArgs A) {
   const int64_t total = A.n[0] * A.n[1] * A.n[2];
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c[3] = {t % A.n[0], (t / A.n[0]) % A.n[1], t / (A.n[0] * A.n[1])};
+  {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n[0]) return;
+    const int64_t c[3] = {i, (int64_t)blockIdx.y, (int64_t)blockIdx.z};
+    const int64_t t = (c[2] * A.n[1] + c[1]) * A.n[0] + c[0];
     const int64_t me = src_node(A, c[0], c[1], c[2]);
     double rho = 0.0;
     for (int s = 0; s < A.n_species; ++s) rho += A.mom[s][me] * A.invV;
@@ -187,10 +194,26 @@ pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_ha
   A.field = ctx->field_buf[b];
   for (int d = 0; d < 3; ++d) A.n[d] = shape[d];
   A.invV = 1.0 / (g.delta[0] * g.delta[1] * g.delta[2]);
+  for (int d = 0; d < 3; ++d) {
+    A.inv_delta[d] = 1.0 / g.delta[d];
+    A.inv_2delta[d] = 1.0 / (2.0 * g.delta[d]);
+  }
   const int64_t total = shape[0] * shape[1] * shape[2];
-  A.chi = ctx->src_buf;
+  // chi and rho-hat go straight into the caller's arrays when they are device
+  // memory (no copy); J-hat always lands in the workspace first, where the
+  // neighbours' rho-hat pass reads it over NVLink
+  auto on_device = [](const void *p) {
+    cudaPointerAttributes at;
+    if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  };
+  const bool chi_dev = on_device(chi), rho_dev = on_device(rho_hat);
+  A.chi = chi_dev ? chi : ctx->src_buf;
   A.J_hat = ctx->src_buf + 9 * total;
-  A.rho_hat = ctx->src_buf + 12 * total;
+  A.rho_hat = rho_dev ? rho_hat : ctx->src_buf + 12 * total;
   for (int sd = 0; sd < 2; ++sd) {
     const Ctx::PeerLink &L = ctx->link[sd];
     A.has_nb[sd] = (g.multi_rank && L.mapped) ? 1 : 0;
@@ -203,23 +226,25 @@ pic_status implicit_sources(Ctx *ctx, double *chi, double *rho_hat, double *J_ha
     A.nb_jh[sd] = L.src ? L.src + 9 * A.nb_total[sd] : nullptr;
     A.nb_xj[sd] = sd == 0 ? L.owned_nx - 1 : 0;
   }
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > kSMs * 16) blocks = kSMs * 16;
+  const dim3 grid((unsigned)((shape[0] + 127) / 128), (unsigned)shape[1], (unsigned)shape[2]);
+  if (shape[1] > 65535 || shape[2] > 65535) return fail(ctx, PIC_EINVAL, "sources: more than 65535 nodes in y or z");
   pic_status st;
   if (g.multi_rank) {   // the neighbours' moments are final (their pic_exchange)
     st = peer_barrier(ctx);
     if (st != PIC_OK) return st;
   }
-  chi_jhat_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(A); ++ctx->launches;
+  chi_jhat_kernel<<<grid, 128, 0, ctx->stream>>>(A); ++ctx->launches;
   if (g.multi_rank) {   // the neighbours' J-hat is complete
     st = peer_barrier(ctx);
     if (st != PIC_OK) return st;
   }
-  rho_hat_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(A); ++ctx->launches;
+  rho_hat_kernel<<<grid, 128, 0, ctx->stream>>>(A); ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
-  if (chi) PIC_CUDA(cudaMemcpyAsync(chi, A.chi, 9 * sizeof(double) * total, cudaMemcpyDefault, ctx->stream));
+  if (chi && !chi_dev)
+    PIC_CUDA(cudaMemcpyAsync(chi, A.chi, 9 * sizeof(double) * total, cudaMemcpyDefault, ctx->stream));
   if (J_hat) PIC_CUDA(cudaMemcpyAsync(J_hat, A.J_hat, 3 * sizeof(double) * total, cudaMemcpyDefault, ctx->stream));
-  if (rho_hat) PIC_CUDA(cudaMemcpyAsync(rho_hat, A.rho_hat, sizeof(double) * total, cudaMemcpyDefault, ctx->stream));
+  if (rho_hat && !rho_dev)
+    PIC_CUDA(cudaMemcpyAsync(rho_hat, A.rho_hat, sizeof(double) * total, cudaMemcpyDefault, ctx->stream));
   PIC_CUDA(cudaStreamSynchronize(ctx->stream));
   return PIC_OK;
 }
