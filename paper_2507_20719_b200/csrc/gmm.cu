@@ -4,18 +4,25 @@
 //
 // bin_kernel: grid-stride over the live particles; per-CTA histogram in
 // shared memory (B <= 24, fp64 shared atomics), merged with global atomics.
-// em_kernel: one CTA of 256 threads runs the whole fit — weighted moments,
-// heaviest-bin + farthest-point seeding (deterministic argmax, lowest index on
-// ties), n_em EM iterations with per-thread partial sums reduced in a fixed
-// order (warp shuffles, then warp partials summed by one thread each).
+// em_kernel: a cluster of EM_CLUSTER CTAs of 256 threads runs the whole fit.
+// Every CTA computes the weighted moments and the heaviest-bin +
+// farthest-point seeding (deterministic argmax, lowest index on ties) itself;
+// in each of the n_em EM iterations the CTAs split the bins, reduce their
+// per-thread partial sums in a fixed order (warp shuffles, then warp partials
+// summed by one thread each), and every CTA adds the CTAs' partials in rank
+// order through distributed shared memory, so all hold the same parameters.
+#include <cooperative_groups.h>
+
 #include "pic_internal.cuh"
 
 namespace pic {
+namespace cg = cooperative_groups;
 
 constexpr int GMM_BMAX_SMEM = 24;   // shared-memory histogram up to 24^3 bins
 constexpr int GMM_BMAX = 64;        // histogram buffer in the workspace: 64^3
 constexpr int GMM_MMAX = 8;         // components (per-thread accumulators in registers)
 constexpr int EM_THREADS = 256;
+constexpr int EM_CLUSTER = 8;       // CTAs (SMs) per fit (portable cluster size)
 
 struct BinArgs {
   const double *u, *v, *w, *q;
@@ -72,7 +79,7 @@ struct EmArgs {
 // Block sum of K values per thread (fixed order): shuffles within warps, then
 // thread k sums the warps' partials for value k.  out[k] valid for all threads.
 template <int K>
-__device__ void block_sum(double (&v)[K], double *scratch /* [8][K] */, double *out /* [K] */) {
+__device__ void block_sum(double (&v)[K], double *scratch /* [EM_THREADS / 32][K] */, double *out /* [K] */) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -107,14 +114,21 @@ __device__ void block_argmax(double val, int64_t idx, double *sv, int64_t *si, d
   __syncthreads();
 }
 
+// MM: the number of components (a template parameter, so that the per-thread
+// accumulators of the EM loop are exactly M x 10 registers)
+template <int MM>
 __global__ void __launch_bounds__(EM_THREADS) em_kernel(const EmArgs A) {
-  __shared__ double scratch[8 * GMM_MMAX * 10];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  __shared__ double part[2][MM * 10];            // this CTA's partial sums, by iteration parity
+  __shared__ double s_alpha[MM], s_mu[MM][3], s_sig[MM][6];
+  __shared__ double scratch[(EM_THREADS / 32) * GMM_MMAX * 10];
   __shared__ double red[GMM_MMAX * 10];
   __shared__ double sv[EM_THREADS];
   __shared__ int64_t si[EM_THREADS];
   __shared__ double par_inv[GMM_MMAX][6], par_nrm[GMM_MMAX];
   __shared__ double smu[GMM_MMAX][3];
-  const int B = A.B, M = A.M;
+  const int B = A.B, M = MM;
   const int64_t nb = (int64_t)B * B * B;
   const double bw = 2.0 * A.vmax / (double)B, eps = 1e-6 * bw * bw;
   const double two_pi3 = pow(2.0 * 3.14159265358979323846, 1.5);
@@ -192,49 +206,57 @@ __global__ void __launch_bounds__(EM_THREADS) em_kernel(const EmArgs A) {
     }
   }
   if (threadIdx.x < M) {
-    A.alpha[threadIdx.x] = 1.0 / (double)M;
-    for (int d = 0; d < 3; ++d) A.mu[3 * threadIdx.x + d] = smu[threadIdx.x][d];
-    for (int k = 0; k < 6; ++k) A.sigma[6 * threadIdx.x + k] = cov[k];
+    s_alpha[threadIdx.x] = 1.0 / (double)M;
+    for (int d = 0; d < 3; ++d) s_mu[threadIdx.x][d] = smu[threadIdx.x][d];
+    for (int k = 0; k < 6; ++k) s_sig[threadIdx.x][k] = cov[k];
   }
   __syncthreads();
   const int ia[6] = {0, 0, 0, 1, 1, 2}, ib[6] = {0, 1, 2, 1, 2, 2};
   for (int it = 0; it < A.n_em; ++it) {
     if (threadIdx.x < M) {
-      const double *S = A.sigma + 6 * threadIdx.x;
+      const double *S = s_sig[threadIdx.x];
       const double a = S[0], b = S[1], c = S[2], d = S[3], e = S[4], f = S[5];
       const double iA = d * f - e * e, iB = -(b * f - c * e), iC = b * e - c * d;
       const double iD = a * f - c * c, iE = -(a * e - b * c), iF = a * d - b * b;
       const double det = a * iA + b * iB + c * iC;
       double *o = par_inv[threadIdx.x];
       o[0] = iA / det; o[1] = iB / det; o[2] = iC / det; o[3] = iD / det; o[4] = iE / det; o[5] = iF / det;
-      par_nrm[threadIdx.x] = A.alpha[threadIdx.x] / (two_pi3 * sqrt(det));
-      for (int dd = 0; dd < 3; ++dd) smu[threadIdx.x][dd] = A.mu[3 * threadIdx.x + dd];
+      par_nrm[threadIdx.x] = s_alpha[threadIdx.x] / (two_pi3 * sqrt(det));
+      for (int dd = 0; dd < 3; ++dd) smu[threadIdx.x][dd] = s_mu[threadIdx.x][dd];
     }
     __syncthreads();
-    double acc[GMM_MMAX * 10];
+    double acc[MM * 10];
 #pragma unroll
-    for (int k = 0; k < GMM_MMAX * 10; ++k) acc[k] = 0.0;
-    for (int64_t bb = threadIdx.x; bb < nb; bb += EM_THREADS) {
+    for (int k = 0; k < MM * 10; ++k) acc[k] = 0.0;
+    // this thread's bins b = b0 + j S (S = all threads of the cluster), their
+    // (ix, iy, iz) advanced incrementally (no 64-bit division per bin)
+    constexpr int S = EM_THREADS * EM_CLUSTER;
+    const int b0 = rank * EM_THREADS + (int)threadIdx.x;
+    const int dX = S % B, dY = (S / B) % B, dZ = S / (B * B);
+    int ix = b0 % B, iy = (b0 / B) % B, iz = b0 / (B * B);
+    for (int64_t bb = b0; bb < nb; bb += S) {
       const double h = A.hist[bb];
+      const double cx = -A.vmax + ((double)ix + 0.5) * bw, cy = -A.vmax + ((double)iy + 0.5) * bw,
+                   cz = -A.vmax + ((double)iz + 0.5) * bw;
+      ix += dX;
+      if (ix >= B) { ix -= B; ++iy; }
+      iy += dY;
+      if (iy >= B) { iy -= B; ++iz; }
+      iz += dZ;
       if (!(h > 0.0)) continue;
-      const double cx = centre(bb, 0), cy = centre(bb, 1), cz = centre(bb, 2);
-      double r[GMM_MMAX], tot = 0.0;
+      double r[MM], tot = 0.0;
 #pragma unroll
-      for (int i = 0; i < GMM_MMAX; ++i) {
-        r[i] = 0.0;
-        if (i < M) {
-          const double x = cx - smu[i][0], y = cy - smu[i][1], z = cz - smu[i][2];
-          const double *Q = par_inv[i];
-          const double q2 = Q[0] * x * x + Q[3] * y * y + Q[5] * z * z + 2.0 * (Q[1] * x * y + Q[2] * x * z + Q[4] * y * z);
-          r[i] = par_nrm[i] * exp(-0.5 * q2);
-          tot += r[i];
-        }
+      for (int i = 0; i < MM; ++i) {
+        const double x = cx - smu[i][0], y = cy - smu[i][1], z = cz - smu[i][2];
+        const double *Q = par_inv[i];
+        const double q2 = Q[0] * x * x + Q[3] * y * y + Q[5] * z * z + 2.0 * (Q[1] * x * y + Q[2] * x * z + Q[4] * y * z);
+        r[i] = par_nrm[i] * exp(-0.5 * q2);
+        tot += r[i];
       }
       if (!(tot > 0.0)) continue;
       const double cc[3] = {cx, cy, cz};
 #pragma unroll
-      for (int i = 0; i < GMM_MMAX; ++i) {
-        if (i >= M) break;
+      for (int i = 0; i < MM; ++i) {
         const double wr = h * (r[i] / tot);
         double *a = acc + 10 * i;
         a[0] += wr;
@@ -244,20 +266,37 @@ __global__ void __launch_bounds__(EM_THREADS) em_kernel(const EmArgs A) {
         for (int k = 0; k < 6; ++k) a[4 + k] += wr * cc[ia[k]] * cc[ib[k]];
       }
     }
-    block_sum<GMM_MMAX * 10>(acc, scratch, red);
+    block_sum<MM * 10>(acc, scratch, red);
+    // the cluster's sum of the CTAs' partials, in rank order, in every CTA
+    double *mine = part[it & 1];
+    if (threadIdx.x < MM * 10) mine[threadIdx.x] = red[threadIdx.x];
+    cluster.sync();
+    if (threadIdx.x < MM * 10) {
+      double t = 0.0;
+      for (int r = 0; r < EM_CLUSTER; ++r) t += cluster.map_shared_rank(mine, r)[threadIdx.x];
+      red[threadIdx.x] = t;
+    }
+    __syncthreads();
     if (threadIdx.x < M) {
       const double *a = red + 10 * threadIdx.x;
       if (a[0] > 0.0) {
         const int i = threadIdx.x;
-        A.alpha[i] = a[0] / W;
-        for (int d = 0; d < 3; ++d) A.mu[3 * i + d] = a[1 + d] / a[0];
+        s_alpha[i] = a[0] / W;
+        for (int d = 0; d < 3; ++d) s_mu[i][d] = a[1 + d] / a[0];
         for (int k = 0; k < 6; ++k)
-          A.sigma[6 * i + k] = a[4 + k] / a[0] - A.mu[3 * i + ia[k]] * A.mu[3 * i + ib[k]] + ((ia[k] == ib[k]) ? eps : 0.0);
+          s_sig[i][k] = a[4 + k] / a[0] - s_mu[i][ia[k]] * s_mu[i][ib[k]] + ((ia[k] == ib[k]) ? eps : 0.0);
       }
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *A.status = 0;
+  if (rank == 0 && threadIdx.x < M) {
+    const int i = threadIdx.x;
+    A.alpha[i] = s_alpha[i];
+    for (int d = 0; d < 3; ++d) A.mu[3 * i + d] = s_mu[i][d];
+    for (int k = 0; k < 6; ++k) A.sigma[6 * i + k] = s_sig[i][k];
+  }
+  if (rank == 0 && threadIdx.x == 0) *A.status = 0;
+  cluster.sync();   // no CTA leaves while another may still read its partials
 }
 
 pic_status gmm_fit(Ctx *ctx, int s, int B, double vmax, int M, int n_em, double *alpha, double *mu, double *sigma,
@@ -295,7 +334,30 @@ pic_status gmm_fit(Ctx *ctx, int s, int B, double vmax, int M, int n_em, double 
   E.mu = par + GMM_MMAX;
   E.sigma = par + 4 * GMM_MMAX;
   E.status = status;
-  em_kernel<<<1, EM_THREADS, 0, ctx->stream>>>(E); ++ctx->launches;
+  {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(EM_CLUSTER);
+    lc.blockDim = dim3(EM_THREADS);
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = EM_CLUSTER;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    switch (M) {
+      case 1: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<1>, E)); break;
+      case 2: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<2>, E)); break;
+      case 3: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<3>, E)); break;
+      case 4: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<4>, E)); break;
+      case 5: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<5>, E)); break;
+      case 6: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<6>, E)); break;
+      case 7: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<7>, E)); break;
+      default: PIC_CUDA(cudaLaunchKernelEx(&lc, em_kernel<8>, E)); break;
+    }
+  }
+  ++ctx->launches;
   PIC_CUDA(cudaGetLastError());
   int st_h = 0;
   unsigned long long clip_h = 0;
