@@ -208,21 +208,22 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
       continue;
     }
     __syncwarp();
-    // bitonic sort by (key, id)
+    // bitonic sort by (key, id); each lane takes compare-exchange pairs (i,
+    // i + j) directly (i = the pair index with a 0 bit inserted at j), so no
+    // lane idles on the upper halves
     for (int kk = 2; kk <= N; kk <<= 1) {
       for (int j = kk >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < N; i += 32) {
-          const int l = i ^ j;
-          if (l > i) {
-            const bool up = (i & kk) == 0;
-            const uint64_t ka = key[i], kb = key[l];
-            const int64_t ia = ids[i], ib = ids[l];
-            const bool b_less = kb < ka || (kb == ka && ib < ia);
-            if (b_less == up) {
-              key[i] = kb; key[l] = ka;
-              ids[i] = ib; ids[l] = ia;
-              const int32_t t = ix[i]; ix[i] = ix[l]; ix[l] = t;
-            }
+        for (int q = lane; q < (N >> 1); q += 32) {
+          const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+          const int l = i | j;
+          const bool up = (i & kk) == 0;
+          const uint64_t ka = key[i], kb = key[l];
+          const int64_t ia = ids[i], ib = ids[l];
+          const bool b_less = kb < ka || (kb == ka && ib < ia);
+          if (b_less == up) {
+            key[i] = kb; key[l] = ka;
+            ids[i] = ib; ids[l] = ia;
+            const int32_t t = ix[i]; ix[i] = ix[l]; ix[l] = t;
           }
         }
         __syncwarp();
