@@ -5,8 +5,8 @@
 // the particle id decide and orient the split; the second child is appended
 // and ranked as an arrival (the order is rebuilt afterwards).  Coalescence:
 // one CTA per tile, one warp per cell at a time; the cell's particles are
-// bitonic-sorted in shared memory by (velocity bins, id), lane 0 picks the
-// pairs, the lanes merge them (the keeper is written in place, the partner's
+// bitonic-sorted in shared memory by (velocity bins, id), the warp picks the
+// pairs (the definition's sequential scan, 32 records at a time), the lanes merge them (the keeper is written in place, the partner's
 // key becomes KEY_DEAD) and the order is recounted.
 #include "pic_internal.cuh"
 
@@ -229,20 +229,34 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
         __syncwarp();
       }
     }
-    // pairs in sorted order (lane 0, sequential like the definition)
-    int np = 0;
-    if (lane == 0) {
-      const int mc = (int)floor(A.frac * (double)nc);
-      for (int t = 0; t + 1 < nc && np < mc;) {
-        if (key[t] == key[t + 1]) {
-          pairs[np++] = t;
-          t += 2;
-        } else {
-          t += 1;
-        }
+    // pairs in sorted order.  The definition's sequential scan (pair t with
+    // t + 1 when their bins agree, then skip both) pairs, within each run of
+    // equal bins, the records at even offsets from the run's start with their
+    // successors, and stops after mc pairs; the warp finds those records 32
+    // at a time: run starts by a max-scan, leaders by offset parity, their
+    // order by a ballot prefix.
+    const int mc = (int)floor(A.frac * (double)nc);
+    int np = 0, run0 = 0;
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+      const int t = c0 + lane;
+      const bool valid = t < nc;
+      const uint64_t k = valid ? key[t] : ~0ull;
+      const bool start = valid && (t == 0 || key[t - 1] != k);
+      int st = start ? t : -1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, st, o);
+        if (lane >= o) st = max(st, v);
       }
+      st = max(st, run0);
+      const bool leader = valid && ((t - st) & 1) == 0 && t + 1 < nc && key[t + 1] == k;
+      const unsigned bal = __ballot_sync(0xffffffffu, leader);
+      const int idx = np + __popc(bal & ((1u << lane) - 1u));
+      if (leader && idx < mc) pairs[idx] = t;
+      np += __popc(bal);
+      run0 = __shfl_sync(0xffffffffu, st, 31);
     }
-    np = __shfl_sync(0xffffffffu, np, 0);
+    np = min(np, mc);
     __syncwarp();
     for (int m = lane; m < np; m += 32) {
       const int t = pairs[m];
