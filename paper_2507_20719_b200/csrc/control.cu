@@ -157,6 +157,73 @@ __device__ __forceinline__ uint64_t pack_bins(int64_t bx, int64_t by, int64_t bz
   return ((uint64_t)(bx + COAL_BIN_LIM) << 42) | ((uint64_t)(by + COAL_BIN_LIM) << 21) | (uint64_t)(bz + COAL_BIN_LIM);
 }
 
+
+// Bitonic sort of N <= 256 records (key, id, index) held in registers, element
+// i = lane + 32 r in slot r: the stages with j >= 32 compare two slots of the
+// same lane, the others exchange with lane ^ j by shuffles.  Same network and
+// comparisons as the shared-memory sort, so the same order.
+constexpr int COAL_RREG = 8;
+__device__ __forceinline__ void cx_slots(uint64_t (&k)[COAL_RREG], int64_t (&d)[COAL_RREG], int (&x)[COAL_RREG],
+                                         int a, int b, bool up) {
+  const bool b_less = k[b] < k[a] || (k[b] == k[a] && d[b] < d[a]);
+  if (b_less == up) {
+    const uint64_t tk = k[a]; k[a] = k[b]; k[b] = tk;
+    const int64_t td = d[a]; d[a] = d[b]; d[b] = td;
+    const int tx = x[a]; x[a] = x[b]; x[b] = tx;
+  }
+}
+__device__ __forceinline__ void warp_sort_regs(uint64_t *key, int64_t *ids, int32_t *ix, int N, int lane) {
+  uint64_t k[COAL_RREG];
+  int64_t d[COAL_RREG];
+  int x[COAL_RREG];
+#pragma unroll
+  for (int r = 0; r < COAL_RREG; ++r) {
+    const int i = lane + 32 * r;
+    const bool in = i < N;
+    k[r] = in ? key[i] : ~0ull;
+    d[r] = in ? ids[i] : INT64_MAX;
+    x[r] = in ? ix[i] : -1;
+  }
+  for (int kk = 2; kk <= N; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int js = j >> 5;   // slot distance 1, 2 or 4
+#pragma unroll
+        for (int r = 0; r < COAL_RREG; ++r) {
+          const bool up = ((lane + 32 * r) & kk) == 0;
+          if (js == 1 && !(r & 1)) cx_slots(k, d, x, r, r + 1 < COAL_RREG ? r + 1 : r, up);
+          if (js == 2 && !(r & 2)) cx_slots(k, d, x, r, r + 2 < COAL_RREG ? r + 2 : r, up);
+          if (js == 4 && !(r & 4)) cx_slots(k, d, x, r, r + 4 < COAL_RREG ? r + 4 : r, up);
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int r = 0; r < COAL_RREG; ++r) {
+          const bool up = ((lane + 32 * r) & kk) == 0;
+          const uint64_t pk = __shfl_xor_sync(0xffffffffu, k[r], j);
+          const int64_t pd = __shfl_xor_sync(0xffffffffu, d[r], j);
+          const int px = __shfl_xor_sync(0xffffffffu, x[r], j);
+          const bool p_less = pk < k[r] || (pk == k[r] && pd < d[r]);
+          if (p_less == (lower == up)) {
+            k[r] = pk;
+            d[r] = pd;
+            x[r] = px;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < COAL_RREG; ++r) {
+    const int i = lane + 32 * r;
+    if (i < N) {
+      key[i] = k[r];
+      ix[i] = x[r];
+    }
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -208,10 +275,11 @@ __global__ void __launch_bounds__(32 * COAL_WARPS) coalesce_kernel(const CoalArg
       continue;
     }
     __syncwarp();
-    // bitonic sort by (key, id); each lane takes compare-exchange pairs (i,
-    // i + j) directly (i = the pair index with a 0 bit inserted at j), so no
-    // lane idles on the upper halves
-    for (int kk = 2; kk <= N; kk <<= 1) {
+    // bitonic sort by (key, id): in registers up to 256 records; above, in
+    // shared memory, each lane taking compare-exchange pairs (i, i + j)
+    // directly (i = the pair index with a 0 bit inserted at j)
+    if (N <= 32 * COAL_RREG) warp_sort_regs(key, ids, ix, N, lane);
+    else for (int kk = 2; kk <= N; kk <<= 1) {
       for (int j = kk >> 1; j > 0; j >>= 1) {
         for (int q = lane; q < (N >> 1); q += 32) {
           const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
