@@ -302,12 +302,12 @@ __device__ __forceinline__ bool gather_mma(const double *__restrict__ fld, const
 
 // ----------------------------------------------------------------- mover ----
 #ifndef PIC_MOVER_MINB
-#define PIC_MOVER_MINB 2
+#define PIC_MOVER_MINB 4
 #endif
 // NIT > 0: the iteration count is a compile-time constant (fully unrolled);
 // NIT == 0: runtime A.n_iter.
 #ifndef PIC_MOVER_WARPS
-#define PIC_MOVER_WARPS 8
+#define PIC_MOVER_WARPS 4
 #endif
 constexpr int MOVER_WARPS = PIC_MOVER_WARPS;
 constexpr int MOVER_THREADS = 32 * MOVER_WARPS;
