@@ -55,3 +55,8 @@ def test_gpu_arm_fp64_roofline_on_c3_clone():
     assert r is not None and r["bound"] == "alu" and r["unit"] == "TFLOP/s"
     assert 20 < r["peak"] < 60 and 0 < r["frac"] < 1 and r["flops_per_update"] > 300
     assert d["roofline"]["traffic"] > 0 and d["roofline"]["traffic_source"]["kind"].startswith("static")
+    # the mover against its binding unit (shared-memory crossbar at the run's clock)
+    sm = d["roofline_smem"]
+    assert sm is not None and sm["bound"] == "smem" and sm["unit"] == "GB/s"
+    assert 0 < sm["frac"] < 1 and abs(sm["frac"] - sm["achieved"] / sm["peak"]) < 1e-9
+    assert sm["wavefronts_source"]["kind"].startswith("static")
